@@ -1,0 +1,269 @@
+/*
+ * aggmg_b200.h — C-ABI drop-in boundary of the B200-native unsmoothed-aggregation AMG.
+ *
+ * Every entry point replaces one public function of the reference C++ library
+ * `aggmg` (/root/reference/proj/core/include/aggmg/...).  The reference has no FFI of
+ * its own; these signatures are what a ctypes / cgo / JNI binding of that C++ API
+ * would bind: plain pointers and sizes, int64 host indices (reference types.hpp:12),
+ * fp64 values (types.hpp:16), no C++ or torch types.
+ *
+ * Conventions
+ *   - Every function returns AGGMG_OK (0) on success.  Failures that the reference
+ *     reports as `aggmg::Error` (error.hpp:14-27) return AGGMG_ERR and leave the same
+ *     message text in aggmg_last_error() (tests grep the reference substrings:
+ *     "rebuild", "too large", "row i", "use fgmres", "length", "aggregate", "pivot",
+ *     "diagonal", "outside shape").  CUDA failures return AGGMG_ERR_CUDA.
+ *   - Host arrays in, host arrays out.  The computation runs on the current CUDA
+ *     device through hand-written sm_100a kernels; there is no CPU fallback.
+ *   - Output matrices are library-allocated aggmg_csr values; release them with
+ *     aggmg_csr_free().
+ *   - Results are independent of the device count and launch configuration (the
+ *     reference's thread-count invariance, parallel.hpp:25-27).
+ */
+#ifndef AGGMG_B200_H
+#define AGGMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AGGMG_OK 0
+#define AGGMG_ERR 1
+#define AGGMG_ERR_CUDA 2
+
+/* ---- value types --------------------------------------------------------- */
+
+/* Canonical CSR (reference sparse.hpp:18-47): row_offsets[n_rows+1], strictly
+ * increasing columns per row.  As an input the arrays are borrowed; as an output
+ * they are owned by the library until aggmg_csr_free(). */
+typedef struct aggmg_csr {
+  int64_t n_rows;
+  int64_t n_cols;
+  int64_t nnz;
+  int64_t* row_offsets;
+  int64_t* col_indices;
+  double* values;
+} aggmg_csr;
+
+/* enums mirror the reference values */
+enum { AGGMG_ZERO_DIAG_POSITIVE = 0, AGGMG_ZERO_DIAG_FAIL = 1 };           /* strength.hpp:15 */
+enum { AGGMG_SMOOTHER_JACOBI = 0, AGGMG_SMOOTHER_DAMPED_JACOBI = 1,
+       AGGMG_SMOOTHER_SGS = 2 };                                          /* smoother.hpp:13 */
+enum { AGGMG_CYCLE_V = 0, AGGMG_CYCLE_K = 1, AGGMG_CYCLE_HYBRID = 2 };     /* cycles.hpp:11 */
+enum { AGGMG_INNER_CG = 0, AGGMG_INNER_GMRES = 1 };                       /* cycles.hpp:12 */
+enum { AGGMG_SOLVER_FGMRES = 0, AGGMG_SOLVER_PCG = 1 };                   /* krylov.hpp:14 */
+
+/* SetupConfig, reference hierarchy.hpp:30-38 (same defaults via aggmg_setup_config_default). */
+typedef struct aggmg_setup_config {
+  double alpha;            /* 0.25 */
+  int64_t coarse_size_max; /* 600 */
+  int32_t max_levels;      /* 25 */
+  int32_t smoother;        /* AGGMG_SMOOTHER_DAMPED_JACOBI */
+  int32_t arnoldi_m;       /* 5 */
+  int32_t reuse_caches;    /* 0; coarse values always follow the cached segment order */
+  uint64_t seed;           /* 42 */
+} aggmg_setup_config;
+
+/* CycleConfig, reference cycles.hpp:17-22. */
+typedef struct aggmg_cycle_config {
+  int32_t kind;     /* AGGMG_CYCLE_HYBRID */
+  int32_t k_levels; /* 2 */
+  double t;         /* 0.25 */
+  int32_t inner;    /* AGGMG_INNER_GMRES */
+} aggmg_cycle_config;
+
+/* SolverConfig, reference krylov.hpp:16-21. */
+typedef struct aggmg_solver_config {
+  int32_t method;    /* AGGMG_SOLVER_FGMRES */
+  double tol;        /* 1e-6 */
+  int32_t max_iters; /* 200 */
+  int32_t restart;   /* 30 */
+} aggmg_solver_config;
+
+/* SolveReport, reference krylov.hpp:23-30.  The caller provides `history` with
+ * room for history_capacity doubles (max_iters + 1 always suffices); the library
+ * writes history_length entries. */
+typedef struct aggmg_solve_report {
+  int32_t converged;
+  int32_t iterations;
+  double* history;
+  int64_t history_capacity;
+  int64_t history_length;
+  double setup_seconds; /* filled by aggmg_setup_and_solve only */
+  double solve_seconds;
+  char note[256];
+} aggmg_solve_report;
+
+typedef struct aggmg_hierarchy aggmg_hierarchy;           /* Hierarchy, hierarchy.hpp:40-48 */
+typedef struct aggmg_galerkin_cache aggmg_galerkin_cache; /* GalerkinCache, galerkin.hpp:25-45 */
+typedef struct aggmg_dmatrix aggmg_dmatrix;               /* device-resident CSR (no reference analogue) */
+
+/* ---- library state --------------------------------------------------------- */
+
+const char* aggmg_version(void);                 /* types.hpp:18 */
+const char* aggmg_last_error(void);              /* message of the last failing call (thread-local) */
+int aggmg_init(int device);                      /* select device, create stream + memory pool */
+int aggmg_synchronize(void);
+void aggmg_set_num_threads(int n);               /* parallel.hpp:27 — accepted, no effect on results */
+int aggmg_num_threads(void);                     /* parallel.hpp:29 — reports the SM count */
+int64_t aggmg_kernel_launches(void);             /* number of kernels this library has launched */
+void aggmg_setup_config_default(aggmg_setup_config* c);
+void aggmg_cycle_config_default(aggmg_cycle_config* c);
+void aggmg_solver_config_default(aggmg_solver_config* c);
+void aggmg_csr_free(aggmg_csr* m);
+
+/* ---- L1 sparse / vector kernels (sparse.hpp, vector_ops.hpp) ---------------- */
+
+int aggmg_spmv(const aggmg_csr* A, const double* x, double* y);            /* sparse.hpp:70-71 */
+int aggmg_transpose(const aggmg_csr* A, aggmg_csr* T);                     /* sparse.hpp:78 */
+int aggmg_dot(int64_t n, const double* a, const double* b, double* out);  /* vector_ops.hpp:20 */
+int aggmg_norm2(int64_t n, const double* a, double* out);                 /* vector_ops.hpp:42 */
+int aggmg_axpy(int64_t n, double a, const double* x, double* y);          /* vector_ops.hpp:45 */
+int aggmg_scale(int64_t n, double a, double* x);                          /* vector_ops.hpp:50 */
+
+/* ---- L2 setup components ----------------------------------------------------- */
+
+/* strength.hpp:22-23 / strength.cpp:28-72 */
+int aggmg_classic_strength(const aggmg_csr* A, double alpha, int zero_diag_policy, aggmg_csr* C);
+/* strength.hpp:27 / strength.cpp:74-78; counts has C->n_cols entries */
+int aggmg_influence_counts(const aggmg_csr* C, int64_t* counts);
+/* strength.hpp:31 / strength.cpp:80-111 */
+int aggmg_symmetrize_pattern(const aggmg_csr* C, aggmg_csr* S);
+/* aggregation.hpp:28-29 / aggregation.cpp:45-86.  state[n] in {+1,-1}; roots are the
+ * nodes with state +1, ascending. */
+int aggmg_mis2(const aggmg_csr* S, const int64_t* influence, uint64_t seed, int8_t* state,
+               int64_t* n_roots, int32_t* sweeps);
+/* aggregation.hpp:45 / aggregation.cpp:88-159.  representatives has room for n. */
+int aggmg_aggregate(const aggmg_csr* S, const aggmg_csr* A, const int8_t* state,
+                    int64_t* assignment, int64_t* representatives, int64_t* n_aggregates);
+/* transfer.hpp:24 / transfer.cpp:15-49 */
+int aggmg_build_transfer(int64_t n_fine, int64_t n_aggregates, const int64_t* assignment,
+                         const double* fine_b, aggmg_csr* P, aggmg_csr* R, double* coarse_b);
+/* galerkin.hpp:16 — explicit R*A*P (two row-wise products, sparse.cpp:71-131 order) */
+int aggmg_galerkin_direct(const aggmg_csr* R, const aggmg_csr* A, const aggmg_csr* P,
+                          aggmg_csr* Ac);
+/* galerkin.hpp:47 / galerkin.cpp:38-96 */
+int aggmg_build_galerkin_cache(const aggmg_csr* A, int64_t n_aggregates, const int64_t* assignment,
+                               aggmg_galerkin_cache** out);
+/* sizes of the cache arrays: nnz_fine = entry length, nnz_coarse = segments */
+int aggmg_galerkin_cache_info(const aggmg_galerkin_cache* c, int64_t* n_fine, int64_t* n_coarse,
+                              int64_t* nnz_fine, int64_t* nnz_coarse);
+/* copies the GalerkinCache fields (galerkin.hpp:29-44) to caller arrays; any pointer may be NULL */
+int aggmg_galerkin_cache_export(const aggmg_galerkin_cache* c, int64_t* coarse_row_offsets,
+                                int64_t* coarse_col_indices, int64_t* entry, int64_t* entry_row,
+                                int64_t* segment_offsets, int64_t* slot_of_csr,
+                                int64_t* rows_by_coarse, int64_t* agg_row_offsets);
+/* galerkin.hpp:52-53 / galerkin.cpp:98-137 */
+int aggmg_apply_galerkin_cache(const aggmg_galerkin_cache* c, const aggmg_csr* A,
+                               const aggmg_csr* P, aggmg_csr* Ac);
+void aggmg_galerkin_cache_free(aggmg_galerkin_cache* c);
+/* smoother.hpp:31-32 / smoother.cpp:86-99; inv_diag has n entries (may be NULL) */
+int aggmg_setup_smoother(const aggmg_csr* A, int kind, int arnoldi_m, uint64_t seed,
+                         double* inv_diag, double* omega, double* rho_est);
+/* smoother.hpp:37 / smoother.cpp:101-124; x is updated in place */
+int aggmg_smooth(int kind, const double* inv_diag, double omega, const aggmg_csr* A,
+                 const double* b, double* x);
+/* dense.hpp:45 / dense.cpp:104-212 (host routine used by the smoother setup) */
+int aggmg_hessenberg_eigenvalues(int64_t n, const double* H_row_major, double* re, double* im);
+
+/* ---- L3 hierarchy ---------------------------------------------------------------- */
+
+/* hierarchy.hpp:57 / hierarchy.cpp:34-88 */
+int aggmg_setup_hierarchy(const aggmg_csr* A0, const double* B0, const aggmg_setup_config* cfg,
+                          aggmg_hierarchy** out);
+/* hierarchy.hpp:64 / hierarchy.cpp:90-104 (in place) */
+int aggmg_refresh_values(aggmg_hierarchy* h, const double* new_values, int64_t count);
+void aggmg_hierarchy_free(aggmg_hierarchy* h);
+int64_t aggmg_hierarchy_n_levels(const aggmg_hierarchy* h);                 /* hierarchy.hpp:46 */
+int aggmg_hierarchy_level_size(const aggmg_hierarchy* h, int64_t k, int64_t* n, int64_t* nnz);
+int aggmg_hierarchy_level_A(const aggmg_hierarchy* h, int64_t k, aggmg_csr* A); /* Level::A */
+int aggmg_hierarchy_level_P(const aggmg_hierarchy* h, int64_t k, aggmg_csr* P); /* Level::P */
+int aggmg_hierarchy_level_R(const aggmg_hierarchy* h, int64_t k, aggmg_csr* R); /* Level::R */
+int aggmg_hierarchy_level_B(const aggmg_hierarchy* h, int64_t k, double* B);    /* Level::B */
+/* aggregation of level k -> k+1 (GalerkinCache::assignment) and its MIS sweeps */
+int aggmg_hierarchy_level_aggregation(const aggmg_hierarchy* h, int64_t k, int64_t* assignment,
+                                      int64_t* n_aggregates, int32_t* mis_sweeps);
+/* Level::smoother (smoother.hpp:18-24); inv_diag may be NULL */
+int aggmg_hierarchy_level_smoother(const aggmg_hierarchy* h, int64_t k, double* omega,
+                                   double* rho_est, double* inv_diag);
+int64_t aggmg_hierarchy_n_warnings(const aggmg_hierarchy* h);              /* Hierarchy::warnings */
+const char* aggmg_hierarchy_warning(const aggmg_hierarchy* h, int64_t i);
+/* hierarchy.hpp:78 */
+int aggmg_hierarchy_report(const aggmg_hierarchy* h, double* grid_complexity,
+                           double* operator_complexity);
+/* device time of the last setup (ms) split into phases */
+int aggmg_hierarchy_setup_ms(const aggmg_hierarchy* h, double* total_ms);
+
+/* ---- L4 cycles --------------------------------------------------------------- */
+
+int aggmg_vcycle(const aggmg_hierarchy* h, int64_t k, const double* b, double* x);   /* cycles.hpp:28 */
+int aggmg_kcycle(const aggmg_hierarchy* h, const aggmg_cycle_config* cfg, int64_t k,
+                 const double* b, double* x);                                      /* cycles.hpp:37 */
+int aggmg_apply_preconditioner(const aggmg_hierarchy* h, const aggmg_cycle_config* cfg,
+                               const double* r, double* z);                        /* cycles.hpp:42 */
+
+/* ---- L4 Krylov --------------------------------------------------------------- */
+
+/* krylov.hpp:43-50.  M == NULL is the identity preconditioner (krylov.cpp:23-25);
+ * otherwise M is apply_preconditioner(M, cycle, .) exactly as the reference CLI wires it
+ * (aggmg_main.cpp:194-196). */
+int aggmg_pcg(const aggmg_csr* A, const double* b, const double* x0, const aggmg_hierarchy* M,
+              const aggmg_cycle_config* cycle, const aggmg_solver_config* cfg, double* x,
+              aggmg_solve_report* report);
+int aggmg_fgmres(const aggmg_csr* A, const double* b, const double* x0, const aggmg_hierarchy* M,
+                 const aggmg_cycle_config* cycle, const aggmg_solver_config* cfg, double* x,
+                 aggmg_solve_report* report);
+
+/* One call = reference CLI `solve` pipeline (aggmg_main.cpp:163-210): setup_hierarchy(A, B0)
+ * then pcg/fgmres(A, b, x0) preconditioned by the hierarchy.  B0/x0 may be NULL (ones / zeros).
+ * Host buffers in and out; this is the end-to-end entry point bench.py times. */
+int aggmg_setup_and_solve(const aggmg_csr* A, const double* b, const double* B0, const double* x0,
+                          const aggmg_setup_config* setup, const aggmg_cycle_config* cycle,
+                          const aggmg_solver_config* solver, double* x,
+                          aggmg_solve_report* report);
+
+/* ---- inputs (poisson.hpp) ------------------------------------------------------ */
+
+/* poisson.hpp:17-26 / poisson.cpp:15-77, host generator */
+int aggmg_generate_poisson(int dims, int64_t nx, int64_t ny, int64_t nz, double epsilon,
+                           int weak_axis, aggmg_csr* A);
+/* 27-point variable-coefficient diffusion with coefficient jumps (BASELINE config 4;
+ * no reference generator exists, definition in DESIGN.md) */
+int aggmg_generate_jump27(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,
+                          aggmg_csr* A);
+
+/* ---- device-resident path (inputs already in HBM; no reference analogue) ----------- */
+
+int aggmg_dmatrix_from_host(const aggmg_csr* A, aggmg_dmatrix** out);
+/* same matrix as aggmg_generate_poisson, generated directly in HBM */
+int aggmg_dmatrix_poisson(int dims, int64_t nx, int64_t ny, int64_t nz, double epsilon,
+                          int weak_axis, aggmg_dmatrix** out);
+int aggmg_dmatrix_jump27(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,
+                         aggmg_dmatrix** out);
+int aggmg_dmatrix_size(const aggmg_dmatrix* A, int64_t* n_rows, int64_t* nnz);
+int aggmg_dmatrix_to_host(const aggmg_dmatrix* A, aggmg_csr* out);
+void aggmg_dmatrix_free(aggmg_dmatrix* A);
+/* setup_hierarchy on a device matrix (B0 = ones); the hierarchy shares A's storage */
+int aggmg_setup_hierarchy_device(const aggmg_dmatrix* A0, const aggmg_setup_config* cfg,
+                                 aggmg_hierarchy** out);
+/* pcg/fgmres on level 0 of h with b = ones, x0 = 0, everything resident in HBM;
+ * x (host, may be NULL) receives the solution */
+int aggmg_solve_device(const aggmg_hierarchy* h, const aggmg_cycle_config* cycle,
+                       const aggmg_solver_config* cfg, double* x, aggmg_solve_report* report);
+
+/* ---- measurement ------------------------------------------------------------------ */
+
+/* Per-kernel-family CUDA-event timing on the library stream (0 = off).  family ids are
+ * listed in DESIGN.md (1 = level-0 smoother sweep, 2 = level-0 SpMV/residual). */
+int aggmg_profile_enable(int family);
+int aggmg_profile_read(int family, double* total_ms, int64_t* launches, double* bytes);
+/* SpMV micro-benchmark on a device matrix: average ms per launch over `reps` launches */
+int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AGGMG_B200_H */

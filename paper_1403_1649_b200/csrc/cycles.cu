@@ -1,0 +1,313 @@
+// cycles.cu — V-cycle (Alg. 4) and K-cycle (Alg. 5) recursion on device buffers.
+#include <cmath>
+#include <cstdio>
+
+#include "cycles.cuh"
+
+namespace aggmg_b200 {
+
+namespace {
+
+constexpr int kB = 256;
+unsigned egrid(int64_t n) { return grid_for(n, kB, 8 * static_cast<int64_t>(sm_count())); }
+
+int* warn_bits() {
+  static int* p = nullptr;
+  if (!p) {
+    AGG_CUDA(cudaMalloc(&p, 2 * sizeof(int)));
+    AGG_CUDA(cudaMemset(p, 0, 2 * sizeof(int)));
+  }
+  return p;
+}
+
+inline __device__ bool on(const int* pred) { return !pred || *pred; }
+
+// x = 0 + wd .* (b - 0): first damped-Jacobi sweep from the zero guess
+// (smoother.cpp:121-123 with x = 0, A*0 = +0).
+__global__ void k_jacobi_zero(int64_t n, const double* __restrict__ wd,
+                              const double* __restrict__ b, double* __restrict__ x,
+                              const int* pred) {
+  if (!on(pred)) return;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    x[i] = __dadd_rn(0.0, __dmul_rn(wd[i], b[i]));
+}
+
+// t = x + P xc  (prolongate_add, cycles.cpp:37-44: x + (0 + p*xc))
+__global__ void k_prolong(int64_t n, const double* __restrict__ x, const idx* __restrict__ agg,
+                          const double* __restrict__ pval, const double* __restrict__ xc,
+                          double* __restrict__ t, const int* pred) {
+  if (!on(pred)) return;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    t[i] = __dadd_rn(x[i], __dadd_rn(0.0, __dmul_rn(pval[i], xc[agg[i]])));
+}
+
+__global__ void k_copy(int64_t n, const double* __restrict__ a, double* __restrict__ b,
+                       const int* pred) {
+  if (!on(pred)) return;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    b[i] = a[i];
+}
+
+// rt = rc + (-s1) v ; ||rt||^2, ||rc||^2 ; flag2 = !(||rt|| <= t ||rc||)  (cycles.cpp:101-104)
+__global__ void __launch_bounds__(kB) k_kstep1(int64_t n, const double* __restrict__ rc,
+                                               const double* __restrict__ v,
+                                               double* __restrict__ rt, KScalars* ks, double tt,
+                                               const int* pred, double* partials,
+                                               unsigned* ticket, int* warn, int level) {
+  __shared__ double smem[64];
+  if (!on(pred) || ks->rho1 == 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ks->flag2 = 0;
+      if (on(pred)) atomicOr(&warn[0], 1 << (level & 31));
+    }
+    return;
+  }
+  const double s1 = __ddiv_rn(ks->alpha1, ks->rho1);
+  const double ms1 = -s1;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double r = rc[i];
+    const double z = __dadd_rn(r, __dmul_rn(ms1, v[i]));
+    rt[i] = z;
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(z, z));
+    acc[1] = __dadd_rn(acc[1], __dmul_rn(r, r));
+  }
+  block_reduce<2>(acc, smem);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x * 2] = acc[0];
+    partials[blockIdx.x * 2 + 1] = acc[1];
+  }
+  if (finish_reduction<2>(partials, ticket, &ks->nrt, smem) && threadIdx.x == 0) {
+    const double nrt = __dsqrt_rn(ks->nrt), nrc = __dsqrt_rn(ks->nrc);
+    ks->flag2 = (nrt <= __dmul_rn(tt, nrc)) ? 0 : 1;
+  }
+}
+
+// Final coarse correction of the K-cycle (cycles.cpp:96-132):
+//   rho1 == 0           -> xc = c
+//   accepted one step   -> xc = c * s1
+//   rho2 == 0           -> xc = c * s1
+//   otherwise           -> xc = c * (s1 - gamma*alpha2/(rho1*rho2)) + (alpha2/rho2) * d
+__global__ void k_kcombine(int64_t n, const double* __restrict__ c, const double* __restrict__ d,
+                           double* __restrict__ xc, const KScalars* ks, const int* pred,
+                           int* warn, int level) {
+  if (!on(pred)) return;
+  const double rho1 = ks->rho1;
+  int mode;
+  double cc = 1.0, cd = 0.0;
+  if (rho1 == 0.0) {
+    mode = 0;
+  } else {
+    const double s1 = __ddiv_rn(ks->alpha1, rho1);
+    if (!ks->flag2) {
+      mode = 1;
+      cc = s1;
+    } else {
+      const double g = ks->gamma, be = ks->beta, a2 = ks->alpha2;
+      const double rho2 = __dsub_rn(be, __ddiv_rn(__dmul_rn(g, g), rho1));
+      if (rho2 == 0.0) {
+        mode = 1;
+        cc = s1;
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&warn[1], 1 << (level & 31));
+      } else {
+        mode = 2;
+        cc = __dsub_rn(s1, __ddiv_rn(__dmul_rn(g, a2), __dmul_rn(rho1, rho2)));
+        cd = __ddiv_rn(a2, rho2);
+      }
+    }
+  }
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double ci = c[i];
+    double v;
+    if (mode == 0)
+      v = ci;
+    else if (mode == 1)
+      v = __dmul_rn(ci, cc);
+    else
+      v = __dadd_rn(__dmul_rn(ci, cc), __dmul_rn(cd, d[i]));
+    xc[i] = v;
+  }
+}
+
+// x = Ainv b, warp per row (coarsest level, n <= 5000)
+__global__ void k_gemv(int64_t n, const double* __restrict__ M, const double* __restrict__ b,
+                       double* __restrict__ x, const int* pred) {
+  if (!on(pred)) return;
+  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* m = M + row * n;
+  double s = 0.0;
+  for (int64_t j = lane; j < n; j += 32) s = fma(m[j], b[j], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) x[row] = s;
+}
+
+bool accelerated(const CycleCfg& c, int64_t k) {  // cycles.cpp:16-20
+  if (c.kind == 1) return true;
+  if (c.kind == 2) return k < c.k_levels;
+  return false;
+}
+
+void presmooth(DevLevel& L, const double* b, const double* x_in, double* x_out, const int* pred,
+               bool top) {
+  const int64_t n = L.A->n_rows;
+  if (L.smoother.kind == 2) {  // sgs, in place
+    if (x_in)
+      AGG_LAUNCH(k_copy, egrid(n), kB, 0, n, x_in, x_out, pred);
+    else
+      fill_double(x_out, n, 0.0);
+    smooth_sgs(L.smoother, *L.A, b, x_out);
+    return;
+  }
+  if (x_in)
+    smooth_sweep(L.smoother, *L.A, b, x_in, x_out, pred, top ? kProfSmoothL0 : 0);
+  else
+    AGG_LAUNCH(k_jacobi_zero, egrid(n), kB, 0, n, L.smoother.wdiag.get(), b, x_out, pred);
+}
+
+void postsmooth(DevLevel& L, const double* b, double* x, const int* pred, bool top) {
+  const int64_t n = L.A->n_rows;
+  AGG_LAUNCH(k_prolong, egrid(n), kB, 0, n, x, L.agg.assignment.get(), L.tr.pval.get(),
+             L.xc.get(), L.t.get(), pred);
+  if (L.smoother.kind == 2) {
+    AGG_LAUNCH(k_copy, egrid(n), kB, 0, n, L.t.get(), x, pred);
+    smooth_sgs(L.smoother, *L.A, b, x);
+    return;
+  }
+  smooth_sweep(L.smoother, *L.A, b, L.t.get(), x, pred, top ? kProfSmoothL0 : 0);
+}
+
+void descend(DevHierarchy& h, int64_t k, const double* b, double* x_out, const int* pred) {
+  DevLevel& L = h.levels[k];
+  SpmvArgs ra;
+  ra.x = x_out;
+  ra.y = L.r.get();
+  ra.b = b;
+  ra.pred = pred;
+  spmv_run(*L.A, Epi::kResidual, ra, k == 0 ? kProfSpmvL0 : 0);  // cycles.cpp:30-35
+  SpmvArgs rr;
+  rr.x = L.r.get();
+  rr.y = L.rc.get();
+  rr.pred = pred;
+  spmv_run(*L.tr.R, Epi::kSpmv, rr);  // restriction = spmv(R, r), cycles.cpp:56-57
+}
+
+void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in, double* x_out,
+                const int* pred);
+void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
+                const double* x_in, double* x_out, const int* pred);
+
+void inner_cycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b, double* x_out,
+                 const int* pred) {
+  if (accelerated(cfg, k))
+    kcycle_dev(h, cfg, k, b, nullptr, x_out, pred);
+  else
+    vcycle_dev(h, k, b, nullptr, x_out, pred);
+}
+
+void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in, double* x_out,
+                const int* pred) {
+  if (k == h.coarsest()) {
+    coarse_solve(h, b, x_out, pred);
+    return;
+  }
+  DevLevel& L = h.levels[k];
+  presmooth(L, b, x_in, x_out, pred, k == 0);
+  descend(h, k, b, x_out, pred);
+  if (k + 1 == h.coarsest())
+    coarse_solve(h, L.rc.get(), L.xc.get(), pred);
+  else
+    vcycle_dev(h, k + 1, L.rc.get(), nullptr, L.xc.get(), pred);
+  postsmooth(L, b, x_out, pred, k == 0);
+}
+
+void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
+                const double* x_in, double* x_out, const int* pred) {
+  if (k == h.coarsest()) {
+    coarse_solve(h, b, x_out, pred);
+    return;
+  }
+  DevLevel& L = h.levels[k];
+  presmooth(L, b, x_in, x_out, pred, k == 0);
+  descend(h, k, b, x_out, pred);
+  if (k + 1 == h.coarsest()) {
+    coarse_solve(h, L.rc.get(), L.xc.get(), pred);
+  } else {
+    const DevCsr& Ac = *h.levels[k + 1].A;
+    const int64_t nc = Ac.n_rows;
+    const bool cg = cfg.inner == 0;
+    inner_cycle(h, cfg, k + 1, L.rc.get(), L.c.get(), pred);
+    SpmvArgs a1;  // v = Ac c ; rho1, alpha1  (cycles.cpp:86-95)
+    a1.x = L.c.get();
+    a1.y = L.v.get();
+    a1.c = L.rc.get();
+    a1.dot_with_x = cg ? 1 : 0;
+    a1.dots_out = &L.ks.get()->rho1;
+    a1.pred = pred;
+    spmv_run(Ac, Epi::kSpmvDot2, a1);
+    const unsigned g = reduce_grid(nc);
+    AGG_LAUNCH(k_kstep1, g, kB, 0, nc, L.rc.get(), L.v.get(), L.rt.get(), L.ks.get(), cfg.t, pred,
+               reduce_partials(), reduce_ticket(), warn_bits(), static_cast<int>(k + 1));
+    const int* p2 = &L.ks.get()->flag2;
+    inner_cycle(h, cfg, k + 1, L.rt.get(), L.d.get(), p2);
+    SpmvArgs a2;  // w = Ac d ; gamma, beta, alpha2  (cycles.cpp:110-121)
+    a2.x = L.d.get();
+    a2.y = L.w.get();
+    a2.u = L.v.get();
+    a2.c = L.rt.get();
+    a2.dot_with_x = cg ? 1 : 0;
+    a2.dots_out = &L.ks.get()->gamma;
+    a2.pred = p2;
+    spmv_run(Ac, Epi::kSpmvDot3, a2);
+    AGG_LAUNCH(k_kcombine, egrid(nc), kB, 0, nc, L.c.get(), L.d.get(), L.xc.get(), L.ks.get(), pred,
+               warn_bits(), static_cast<int>(k + 1));
+  }
+  postsmooth(L, b, x_out, pred, k == 0);
+}
+
+}  // namespace
+
+void coarse_solve(DevHierarchy& h, const double* b, double* x, const int* pred) {
+  const int64_t n = h.levels.back().A->n_rows;
+  if (n == 0) return;
+  AGG_LAUNCH(k_gemv, grid_for(n * 32, 256), 256, 0, n, h.coarse_inv.get(), b, x, pred);
+}
+
+void cycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, bool accelerated_top, const double* b,
+           const double* x_in, double* x_out, const int* pred) {
+  h.ensure_workspace();
+  if (accelerated_top)
+    kcycle_dev(h, cfg, k, b, x_in, x_out, pred);
+  else
+    vcycle_dev(h, k, b, x_in, x_out, pred);
+}
+
+void apply_preconditioner(DevHierarchy& h, const CycleCfg& cfg, const double* r, double* z) {
+  h.ensure_workspace();
+  inner_cycle(h, cfg, 0, r, z, nullptr);
+}
+
+void flush_cycle_warnings() {
+  int w[2];
+  AGG_CUDA(cudaMemcpyAsync(w, warn_bits(), sizeof(w), cudaMemcpyDeviceToHost, stream()));
+  AGG_CUDA(cudaStreamSynchronize(stream()));
+  if (w[0] == 0 && w[1] == 0) return;
+  for (int l = 0; l < 32; ++l) {
+    if (w[0] & (1 << l))
+      std::fprintf(stderr, "kcycle: zero curvature at level %d, keeping the unscaled correction\n", l);
+    if (w[1] & (1 << l))
+      std::fprintf(stderr,
+                   "kcycle: singular inner Gram matrix at level %d, keeping the one-step correction\n",
+                   l);
+  }
+  AGG_CUDA(cudaMemsetAsync(warn_bits(), 0, 2 * sizeof(int), stream()));
+}
+
+}  // namespace aggmg_b200

@@ -1,0 +1,138 @@
+// hierarchy.cu — Algorithm 1 setup loop on the device (hierarchy.cpp:34-104).
+#include <algorithm>
+#include <cmath>
+#include <sstream>
+
+#include "hierarchy.cuh"
+#include "vecops.cuh"
+
+namespace aggmg_b200 {
+
+constexpr int64_t kDenseSolveCap = 5000;  // hierarchy.cpp:23
+
+void factor_coarsest(DevHierarchy& h) {
+  DevLevel& L = h.levels.back();
+  const int64_t nL = L.A->n_rows;
+  require(nL <= std::max<int64_t>(h.cfg.coarse_size_max, kDenseSolveCap),
+          "setup: coarsest level has " + std::to_string(nL) + " unknowns, too large for a dense solve");
+  std::vector<int64_t> rp(nL + 1), col(L.A->nnz);
+  std::vector<double> val(L.A->nnz);
+  download_csr(*L.A, rp.data(), col.data(), val.data());
+  std::vector<double> dense(static_cast<size_t>(nL) * nL, 0.0);  // dense.cpp:16-22
+  for (int64_t i = 0; i < nL; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) dense[i * nL + col[k]] = val[k];
+  h.coarse_lu.factor(std::move(dense), nL);
+  const std::vector<double> inv = h.coarse_lu.inverse();
+  h.coarse_inv.resize(static_cast<int64_t>(inv.size()));
+  h.coarse_inv.upload(inv.data(), static_cast<int64_t>(inv.size()));
+  sync();
+}
+
+std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev,
+                                              const SetupCfg& cfg) {
+  require(A0->n_rows == A0->n_cols, "setup: matrix must be square");
+  require(cfg.coarse_size_max >= 1, "setup: coarse_size_max must be at least 1");
+  require(cfg.max_levels >= 1, "setup: max_levels must be at least 1");
+  cudaEvent_t e0, e1;
+  AGG_CUDA(cudaEventCreate(&e0));
+  AGG_CUDA(cudaEventCreate(&e1));
+  AGG_CUDA(cudaEventRecord(e0, stream()));
+
+  auto h = std::make_unique<DevHierarchy>();
+  h->cfg = cfg;
+  h->levels.emplace_back();
+  h->levels[0].A = A0;
+  h->levels[0].B.resize(A0->n_rows);
+  if (B0_dev)
+    copy_double(h->levels[0].B.get(), B0_dev, A0->n_rows);
+  else
+    fill_double(h->levels[0].B.get(), A0->n_rows, 1.0);
+  const double nb = std::sqrt(dot_host(h->levels[0].B.get(), h->levels[0].B.get(), A0->n_rows));
+  require(nb > 0.0, "setup: near-null-space vector is zero");
+
+  while (h->levels.back().A->n_rows > cfg.coarse_size_max &&
+         static_cast<int>(h->levels.size()) < cfg.max_levels) {
+    const int64_t k = h->coarsest();
+    DevLevel& fine = h->levels[k];
+    const DevCsr& A = *fine.A;
+    const int64_t n = A.n_rows;
+
+    DevCsrPtr C = classic_strength(A, cfg.alpha, 0);
+    DevBuf<idx> influence;
+    DevCsrPtr S;
+    influence_and_symmetrize(*C, influence, S);
+    C.reset();
+    Mis2Dev mis = mis2(*S, influence.get(), level_seed(cfg.seed, k, kMisTag));
+    AggDev agg = aggregate(*S, A, mis.state.get());
+    S.reset();
+
+    if (static_cast<double>(agg.n_agg) >= 0.95 * static_cast<double>(n)) {
+      std::ostringstream msg;
+      msg << "coarsening stalled at level " << k << " (" << n << " -> " << agg.n_agg
+          << " aggregates); solving this level directly";
+      h->warnings.push_back(msg.str());
+      break;
+    }
+    fine.mis_sweeps = mis.sweeps;
+    fine.tr = build_transfer(agg, fine.B.get());
+    fine.gal = build_galerkin_cache(A, agg);
+    DevCsrPtr Ac = apply_galerkin_cache(fine.gal, A, fine.tr.pval.get());
+    setup_smoother(A, cfg.smoother, cfg.arnoldi_m, level_seed(cfg.seed, k, kSmootherTag),
+                   fine.smoother);
+    fine.has_smoother = true;
+    fine.agg = std::move(agg);
+    fine.has_next = true;
+    DevLevel next;
+    next.A = Ac;
+    next.B = std::move(fine.tr.coarse_b);
+    h->levels.push_back(std::move(next));
+  }
+  factor_coarsest(*h);
+  AGG_CUDA(cudaEventRecord(e1, stream()));
+  AGG_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  AGG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  h->setup_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return h;
+}
+
+// hierarchy.cpp:90-104: numeric half only; aggregates, P and R are untouched.
+void refresh_values(DevHierarchy& h, const double* new_values_dev) {
+  DevLevel& L0 = h.levels[0];
+  copy_double(L0.A->val.get(), new_values_dev, L0.A->nnz);
+  for (int64_t k = 0; k + 1 < h.n_levels(); ++k) {
+    DevLevel& fine = h.levels[k];
+    DevCsrPtr Ac = apply_galerkin_cache(fine.gal, *fine.A, fine.tr.pval.get());
+    copy_double(h.levels[k + 1].A->val.get(), Ac->val.get(), Ac->nnz);
+    setup_smoother(*fine.A, h.cfg.smoother, h.cfg.arnoldi_m,
+                   level_seed(h.cfg.seed, k, kSmootherTag), fine.smoother);
+  }
+  factor_coarsest(h);
+}
+
+void DevHierarchy::ensure_workspace() {
+  if (workspace_ready) return;
+  for (int64_t k = 0; k < n_levels(); ++k) {
+    DevLevel& L = levels[k];
+    const int64_t n = L.A->n_rows;
+    L.r.resize(n);
+    L.t.resize(n);
+    if (k + 1 < n_levels()) {
+      const int64_t nc = levels[k + 1].A->n_rows;
+      L.rc.resize(nc);
+      L.xc.resize(nc);
+      L.c.resize(nc);
+      L.v.resize(nc);
+      L.rt.resize(nc);
+      L.d.resize(nc);
+      L.w.resize(nc);
+      L.ks.resize(1);
+      L.ks.zero();
+    }
+  }
+  workspace_ready = true;
+}
+
+}  // namespace aggmg_b200

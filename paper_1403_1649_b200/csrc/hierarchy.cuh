@@ -1,0 +1,71 @@
+// hierarchy.cuh — device-resident AMG hierarchy (reference hierarchy.hpp:21-48) and the
+// setup loop (hierarchy.cpp:34-104).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "dense_host.hpp"
+#include "setup.cuh"
+#include "smoother.cuh"
+
+namespace aggmg_b200 {
+
+struct SetupCfg {
+  double alpha = 0.25;
+  int64_t coarse_size_max = 600;
+  int max_levels = 25;
+  int smoother = 1;
+  int arnoldi_m = 5;
+  int reuse_caches = 0;
+  uint64_t seed = 42;
+};
+
+// K-cycle scalars of one level, resident in device memory (cycles.cpp:88-132).
+struct KScalars {
+  double rho1, alpha1;       // written by the fused SpMV+dot of c
+  double nrt, nrc;           // ||rt||^2, ||rc||^2
+  double gamma, beta, alpha2;  // written by the fused SpMV+dot of d
+  int flag2;                 // run the second inner cycle
+  int pad;
+};
+
+struct DevLevel {
+  DevCsrPtr A;
+  DevBuf<double> B;  // near-null-space vector on this level
+  SmootherDev smoother;
+  bool has_smoother = false;
+  // transfer to the next level (empty on the coarsest level)
+  bool has_next = false;
+  AggDev agg;
+  TransferDev tr;
+  GalerkinDev gal;
+  int mis_sweeps = 0;
+  // cycle workspace on this level (size n_k)
+  DevBuf<double> r, t;
+  // coarse-side vectors owned by this level's cycle (size n_{k+1})
+  DevBuf<double> rc, xc, c, v, rt, d, w;
+  DevBuf<KScalars> ks;
+};
+
+struct DevHierarchy {
+  std::vector<DevLevel> levels;
+  SetupCfg cfg;
+  std::vector<std::string> warnings;
+  HostLu coarse_lu;
+  DevBuf<double> coarse_inv;  // explicit inverse of the coarsest operator (row-major)
+  double setup_ms = 0.0;
+  bool workspace_ready = false;
+
+  int64_t n_levels() const { return static_cast<int64_t>(levels.size()); }
+  int64_t coarsest() const { return n_levels() - 1; }
+  void ensure_workspace();
+};
+
+// B0 == nullptr means ones (aggmg_main.cpp:177).
+std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev,
+                                              const SetupCfg& cfg);
+void refresh_values(DevHierarchy& h, const double* new_values_dev);
+void factor_coarsest(DevHierarchy& h);
+
+}  // namespace aggmg_b200

@@ -1,0 +1,305 @@
+// krylov.cu — device PCG / FGMRES.  Vector work is fused into few HBM passes; the
+// per-iteration host readback is one small pinned copy (the residual or the Hessenberg
+// column the host's Givens recurrence needs).
+#include <chrono>
+#include <algorithm>
+#include <cmath>
+
+#include "krylov.cuh"
+#include "vecops.cuh"
+
+namespace aggmg_b200 {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+constexpr int kB = 256;
+
+struct PcgSlots {
+  double pAp;
+  double res2;
+  double q[2][2];  // q[par] = {r.z, r_old.z} of the iteration that produced it
+  double pad[2];
+};
+
+// alpha = rz/pAp; x += alpha p; rn = r + (-alpha) Ap; res2 = ||rn||^2  (krylov.cpp:181-186)
+__global__ void __launch_bounds__(kB) k_pcg_update(int64_t n, PcgSlots* s, int par,
+                                                   const double* __restrict__ p,
+                                                   const double* __restrict__ Ap,
+                                                   const double* __restrict__ r, double* __restrict__ x,
+                                                   double* __restrict__ rn, double* partials,
+                                                   unsigned* ticket) {
+  __shared__ double smem[32];
+  const double alpha = __ddiv_rn(s->q[par][0], s->pAp);
+  const double malpha = -alpha;
+  double acc[1] = {0.0};
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    const double v = __dadd_rn(r[i], __dmul_rn(malpha, Ap[i]));
+    rn[i] = v;
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(v, v));
+  }
+  block_reduce<1>(acc, smem);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
+  finish_reduction<1>(partials, ticket, &s->res2, smem);
+}
+
+// beta = (rz_new - r_old.z) / rz ; p = z + beta p  (krylov.cpp:191-195)
+__global__ void k_pcg_p(int64_t n, const PcgSlots* s, int cur, const double* __restrict__ z,
+                        double* __restrict__ p) {
+  const double beta = __ddiv_rn(__dsub_rn(s->q[cur][0], s->q[cur][1]), s->q[cur ^ 1][0]);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+}
+
+// MGS step i of column j (krylov.cpp:85-89): w = w + (-h_i) V_i, then the next
+// coefficient dot(V_{i+1}, w) or, after the last basis vector, ||w||^2.
+__global__ void __launch_bounds__(kB) k_mgs_step(int64_t n, const double* hcol, int i,
+                                                 const double* __restrict__ Vi,
+                                                 const double* __restrict__ Vnext,
+                                                 double* __restrict__ w, double* out,
+                                                 double* partials, unsigned* ticket) {
+  __shared__ double smem[32];
+  const double mh = -hcol[i];
+  double acc[1] = {0.0};
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = __dadd_rn(w[t], __dmul_rn(mh, Vi[t]));
+    w[t] = v;
+    const double o = Vnext ? Vnext[t] : v;
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(o, v));
+  }
+  block_reduce<1>(acc, smem);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
+  finish_reduction<1>(partials, ticket, out, smem);
+}
+
+struct AxpyList {
+  const double* z[32];
+  double y[32];
+  int count;
+};
+// x = x + y_0 Z_0, then + y_1 Z_1, ... (krylov.cpp:128), one pass over x
+__global__ void k_multi_axpy(int64_t n, AxpyList L, double* __restrict__ x) {
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double v = x[t];
+    for (int i = 0; i < L.count; ++i) v = __dadd_rn(v, __dmul_rn(L.y[i], L.z[i][t]));
+    x[t] = v;
+  }
+}
+
+unsigned egrid(int64_t n) { return grid_for(n, kB, 8 * static_cast<int64_t>(sm_count())); }
+
+void apply_M(const Precond& M, const double* r, double* z, int64_t n) {
+  if (M.h)
+    apply_preconditioner(*M.h, M.cfg, r, z);
+  else
+    copy_double(z, r, n);
+}
+
+void residual(const DevCsr& A, const double* b, const double* x, double* r) {
+  SpmvArgs a;
+  a.x = x;
+  a.y = r;
+  a.b = b;
+  spmv_run(A, Epi::kResidual, a);
+}
+
+double norm_host(const double* v, int64_t n) { return std::sqrt(dot_host(v, v, n)); }
+
+double seconds_since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+}  // namespace
+
+SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, const SolverCfg& cfg) {
+  require(A.n_rows == A.n_cols, "pcg: matrix must be square");
+  require(cfg.tol > 0.0, "pcg: tol must be positive");
+  const auto t0 = Clock::now();
+  const int64_t n = A.n_rows;
+  SolveOut out;
+  const double norm_b = norm_host(b, n);
+  if (norm_b == 0.0) {
+    fill_double(x, n, 0.0);
+    out.converged = true;
+    out.history.push_back(0.0);
+    sync();
+    out.solve_seconds = seconds_since(t0);
+    return out;
+  }
+  const double target = cfg.tol * norm_b;
+  DevBuf<double> rA(n), rB(n), z(n), p(n), Ap(n);
+  DevBuf<PcgSlots> slots(1);
+  slots.zero();
+  double* r = rA.get();
+  double* rn = rB.get();
+  residual(A, b, x, r);
+  double res = norm_host(r, n);
+  out.history.push_back(res);
+  apply_M(M, r, z.get(), n);
+  copy_double(p.get(), z.get(), n);
+  {
+    DotArgs d{};
+    d.a[0] = r;
+    d.b[0] = z.get();
+    d.np = 1;
+    dot_device(d, n, &slots.get()->q[0][0]);
+  }
+  double* pinned = pinned_scratch(8);
+  int par = 0;  // q[par][0] holds the current r.z
+  while (res > target && out.iterations < cfg.max_iters) {
+    SpmvArgs a;  // Ap = A p ; pAp
+    a.x = p.get();
+    a.y = Ap.get();
+    a.u = p.get();
+    a.dots_out = &slots.get()->pAp;
+    spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
+    AGG_LAUNCH(k_pcg_update, reduce_grid(n), kB, 0, n, slots.get(), par, p.get(), Ap.get(), r, x,
+               rn, reduce_partials(), reduce_ticket());
+    AGG_CUDA(cudaMemcpyAsync(pinned, slots.get(), 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                             stream()));
+    sync();
+    const double pAp = pinned[0];
+    require(pAp > 0.0, "pcg: non-positive curvature (matrix not positive definite); use fgmres");
+    ++out.iterations;
+    res = std::sqrt(pinned[1]);
+    out.history.push_back(res);
+    std::swap(r, rn);  // r = new residual, rn = r_old
+    if (res <= target) break;
+    apply_M(M, r, z.get(), n);
+    DotArgs d{};
+    d.a[0] = r;
+    d.b[0] = z.get();
+    d.a[1] = rn;
+    d.b[1] = z.get();
+    d.np = 2;
+    const int cur = par ^ 1;
+    dot_device(d, n, &slots.get()->q[cur][0]);  // {r.z, r_old.z}
+    AGG_LAUNCH(k_pcg_p, egrid(n), kB, 0, n, slots.get(), cur, z.get(), p.get());
+    par = cur;
+  }
+  if (M.h) flush_cycle_warnings();
+  out.converged = res <= target;
+  sync();
+  out.solve_seconds = seconds_since(t0);
+  return out;
+}
+
+SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
+                const SolverCfg& cfg) {
+  require(A.n_rows == A.n_cols, "fgmres: matrix must be square");
+  require(cfg.tol > 0.0, "fgmres: tol must be positive");
+  require(cfg.restart >= 1, "fgmres: restart must be at least 1");
+  const auto t0 = Clock::now();
+  const int64_t n = A.n_rows;
+  const int m = cfg.restart;
+  SolveOut out;
+  const double norm_b = norm_host(b, n);
+  if (norm_b == 0.0) {
+    fill_double(x, n, 0.0);
+    out.converged = true;
+    out.history.push_back(0.0);
+    sync();
+    out.solve_seconds = seconds_since(t0);
+    return out;
+  }
+  const double target = cfg.tol * norm_b;
+  DevBuf<double> r(n), w(n), hcol(m + 2);
+  std::vector<DevBuf<double>> V, Z;
+  residual(A, b, x, r.get());
+  double beta = norm_host(r.get(), n);
+  out.history.push_back(beta);
+  std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0);  // column-major, ld m+1
+  auto h = [&](int i, int j) -> double& { return H[static_cast<size_t>(j) * (m + 1) + i]; };
+  std::vector<double> cs(m), sn(m), g(m + 1);
+  double* pinned = pinned_scratch(m + 2);
+  double prev_outer = beta;
+  while (beta > target && out.iterations < cfg.max_iters) {
+    if (V.empty()) V.emplace_back(n);
+    vec_scale_into(n, 1.0 / beta, r.get(), V[0].get());
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    std::fill(H.begin(), H.end(), 0.0);
+    int j = 0;
+    for (; j < m && out.iterations < cfg.max_iters; ++j) {
+      if (static_cast<int>(Z.size()) <= j) Z.emplace_back(n);
+      apply_M(M, V[j].get(), Z[j].get(), n);
+      SpmvArgs a;  // w = A Z_j ; h(0,j) = V_0 . w
+      a.x = Z[j].get();
+      a.y = w.get();
+      a.u = V[0].get();
+      a.dots_out = hcol.get();
+      spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
+      for (int i = 0; i <= j; ++i) {
+        const double* vnext = (i < j) ? V[i + 1].get() : nullptr;
+        AGG_LAUNCH(k_mgs_step, reduce_grid(n), kB, 0, n, hcol.get(), i, V[i].get(), vnext, w.get(),
+                   hcol.get() + i + 1, reduce_partials(), reduce_ticket());
+      }
+      AGG_CUDA(cudaMemcpyAsync(pinned, hcol.get(), sizeof(double) * (j + 2),
+                               cudaMemcpyDeviceToHost, stream()));
+      sync();
+      for (int i = 0; i <= j; ++i) h(i, j) = pinned[i];
+      h(j + 1, j) = std::sqrt(pinned[j + 1]);
+      const bool breakdown = (h(j + 1, j) == 0.0);
+      if (!breakdown) {
+        if (static_cast<int>(V.size()) <= j + 1) V.emplace_back(n);
+        vec_scale_into(n, 1.0 / h(j + 1, j), w.get(), V[j + 1].get());
+      }
+      for (int i = 0; i < j; ++i) {  // apply previous rotations (krylov.cpp:95-99)
+        const double t = cs[i] * h(i, j) + sn[i] * h(i + 1, j);
+        h(i + 1, j) = -sn[i] * h(i, j) + cs[i] * h(i + 1, j);
+        h(i, j) = t;
+      }
+      const double denom = std::hypot(h(j, j), h(j + 1, j));
+      if (denom == 0.0) {
+        cs[j] = 1.0;
+        sn[j] = 0.0;
+      } else {
+        cs[j] = h(j, j) / denom;
+        sn[j] = h(j + 1, j) / denom;
+      }
+      h(j, j) = cs[j] * h(j, j) + sn[j] * h(j + 1, j);
+      h(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++out.iterations;
+      out.history.push_back(std::abs(g[j + 1]));
+      if (std::abs(g[j + 1]) <= target || breakdown) {
+        ++j;
+        break;
+      }
+    }
+    std::vector<double> y(j);  // krylov.cpp:122-127
+    for (int i = j - 1; i >= 0; --i) {
+      double s = g[i];
+      for (int l = i + 1; l < j; ++l) s -= h(i, l) * y[l];
+      y[i] = s / h(i, i);
+    }
+    for (int i0 = 0; i0 < j; i0 += 32) {  // same left-to-right sequence per element
+      AxpyList L{};
+      L.count = std::min(32, j - i0);
+      for (int i = 0; i < L.count; ++i) {
+        L.z[i] = Z[i0 + i].get();
+        L.y[i] = y[i0 + i];
+      }
+      AGG_LAUNCH(k_multi_axpy, egrid(n), kB, 0, n, L, x);
+    }
+    residual(A, b, x, r.get());
+    beta = norm_host(r.get(), n);
+    out.history.back() = beta;
+    if (beta > target && beta >= prev_outer && j == m)
+      out.note = "stagnation: no residual decrease over a full restart cycle";
+    prev_outer = beta;
+  }
+  if (M.h) flush_cycle_warnings();
+  out.converged = beta <= target;
+  sync();
+  out.solve_seconds = seconds_since(t0);
+  return out;
+}
+
+}  // namespace aggmg_b200

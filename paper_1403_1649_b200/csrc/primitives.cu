@@ -1,0 +1,221 @@
+// primitives.cu — scans, deterministic reductions, segmented rank sort.
+#include "primitives.cuh"
+
+namespace aggmg_b200 {
+
+namespace {
+
+constexpr int kScanBlock = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanBlock * kScanItems;
+
+// Exclusive scan of one 2048-element tile per block.  Loads are striped (coalesced),
+// each thread scans 8 consecutive elements from shared memory, thread totals are
+// combined with warp shuffles.  Writes the tile total to tile_sums[blockIdx.x].
+__global__ void __launch_bounds__(kScanBlock) k_scan_tiles(const idx* in, idx* out, idx* tile_sums,
+                                                           int64_t n) {
+  __shared__ idx tile[kScanTile];
+  __shared__ idx warp_tot[kScanBlock / 32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t g = base + j * kScanBlock + threadIdx.x;
+    tile[j * kScanBlock + threadIdx.x] = g < n ? in[g] : 0;
+  }
+  __syncthreads();
+  idx local[kScanItems];
+  idx run = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    local[j] = run;
+    run += tile[threadIdx.x * kScanItems + j];
+  }
+  // inclusive warp scan of thread totals
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  idx incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    idx t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    idx w = lane < kScanBlock / 32 ? warp_tot[lane] : 0;
+    idx wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      idx t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < kScanBlock / 32) warp_tot[lane] = wi - w;  // exclusive warp offsets
+    if (lane == kScanBlock / 32 - 1) tile_sums[blockIdx.x] = wi;
+  }
+  __syncthreads();
+  const idx off = warp_tot[warp] + (incl - run);
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) tile[threadIdx.x * kScanItems + j] = local[j] + off;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t g = base + j * kScanBlock + threadIdx.x;
+    if (g < n) out[g] = tile[j * kScanBlock + threadIdx.x];
+  }
+}
+
+__global__ void k_add_tile_offsets(idx* out, const idx* tile_offsets, int64_t n) {
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < n) out[g] += tile_offsets[g / kScanTile];
+}
+
+// out[0..n) exclusive scan; *total = sum (device)
+void scan_rec(const idx* in, idx* out, int64_t n, idx* total) {
+  const int64_t nt = (n + kScanTile - 1) / kScanTile;
+  if (nt <= 1) {
+    AGG_LAUNCH(k_scan_tiles, 1, kScanBlock, 0, in, out, total, n);
+    return;
+  }
+  DevBuf<idx> sums(nt);
+  AGG_LAUNCH(k_scan_tiles, static_cast<unsigned>(nt), kScanBlock, 0, in, out, sums.get(), n);
+  scan_rec(sums.get(), sums.get(), nt, total);
+  AGG_LAUNCH(k_add_tile_offsets, grid_for(n, 256), 256, 0, out, sums.get(), n);
+}
+
+}  // namespace
+
+void scan_to_offsets_async(const idx* counts, idx* offsets, int64_t n) {
+  if (n == 0) {
+    AGG_CUDA(cudaMemsetAsync(offsets, 0, sizeof(idx), stream()));
+    return;
+  }
+  scan_rec(counts, offsets, n, offsets + n);
+}
+
+int64_t scan_to_offsets(const idx* counts, idx* offsets, int64_t n) {
+  scan_to_offsets_async(counts, offsets, n);
+  return read_scalar(offsets + n);
+}
+
+// ---- reductions ----------------------------------------------------------------
+
+namespace {
+constexpr int kRedBlock = 256;
+struct RedScratch {
+  double* partials = nullptr;
+  unsigned* ticket = nullptr;
+  int cap = 0;
+};
+RedScratch& red() {
+  static RedScratch r;
+  if (!r.partials) {
+    r.cap = 1 << 20;
+    AGG_CUDA(cudaMalloc(&r.partials, sizeof(double) * 3 * r.cap));
+    AGG_CUDA(cudaMalloc(&r.ticket, sizeof(unsigned) * 64));
+    AGG_CUDA(cudaMemset(r.ticket, 0, sizeof(unsigned) * 64));
+  }
+  return r;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(kRedBlock) k_dot(DotArgs args, int64_t n, double* partials,
+                                                   unsigned* ticket, double* out, const int* pred) {
+  __shared__ double smem[32 * NP];
+  if (pred && !*pred) return;
+  double v[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) v[k] = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) v[k] = __dadd_rn(v[k], __dmul_rn(args.a[k][i], args.b[k][i]));
+  }
+  block_reduce<NP>(v, smem);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < NP; ++k) partials[blockIdx.x * NP + k] = v[k];
+  finish_reduction<NP>(partials, ticket, out, smem);
+}
+}  // namespace
+
+unsigned reduce_grid(int64_t n) {
+  const int64_t want = (n + kRedBlock * 8 - 1) / (kRedBlock * 8);
+  const int64_t cap = 4 * static_cast<int64_t>(sm_count());
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min(want, cap)));
+}
+double* reduce_partials() { return red().partials; }
+unsigned* reduce_ticket() { return red().ticket; }
+
+void dot_device(const DotArgs& args, int64_t n, double* out, const int* pred) {
+  RedScratch& r = red();
+  const unsigned g = reduce_grid(n);
+  switch (args.np) {
+    case 1: AGG_LAUNCH(k_dot<1>, g, kRedBlock, 0, args, n, r.partials, r.ticket, out, pred); break;
+    case 2: AGG_LAUNCH(k_dot<2>, g, kRedBlock, 0, args, n, r.partials, r.ticket, out, pred); break;
+    case 3: AGG_LAUNCH(k_dot<3>, g, kRedBlock, 0, args, n, r.partials, r.ticket, out, pred); break;
+    default: throw Error("dot_device: np must be 1..3");
+  }
+}
+
+double dot_host(const double* a, const double* b, int64_t n) {
+  DevBuf<double> out(1);
+  DotArgs d{};
+  d.a[0] = a;
+  d.b[0] = b;
+  d.np = 1;
+  dot_device(d, n, out.get());
+  return read_scalar(out.get());
+}
+
+// ---- segmented sort --------------------------------------------------------------
+
+namespace {
+// Warp per segment; rank of a key = number of smaller keys in its segment (keys are
+// unique).  Segment keys are read through L1 as broadcast loads.
+__global__ void k_segsort(const idx* offsets, int64_t nseg, const idx* kin, idx* kout,
+                          const double* vin, double* vout) {
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= nseg) return;
+  const idx lo = offsets[warp], hi = offsets[warp + 1];
+  const idx L = hi - lo;
+  for (idx e = lane; e < L; e += 32) {
+    const idx key = kin[lo + e];
+    idx rank = 0;
+    for (idx q = 0; q < L; ++q) rank += (kin[lo + q] < key) ? 1 : 0;
+    kout[lo + rank] = key;
+    if (vout) vout[lo + rank] = vin[lo + e];
+  }
+}
+}  // namespace
+
+void segmented_sort(const idx* offsets, int64_t nseg, const idx* kin, idx* kout, const double* vin,
+                    double* vout) {
+  if (nseg <= 0) return;
+  AGG_LAUNCH(k_segsort, grid_for(nseg * 32, 256), 256, 0, offsets, nseg, kin, kout, vin, vout);
+}
+
+// ---- helpers -----------------------------------------------------------------------
+
+namespace {
+__global__ void k_fill_int(idx* p, int64_t n, idx v) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+__global__ void k_fill_double(double* p, int64_t n, double v) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+}  // namespace
+
+void fill_int(idx* p, int64_t n, idx v) {
+  if (n > 0) AGG_LAUNCH(k_fill_int, grid_for(n, 256), 256, 0, p, n, v);
+}
+void fill_double(double* p, int64_t n, double v) {
+  if (n > 0) AGG_LAUNCH(k_fill_double, grid_for(n, 256), 256, 0, p, n, v);
+}
+void copy_double(double* dst, const double* src, int64_t n) {
+  if (n > 0)
+    AGG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream()));
+}
+
+}  // namespace aggmg_b200

@@ -1,0 +1,92 @@
+// runtime.cuh — device context (one stream per process, stream-ordered memory pool),
+// RAII device buffers, pinned scalar readback, kernel-family profiling.
+#pragma once
+
+#include <cstring>
+#include <memory>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace aggmg_b200 {
+
+void ensure_init();
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+
+// Move-only device array allocated from the stream-ordered pool.
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(int64_t n) { resize(n); }
+  ~DevBuf() { reset(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { reset(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    return *this;
+  }
+  void resize(int64_t n) {
+    reset();
+    n_ = n;
+    // +32 bytes of tail padding: vectorised loads may read past the end of a row block
+    if (n > 0) p_ = static_cast<T*>(dev_alloc(sizeof(T) * static_cast<size_t>(n) + 32));
+  }
+  void reset() {
+    if (p_) dev_free(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  int64_t size() const { return n_; }
+  void zero() const {
+    if (n_ > 0) AGG_CUDA(cudaMemsetAsync(p_, 0, sizeof(T) * n_, stream()));
+  }
+  void upload(const T* h, int64_t n) const {
+    if (n > 0) AGG_CUDA(cudaMemcpyAsync(p_, h, sizeof(T) * n, cudaMemcpyHostToDevice, stream()));
+  }
+  void download(T* h, int64_t n) const {
+    if (n > 0) AGG_CUDA(cudaMemcpyAsync(h, p_, sizeof(T) * n, cudaMemcpyDeviceToHost, stream()));
+  }
+  std::vector<T> to_host() const {
+    std::vector<T> v(n_);
+    download(v.data(), n_);
+    AGG_CUDA(cudaStreamSynchronize(stream()));
+    return v;
+  }
+
+ private:
+  T* p_ = nullptr;
+  int64_t n_ = 0;
+};
+
+void sync();
+
+// Read `count` values of type T from device memory (synchronises the stream).
+template <class T>
+T read_scalar(const T* dptr) {
+  T v;
+  AGG_CUDA(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, stream()));
+  AGG_CUDA(cudaStreamSynchronize(stream()));
+  return v;
+}
+
+// Small pinned staging area for scalar readbacks that avoid pageable copies.
+double* pinned_scratch(int n_doubles);
+
+// Kernel-family timing (CUDA events on the library stream).
+enum ProfileFamily { kProfNone = 0, kProfSmoothL0 = 1, kProfSpmvL0 = 2, kProfFamilies = 3 };
+struct ProfileScope {
+  ProfileScope(int family, double bytes);
+  ~ProfileScope();
+  int family_;
+  int slot_;
+};
+void profile_enable(int family);
+void profile_read(int family, double* total_ms, int64_t* launches, double* bytes);
+int64_t launch_count();
+
+}  // namespace aggmg_b200

@@ -1,0 +1,715 @@
+// setup.cu — strength, symmetrization, MIS(2), aggregation, transfer and the Galerkin
+// sort / segmented reduce.  Every kernel reproduces the reference's arithmetic and
+// tie-breaking exactly; the file is compiled with --fmad=false and
+// uses explicit _rn intrinsics where a rounding sequence is part of the contract.
+#include <algorithm>
+#include <string>
+
+#include "setup.cuh"
+
+namespace aggmg_b200 {
+
+namespace {
+
+__device__ inline double dmax_ref(double a, double b) { return (a < b) ? b : a; }  // std::max
+
+// ---- a3 strength ---------------------------------------------------------------------
+// mode 0: count (cnt[i]); mode 1: fill columns at out_rowptr[i].
+__global__ void k_strength(const idx* __restrict__ rowptr, const idx* __restrict__ col,
+                           const double* __restrict__ val, int64_t n, double alpha, int fail_zero,
+                           int mode, const idx* out_rowptr, idx* out, int* bad_row) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const idx lo = rowptr[i], hi = rowptr[i + 1];
+  double d = 0.0;
+  for (idx k = lo; k < hi; ++k)
+    if (col[k] == i) d = val[k];
+  double s;
+  if (d == 0.0) {  // strength.cpp:18-21
+    if (fail_zero) atomicMin(bad_row, static_cast<int>(i));
+    s = 1.0;
+  } else {
+    s = d > 0.0 ? 1.0 : -1.0;
+  }
+  const double ns = -s;
+  double m = 0.0;
+  for (idx k = lo; k < hi; ++k) {
+    if (col[k] == i) continue;
+    m = dmax_ref(m, __dmul_rn(ns, val[k]));
+  }
+  const double thr = __dmul_rn(alpha, m);
+  if (mode == 0) {
+    idx c = 0;
+    if (m > 0.0)
+      for (idx k = lo; k < hi; ++k)
+        if (col[k] != i && __dmul_rn(ns, val[k]) > thr) ++c;
+    out[i] = c;
+  } else {
+    if (!(m > 0.0)) return;
+    idx p = out_rowptr[i];
+    for (idx k = lo; k < hi; ++k)
+      if (col[k] != i && __dmul_rn(ns, val[k]) > thr) out[p++] = col[k];
+  }
+}
+
+// ---- a4/a5 influence + symmetrize -------------------------------------------------------
+__global__ void k_col_count(const idx* col, int64_t nnz, idx* cnt) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < nnz) atomicAdd(&cnt[col[k]], 1);
+}
+__global__ void k_scatter_pattern_t(const idx* rowptr, const idx* col, int64_t n, const idx* trow,
+                                    idx* cursor, idx* tcol) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (idx k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+    const idx j = col[k];
+    tcol[trow[j] + atomicAdd(&cursor[j], 1)] = static_cast<idx>(i);
+  }
+}
+// Sorted merge of C row i and C^T row i (strength.cpp:86-103).  mode 0 counts.
+__global__ void k_merge_rows(const idx* crp, const idx* ccol, const idx* trp, const idx* tcol,
+                             int64_t n, int mode, const idx* srp, idx* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  idx a = crp[i], ae = crp[i + 1], b = trp[i], be = trp[i + 1];
+  idx cnt = 0;
+  idx* o = mode ? out + srp[i] : nullptr;
+  while (a < ae || b < be) {
+    idx j;
+    if (b >= be || (a < ae && ccol[a] <= tcol[b])) {
+      j = ccol[a];
+      if (b < be && tcol[b] == j) ++b;
+      ++a;
+    } else {
+      j = tcol[b++];
+    }
+    if (o) o[cnt] = j;
+    ++cnt;
+  }
+  if (!mode) out[i] = cnt;
+}
+
+// ---- a6 MIS(2) ---------------------------------------------------------------------------
+struct __align__(16) Tuple {
+  double v;
+  int i;
+  int s;
+};
+// lexicographic (s, v, i) — aggregation.cpp:24-28
+__device__ inline bool tuple_less(const Tuple& a, const Tuple& b) {
+  if (a.s != b.s) return a.s < b.s;
+  if (a.v != b.v) return a.v < b.v;
+  return a.i < b.i;
+}
+__device__ inline Tuple load_tuple(const Tuple* p) {
+  const double2 raw = __ldg(reinterpret_cast<const double2*>(p));
+  Tuple t;
+  t.v = raw.x;
+  const int2 is = *reinterpret_cast<const int2*>(&raw.y);
+  t.i = is.x;
+  t.s = is.y;
+  return t;
+}
+struct MisCtl {
+  int undecided;
+  int active;
+  int sweeps;
+  int pad;
+};
+
+__global__ void k_mis_init(const idx* infl, int64_t n, uint64_t seed, Tuple* cur, int8_t* state) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Tuple t;
+  t.v = __dadd_rn(static_cast<double>(infl[i]), uniform_open01(seed, static_cast<uint64_t>(i)));
+  t.i = static_cast<int>(i);
+  t.s = 0;
+  cur[i] = t;
+  state[i] = 0;
+}
+
+// mid_i = max over {i} u N(i) of cur (aggregation.cpp:31-41)
+__global__ void k_mis_pass1(const idx* __restrict__ rp, const idx* __restrict__ col, int64_t n,
+                            const Tuple* cur, Tuple* mid, MisCtl* ctl) {
+  const int undecided = *reinterpret_cast<volatile int*>(&ctl->undecided);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->active = undecided > 0 ? 1 : 0;
+    if (undecided > 0) ctl->sweeps += 1;
+  }
+  if (undecided == 0) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Tuple best = load_tuple(cur + i);
+  for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+    const Tuple t = load_tuple(cur + col[k]);
+    if (tuple_less(best, t)) best = t;
+  }
+  mid[i] = best;
+}
+
+// far_i = max over {i} u N(i) of mid; decide; broadcast the state (aggregation.cpp:64-79)
+__global__ void k_mis_pass2(const idx* __restrict__ rp, const idx* __restrict__ col, int64_t n,
+                            const Tuple* mid, Tuple* cur, int8_t* state, MisCtl* ctl) {
+  if (!ctl->active) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int decided = 0;
+  if (i < n && state[i] == 0) {
+    Tuple far = load_tuple(mid + i);
+    for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+      const Tuple t = load_tuple(mid + col[k]);
+      if (tuple_less(far, t)) far = t;
+    }
+    int8_t st = 0;
+    if (far.i == static_cast<int>(i))
+      st = 1;
+    else if (far.s == 1)
+      st = -1;
+    if (st != 0) {
+      state[i] = st;
+      cur[i].s = st;
+      decided = 1;
+    }
+  }
+  const unsigned ballot = __ballot_sync(0xffffffffu, decided);
+  if ((threadIdx.x & 31) == 0 && ballot) atomicSub(&ctl->undecided, __popc(ballot));
+}
+
+// ---- a7 aggregation ------------------------------------------------------------------------
+// rep[i] = representative node of i's aggregate after pass 1 (roots: themselves).
+__global__ void k_agg_pass1(const idx* rp, const idx* col, int64_t n, const int8_t* state,
+                            idx* rep) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  idx r = -1;
+  if (state[i] == 1) {
+    r = static_cast<idx>(i);
+  } else {
+    for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+      const idx j = col[k];
+      if (state[j] == 1) {
+        r = j;
+        break;
+      }
+    }
+  }
+  rep[i] = r;
+}
+
+__device__ inline double csr_at(const idx* rp, const idx* col, const double* val, idx i, idx j) {
+  idx lo = rp[i], hi = rp[i + 1];
+  while (lo < hi) {  // lower_bound (sparse.cpp:15-20)
+    const idx mid = lo + ((hi - lo) >> 1);
+    if (col[mid] < j)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return (lo < rp[i + 1] && col[lo] == j) ? val[lo] : 0.0;
+}
+
+// Pass 2 against the pass-1 snapshot (aggregation.cpp:118-136); leftovers become
+// their own representative (aggregation.cpp:139-144).  Comparing representative node
+// ids is equivalent to comparing the reference's pre-ids, which are root ranks.
+__global__ void k_agg_pass2(const idx* srp, const idx* scol, const idx* arp, const idx* acol,
+                            const double* aval, int64_t n, const idx* rep, idx* rep2,
+                            idx* isrep) {
+  const int64_t ii = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (ii >= n) return;
+  const idx i = static_cast<idx>(ii);
+  idx r = rep[i];
+  if (r == -1) {
+    idx best = -1;
+    double best_w = -1.0;
+    for (idx k = srp[i]; k < srp[i + 1]; ++k) {
+      const idx j = scol[k];
+      const idx ja = rep[j];
+      if (ja == -1) continue;
+      const double w = dmax_ref(fabs(csr_at(arp, acol, aval, i, j)), fabs(csr_at(arp, acol, aval, j, i)));
+      if (w > best_w || (w == best_w && ja < best)) {
+        best_w = w;
+        best = ja;
+      }
+    }
+    r = best == -1 ? i : best;
+  }
+  rep2[i] = r;
+  isrep[i] = (r == i) ? 1 : 0;
+}
+
+__global__ void k_agg_assign(const idx* rep2, const idx* rank, int64_t n, idx* assignment,
+                             idx* representatives) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const idx r = rep2[i];
+  assignment[i] = rank[r];
+  if (r == static_cast<idx>(i)) representatives[rank[i]] = static_cast<idx>(i);
+}
+
+__global__ void k_group_scatter(const idx* assignment, int64_t n, const idx* off, idx* cursor,
+                                idx* rows) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const idx a = assignment[i];
+  rows[off[a] + atomicAdd(&cursor[a], 1)] = static_cast<idx>(i);
+}
+
+// ---- a8 transfer ---------------------------------------------------------------------------
+// sq_J = sum_{i in J ascending} b_i*b_i (transfer.cpp:21-22); also counts the nonzero rows
+__global__ void k_transfer_norms(const idx* goff, const idx* rows, const double* b, int64_t nc,
+                                 double* coarse_b, idx* rcnt, int* bad_agg) {
+  const int64_t J = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (J >= nc) return;
+  double sq = 0.0;
+  idx c = 0;
+  for (idx m = goff[J]; m < goff[J + 1]; ++m) {
+    const double bi = b[rows[m]];
+    sq = __dadd_rn(sq, __dmul_rn(bi, bi));
+    c += (bi != 0.0) ? 1 : 0;
+  }
+  if (!(sq > 0.0)) atomicMin(bad_agg, static_cast<int>(J));
+  coarse_b[J] = __dsqrt_rn(sq);
+  rcnt[J] = c;
+}
+__global__ void k_transfer_pval(const idx* assignment, const double* b, const double* coarse_b,
+                                int64_t n, double* pval) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double bi = b[i];
+  pval[i] = (bi != 0.0) ? __ddiv_rn(bi, coarse_b[assignment[i]]) : 0.0;
+}
+// R = P^T: rows = aggregates, entries = member rows with b_i != 0, ascending.
+__global__ void k_transfer_R(const idx* goff, const idx* rows, const double* pval, int64_t nc,
+                             const idx* rrp, idx* rcol, double* rval) {
+  const int64_t J = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (J >= nc) return;
+  idx p = rrp[J];
+  for (idx m = goff[J]; m < goff[J + 1]; ++m) {
+    const idx i = rows[m];
+    const double w = pval[i];
+    if (w != 0.0) {
+      rcol[p] = i;
+      rval[p] = w;
+      ++p;
+    }
+  }
+}
+
+// ---- a9/a10 Galerkin -------------------------------------------------------------------------
+__global__ void k_group_entry_counts(const idx* goff, const idx* rows, const idx* arp, int64_t nc,
+                                     idx* ecnt) {
+  const int64_t J = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (J >= nc) return;
+  idx c = 0;
+  for (idx m = goff[J]; m < goff[J + 1]; ++m) {
+    const idx i = rows[m];
+    c += arp[i + 1] - arp[i];
+  }
+  ecnt[J] = c;
+}
+
+constexpr int kGalWarps = 4;
+constexpr int kGalCap = 1024;  // fine entries per coarse row handled in shared memory
+
+// Warp per coarse row I: gather the fine entries of I's member rows in (row asc, storage
+// order) = global storage order, sort them by coarse column J with the gather position
+// as the tie-break (= the reference's stable sort by key I*nc+J, galerkin.cpp:52-62),
+// and emit entry / entry_row / sorted J; count the distinct J (coarse row length).
+__global__ void __launch_bounds__(kGalWarps * 32)
+    k_gal_symbolic(const idx* goff, const idx* rows, const idx* arp, const idx* acol,
+                   const idx* assignment, int64_t nc, const idx* eoff, idx* entry, idx* entry_row,
+                   idx* sorted_j, idx* cnnz, idx* big_list, int* big_count) {
+  extern __shared__ unsigned long long gsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t I = static_cast<int64_t>(blockIdx.x) * kGalWarps + w;
+  if (I >= nc) return;
+  unsigned long long* skey = gsm + w * kGalCap;
+  idx* skk = reinterpret_cast<idx*>(gsm + kGalWarps * kGalCap) + w * kGalCap;
+  idx* sri = reinterpret_cast<idx*>(gsm + kGalWarps * kGalCap) + kGalWarps * kGalCap + w * kGalCap;
+  idx* sj = sri + kGalWarps * kGalCap;  // sorted coarse columns, per warp
+  const idx base_e = eoff[I];
+  const idx L = eoff[I + 1] - base_e;
+  if (L > kGalCap) {
+    if (lane == 0) big_list[atomicAdd(big_count, 1)] = static_cast<idx>(I);
+    return;
+  }
+  idx p = 0;
+  for (idx m = goff[I]; m < goff[I + 1]; ++m) {
+    const idx i = rows[m];
+    const idx lo = arp[i], len = arp[i + 1] - lo;
+    for (idx t = lane; t < len; t += 32) {
+      const idx k = lo + t;
+      skey[p + t] = (static_cast<unsigned long long>(assignment[acol[k]]) << 32) |
+                    static_cast<unsigned long long>(p + t);
+      skk[p + t] = k;
+      sri[p + t] = i;
+    }
+    p += len;
+  }
+  __syncwarp();
+  for (idx q = lane; q < L; q += 32) {
+    const unsigned long long key = skey[q];
+    idx rank = 0;
+    for (idx z = 0; z < L; ++z) rank += (skey[z] < key) ? 1 : 0;
+    entry[base_e + rank] = skk[q];
+    entry_row[base_e + rank] = sri[q];
+    sj[rank] = static_cast<idx>(key >> 32);
+  }
+  __syncwarp();
+  idx cnt = 0;
+  for (idx b = 0; b < L; b += 32) {
+    const idx r = b + lane;
+    const bool st = r < L && (r == 0 || sj[r] != sj[r - 1]);
+    cnt += __popc(__ballot_sync(0xffffffffu, st));
+    if (r < L) sorted_j[base_e + r] = sj[r];
+  }
+  if (lane == 0) cnnz[I] = cnt;
+}
+
+// Block per oversized coarse row; keys staged in global scratch.
+__global__ void k_gal_symbolic_big(const idx* big_list, const idx* goff, const idx* rows,
+                                   const idx* arp, const idx* acol, const idx* assignment,
+                                   const idx* eoff, unsigned long long* gkey, idx* gkk, idx* gri,
+                                   idx* entry, idx* entry_row, idx* sorted_j, idx* cnnz) {
+  __shared__ idx s_cnt;
+  const idx I = big_list[blockIdx.x];
+  const idx base_e = eoff[I];
+  const idx L = eoff[I + 1] - base_e;
+  idx p = 0;
+  for (idx m = goff[I]; m < goff[I + 1]; ++m) {
+    const idx i = rows[m];
+    const idx lo = arp[i], len = arp[i + 1] - lo;
+    for (idx t = threadIdx.x; t < len; t += blockDim.x) {
+      const idx k = lo + t;
+      gkey[base_e + p + t] = (static_cast<unsigned long long>(assignment[acol[k]]) << 32) |
+                             static_cast<unsigned long long>(p + t);
+      gkk[base_e + p + t] = k;
+      gri[base_e + p + t] = i;
+    }
+    p += len;
+  }
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  for (idx q = threadIdx.x; q < L; q += blockDim.x) {
+    const unsigned long long key = gkey[base_e + q];
+    idx rank = 0;
+    for (idx z = 0; z < L; ++z) rank += (gkey[base_e + z] < key) ? 1 : 0;
+    entry[base_e + rank] = gkk[base_e + q];
+    entry_row[base_e + rank] = gri[base_e + q];
+    sorted_j[base_e + rank] = static_cast<idx>(key >> 32);
+  }
+  __syncthreads();
+  __threadfence_block();
+  idx c = 0;
+  for (idx r = threadIdx.x; r < L; r += blockDim.x)
+    c += (r == 0 || sorted_j[base_e + r] != sorted_j[base_e + r - 1]) ? 1 : 0;
+  atomicAdd(&s_cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) cnnz[I] = s_cnt;
+}
+
+// Warp per coarse row: segment boundaries -> coarse columns, segment offsets, slot_of_csr.
+__global__ void k_gal_fill(int64_t nc, const idx* eoff, const idx* sorted_j, const idx* entry,
+                           const idx* crp, idx* ccol, idx* seg_off, idx* slot_of_csr) {
+  const int64_t I = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (I >= nc) return;
+  const idx base_e = eoff[I], L = eoff[I + 1] - base_e;
+  idx carry = crp[I] - 1;
+  for (idx b = 0; b < L; b += 32) {
+    const idx r = b + lane;
+    idx jc = 0;
+    bool st = false;
+    if (r < L) {
+      jc = sorted_j[base_e + r];
+      st = (r == 0) || jc != sorted_j[base_e + r - 1];
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, st);
+    const idx seg = carry + __popc(bal & ((2u << lane) - 1u));
+    if (r < L) {
+      if (st) {
+        ccol[seg] = jc;
+        seg_off[seg] = base_e + r;
+      }
+      slot_of_csr[entry[base_e + r]] = seg;
+    }
+    carry += __popc(bal);
+  }
+}
+
+// Ac[s] = sum over the segment, in stored order, of (pv[row] * a_e) * pv[col_e]
+// (galerkin.cpp:128-135).
+__global__ void k_gal_numeric(int64_t nnz_c, const idx* seg_off, const idx* entry,
+                              const idx* entry_row, const idx* acol, const double* aval,
+                              const double* pv, double* out) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= nnz_c) return;
+  double acc = 0.0;
+  for (idx p = seg_off[s]; p < seg_off[s + 1]; ++p) {
+    const idx e = entry[p];
+    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(pv[entry_row[p]], aval[e]), pv[acol[e]]));
+  }
+  out[s] = acc;
+}
+
+__global__ void k_fingerprint(const idx* rowptr, int64_t n, const idx* col, int64_t nnz,
+                              const idx* assignment, unsigned long long* out) {
+  unsigned long long h = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t total = (n + 1) + nnz + n;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
+    unsigned long long v;
+    if (t <= n)
+      v = static_cast<unsigned long long>(rowptr[t]);
+    else if (t <= n + nnz)
+      v = static_cast<unsigned long long>(col[t - n - 1]);
+    else
+      v = static_cast<unsigned long long>(assignment[t - n - 1 - nnz]);
+    h += hash_mix(hash_mix(static_cast<uint64_t>(t)) ^ v);
+  }
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_down_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+
+}  // namespace
+
+// ---- host drivers ---------------------------------------------------------------------------
+
+DevCsrPtr classic_strength(const DevCsr& A, double alpha, int zero_diag_policy) {
+  require(A.n_rows == A.n_cols, "strength: matrix must be square");
+  require(alpha > 0.0 && alpha < 1.0, "strength: alpha must be in (0, 1)");
+  const int64_t n = A.n_rows;
+  auto C = std::make_shared<DevCsr>();
+  C->n_rows = C->n_cols = n;
+  C->rowptr.resize(n + 1);
+  DevBuf<idx> cnt(n);
+  DevBuf<int> bad(1);
+  fill_int(bad.get(), 1, INT32_MAX);
+  if (n > 0)
+    AGG_LAUNCH(k_strength, grid_for(n, 256), 256, 0, A.rowptr.get(), A.col.get(), A.val.get(), n,
+               alpha, zero_diag_policy, 0, nullptr, cnt.get(), bad.get());
+  C->nnz = scan_to_offsets(cnt.get(), C->rowptr.get(), n);
+  if (zero_diag_policy) {
+    const int b = read_scalar(bad.get());
+    if (b != INT32_MAX)
+      throw Error("strength: zero or missing diagonal at row " + std::to_string(b));
+  }
+  C->col.resize(C->nnz);
+  if (n > 0 && C->nnz > 0)
+    AGG_LAUNCH(k_strength, grid_for(n, 256), 256, 0, A.rowptr.get(), A.col.get(), A.val.get(), n,
+               alpha, 0, 1, C->rowptr.get(), C->col.get(), bad.get());
+  return C;
+}
+
+void influence_and_symmetrize(const DevCsr& C, DevBuf<idx>& influence, DevCsrPtr& S) {
+  require(C.n_rows == C.n_cols, "symmetrize: matrix must be square");
+  const int64_t n = C.n_rows;
+  influence.resize(n);
+  influence.zero();
+  if (C.nnz > 0) AGG_LAUNCH(k_col_count, grid_for(C.nnz, 256), 256, 0, C.col.get(), C.nnz, influence.get());
+  DevBuf<idx> trp(n + 1), cursor(n), tmp(C.nnz), tcol(C.nnz);
+  scan_to_offsets_async(influence.get(), trp.get(), n);
+  cursor.zero();
+  if (n > 0)
+    AGG_LAUNCH(k_scatter_pattern_t, grid_for(n, 256), 256, 0, C.rowptr.get(), C.col.get(), n,
+               trp.get(), cursor.get(), tmp.get());
+  segmented_sort(trp.get(), n, tmp.get(), tcol.get());
+  S = std::make_shared<DevCsr>();
+  S->n_rows = S->n_cols = n;
+  S->rowptr.resize(n + 1);
+  DevBuf<idx> scnt(n);
+  if (n > 0)
+    AGG_LAUNCH(k_merge_rows, grid_for(n, 256), 256, 0, C.rowptr.get(), C.col.get(), trp.get(),
+               tcol.get(), n, 0, nullptr, scnt.get());
+  S->nnz = scan_to_offsets(scnt.get(), S->rowptr.get(), n);
+  S->col.resize(S->nnz);
+  if (n > 0 && S->nnz > 0)
+    AGG_LAUNCH(k_merge_rows, grid_for(n, 256), 256, 0, C.rowptr.get(), C.col.get(), trp.get(),
+               tcol.get(), n, 1, S->rowptr.get(), S->col.get());
+}
+
+Mis2Dev mis2(const DevCsr& S, const idx* influence, uint64_t seed) {
+  require(S.n_rows == S.n_cols, "mis2: graph must be square");
+  const int64_t n = S.n_rows;
+  Mis2Dev res;
+  res.state.resize(n);
+  if (n == 0) return res;
+  DevBuf<Tuple> cur(n), mid(n);
+  DevBuf<MisCtl> ctl(1);
+  MisCtl h0{static_cast<int>(n), 0, 0, 0};
+  ctl.upload(&h0, 1);
+  AGG_LAUNCH(k_mis_init, grid_for(n, 256), 256, 0, influence, n, seed, cur.get(), res.state.get());
+  const unsigned g = grid_for(n, 256);
+  // Sweeps are issued in batches; once every node is decided the kernels exit at entry,
+  // so the device-side sweep counter matches the reference's loop count exactly.
+  int batch = 8;
+  while (true) {
+    for (int b = 0; b < batch; ++b) {
+      AGG_LAUNCH(k_mis_pass1, g, 256, 0, S.rowptr.get(), S.col.get(), n, cur.get(), mid.get(), ctl.get());
+      AGG_LAUNCH(k_mis_pass2, g, 256, 0, S.rowptr.get(), S.col.get(), n, mid.get(), cur.get(),
+                 res.state.get(), ctl.get());
+    }
+    const MisCtl h = read_scalar(ctl.get());
+    if (h.sweeps > n) throw Error("mis2: failed to decide all nodes");
+    if (h.undecided == 0) {
+      res.sweeps = h.sweeps;
+      break;
+    }
+    batch = 4;
+  }
+  return res;
+}
+
+AggDev aggregate(const DevCsr& S, const DevCsr& A, const int8_t* state) {
+  require(S.n_rows == S.n_cols && A.n_rows == A.n_cols && S.n_rows == A.n_rows,
+          "aggregate: graph and matrix shapes disagree");
+  const int64_t n = S.n_rows;
+  AggDev agg;
+  agg.n_fine = n;
+  agg.assignment.resize(n);
+  DevBuf<idx> rep(n), rep2(n), isrep(n), rank(n + 1);
+  if (n > 0) {
+    AGG_LAUNCH(k_agg_pass1, grid_for(n, 256), 256, 0, S.rowptr.get(), S.col.get(), n, state, rep.get());
+    AGG_LAUNCH(k_agg_pass2, grid_for(n, 256), 256, 0, S.rowptr.get(), S.col.get(), A.rowptr.get(),
+               A.col.get(), A.val.get(), n, rep.get(), rep2.get(), isrep.get());
+  }
+  agg.n_agg = scan_to_offsets(isrep.get(), rank.get(), n);
+  agg.representatives.resize(agg.n_agg);
+  if (n > 0)
+    AGG_LAUNCH(k_agg_assign, grid_for(n, 256), 256, 0, rep2.get(), rank.get(), n,
+               agg.assignment.get(), agg.representatives.get());
+  build_groups(agg);
+  return agg;
+}
+
+void build_groups(AggDev& agg) {
+  const int64_t n = agg.n_fine, nc = agg.n_agg;
+  DevBuf<idx> cnt(nc), tmp(n);
+  cnt.zero();
+  agg.agg_row_offsets.resize(nc + 1);
+  agg.rows_by_coarse.resize(n);
+  if (n > 0) AGG_LAUNCH(k_col_count, grid_for(n, 256), 256, 0, agg.assignment.get(), n, cnt.get());
+  scan_to_offsets_async(cnt.get(), agg.agg_row_offsets.get(), nc);
+  cnt.zero();
+  if (n > 0)
+    AGG_LAUNCH(k_group_scatter, grid_for(n, 256), 256, 0, agg.assignment.get(), n,
+               agg.agg_row_offsets.get(), cnt.get(), tmp.get());
+  segmented_sort(agg.agg_row_offsets.get(), nc, tmp.get(), agg.rows_by_coarse.get());
+}
+
+TransferDev build_transfer(const AggDev& agg, const double* fine_b) {
+  const int64_t n = agg.n_fine, nc = agg.n_agg;
+  TransferDev t;
+  t.pval.resize(n);
+  t.coarse_b.resize(nc);
+  DevBuf<idx> rcnt(nc);
+  DevBuf<int> bad(1);
+  fill_int(bad.get(), 1, INT32_MAX);
+  if (nc > 0)
+    AGG_LAUNCH(k_transfer_norms, grid_for(nc, 256), 256, 0, agg.agg_row_offsets.get(),
+               agg.rows_by_coarse.get(), fine_b, nc, t.coarse_b.get(), rcnt.get(), bad.get());
+  t.R = std::make_shared<DevCsr>();
+  t.R->n_rows = nc;
+  t.R->n_cols = n;
+  t.R->rowptr.resize(nc + 1);
+  t.p_nnz = t.R->nnz = scan_to_offsets(rcnt.get(), t.R->rowptr.get(), nc);
+  const int b = read_scalar(bad.get());
+  if (b != INT32_MAX)
+    throw Error("transfer: near-null-space vector vanishes on aggregate " + std::to_string(b));
+  if (n > 0)
+    AGG_LAUNCH(k_transfer_pval, grid_for(n, 256), 256, 0, agg.assignment.get(), fine_b,
+               t.coarse_b.get(), n, t.pval.get());
+  t.R->col.resize(t.R->nnz);
+  t.R->val.resize(t.R->nnz);
+  if (nc > 0)
+    AGG_LAUNCH(k_transfer_R, grid_for(nc, 256), 256, 0, agg.agg_row_offsets.get(),
+               agg.rows_by_coarse.get(), t.pval.get(), nc, t.R->rowptr.get(), t.R->col.get(),
+               t.R->val.get());
+  t.R->plan();
+  return t;
+}
+
+GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg) {
+  require(A.n_rows == A.n_cols, "galerkin: matrix must be square");
+  require(agg.n_fine == A.n_rows, "galerkin: aggregation size mismatch");
+  const int64_t nc = agg.n_agg;
+  GalerkinDev g;
+  g.n_fine = A.n_rows;
+  g.n_coarse = nc;
+  g.nnz_fine = A.nnz;
+  g.entry.resize(A.nnz);
+  g.entry_row.resize(A.nnz);
+  g.slot_of_csr.resize(A.nnz);
+  DevBuf<idx> ecnt(nc), eoff(nc + 1), sorted_j(A.nnz), cnnz(nc), big_list(nc > 0 ? nc : 1);
+  DevBuf<int> big_count(1);
+  big_count.zero();
+  if (nc > 0)
+    AGG_LAUNCH(k_group_entry_counts, grid_for(nc, 256), 256, 0, agg.agg_row_offsets.get(),
+               agg.rows_by_coarse.get(), A.rowptr.get(), nc, ecnt.get());
+  const int64_t total = scan_to_offsets(ecnt.get(), eoff.get(), nc);
+  require(total == A.nnz, "galerkin: aggregation does not cover the matrix rows");
+  const size_t smem = static_cast<size_t>(kGalWarps) * kGalCap * (8 + 4 + 4 + 4);
+  static bool raised = false;
+  if (!raised) {
+    AGG_CUDA(cudaFuncSetAttribute(k_gal_symbolic, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    raised = true;
+  }
+  if (nc > 0)
+    AGG_LAUNCH(k_gal_symbolic, static_cast<unsigned>((nc + kGalWarps - 1) / kGalWarps),
+               kGalWarps * 32, smem, agg.agg_row_offsets.get(), agg.rows_by_coarse.get(),
+               A.rowptr.get(), A.col.get(), agg.assignment.get(), nc, eoff.get(), g.entry.get(),
+               g.entry_row.get(), sorted_j.get(), cnnz.get(), big_list.get(), big_count.get());
+  const int nbig = read_scalar(big_count.get());
+  if (nbig > 0) {
+    DevBuf<unsigned long long> gkey(A.nnz);
+    DevBuf<idx> gkk(A.nnz), gri(A.nnz);
+    AGG_LAUNCH(k_gal_symbolic_big, static_cast<unsigned>(nbig), 256, 0, big_list.get(),
+               agg.agg_row_offsets.get(), agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(),
+               agg.assignment.get(), eoff.get(), gkey.get(), gkk.get(), gri.get(), g.entry.get(),
+               g.entry_row.get(), sorted_j.get(), cnnz.get());
+  }
+  g.coarse_rowptr.resize(nc + 1);
+  g.nnz_coarse = scan_to_offsets(cnnz.get(), g.coarse_rowptr.get(), nc);
+  g.coarse_col.resize(g.nnz_coarse);
+  g.segment_offsets.resize(g.nnz_coarse + 1);
+  if (nc > 0)
+    AGG_LAUNCH(k_gal_fill, grid_for(nc * 32, 256), 256, 0, nc, eoff.get(), sorted_j.get(),
+               g.entry.get(), g.coarse_rowptr.get(), g.coarse_col.get(), g.segment_offsets.get(),
+               g.slot_of_csr.get());
+  const idx nnz32 = static_cast<idx>(A.nnz);
+  AGG_CUDA(cudaMemcpyAsync(g.segment_offsets.get() + g.nnz_coarse, &nnz32, sizeof(idx),
+                           cudaMemcpyHostToDevice, stream()));
+  sync();  // nnz32 lives on the host stack
+  g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
+  return g;
+}
+
+DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const double* pval) {
+  auto Ac = std::make_shared<DevCsr>();
+  Ac->n_rows = Ac->n_cols = g.n_coarse;
+  Ac->nnz = g.nnz_coarse;
+  Ac->rowptr.resize(g.n_coarse + 1);
+  Ac->col.resize(g.nnz_coarse);
+  Ac->val.resize(g.nnz_coarse);
+  AGG_CUDA(cudaMemcpyAsync(Ac->rowptr.get(), g.coarse_rowptr.get(), sizeof(idx) * (g.n_coarse + 1),
+                           cudaMemcpyDeviceToDevice, stream()));
+  if (g.nnz_coarse > 0) {
+    AGG_CUDA(cudaMemcpyAsync(Ac->col.get(), g.coarse_col.get(), sizeof(idx) * g.nnz_coarse,
+                             cudaMemcpyDeviceToDevice, stream()));
+    AGG_LAUNCH(k_gal_numeric, grid_for(g.nnz_coarse, 256), 256, 0, g.nnz_coarse,
+               g.segment_offsets.get(), g.entry.get(), g.entry_row.get(), A.col.get(), A.val.get(),
+               pval, Ac->val.get());
+  }
+  Ac->plan();
+  return Ac;
+}
+
+uint64_t pattern_fingerprint(const DevCsr& A, const idx* assignment) {
+  DevBuf<unsigned long long> h(1);
+  h.zero();
+  AGG_LAUNCH(k_fingerprint, grid_for(A.n_rows + A.nnz + 1, 256, 4 * sm_count()), 256, 0,
+             A.rowptr.get(), A.n_rows, A.col.get(), A.nnz, assignment, h.get());
+  return read_scalar(h.get());
+}
+
+}  // namespace aggmg_b200

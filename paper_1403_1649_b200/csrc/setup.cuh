@@ -1,0 +1,60 @@
+// setup.cuh — the AMG setup kernels, bit-exact with the
+// reference's `reuse_caches=true` path.
+#pragma once
+
+#include <vector>
+
+#include "sparse.cuh"
+
+namespace aggmg_b200 {
+
+// a3: classic strength (strength.cpp:28-72).  Pattern only (values not stored on device).
+DevCsrPtr classic_strength(const DevCsr& A, double alpha, int zero_diag_policy);
+// a4 + a5: influence counts (column counts of C) and S = pattern(C u C^T).
+void influence_and_symmetrize(const DevCsr& C, DevBuf<idx>& influence, DevCsrPtr& S);
+
+// a6: MIS(2) (aggregation.cpp:45-86).  state[i] in {+1,-1}.
+struct Mis2Dev {
+  DevBuf<int8_t> state;
+  int sweeps = 0;
+};
+Mis2Dev mis2(const DevCsr& S, const idx* influence, uint64_t seed);
+
+// a7: aggregation (aggregation.cpp:88-159).
+struct AggDev {
+  int64_t n_fine = 0, n_agg = 0;
+  DevBuf<idx> assignment;       // fine -> aggregate
+  DevBuf<idx> representatives;  // aggregate -> representative node
+  // grouping of fine rows by aggregate, ascending inside a group (galerkin.cpp:87-94)
+  DevBuf<idx> agg_row_offsets;  // n_agg + 1
+  DevBuf<idx> rows_by_coarse;   // n_fine
+};
+AggDev aggregate(const DevCsr& S, const DevCsr& A, const int8_t* state);
+void build_groups(AggDev& agg);  // agg_row_offsets / rows_by_coarse from assignment
+
+// a8: transfer (transfer.cpp:15-49).  pval[i] = P value of row i (0 for empty rows);
+// coarse_b[J] = ||b restricted to J||; R = P^T as CSR (rows ascending fine index).
+struct TransferDev {
+  DevBuf<double> pval;
+  DevBuf<double> coarse_b;
+  DevCsrPtr R;
+  int64_t p_nnz = 0;
+};
+TransferDev build_transfer(const AggDev& agg, const double* fine_b);
+
+// a9/a10: Galerkin cache and numeric reduce (galerkin.cpp:38-137).
+struct GalerkinDev {
+  int64_t n_fine = 0, n_coarse = 0, nnz_fine = 0, nnz_coarse = 0;
+  DevBuf<idx> coarse_rowptr, coarse_col;
+  DevBuf<idx> entry, entry_row, segment_offsets, slot_of_csr;
+  uint64_t pattern_hash = 0;
+};
+GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg);
+// Ac values for the cached pattern.  pval: per fine row P weight.
+DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const double* pval);
+uint64_t pattern_fingerprint(const DevCsr& A, const idx* assignment);
+
+// galerkin_direct: R*A*P by two row-wise products in the reference spmm order.
+DevCsrPtr spmm(const DevCsr& A, const DevCsr& B);
+
+}  // namespace aggmg_b200

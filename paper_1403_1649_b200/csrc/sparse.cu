@@ -1,0 +1,434 @@
+// sparse.cu — device CSR, upload/validation, CSR-stream SpMV family, transpose and
+// the device-side problem generators.
+#include <algorithm>
+#include <vector>
+
+#include "sparse.cuh"
+
+namespace aggmg_b200 {
+
+// ---- upload / validation ------------------------------------------------------------
+
+namespace {
+
+__global__ void k_convert_rowptr(const int64_t* in, idx* out, int64_t n_rows, int64_t nnz,
+                                 int* bad_row) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i > n_rows) return;
+  const int64_t v = in[i];
+  out[i] = static_cast<idx>(v);
+  if (i < n_rows) {
+    const int64_t nx = in[i + 1];
+    if (nx < v || v < 0 || nx > nnz) atomicMin(bad_row, static_cast<int>(i));
+  }
+}
+
+// One thread per row: columns in range and strictly increasing.
+__global__ void k_convert_cols(const int64_t* rp, const int64_t* in, idx* out, int64_t n_rows,
+                               int64_t n_cols, int* bad_row, int check) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_rows) return;
+  const int64_t lo = rp[i], hi = rp[i + 1];
+  if (hi < lo || lo < 0) return;  // reported by k_convert_rowptr
+  int64_t prev = -1;
+  bool bad = false;
+  for (int64_t k = lo; k < hi; ++k) {
+    const int64_t c = in[k];
+    out[k] = static_cast<idx>(c);
+    if (check && (c < 0 || c >= n_cols || (k > lo && prev >= c))) bad = true;
+    prev = c;
+  }
+  if (bad) atomicMin(bad_row, static_cast<int>(i));
+}
+
+__global__ void k_widen(const idx* in, int64_t* out, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
+__global__ void k_max_row(const idx* rowptr, int64_t n, int* out) {
+  int m = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = max(m, rowptr[i + 1] - rowptr[i]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+}  // namespace
+
+constexpr int kStreamThreads = 256;
+constexpr int kStreamCap = 4096;  // staged products per block in the common case (32 KB)
+
+void DevCsr::plan() {
+  max_row = 0;
+  if (n_rows > 0) {
+    DevBuf<int> m(1);
+    m.zero();
+    AGG_LAUNCH(k_max_row, grid_for(n_rows, 256, 4 * sm_count()), 256, 0, rowptr.get(), n_rows,
+               m.get());
+    max_row = read_scalar(m.get());
+  }
+  const int mr = std::max(1, max_row);
+  rows_per_block = std::max(1, std::min(kStreamThreads, kStreamCap / mr));
+  smem_entries = rows_per_block * mr + 4;
+  // rows longer than the opt-in shared-memory limit (~28k entries) are not supported
+  require(static_cast<int64_t>(smem_entries) * 8 <= 227 * 1024,
+          "spmv: a row has " + std::to_string(max_row) +
+              " entries, beyond the CSR-stream staging capacity");
+}
+
+DevCsrPtr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, const int64_t* col,
+                     const double* val, bool validate) {
+  require(n_rows >= 0 && n_cols >= 0, "negative dimensions");
+  const int64_t nnz = rowptr[n_rows];
+  if (validate) {
+    require(rowptr[0] == 0, "row_offsets[0] must be 0");
+    require(nnz >= 0, "row_offsets[n_rows] must equal nnz");
+  }
+  require(n_rows < (1LL << 31) - 1 && n_cols < (1LL << 31) - 1 && nnz < (1LL << 31) - 1,
+          "matrix exceeds the int32 device index range (2^31 rows / nonzeros per GPU)");
+  auto A = std::make_shared<DevCsr>();
+  A->n_rows = n_rows;
+  A->n_cols = n_cols;
+  A->nnz = nnz;
+  A->rowptr.resize(n_rows + 1);
+  A->col.resize(nnz);
+  A->val.resize(nnz);
+  DevBuf<int64_t> rp64(n_rows + 1), c64(nnz);
+  DevBuf<int> bad(1);
+  fill_int(bad.get(), 1, INT32_MAX);
+  rp64.upload(rowptr, n_rows + 1);
+  c64.upload(col, nnz);
+  A->val.upload(val, nnz);
+  AGG_LAUNCH(k_convert_rowptr, grid_for(n_rows + 1, 256), 256, 0, rp64.get(), A->rowptr.get(),
+             n_rows, nnz, bad.get());
+  if (n_rows > 0)
+    AGG_LAUNCH(k_convert_cols, grid_for(n_rows, 256), 256, 0, rp64.get(), c64.get(), A->col.get(),
+               n_rows, n_cols, bad.get(), validate ? 1 : 0);
+  const int bad_row = read_scalar(bad.get());
+  if (bad_row != INT32_MAX) {
+    // Reproduce the reference's first failing check for that row (sparse.cpp:29-38).
+    const int64_t i = bad_row;
+    if (rowptr[i] > rowptr[i + 1]) throw Error("row_offsets must be non-decreasing");
+    if (rowptr[i] < 0 || rowptr[i + 1] > nnz) throw Error("row_offsets[n_rows] must equal nnz");
+    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+      if (col[k] < 0 || col[k] >= n_cols)
+        throw Error("column index out of range in row " + std::to_string(i));
+      if (k > rowptr[i] && col[k - 1] >= col[k])
+        throw Error("columns must be strictly increasing in row " + std::to_string(i));
+    }
+  }
+  A->plan();
+  return A;
+}
+
+void download_csr(const DevCsr& A, int64_t* rowptr, int64_t* col, double* val) {
+  DevBuf<int64_t> rp(A.n_rows + 1), c(A.nnz);
+  AGG_LAUNCH(k_widen, grid_for(A.n_rows + 1, 256), 256, 0, A.rowptr.get(), rp.get(), A.n_rows + 1);
+  if (A.nnz > 0) AGG_LAUNCH(k_widen, grid_for(A.nnz, 256), 256, 0, A.col.get(), c.get(), A.nnz);
+  rp.download(rowptr, A.n_rows + 1);
+  if (col) c.download(col, A.nnz);
+  if (val) A.val.download(val, A.nnz);
+  sync();
+}
+
+// ---- CSR-stream SpMV family ----------------------------------------------------------
+
+namespace {
+
+template <Epi E>
+struct EpiTraits {
+  static constexpr int np = (E == Epi::kSpmvDot1) ? 1 : (E == Epi::kSpmvDot2) ? 2 : (E == Epi::kSpmvDot3) ? 3 : 0;
+};
+
+template <Epi E>
+__global__ void __launch_bounds__(kStreamThreads)
+    k_csr_stream(const idx* __restrict__ rowptr, const idx* __restrict__ col,
+                 const double* __restrict__ val, int64_t n_rows, int rpb, SpmvArgs a,
+                 double* partials, unsigned* ticket) {
+  extern __shared__ double prod[];
+  constexpr int NP = EpiTraits<E>::np;
+  constexpr int NPX = NP > 0 ? NP : 1;
+  __shared__ double red_smem[32 * 3 + 1];
+  if (a.pred && !*a.pred) return;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rpb;
+  const int64_t r1 = min(r0 + static_cast<int64_t>(rpb), n_rows);
+  const idx e0 = rowptr[r0], e1 = rowptr[r1];
+  const double* __restrict__ x = a.x;
+
+  // Phase 1: stream the block's contiguous nonzero range with 128-bit loads.
+  for (idx e = (e0 & ~3) + 4 * static_cast<idx>(threadIdx.x); e < e1; e += 4 * kStreamThreads) {
+    const int4 c4 = __ldcs(reinterpret_cast<const int4*>(col + e));
+    const double2 v01 = __ldcs(reinterpret_cast<const double2*>(val + e));
+    const double2 v23 = __ldcs(reinterpret_cast<const double2*>(val + e + 2));
+    if (e >= e0) prod[e - e0] = __dmul_rn(v01.x, __ldg(x + c4.x));
+    if (e + 1 >= e0 && e + 1 < e1) prod[e + 1 - e0] = __dmul_rn(v01.y, __ldg(x + c4.y));
+    if (e + 2 >= e0 && e + 2 < e1) prod[e + 2 - e0] = __dmul_rn(v23.x, __ldg(x + c4.z));
+    if (e + 3 >= e0 && e + 3 < e1) prod[e + 3 - e0] = __dmul_rn(v23.y, __ldg(x + c4.w));
+  }
+  __syncthreads();
+
+  // Phase 2: one thread per row, sequential sum in storage order (sparse.cpp:58-61).
+  const int64_t r = r0 + threadIdx.x;
+  const bool active = threadIdx.x < rpb && r < r1;
+  double sum = 0.0;
+  if (active) {
+    const idx s = rowptr[r] - e0, t = rowptr[r + 1] - e0;
+    for (idx k = s; k < t; ++k) sum = __dadd_rn(sum, prod[k]);
+  }
+  if constexpr (E == Epi::kSpmv || NP > 0) {
+    if (active) a.y[r] = sum;
+  } else if constexpr (E == Epi::kResidual) {
+    if (active) a.y[r] = __dsub_rn(a.b[r], sum);
+  } else if constexpr (E == Epi::kJacobi) {
+    if (active) a.y[r] = __dadd_rn(x[r], __dmul_rn(a.d[r], __dsub_rn(a.b[r], sum)));
+  } else if constexpr (E == Epi::kScaleDiag) {
+    if (active) a.y[r] = __dmul_rn(sum, a.d[r]);
+  }
+  if constexpr (NP > 0) {
+    double v[NPX];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) v[k] = 0.0;
+    if (active) {
+      const double lhs = a.dot_with_x ? x[r] : sum;
+      if constexpr (NP == 1) {
+        v[0] = __dmul_rn(a.u[r], sum);
+      } else if constexpr (NP == 2) {
+        v[0] = __dmul_rn(lhs, sum);     // rho  = v.v (gmres) | c.v (cg)
+        v[1] = __dmul_rn(lhs, a.c[r]);  // alpha = v.rc       | c.rc
+      } else {
+        v[0] = __dmul_rn(lhs, a.u[r]);  // gamma = w.v | d.v
+        v[1] = __dmul_rn(lhs, sum);     // beta  = w.w | d.w
+        v[2] = __dmul_rn(lhs, a.c[r]);  // alpha2 = w.rt | d.rt
+      }
+    }
+    block_reduce<NPX>(v, red_smem);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int k = 0; k < NP; ++k) partials[blockIdx.x * NP + k] = v[k];
+    finish_reduction<NPX>(partials, ticket, a.dots_out, red_smem);
+  }
+}
+
+template <Epi E>
+void launch_stream(const DevCsr& A, const SpmvArgs& a) {
+  const int64_t blocks = (A.n_rows + A.rows_per_block - 1) / A.rows_per_block;
+  const size_t smem = sizeof(double) * A.smem_entries;
+  if (smem > 48 * 1024) {
+    static bool raised = false;
+    if (!raised) {
+      AGG_CUDA(cudaFuncSetAttribute(k_csr_stream<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    227 * 1024));
+      raised = true;
+    }
+  }
+  require(blocks < (1 << 20), "spmv: too many row blocks for the reduction scratch");
+  AGG_LAUNCH(k_csr_stream<E>, static_cast<unsigned>(blocks), kStreamThreads, smem, A.rowptr.get(),
+             A.col.get(), A.val.get(), A.n_rows, A.rows_per_block, a, reduce_partials(),
+             reduce_ticket());
+}
+
+}  // namespace
+
+double spmv_bytes(const DevCsr& A, Epi epi) {
+  const double n = static_cast<double>(A.n_rows), nnz = static_cast<double>(A.nnz);
+  double b = 12.0 * nnz + 4.0 * (n + 1) + 8.0 * static_cast<double>(A.n_cols) + 8.0 * n;
+  switch (epi) {
+    case Epi::kResidual: b += 8.0 * n; break;
+    case Epi::kJacobi: b += 16.0 * n; break;
+    case Epi::kScaleDiag: b += 8.0 * n; break;
+    case Epi::kSpmvDot1: b += 8.0 * n; break;
+    case Epi::kSpmvDot2: b += 8.0 * n; break;
+    case Epi::kSpmvDot3: b += 16.0 * n; break;
+    default: break;
+  }
+  return b;
+}
+
+void spmv_run(const DevCsr& A, Epi epi, const SpmvArgs& a, int prof_family) {
+  if (A.n_rows == 0) return;
+  ProfileScope scope(prof_family, prof_family ? spmv_bytes(A, epi) : 0.0);
+  switch (epi) {
+    case Epi::kSpmv: launch_stream<Epi::kSpmv>(A, a); break;
+    case Epi::kResidual: launch_stream<Epi::kResidual>(A, a); break;
+    case Epi::kJacobi: launch_stream<Epi::kJacobi>(A, a); break;
+    case Epi::kScaleDiag: launch_stream<Epi::kScaleDiag>(A, a); break;
+    case Epi::kSpmvDot1: launch_stream<Epi::kSpmvDot1>(A, a); break;
+    case Epi::kSpmvDot2: launch_stream<Epi::kSpmvDot2>(A, a); break;
+    case Epi::kSpmvDot3: launch_stream<Epi::kSpmvDot3>(A, a); break;
+  }
+}
+
+// ---- transpose ----------------------------------------------------------------------
+
+namespace {
+__global__ void k_count_cols(const idx* col, int64_t nnz, idx* cnt) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < nnz) atomicAdd(&cnt[col[k]], 1);
+}
+__global__ void k_scatter_transpose(const idx* rowptr, const idx* col, const double* val,
+                                    int64_t n_rows, const idx* trow, idx* cursor, idx* tcol,
+                                    double* tval) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_rows) return;
+  for (idx k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+    const idx j = col[k];
+    const idx p = trow[j] + atomicAdd(&cursor[j], 1);
+    tcol[p] = static_cast<idx>(i);
+    if (tval) tval[p] = val[k];
+  }
+}
+}  // namespace
+
+DevCsrPtr transpose(const DevCsr& A) {
+  auto T = std::make_shared<DevCsr>();
+  T->n_rows = A.n_cols;
+  T->n_cols = A.n_rows;
+  T->nnz = A.nnz;
+  T->rowptr.resize(A.n_cols + 1);
+  T->col.resize(A.nnz);
+  T->val.resize(A.nnz);
+  DevBuf<idx> cnt(A.n_cols), tmpc(A.nnz);
+  DevBuf<double> tmpv(A.nnz);
+  cnt.zero();
+  if (A.nnz > 0) AGG_LAUNCH(k_count_cols, grid_for(A.nnz, 256), 256, 0, A.col.get(), A.nnz, cnt.get());
+  scan_to_offsets_async(cnt.get(), T->rowptr.get(), A.n_cols);
+  cnt.zero();
+  if (A.n_rows > 0)
+    AGG_LAUNCH(k_scatter_transpose, grid_for(A.n_rows, 256), 256, 0, A.rowptr.get(), A.col.get(),
+               A.val.get(), A.n_rows, T->rowptr.get(), cnt.get(), tmpc.get(), tmpv.get());
+  segmented_sort(T->rowptr.get(), A.n_cols, tmpc.get(), T->col.get(), tmpv.get(), T->val.get());
+  T->plan();
+  return T;
+}
+
+// ---- generators ---------------------------------------------------------------------
+
+namespace {
+
+// Same stencil, ordering and arithmetic as poisson.cpp:32-75.
+__global__ void k_poisson_count(int64_t nx, int64_t ny, int64_t nz, idx* cnt) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nx * ny * nz) return;
+  const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
+  cnt[r] = 1 + (i > 0) + (i + 1 < nx) + (j > 0) + (j + 1 < ny) + (k > 0) + (k + 1 < nz);
+}
+__global__ void k_poisson_fill(int64_t nx, int64_t ny, int64_t nz, double cx, double cy, double cz,
+                               double diag, const idx* rowptr, idx* col, double* val) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nx * ny * nz) return;
+  const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
+  idx p = rowptr[r];
+  auto put = [&](int64_t c, double v) {
+    col[p] = static_cast<idx>(c);
+    val[p] = v;
+    ++p;
+  };
+  if (k > 0) put(r - nx * ny, cz);
+  if (j > 0) put(r - nx, cy);
+  if (i > 0) put(r - 1, cx);
+  put(r, diag);
+  if (i + 1 < nx) put(r + 1, cx);
+  if (j + 1 < ny) put(r + nx, cy);
+  if (k + 1 < nz) put(r + nx * ny, cz);
+}
+
+__device__ inline double jump_kappa(int64_t x, int64_t y, int64_t z, int64_t block, double jump) {
+  return (((x / block) + (y / block) + (z / block)) & 1) ? jump : 1.0;
+}
+
+__global__ void k_jump27_count(int64_t nx, int64_t ny, int64_t nz, idx* cnt) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nx * ny * nz) return;
+  const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
+  const int cxn = 1 + (i > 0) + (i + 1 < nx), cyn = 1 + (j > 0) + (j + 1 < ny),
+            czn = 1 + (k > 0) + (k + 1 < nz);
+  cnt[r] = cxn * cyn * czn;
+}
+
+// 27-point variable-coefficient operator: off-diagonal -kappa_ij with
+// kappa_ij = 2 k_i k_j / (k_i + k_j); diagonal = sum over the 26 neighbour slots of
+// kappa_ij (kappa_i for Dirichlet-eliminated slots), accumulated in slot order.
+__global__ void k_jump27_fill(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,
+                              const idx* rowptr, idx* col, double* val) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nx * ny * nz) return;
+  const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
+  const double ki = jump_kappa(i, j, k, block, jump);
+  double diag = 0.0;
+  idx p = rowptr[r];
+  idx pdiag = -1;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int64_t x = i + dx, y = j + dy, z = k + dz;
+        const bool inside = x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz;
+        if (dx == 0 && dy == 0 && dz == 0) {
+          pdiag = p;
+          col[p] = static_cast<idx>(r);
+          ++p;
+          continue;
+        }
+        if (!inside) {
+          diag = __dadd_rn(diag, ki);
+          continue;
+        }
+        const double kj = jump_kappa(x, y, z, block, jump);
+        const double kij = __ddiv_rn(__dmul_rn(__dmul_rn(2.0, ki), kj), __dadd_rn(ki, kj));
+        diag = __dadd_rn(diag, kij);
+        col[p] = static_cast<idx>((z * ny + y) * nx + x);
+        val[p] = -kij;
+        ++p;
+      }
+  val[pdiag] = diag;
+}
+
+}  // namespace
+
+DevCsrPtr generate_poisson_device(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
+                                  int weak_axis) {
+  require(dims == 2 || dims == 3, "poisson: dims must be 2 or 3");
+  if (dims == 2) nz = 1;
+  require(nx >= 1 && ny >= 1 && nz >= 1, "poisson: grid extents must be positive");
+  require(eps > 0.0, "poisson: epsilon must be positive");
+  int weak = weak_axis < 0 ? (dims == 2 ? 1 : 2) : weak_axis;
+  require(weak < dims, "poisson: weak axis " + std::to_string(weak) + " out of range for " +
+                           std::to_string(dims) + "D");
+  const int64_t n = nx * ny * nz;
+  const double cx = weak == 0 ? -eps : -1.0, cy = weak == 1 ? -eps : -1.0,
+               cz = weak == 2 ? -eps : -1.0;
+  const double diag = -2.0 * (cx + cy + (dims == 3 ? cz : 0.0));
+  auto A = std::make_shared<DevCsr>();
+  A->n_rows = A->n_cols = n;
+  A->rowptr.resize(n + 1);
+  DevBuf<idx> cnt(n);
+  AGG_LAUNCH(k_poisson_count, grid_for(n, 256), 256, 0, nx, ny, nz, cnt.get());
+  A->nnz = scan_to_offsets(cnt.get(), A->rowptr.get(), n);
+  A->col.resize(A->nnz);
+  A->val.resize(A->nnz);
+  AGG_LAUNCH(k_poisson_fill, grid_for(n, 256), 256, 0, nx, ny, nz, cx, cy, cz, diag,
+             A->rowptr.get(), A->col.get(), A->val.get());
+  A->plan();
+  return A;
+}
+
+DevCsrPtr generate_jump27_device(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block) {
+  require(nx >= 1 && ny >= 1 && nz >= 1 && block >= 1, "jump27: extents must be positive");
+  require(jump > 0.0, "jump27: jump must be positive");
+  const int64_t n = nx * ny * nz;
+  auto A = std::make_shared<DevCsr>();
+  A->n_rows = A->n_cols = n;
+  A->rowptr.resize(n + 1);
+  DevBuf<idx> cnt(n);
+  AGG_LAUNCH(k_jump27_count, grid_for(n, 256), 256, 0, nx, ny, nz, cnt.get());
+  A->nnz = scan_to_offsets(cnt.get(), A->rowptr.get(), n);
+  A->col.resize(A->nnz);
+  A->val.resize(A->nnz);
+  AGG_LAUNCH(k_jump27_fill, grid_for(n, 256), 256, 0, nx, ny, nz, jump, block, A->rowptr.get(),
+             A->col.get(), A->val.get());
+  A->plan();
+  return A;
+}
+
+}  // namespace aggmg_b200

@@ -1,0 +1,82 @@
+// sparse.cuh — device CSR and the CSR-stream SpMV family.
+//
+// Layout in HBM: row_offsets int32[n+1], col int32[nnz], val f64[nnz].
+//
+// SpMV = "CSR-stream with shared-memory staging": a block owns a run of
+// rows_per_block consecutive rows; its threads stream the run's contiguous
+// val/col range with 128-bit loads (2 doubles + 4 int32 per thread-step), multiply by
+// the gathered x and stage the products in shared memory; then one thread per row sums
+// its products sequentially in storage order.  That is exactly the reference's
+// row-sequential `sum += a * x` (sparse.cpp:57-62), so every SpMV-family kernel is
+// bit-identical to the CPU oracle (built without FMA).
+#pragma once
+
+#include <memory>
+
+#include "primitives.cuh"
+
+namespace aggmg_b200 {
+
+struct DevCsr {
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  DevBuf<idx> rowptr, col;
+  DevBuf<double> val;
+  int max_row = 0;         // longest row
+  int rows_per_block = 0;  // CSR-stream plan
+  int smem_entries = 0;
+
+  void plan();  // computes max_row / rows_per_block (synchronises)
+};
+using DevCsrPtr = std::shared_ptr<DevCsr>;
+
+// Upload a host int64 CSR; validates canonical form on the device with the
+// reference's messages (sparse.cpp:22-39).
+DevCsrPtr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, const int64_t* col,
+                     const double* val, bool validate);
+// Download to host int64 arrays (caller allocates).
+void download_csr(const DevCsr& A, int64_t* rowptr, int64_t* col, double* val);
+
+// ---- SpMV epilogues ---------------------------------------------------------------
+enum class Epi {
+  kSpmv,       // y = A x
+  kResidual,   // y = b - A x
+  kJacobi,     // y = x + wd .* (b - A x)          (wd = omega * inv_diag)
+  kScaleDiag,  // y = (A x) .* d                   (Arnoldi, smoother.cpp:53-54)
+  kSpmvDot2,   // y = A x ; dots (y.y, y.c) [gmres inner] or (x.y, x.c) [cg inner]
+  kSpmvDot3,   // y = A x ; dots (y.u, y.y, y.c) [gmres] or (x.u, x.y, x.c) [cg]
+  kSpmvDot1,   // y = A x ; dot (u . y)
+};
+
+struct SpmvArgs {
+  const double* x = nullptr;
+  double* y = nullptr;
+  const double* b = nullptr;   // residual / jacobi rhs
+  const double* d = nullptr;   // wd (jacobi) or inv_diag (scale)
+  const double* c = nullptr;   // second dot operand
+  const double* u = nullptr;   // third dot operand
+  int dot_with_x = 0;          // cg-style inner products use x instead of y
+  double* dots_out = nullptr;  // device slots for the dot results
+  const int* pred = nullptr;   // device predicate: skip the launch body when *pred == 0
+};
+
+void spmv_run(const DevCsr& A, Epi epi, const SpmvArgs& a, int prof_family = 0);
+
+inline void spmv(const DevCsr& A, const double* x, double* y, const int* pred = nullptr) {
+  SpmvArgs a;
+  a.x = x;
+  a.y = y;
+  a.pred = pred;
+  spmv_run(A, Epi::kSpmv, a);
+}
+
+// Transpose with values; output rows sorted (sparse.cpp:133-151).
+DevCsrPtr transpose(const DevCsr& A);
+
+// device Poisson / 27-point generators (poisson.cpp:15-77 semantics)
+DevCsrPtr generate_poisson_device(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
+                                  int weak_axis);
+DevCsrPtr generate_jump27_device(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block);
+
+double spmv_bytes(const DevCsr& A, Epi epi);
+
+}  // namespace aggmg_b200

@@ -1,0 +1,160 @@
+"""Solve-stage parity against the unmodified reference (oracle/_ref).  SpMV / smoothers /
+restriction / prolongation are bit-exact (row-sequential sums, no FMA); cycles and
+Krylov histories agree within 1e-10 relative (only dot-product summation order differs,
+SURVEY §8a rows a14-a20); outer iteration counts are equal."""
+import numpy as np
+import pytest
+
+from paper_1403_1649_b200 import aggmg as M
+
+from helpers import bits, laplacian_1d, max_rel, random_sparse, random_spd, rel_norm
+
+pytestmark = pytest.mark.gpu
+
+
+def test_spmv_bit_exact(gpu, ref):
+    rng = np.random.default_rng(0)
+    mats = [ref.generate_poisson(2, 33, 31), ref.generate_poisson(3, 17, 9, 11, 0.1),
+            random_sparse(300, 200, 0.05, 3), random_spd(257, 0.2, 5), laplacian_1d(1000),
+            random_sparse(50, 50, 0.9, 8), gpu.generate_jump27(9, 8, 7, 1e6, 2)]
+    for A in mats:
+        x = rng.uniform(-1, 1, A.n_cols)
+        np.testing.assert_array_equal(bits(gpu.spmv(A, x)), bits(ref.spmv(A, x)))
+
+
+def test_spmv_long_rows(gpu, ref):
+    # rows longer than one staging block (dense-ish rows of a coarse operator)
+    A = random_sparse(40, 9000, 0.6, 2)
+    x = np.random.default_rng(1).uniform(-1, 1, 9000)
+    np.testing.assert_array_equal(bits(gpu.spmv(A, x)), bits(ref.spmv(A, x)))
+
+
+def test_transpose(gpu, ref):
+    for s in range(3):
+        A = random_sparse(120, 90, 0.07, s)
+        T1, T2 = gpu.transpose(A), ref.transpose(A)
+        np.testing.assert_array_equal(T1.row_offsets, T2.row_offsets)
+        np.testing.assert_array_equal(T1.col_indices, T2.col_indices)
+        np.testing.assert_array_equal(bits(T1.values), bits(T2.values))
+
+
+def test_vector_ops(gpu, ref):
+    rng = np.random.default_rng(2)
+    for n in (1, 1000, 100_003):
+        a, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        assert abs(gpu.dot(a, b) - ref.dot(a, b)) <= 1e-13 * np.sum(np.abs(a * b))
+        assert abs(gpu.norm2(a) - ref.norm2(a)) <= 1e-14 * ref.norm2(a)
+        np.testing.assert_array_equal(bits(gpu.axpy(0.3, a, b)), bits(ref.axpy(0.3, a, b)))
+        np.testing.assert_array_equal(bits(gpu.scale(-1.7, a)), bits(ref.scale(-1.7, a)))
+
+
+def test_smoothers_bit_exact(gpu, ref):
+    rng = np.random.default_rng(4)
+    A = ref.generate_poisson(2, 20, 20)
+    s = ref.setup_smoother(A, M.DAMPED_JACOBI, 5, 9)
+    b, x = rng.uniform(-1, 1, A.n_rows), rng.uniform(-1, 1, A.n_rows)
+    for kind in (M.JACOBI, M.DAMPED_JACOBI, M.SGS):
+        st = M.SmootherState(kind, s.inv_diag, s.omega, s.rho_est)
+        np.testing.assert_array_equal(bits(gpu.smooth(st, A, b, x)), bits(ref.smooth(st, A, b, x)))
+
+
+CFGS = [M.CycleConfig(), M.CycleConfig(kind=M.CYCLE_V), M.CycleConfig(kind=M.CYCLE_K),
+        M.CycleConfig(inner=M.INNER_CG), M.CycleConfig(t=1e9), M.CycleConfig(t=0.0)]
+
+
+@pytest.mark.parametrize("ci", range(len(CFGS)))
+def test_preconditioner_matches(gpu, ref, ci):
+    A = ref.generate_poisson(2, 60, 60)
+    cfg = M.SetupConfig(coarse_size_max=40, reuse_caches=True)
+    hg, hr = gpu.setup_hierarchy(A, None, cfg), ref.setup_hierarchy(A, None, cfg)
+    r = np.random.default_rng(5).uniform(-1, 1, A.n_rows)
+    zg, zr = gpu.apply_preconditioner(hg, CFGS[ci], r), ref.apply_preconditioner(hr, CFGS[ci], r)
+    assert rel_norm(zg, zr) <= 1e-12
+
+
+def test_cycles_nonzero_guess(gpu, ref):
+    A = ref.generate_poisson(3, 12, 12, 12)
+    cfg = M.SetupConfig(alpha=0.5, coarse_size_max=30, reuse_caches=True)
+    hg, hr = gpu.setup_hierarchy(A, None, cfg), ref.setup_hierarchy(A, None, cfg)
+    rng = np.random.default_rng(6)
+    b, x = rng.uniform(-1, 1, A.n_rows), rng.uniform(-1, 1, A.n_rows)
+    assert rel_norm(gpu.vcycle(hg, 0, b, x), ref.vcycle(hr, 0, b, x)) <= 1e-12
+    cc = M.CycleConfig()
+    assert rel_norm(gpu.kcycle(hg, cc, 0, b, x), ref.kcycle(hr, cc, 0, b, x)) <= 1e-12
+    n1 = hg.levels[1].n
+    b1, x1 = rng.uniform(-1, 1, n1), np.zeros(n1)
+    assert rel_norm(gpu.vcycle(hg, 1, b1, x1), ref.vcycle(hr, 1, b1, x1)) <= 1e-12
+
+
+def check_solve(gpu, ref, A, alpha, method, tol=1e-8, cycle=None, restart=30):
+    cfg = M.SetupConfig(alpha=alpha, reuse_caches=True)
+    hg, hr = gpu.setup_hierarchy(A, None, cfg), ref.setup_hierarchy(A, None, cfg)
+    sc = M.SolverConfig(method=method, tol=tol, max_iters=500, restart=restart)
+    b = np.ones(A.n_rows)
+    f = gpu.pcg if method == M.PCG else gpu.fgmres
+    g = ref.pcg if method == M.PCG else ref.fgmres
+    rg, rr = f(A, b, None, hg, cycle, sc), g(A, b, None, hr, cycle, sc)
+    assert rg.report.iterations == rr.report.iterations
+    assert rg.report.converged == rr.report.converged
+    assert max_rel(rg.report.residual_history, rr.report.residual_history) <= 1e-10
+    assert rel_norm(rg.x, rr.x) <= 1e-10
+    return rg
+
+
+def test_pcg_2d(gpu, ref):
+    check_solve(gpu, ref, ref.generate_poisson(2, 128, 128), 0.25, M.PCG)
+
+
+def test_pcg_3d(gpu, ref):
+    check_solve(gpu, ref, ref.generate_poisson(3, 32, 32, 32), 0.5, M.PCG)
+
+
+def test_fgmres_3d_aniso(gpu, ref):
+    check_solve(gpu, ref, ref.generate_poisson(3, 32, 32, 32, 1e-3), 0.5, M.FGMRES)
+
+
+def test_fgmres_small_restart(gpu, ref):
+    check_solve(gpu, ref, ref.generate_poisson(2, 64, 64, 1, 0.01), 0.25, M.FGMRES, 1e-10,
+                M.CycleConfig(kind=M.CYCLE_V), restart=5)
+
+
+def test_unpreconditioned(gpu, ref):
+    A = random_spd(200, 0.05, 3)
+    b = np.random.default_rng(1).uniform(-1, 1, 200)
+    for name in ("pcg", "fgmres"):
+        sc = M.SolverConfig(method=M.PCG if name == "pcg" else M.FGMRES, tol=1e-10, max_iters=300,
+                            restart=20)
+        rg = getattr(gpu, name)(A, b, None, None, None, sc)
+        rr = getattr(ref, name)(A, b, None, None, None, sc)
+        assert rg.report.iterations == rr.report.iterations
+        assert max_rel(rg.report.residual_history, rr.report.residual_history) <= 1e-9
+
+
+def test_pcg_rejects_indefinite(gpu, ref):
+    A = M.SparseMatrix(2, 2, np.array([0, 1, 2]), np.array([0, 1]), np.array([1.0, -1.0]))
+    with pytest.raises(M.Error, match="use fgmres"):
+        gpu.pcg(A, np.array([1.0, 1.0]), None, None, None, M.SolverConfig(method=M.PCG))
+
+
+def test_setup_and_solve(gpu, ref):
+    A = ref.generate_poisson(3, 24, 24, 24)
+    s = M.SetupConfig(alpha=0.5, reuse_caches=True)
+    sc = M.SolverConfig(method=M.PCG, tol=1e-8, max_iters=500)
+    rg = gpu.setup_and_solve(A, np.ones(A.n_rows), s, M.CycleConfig(), sc)
+    rr = ref.setup_and_solve(A, np.ones(A.n_rows), s, M.CycleConfig(), sc)
+    assert rg.report.iterations == rr.report.iterations
+    assert max_rel(rg.report.residual_history, rr.report.residual_history) <= 1e-10
+
+
+def test_refresh_values(gpu, ref):
+    A = ref.generate_poisson(2, 40, 40)
+    cfg = M.SetupConfig(reuse_caches=True, coarse_size_max=30)
+    hg, hr = gpu.setup_hierarchy(A, None, cfg), ref.setup_hierarchy(A, None, cfg)
+    v = A.values * 2.0
+    gpu.refresh_values(hg, v)
+    ref.refresh_values(hr, v)
+    for k in range(hg.n_levels()):
+        np.testing.assert_array_equal(bits(hg.levels[k].A.values), bits(hr.levels[k].A.values))
+    h0 = gpu.setup_hierarchy(A, None, M.SetupConfig(coarse_size_max=30))
+    with pytest.raises(M.Error, match="without caches"):
+        gpu.refresh_values(h0, v)
