@@ -255,10 +255,14 @@ int aggmg_solve_device(const aggmg_hierarchy* h, const aggmg_cycle_config* cycle
 
 /* ---- measurement ------------------------------------------------------------------ */
 
-/* Per-kernel-family CUDA-event timing on the library stream (0 = off).  family ids are
- * listed in DESIGN.md (1 = level-0 smoother sweep, 2 = level-0 SpMV/residual). */
-int aggmg_profile_enable(int family);
+/* Per-kernel-family CUDA-event timing on the library stream.  mask has bit (1 << f) set
+ * for every timed family f (0 = off); ids in DESIGN.md (1 = level-0 damped-Jacobi sweep,
+ * 2 = level-0 SpMV / residual). */
+int aggmg_profile_enable(int mask);
 int aggmg_profile_read(int family, double* total_ms, int64_t* launches, double* bytes);
+/* device time on the library stream between the two calls (ms) */
+int aggmg_timer_start(void);
+int aggmg_timer_stop(double* ms);
 /* SpMV micro-benchmark on a device matrix: average ms per launch over `reps` launches */
 int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* bytes);
 

@@ -149,6 +149,8 @@ SIGNATURES = {
     "profile_enable": (I, [I]),
     "profile_read": (I, [I, f64p, i64p, f64p]),
     "bench_spmv": (I, [vp, I, f64p, f64p]),
+    "timer_start": (I, []),
+    "timer_stop": (I, [f64p]),
     "setup_config_default": (None, [C.POINTER(SetupConfigC)]),
     "cycle_config_default": (None, [C.POINTER(CycleConfigC)]),
     "solver_config_default": (None, [C.POINTER(SolverConfigC)]),

@@ -806,7 +806,9 @@ int aggmg_solve_device(const aggmg_hierarchy* h, const aggmg_cycle_config* cycle
 
 // ---- measurement ----------------------------------------------------------------------------
 
-int aggmg_profile_enable(int family) { return guarded([&] { profile_enable(family); }); }
+int aggmg_profile_enable(int mask) { return guarded([&] { profile_enable(mask); }); }
+int aggmg_timer_start(void) { return guarded([&] { timer_start(); }); }
+int aggmg_timer_stop(double* ms) { return guarded([&] { *ms = timer_stop(); }); }
 int aggmg_profile_read(int family, double* total_ms, int64_t* launches, double* bytes) {
   return guarded([&] { profile_read(family, total_ms, launches, bytes); });
 }

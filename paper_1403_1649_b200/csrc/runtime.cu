@@ -32,10 +32,12 @@ std::atomic<int64_t>& launches() {
 }
 
 struct ProfState {
-  int enabled = 0;
+  int mask = 0;  // bit f set: family f is timed
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
   std::vector<double> bytes;  // per recorded pair
+  std::vector<int> family;    // per recorded pair
   int used = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
 };
 ProfState& prof() {
   static ProfState p;
@@ -112,16 +114,18 @@ void check_launch(const char* file, int line) {
 
 // ---- profiling -------------------------------------------------------------------
 
-void profile_enable(int family) {
+void profile_enable(int mask) {
   ProfState& p = prof();
-  p.enabled = family;
+  sync();
+  p.mask = mask;
   p.used = 0;
   p.bytes.clear();
+  p.family.clear();
 }
 
 ProfileScope::ProfileScope(int family, double bytes) : family_(family), slot_(-1) {
   ProfState& p = prof();
-  if (p.enabled == 0 || p.enabled != family) return;
+  if (family <= 0 || !(p.mask & (1 << family))) return;
   if (p.used == static_cast<int>(p.pool.size())) {
     cudaEvent_t a, b;
     AGG_CUDA(cudaEventCreate(&a));
@@ -130,6 +134,7 @@ ProfileScope::ProfileScope(int family, double bytes) : family_(family), slot_(-1
   }
   slot_ = p.used++;
   p.bytes.push_back(bytes);
+  p.family.push_back(family);
   AGG_CUDA(cudaEventRecord(p.pool[slot_].first, stream()));
 }
 
@@ -143,18 +148,35 @@ void profile_read(int family, double* total_ms, int64_t* n, double* bytes) {
   sync();
   double ms = 0.0, by = 0.0;
   int64_t cnt = 0;
-  if (p.enabled == family) {
-    for (int i = 0; i < p.used; ++i) {
-      float t = 0.f;
-      AGG_CUDA(cudaEventElapsedTime(&t, p.pool[i].first, p.pool[i].second));
-      ms += t;
-      by += p.bytes[i];
-      ++cnt;
-    }
+  for (int i = 0; i < p.used; ++i) {
+    if (p.family[i] != family) continue;
+    float t = 0.f;
+    AGG_CUDA(cudaEventElapsedTime(&t, p.pool[i].first, p.pool[i].second));
+    ms += t;
+    by += p.bytes[i];
+    ++cnt;
   }
   if (total_ms) *total_ms = ms;
   if (n) *n = cnt;
   if (bytes) *bytes = by;
+}
+
+void timer_start() {
+  ProfState& p = prof();
+  if (!p.t0) {
+    AGG_CUDA(cudaEventCreate(&p.t0));
+    AGG_CUDA(cudaEventCreate(&p.t1));
+  }
+  AGG_CUDA(cudaEventRecord(p.t0, stream()));
+}
+
+double timer_stop() {
+  ProfState& p = prof();
+  AGG_CUDA(cudaEventRecord(p.t1, stream()));
+  AGG_CUDA(cudaEventSynchronize(p.t1));
+  float ms = 0.f;
+  AGG_CUDA(cudaEventElapsedTime(&ms, p.t0, p.t1));
+  return ms;
 }
 
 }  // namespace aggmg_b200

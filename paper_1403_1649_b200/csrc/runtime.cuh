@@ -85,7 +85,9 @@ struct ProfileScope {
   int family_;
   int slot_;
 };
-void profile_enable(int family);
+void profile_enable(int mask);  // bit (1 << family) per timed family
+void timer_start();
+double timer_stop();  // ms on the library stream since timer_start()
 void profile_read(int family, double* total_ms, int64_t* launches, double* bytes);
 int64_t launch_count();
 
