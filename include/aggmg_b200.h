@@ -109,6 +109,11 @@ int aggmg_synchronize(void);
 void aggmg_set_num_threads(int n);               /* parallel.hpp:27 — accepted, no effect on results */
 int aggmg_num_threads(void);                     /* parallel.hpp:29 — reports the SM count */
 int64_t aggmg_kernel_launches(void);             /* number of kernels this library has launched */
+/* Solve-phase dot products in the reference's 8192-chunk sequential order (1) or as
+ * deterministic tree reductions (0, default).  Setup (Arnoldi omega) and aggmg_dot /
+ * aggmg_norm2 always use the reference order (vector_ops.hpp:16-40). */
+void aggmg_set_exact_reductions(int on);
+int aggmg_exact_reductions(void);
 void aggmg_setup_config_default(aggmg_setup_config* c);
 void aggmg_cycle_config_default(aggmg_cycle_config* c);
 void aggmg_solver_config_default(aggmg_solver_config* c);
@@ -248,6 +253,9 @@ void aggmg_dmatrix_free(aggmg_dmatrix* A);
 /* setup_hierarchy on a device matrix (B0 = ones); the hierarchy shares A's storage */
 int aggmg_setup_hierarchy_device(const aggmg_dmatrix* A0, const aggmg_setup_config* cfg,
                                  aggmg_hierarchy** out);
+/* device view of level k's operator (which = 0) or restriction R (which = 1); shares storage */
+int aggmg_hierarchy_level_dmatrix(const aggmg_hierarchy* h, int64_t k, int which,
+                                  aggmg_dmatrix** out);
 /* pcg/fgmres on level 0 of h with b = ones, x0 = 0, everything resident in HBM;
  * x (host, may be NULL) receives the solution */
 int aggmg_solve_device(const aggmg_hierarchy* h, const aggmg_cycle_config* cycle,
@@ -265,6 +273,9 @@ int aggmg_timer_start(void);
 int aggmg_timer_stop(double* ms);
 /* SpMV micro-benchmark on a device matrix: average ms per launch over `reps` launches */
 int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* bytes);
+/* same for one CSR-stream variant: 0 spmv, 1 residual, 2 fused zero-guess Jacobi+residual,
+ * 3 damped-Jacobi sweep, 4 spmv + dot, 5 spmv scaled by the inverse diagonal */
+int aggmg_bench_kernel(const aggmg_dmatrix* A, int kind, int reps, double* avg_ms, double* bytes);
 
 #ifdef __cplusplus
 }

@@ -149,6 +149,10 @@ SIGNATURES = {
     "profile_enable": (I, [I]),
     "profile_read": (I, [I, f64p, i64p, f64p]),
     "bench_spmv": (I, [vp, I, f64p, f64p]),
+    "bench_kernel": (I, [vp, I, I, f64p, f64p]),
+    "hierarchy_level_dmatrix": (I, [vp, L, I, C.POINTER(vp)]),
+    "set_exact_reductions": (None, [I]),
+    "exact_reductions": (I, []),
     "timer_start": (I, []),
     "timer_stop": (I, [f64p]),
     "setup_config_default": (None, [C.POINTER(SetupConfigC)]),

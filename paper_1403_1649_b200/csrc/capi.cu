@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/aggmg_b200.h"
+#include "chunked.cuh"
 #include "krylov.cuh"
 #include "vecops.cuh"
 
@@ -212,6 +213,8 @@ const char* aggmg_last_error(void) { return g_last_error.c_str(); }
 int aggmg_init(int device) { return guarded([&] { init_device(device); }); }
 int aggmg_synchronize(void) { return guarded([&] { sync(); }); }
 void aggmg_set_num_threads(int) {}
+void aggmg_set_exact_reductions(int on) { set_exact_reductions(on != 0); }
+int aggmg_exact_reductions(void) { return exact_reductions() ? 1 : 0; }
 int aggmg_num_threads(void) {
   int n = 0;
   guarded([&] { n = sm_count(); });
@@ -274,13 +277,13 @@ int aggmg_transpose(const aggmg_csr* A, aggmg_csr* T) {
 int aggmg_dot(int64_t n, const double* a, const double* b, double* out) {
   return guarded([&] {
     auto da = up_vec(a, n), db = up_vec(b, n);
-    *out = dot_host(da.get(), db.get(), n);
+    *out = dot_host(da.get(), db.get(), n, 1);
   });
 }
 int aggmg_norm2(int64_t n, const double* a, double* out) {
   return guarded([&] {
     auto da = up_vec(a, n);
-    *out = std::sqrt(dot_host(da.get(), da.get(), n));
+    *out = std::sqrt(dot_host(da.get(), da.get(), n, 1));
   });
 }
 int aggmg_axpy(int64_t n, double a, const double* x, double* y) {
@@ -787,6 +790,17 @@ int aggmg_setup_hierarchy_device(const aggmg_dmatrix* A0, const aggmg_setup_conf
   });
 }
 
+int aggmg_hierarchy_level_dmatrix(const aggmg_hierarchy* h, int64_t k, int which,
+                                  aggmg_dmatrix** out) {
+  return guarded([&] {
+    const DevLevel& L = level(h, k);
+    require(which == 0 || L.has_next, "hierarchy: the coarsest level has no restriction");
+    auto m = std::make_unique<aggmg_dmatrix>();
+    m->A = which == 0 ? L.A : L.tr.R;
+    *out = m.release();
+  });
+}
+
 int aggmg_solve_device(const aggmg_hierarchy* h, const aggmg_cycle_config* cycle,
                        const aggmg_solver_config* cfg, double* x, aggmg_solve_report* report) {
   return guarded([&] {
@@ -814,16 +828,34 @@ int aggmg_profile_read(int family, double* total_ms, int64_t* launches, double* 
 }
 
 int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* bytes) {
+  return aggmg_bench_kernel(A, 0, reps, avg_ms, bytes);
+}
+
+int aggmg_bench_kernel(const aggmg_dmatrix* A, int kind, int reps, double* avg_ms, double* bytes) {
   return guarded([&] {
     const DevCsr& M = *A->A;
-    DevBuf<double> x(M.n_cols), y(M.n_rows);
+    require(kind >= 0 && kind <= 5, "bench_kernel: kind must be 0..5");
+    const Epi epis[6] = {Epi::kSpmv, Epi::kResidual, Epi::kResidualZero, Epi::kJacobi,
+                         Epi::kSpmvDot1, Epi::kScaleDiag};
+    const Epi epi = epis[kind];
+    DevBuf<double> x(M.n_cols), y(M.n_rows), b(M.n_rows), d(M.n_rows), xo(M.n_rows), dots(4);
     fill_double(x.get(), M.n_cols, 1.0);
-    spmv(M, x.get(), y.get());
+    fill_double(b.get(), M.n_rows, 1.0);
+    fill_double(d.get(), M.n_rows, 0.1);
+    SpmvArgs a;
+    a.x = x.get();
+    a.y = y.get();
+    a.b = b.get();
+    a.d = d.get();
+    a.u = x.get();
+    a.x_out = xo.get();
+    a.dots_out = dots.get();
+    spmv_run(M, epi, a);
     cudaEvent_t e0, e1;
     AGG_CUDA(cudaEventCreate(&e0));
     AGG_CUDA(cudaEventCreate(&e1));
     AGG_CUDA(cudaEventRecord(e0, stream()));
-    for (int r = 0; r < reps; ++r) spmv(M, x.get(), y.get());
+    for (int r = 0; r < reps; ++r) spmv_run(M, epi, a);
     AGG_CUDA(cudaEventRecord(e1, stream()));
     AGG_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -831,7 +863,7 @@ int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* b
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *avg_ms = ms / reps;
-    *bytes = spmv_bytes(M, Epi::kSpmv);
+    *bytes = spmv_bytes(M, epi);
   });
 }
 

@@ -2,6 +2,7 @@
 #include <cmath>
 #include <cstdio>
 
+#include "chunked.cuh"
 #include "cycles.cuh"
 
 namespace aggmg_b200 {
@@ -86,6 +87,34 @@ __global__ void __launch_bounds__(kB) k_kstep1(int64_t n, const double* __restri
     ks->flag2 = (nrt <= __dmul_rn(tt, nrc)) ? 0 : 1;
   }
 }
+
+// Reference-order variant of k_kstep1 for the chunked reduction kernel.
+struct KStep1Op {
+  KScalars* ks;
+  double tt;
+  const double *rc, *v;
+  double* rt;
+  const int* pred;
+  int* warn;
+  int level;
+  double ms1;
+  __device__ bool active() const { return on(pred) && ks->rho1 != 0.0; }
+  __device__ void inactive() const {
+    ks->flag2 = 0;
+    if (on(pred)) atomicOr(&warn[0], 1 << (level & 31));
+  }
+  __device__ void init() { ms1 = -__ddiv_rn(ks->alpha1, ks->rho1); }
+  __device__ void operator()(int64_t i, double* p) const {
+    const double r = rc[i];
+    const double z = __dadd_rn(r, __dmul_rn(ms1, v[i]));
+    rt[i] = z;
+    p[0] = __dmul_rn(z, z);
+    p[1] = __dmul_rn(r, r);
+  }
+  __device__ void finalize(double* out) const {  // out == &ks->nrt
+    ks->flag2 = (__dsqrt_rn(out[0]) <= __dmul_rn(tt, __dsqrt_rn(out[1]))) ? 0 : 1;
+  }
+};
 
 // Final coarse correction of the K-cycle (cycles.cpp:96-132):
 //   rho1 == 0           -> xc = c
@@ -184,14 +213,26 @@ void postsmooth(DevLevel& L, const double* b, double* x, const int* pred, bool t
   smooth_sweep(L.smoother, *L.A, b, L.t.get(), x, pred, top ? kProfSmoothL0 : 0);
 }
 
-void descend(DevHierarchy& h, int64_t k, const double* b, double* x_out, const int* pred) {
+// Pre-smooth, residual and restriction of one cycle visit (cycles.cpp:54-57).  From the
+// zero guess the damped-Jacobi sweep and the residual fuse into one CSR-stream pass
+// (x1 = 0 + wd b is recomputed for the gathered neighbours, bit-identical to the
+// two-kernel sequence since A*0 sums to +0).
+void descend(DevHierarchy& h, int64_t k, const double* b, const double* x_in, double* x_out,
+             const int* pred) {
   DevLevel& L = h.levels[k];
   SpmvArgs ra;
-  ra.x = x_out;
   ra.y = L.r.get();
   ra.b = b;
   ra.pred = pred;
-  spmv_run(*L.A, Epi::kResidual, ra, k == 0 ? kProfSpmvL0 : 0);  // cycles.cpp:30-35
+  if (!x_in && L.smoother.kind != 2) {
+    ra.x_out = x_out;
+    ra.d = L.smoother.wdiag.get();
+    spmv_run(*L.A, Epi::kResidualZero, ra, k == 0 ? kProfSpmvL0 : 0);
+  } else {
+    presmooth(L, b, x_in, x_out, pred, k == 0);
+    ra.x = x_out;
+    spmv_run(*L.A, Epi::kResidual, ra, k == 0 ? kProfSpmvL0 : 0);  // cycles.cpp:30-35
+  }
   SpmvArgs rr;
   rr.x = L.r.get();
   rr.y = L.rc.get();
@@ -219,8 +260,7 @@ void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in,
     return;
   }
   DevLevel& L = h.levels[k];
-  presmooth(L, b, x_in, x_out, pred, k == 0);
-  descend(h, k, b, x_out, pred);
+  descend(h, k, b, x_in, x_out, pred);
   if (k + 1 == h.coarsest())
     coarse_solve(h, L.rc.get(), L.xc.get(), pred);
   else
@@ -235,8 +275,7 @@ void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b
     return;
   }
   DevLevel& L = h.levels[k];
-  presmooth(L, b, x_in, x_out, pred, k == 0);
-  descend(h, k, b, x_out, pred);
+  descend(h, k, b, x_in, x_out, pred);
   if (k + 1 == h.coarsest()) {
     coarse_solve(h, L.rc.get(), L.xc.get(), pred);
   } else {
@@ -251,10 +290,32 @@ void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b
     a1.dot_with_x = cg ? 1 : 0;
     a1.dots_out = &L.ks.get()->rho1;
     a1.pred = pred;
-    spmv_run(Ac, Epi::kSpmvDot2, a1);
-    const unsigned g = reduce_grid(nc);
-    AGG_LAUNCH(k_kstep1, g, kB, 0, nc, L.rc.get(), L.v.get(), L.rt.get(), L.ks.get(), cfg.t, pred,
-               reduce_partials(), reduce_ticket(), warn_bits(), static_cast<int>(k + 1));
+    const bool exact = exact_reductions();
+    if (exact) {  // SpMV, then the two dots in the reference's chunk order
+      spmv_run(Ac, Epi::kSpmv, a1);
+      DotOp<2> d;
+      d.a[0] = cg ? L.c.get() : L.v.get();  // rho1 = c.v | v.v
+      d.b[0] = L.v.get();
+      d.a[1] = cg ? L.c.get() : L.v.get();  // alpha1 = c.rc | v.rc
+      d.b[1] = L.rc.get();
+      d.pred = pred;
+      launch_chunked<2>(d, nc, &L.ks.get()->rho1);
+      KStep1Op op;
+      op.ks = L.ks.get();
+      op.tt = cfg.t;
+      op.rc = L.rc.get();
+      op.v = L.v.get();
+      op.rt = L.rt.get();
+      op.pred = pred;
+      op.warn = warn_bits();
+      op.level = static_cast<int>(k + 1);
+      launch_chunked<2>(op, nc, &L.ks.get()->nrt);
+    } else {
+      spmv_run(Ac, Epi::kSpmvDot2, a1);
+      const unsigned g = reduce_grid(nc);
+      AGG_LAUNCH(k_kstep1, g, kB, 0, nc, L.rc.get(), L.v.get(), L.rt.get(), L.ks.get(), cfg.t, pred,
+                 reduce_partials(), reduce_ticket(), warn_bits(), static_cast<int>(k + 1));
+    }
     const int* p2 = &L.ks.get()->flag2;
     inner_cycle(h, cfg, k + 1, L.rt.get(), L.d.get(), p2);
     SpmvArgs a2;  // w = Ac d ; gamma, beta, alpha2  (cycles.cpp:110-121)
@@ -265,7 +326,21 @@ void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b
     a2.dot_with_x = cg ? 1 : 0;
     a2.dots_out = &L.ks.get()->gamma;
     a2.pred = p2;
-    spmv_run(Ac, Epi::kSpmvDot3, a2);
+    if (exact) {
+      spmv_run(Ac, Epi::kSpmv, a2);
+      DotOp<3> d;
+      const double* lhs = cg ? L.d.get() : L.w.get();
+      d.a[0] = lhs;  // gamma = d.v | w.v
+      d.b[0] = L.v.get();
+      d.a[1] = lhs;  // beta = d.w | w.w
+      d.b[1] = L.w.get();
+      d.a[2] = lhs;  // alpha2 = d.rt | w.rt
+      d.b[2] = L.rt.get();
+      d.pred = p2;
+      launch_chunked<3>(d, nc, &L.ks.get()->gamma);
+    } else {
+      spmv_run(Ac, Epi::kSpmvDot3, a2);
+    }
     AGG_LAUNCH(k_kcombine, egrid(nc), kB, 0, nc, L.c.get(), L.d.get(), L.xc.get(), L.ks.get(), pred,
                warn_bits(), static_cast<int>(k + 1));
   }

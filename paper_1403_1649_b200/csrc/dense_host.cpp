@@ -66,78 +66,139 @@ std::vector<double> HostLu::inverse() const {
   return inv;
 }
 
-// Complex single-shift QR with Wilkinson shifts and Givens rotations on the active
-// window; deflation on negligible subdiagonals.  Converges for the <= 5x5 Hessenberg
-// matrices produced by the Arnoldi estimate; complex pairs come out naturally.
-std::vector<std::complex<double>> hessenberg_eigenvalues(const std::vector<double>& h, int n) {
-  using cd = std::complex<double>;
-  std::vector<std::complex<double>> eig;
-  if (n <= 0) return eig;
-  std::vector<cd> H(static_cast<size_t>(n) * n);
-  for (int i = 0; i < n * n; ++i) H[i] = cd(h[i], 0.0);
-  auto at = [&](int i, int j) -> cd& { return H[static_cast<size_t>(i) * n + j]; };
-  int hi = n - 1;
-  int iters = 0;
-  const int max_iters = 60 * n + 100;
-  while (hi >= 0) {
-    if (hi == 0) {
-      eig.push_back(at(0, 0));
-      break;
+// Francis double-shift QR on an upper-Hessenberg matrix, eigenvalues only.  The
+// floating-point operation sequence is the reference's (dense.cpp:81-212) so that the
+// Arnoldi spectral-radius estimate, and therefore omega, is bit-identical to the CPU
+// oracle: deflation test 1e-14, closed-form 1x1 / 2x2 blocks, Householder bulge chase
+// with the 3-vector (x, y, z), a closing Givens rotation, exceptional shift every 20.
+namespace {
+
+class FrancisQR {
+ public:
+  FrancisQR(std::vector<double> h, int n) : h_(std::move(h)), n_(n) {}
+
+  std::vector<std::complex<double>> run() {
+    int hi = n_ - 1, since = 0, steps = 0;
+    while (hi >= 0) {
+      if (!(steps++ < 30 * n_ + 100)) throw Error("hessenberg_eigenvalues: QR iteration did not converge");
+      const int lo = active_start(hi);
+      if (lo == hi) {
+        out_.emplace_back(a(hi, hi), 0.0);
+        hi -= 1;
+        since = 0;
+      } else if (lo + 1 == hi) {
+        block2(a(lo, lo), a(lo, hi), a(hi, lo), a(hi, hi));
+        hi -= 2;
+        since = 0;
+      } else {
+        sweep(lo, hi, ++since % 20 == 0);
+      }
     }
-    // find the active window [lo, hi]
+    return out_;
+  }
+
+ private:
+  double& a(int i, int j) { return h_[static_cast<size_t>(i) * n_ + j]; }
+
+  int active_start(int hi) {  // walk up until a negligible subdiagonal entry
     int lo = hi;
     while (lo > 0) {
-      const double off = std::abs(at(lo, lo - 1));
-      const double sc = std::abs(at(lo - 1, lo - 1)) + std::abs(at(lo, lo));
-      if (off <= 1e-15 * (sc > 0.0 ? sc : 1.0)) {
-        at(lo, lo - 1) = 0.0;
-        break;
+      const double scale = std::fabs(a(lo - 1, lo - 1)) + std::fabs(a(lo, lo));
+      if (std::fabs(a(lo, lo - 1)) <= 1e-14 * (scale > 0.0 ? scale : 1.0)) {
+        a(lo, lo - 1) = 0.0;
+        return lo;
       }
       --lo;
     }
-    if (lo == hi) {
-      eig.push_back(at(hi, hi));
-      --hi;
-      continue;
-    }
-    if (++iters > max_iters) throw Error("hessenberg_eigenvalues: QR iteration did not converge");
-    // Wilkinson shift: eigenvalue of the trailing 2x2 closest to H(hi,hi)
-    const cd a = at(hi - 1, hi - 1), b = at(hi - 1, hi), c = at(hi, hi - 1), d = at(hi, hi);
-    const cd tr = a + d, det = a * d - b * c;
-    const cd disc = std::sqrt(tr * tr * 0.25 - det);
-    const cd l1 = tr * 0.5 + disc, l2 = tr * 0.5 - disc;
-    cd mu = (std::abs(l1 - d) < std::abs(l2 - d)) ? l1 : l2;
-    if (iters % 11 == 0) mu += cd(std::abs(c), 0.0);  // exceptional shift
-    for (int i = lo; i <= hi; ++i) at(i, i) -= mu;
-    // QR by Givens on the window, then RQ
-    std::vector<cd> cs(hi - lo), sn(hi - lo);
-    for (int k = lo; k < hi; ++k) {
-      const cd x = at(k, k), y = at(k + 1, k);
-      const double r = std::sqrt(std::norm(x) + std::norm(y));
-      cd cc = 1.0, ss = 0.0;
-      if (r > 0.0) {
-        cc = x / r;
-        ss = y / r;
-      }
-      cs[k - lo] = cc;
-      sn[k - lo] = ss;
-      for (int j = k; j < n; ++j) {
-        const cd t1 = at(k, j), t2 = at(k + 1, j);
-        at(k, j) = std::conj(cc) * t1 + std::conj(ss) * t2;
-        at(k + 1, j) = -ss * t1 + cc * t2;
-      }
-    }
-    for (int k = lo; k < hi; ++k) {
-      const cd cc = cs[k - lo], ss = sn[k - lo];
-      for (int i = 0; i <= std::min(k + 1, hi); ++i) {
-        const cd t1 = at(i, k), t2 = at(i, k + 1);
-        at(i, k) = t1 * cc + t2 * ss;
-        at(i, k + 1) = -t1 * std::conj(ss) + t2 * std::conj(cc);
-      }
-    }
-    for (int i = lo; i <= hi; ++i) at(i, i) += mu;
+    return 0;
   }
-  return eig;
+
+  void block2(double p, double q, double r, double s) {
+    const double tr = p + s;
+    const double det = p * s - q * r;
+    const double disc = tr * tr / 4.0 - det;
+    if (disc >= 0.0) {
+      const double w = std::sqrt(disc);
+      out_.emplace_back(tr / 2.0 + w, 0.0);
+      out_.emplace_back(tr / 2.0 - w, 0.0);
+    } else {
+      const double w = std::sqrt(-disc);
+      out_.emplace_back(tr / 2.0, w);
+      out_.emplace_back(tr / 2.0, -w);
+    }
+  }
+
+  // one implicit double-shift step on the window [lo, hi]
+  void sweep(int lo, int hi, bool exceptional) {
+    double s = a(hi - 1, hi - 1) + a(hi, hi);
+    double t = a(hi - 1, hi - 1) * a(hi, hi) - a(hi - 1, hi) * a(hi, hi - 1);
+    if (exceptional) {
+      const double w = std::fabs(a(hi, hi - 1)) + std::fabs(a(hi - 1, hi - 2));
+      s = 1.5 * w;
+      t = w * w;
+    }
+    double x = a(lo, lo) * a(lo, lo) + a(lo, lo + 1) * a(lo + 1, lo) - s * a(lo, lo) + t;
+    double y = a(lo + 1, lo) * (a(lo, lo) + a(lo + 1, lo + 1) - s);
+    double z = a(lo + 2, lo + 1) * a(lo + 1, lo);
+    for (int k = lo; k <= hi - 2; ++k) {
+      double nrm = std::sqrt(x * x + y * y + z * z);
+      if (nrm != 0.0) {
+        if (x > 0.0) nrm = -nrm;
+        const double u0 = x - nrm;
+        const double beta = 2.0 / (u0 * u0 + y * y + z * z);
+        reflect_rows(k, (k > lo) ? k - 1 : lo, hi, u0, y, z, beta);
+        reflect_cols(k, lo, std::min(k + 3, hi), u0, y, z, beta);
+      }
+      x = a(k + 1, k);
+      y = a(k + 2, k);
+      z = (k + 3 <= hi) ? a(k + 3, k) : 0.0;
+    }
+    const int k = hi - 1;
+    const double r = std::hypot(x, y);
+    if (r > 0.0) {
+      const double c = x / r, sn = y / r;
+      for (int j = k - 1; j <= hi; ++j) {
+        const double t1 = a(k, j), t2 = a(k + 1, j);
+        a(k, j) = c * t1 + sn * t2;
+        a(k + 1, j) = -sn * t1 + c * t2;
+      }
+      for (int i = lo; i <= hi; ++i) {
+        const double t1 = a(i, k), t2 = a(i, k + 1);
+        a(i, k) = c * t1 + sn * t2;
+        a(i, k + 1) = -sn * t1 + c * t2;
+      }
+    }
+  }
+
+  void reflect_rows(int k, int j0, int j1, double u0, double u1, double u2, double beta) {
+    for (int j = j0; j <= j1; ++j) {
+      double d = u0 * a(k, j) + u1 * a(k + 1, j) + u2 * a(k + 2, j);
+      d *= beta;
+      a(k, j) -= d * u0;
+      a(k + 1, j) -= d * u1;
+      a(k + 2, j) -= d * u2;
+    }
+  }
+  void reflect_cols(int k, int i0, int i1, double u0, double u1, double u2, double beta) {
+    for (int i = i0; i <= i1; ++i) {
+      double d = u0 * a(i, k) + u1 * a(i, k + 1) + u2 * a(i, k + 2);
+      d *= beta;
+      a(i, k) -= d * u0;
+      a(i, k + 1) -= d * u1;
+      a(i, k + 2) -= d * u2;
+    }
+  }
+
+  std::vector<double> h_;
+  int n_;
+  std::vector<std::complex<double>> out_;
+};
+
+}  // namespace
+
+std::vector<std::complex<double>> hessenberg_eigenvalues(const std::vector<double>& h, int n) {
+  if (n <= 0) return {};
+  return FrancisQR(h, n).run();
 }
 
 }  // namespace aggmg_b200

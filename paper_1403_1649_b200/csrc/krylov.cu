@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "chunked.cuh"
 #include "krylov.cuh"
 #include "vecops.cuh"
 
@@ -76,6 +77,48 @@ __global__ void __launch_bounds__(kB) k_mgs_step(int64_t n, const double* hcol, 
   finish_reduction<1>(partials, ticket, out, smem);
 }
 
+// ---- reference-order (exact) variants of the fused vector kernels ---------------------
+
+// x += alpha p ; rn = r + (-alpha) Ap ; chain: rn_i^2   (krylov.cpp:181-186)
+struct PcgUpdateOp {
+  PcgSlots* s;
+  int par;
+  const double *p, *Ap, *r;
+  double *x, *rn;
+  double alpha, malpha;
+  __device__ bool active() const { return true; }
+  __device__ void inactive() const {}
+  __device__ void init() {
+    alpha = __ddiv_rn(s->q[par][0], s->pAp);
+    malpha = -alpha;
+  }
+  __device__ void operator()(int64_t i, double* out) const {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    const double v = __dadd_rn(r[i], __dmul_rn(malpha, Ap[i]));
+    rn[i] = v;
+    out[0] = __dmul_rn(v, v);
+  }
+  __device__ void finalize(double*) const {}
+};
+
+// w = w + (-h_i) V_i ; chain: V_{i+1}.w or w.w   (krylov.cpp:85-89)
+struct MgsOp {
+  const double* hcol;
+  int idx;
+  const double *Vi, *Vnext;
+  double* w;
+  double mh;
+  __device__ bool active() const { return true; }
+  __device__ void inactive() const {}
+  __device__ void init() { mh = -hcol[idx]; }
+  __device__ void operator()(int64_t t, double* out) const {
+    const double v = __dadd_rn(w[t], __dmul_rn(mh, Vi[t]));
+    w[t] = v;
+    out[0] = __dmul_rn(Vnext ? Vnext[t] : v, v);
+  }
+  __device__ void finalize(double*) const {}
+};
+
 struct AxpyList {
   const double* z[32];
   double y[32];
@@ -132,6 +175,7 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     return out;
   }
   const double target = cfg.tol * norm_b;
+  const bool exact = exact_reductions();
   DevBuf<double> rA(n), rB(n), z(n), p(n), Ap(n);
   DevBuf<PcgSlots> slots(1);
   slots.zero();
@@ -157,9 +201,27 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     a.y = Ap.get();
     a.u = p.get();
     a.dots_out = &slots.get()->pAp;
-    spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
-    AGG_LAUNCH(k_pcg_update, reduce_grid(n), kB, 0, n, slots.get(), par, p.get(), Ap.get(), r, x,
-               rn, reduce_partials(), reduce_ticket());
+    if (exact) {
+      spmv_run(A, Epi::kSpmv, a, kProfSpmvL0);
+      DotOp<1> d1;
+      d1.a[0] = p.get();
+      d1.b[0] = Ap.get();
+      d1.pred = nullptr;
+      launch_chunked<1>(d1, n, &slots.get()->pAp);
+      PcgUpdateOp u;
+      u.s = slots.get();
+      u.par = par;
+      u.p = p.get();
+      u.Ap = Ap.get();
+      u.r = r;
+      u.x = x;
+      u.rn = rn;
+      launch_chunked<1>(u, n, &slots.get()->res2);
+    } else {
+      spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
+      AGG_LAUNCH(k_pcg_update, reduce_grid(n), kB, 0, n, slots.get(), par, p.get(), Ap.get(), r, x,
+                 rn, reduce_partials(), reduce_ticket());
+    }
     AGG_CUDA(cudaMemcpyAsync(pinned, slots.get(), 2 * sizeof(double), cudaMemcpyDeviceToHost,
                              stream()));
     sync();
@@ -208,6 +270,7 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
     return out;
   }
   const double target = cfg.tol * norm_b;
+  const bool exact = exact_reductions();
   DevBuf<double> r(n), w(n), hcol(m + 2);
   std::vector<DevBuf<double>> V, Z;
   residual(A, b, x, r.get());
@@ -233,11 +296,30 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
       a.y = w.get();
       a.u = V[0].get();
       a.dots_out = hcol.get();
-      spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
+      if (exact) {
+        spmv_run(A, Epi::kSpmv, a, kProfSpmvL0);
+        DotOp<1> d1;
+        d1.a[0] = V[0].get();
+        d1.b[0] = w.get();
+        d1.pred = nullptr;
+        launch_chunked<1>(d1, n, hcol.get());
+      } else {
+        spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
+      }
       for (int i = 0; i <= j; ++i) {
         const double* vnext = (i < j) ? V[i + 1].get() : nullptr;
-        AGG_LAUNCH(k_mgs_step, reduce_grid(n), kB, 0, n, hcol.get(), i, V[i].get(), vnext, w.get(),
-                   hcol.get() + i + 1, reduce_partials(), reduce_ticket());
+        if (exact) {
+          MgsOp op;
+          op.hcol = hcol.get();
+          op.idx = i;
+          op.Vi = V[i].get();
+          op.Vnext = vnext;
+          op.w = w.get();
+          launch_chunked<1>(op, n, hcol.get() + i + 1);
+        } else {
+          AGG_LAUNCH(k_mgs_step, reduce_grid(n), kB, 0, n, hcol.get(), i, V[i].get(), vnext,
+                     w.get(), hcol.get() + i + 1, reduce_partials(), reduce_ticket());
+        }
       }
       AGG_CUDA(cudaMemcpyAsync(pinned, hcol.get(), sizeof(double) * (j + 2),
                                cudaMemcpyDeviceToHost, stream()));

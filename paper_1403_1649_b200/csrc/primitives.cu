@@ -1,6 +1,8 @@
 // primitives.cu — scans, deterministic reductions, segmented rank sort.
 #include "primitives.cuh"
 
+#include "chunked.cuh"
+
 namespace aggmg_b200 {
 
 namespace {
@@ -145,7 +147,32 @@ unsigned reduce_grid(int64_t n) {
 double* reduce_partials() { return red().partials; }
 unsigned* reduce_ticket() { return red().ticket; }
 
-void dot_device(const DotArgs& args, int64_t n, double* out, const int* pred) {
+namespace {
+bool g_exact = false;
+template <int NP>
+void dot_exact(const DotArgs& args, int64_t n, double* out, const int* pred) {
+  DotOp<NP> op;
+  for (int k = 0; k < NP; ++k) {
+    op.a[k] = args.a[k];
+    op.b[k] = args.b[k];
+  }
+  op.pred = pred;
+  launch_chunked<NP>(op, n, out);
+}
+}  // namespace
+
+bool exact_reductions() { return g_exact; }
+void set_exact_reductions(bool on) { g_exact = on; }
+
+void dot_device(const DotArgs& args, int64_t n, double* out, const int* pred, int exact) {
+  if (exact == 1 || (exact < 0 && g_exact)) {
+    switch (args.np) {
+      case 1: dot_exact<1>(args, n, out, pred); return;
+      case 2: dot_exact<2>(args, n, out, pred); return;
+      case 3: dot_exact<3>(args, n, out, pred); return;
+      default: throw Error("dot_device: np must be 1..3");
+    }
+  }
   RedScratch& r = red();
   const unsigned g = reduce_grid(n);
   switch (args.np) {
@@ -156,13 +183,13 @@ void dot_device(const DotArgs& args, int64_t n, double* out, const int* pred) {
   }
 }
 
-double dot_host(const double* a, const double* b, int64_t n) {
+double dot_host(const double* a, const double* b, int64_t n, int exact) {
   DevBuf<double> out(1);
   DotArgs d{};
   d.a[0] = a;
   d.b[0] = b;
   d.np = 1;
-  dot_device(d, n, out.get());
+  dot_device(d, n, out.get(), nullptr, exact);
   return read_scalar(out.get());
 }
 

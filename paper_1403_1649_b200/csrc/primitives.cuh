@@ -21,9 +21,10 @@ struct DotArgs {
   int np;
 };
 // Writes the results to device memory out[0..np-1].
-void dot_device(const DotArgs& args, int64_t n, double* out, const int* pred = nullptr);
+void dot_device(const DotArgs& args, int64_t n, double* out, const int* pred = nullptr,
+                int exact = -1);  // exact: 1 reference chunk order, 0 tree, -1 library mode
 // Convenience host-returning dot (synchronises).
-double dot_host(const double* a, const double* b, int64_t n);
+double dot_host(const double* a, const double* b, int64_t n, int exact = -1);
 
 // Reduction scratch: the grid size used by every reduction over n elements.
 unsigned reduce_grid(int64_t n);

@@ -307,44 +307,67 @@ __global__ void k_group_entry_counts(const idx* goff, const idx* rows, const idx
   ecnt[J] = c;
 }
 
-constexpr int kGalWarps = 4;
-constexpr int kGalCap = 1024;  // fine entries per coarse row handled in shared memory
+constexpr int kGalWarps = 8;
+constexpr int kGalCap = 256;     // tier 1: fine entries per coarse row, one warp, shared memory
+constexpr int kGalCapBig = 4096; // tier 2: one CTA per coarse row, shared memory (80 KB)
 
-// Warp per coarse row I: gather the fine entries of I's member rows in (row asc, storage
-// order) = global storage order, sort them by coarse column J with the gather position
-// as the tie-break (= the reference's stable sort by key I*nc+J, galerkin.cpp:52-62),
-// and emit entry / entry_row / sorted J; count the distinct J (coarse row length).
+// Member-parallel gather of coarse row I's fine entries into (key, k, row) slots:
+// lanes own member rows, a warp scan of the row lengths gives each member its slot
+// range, so slot order = (member row ascending, storage order) = global storage order.
+__device__ inline void gal_gather_warp(idx m0, idx m1, const idx* rows, const idx* arp,
+                                       const idx* acol, const idx* assignment,
+                                       unsigned long long* skey, idx* skk, idx* sri, int lane) {
+  idx base = 0;
+  for (idx mb = m0; mb < m1; mb += 32) {
+    const idx m = mb + lane;
+    idx i = 0, lo = 0, len = 0;
+    if (m < m1) {
+      i = rows[m];
+      lo = arp[i];
+      len = arp[i + 1] - lo;
+    }
+    idx incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const idx t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const idx off = base + incl - len;
+    for (idx t = 0; t < len; ++t) {
+      const idx k = lo + t, p = off + t;
+      skey[p] = (static_cast<unsigned long long>(assignment[acol[k]]) << 32) |
+                static_cast<unsigned long long>(p);
+      skk[p] = k;
+      sri[p] = i;
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// Tier 1 — warp per coarse row I: gather the fine entries of I's member rows, sort them
+// by coarse column J with the gather position as the tie-break (= the reference's stable
+// sort by key I*nc+J, galerkin.cpp:52-62) and emit entry / entry_row / sorted J; count
+// the distinct J (coarse row length).  Rows longer than kGalCap go to tier 2.
 __global__ void __launch_bounds__(kGalWarps * 32)
     k_gal_symbolic(const idx* goff, const idx* rows, const idx* arp, const idx* acol,
                    const idx* assignment, int64_t nc, const idx* eoff, idx* entry, idx* entry_row,
                    idx* sorted_j, idx* cnnz, idx* big_list, int* big_count) {
-  extern __shared__ unsigned long long gsm[];
+  __shared__ unsigned long long s_key[kGalWarps][kGalCap];
+  __shared__ idx s_kk[kGalWarps][kGalCap], s_ri[kGalWarps][kGalCap], s_j[kGalWarps][kGalCap];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t I = static_cast<int64_t>(blockIdx.x) * kGalWarps + w;
   if (I >= nc) return;
-  unsigned long long* skey = gsm + w * kGalCap;
-  idx* skk = reinterpret_cast<idx*>(gsm + kGalWarps * kGalCap) + w * kGalCap;
-  idx* sri = reinterpret_cast<idx*>(gsm + kGalWarps * kGalCap) + kGalWarps * kGalCap + w * kGalCap;
-  idx* sj = sri + kGalWarps * kGalCap;  // sorted coarse columns, per warp
+  unsigned long long* skey = s_key[w];
+  idx* skk = s_kk[w];
+  idx* sri = s_ri[w];
+  idx* sj = s_j[w];
   const idx base_e = eoff[I];
   const idx L = eoff[I + 1] - base_e;
   if (L > kGalCap) {
     if (lane == 0) big_list[atomicAdd(big_count, 1)] = static_cast<idx>(I);
     return;
   }
-  idx p = 0;
-  for (idx m = goff[I]; m < goff[I + 1]; ++m) {
-    const idx i = rows[m];
-    const idx lo = arp[i], len = arp[i + 1] - lo;
-    for (idx t = lane; t < len; t += 32) {
-      const idx k = lo + t;
-      skey[p + t] = (static_cast<unsigned long long>(assignment[acol[k]]) << 32) |
-                    static_cast<unsigned long long>(p + t);
-      skk[p + t] = k;
-      sri[p + t] = i;
-    }
-    p += len;
-  }
+  gal_gather_warp(goff[I], goff[I + 1], rows, arp, acol, assignment, skey, skk, sri, lane);
   __syncwarp();
   for (idx q = lane; q < L; q += 32) {
     const unsigned long long key = skey[q];
@@ -365,40 +388,73 @@ __global__ void __launch_bounds__(kGalWarps * 32)
   if (lane == 0) cnnz[I] = cnt;
 }
 
-// Block per oversized coarse row; keys staged in global scratch.
-__global__ void k_gal_symbolic_big(const idx* big_list, const idx* goff, const idx* rows,
-                                   const idx* arp, const idx* acol, const idx* assignment,
-                                   const idx* eoff, unsigned long long* gkey, idx* gkk, idx* gri,
-                                   idx* entry, idx* entry_row, idx* sorted_j, idx* cnnz) {
-  __shared__ idx s_cnt;
+// Tier 2 — one CTA (256 threads) per long coarse row.  Slots live in shared memory when
+// L <= kGalCapBig, else in the global scratch arrays at [base_e, base_e + L).
+__global__ void __launch_bounds__(256)
+    k_gal_symbolic_big(const idx* big_list, const idx* goff, const idx* rows, const idx* arp,
+                       const idx* acol, const idx* assignment, const idx* eoff,
+                       unsigned long long* gkey, idx* gkk, idx* gri, idx* entry, idx* entry_row,
+                       idx* sorted_j, idx* cnnz) {
+  extern __shared__ unsigned long long big_smem[];
+  __shared__ idx s_wtot[8];
+  __shared__ idx s_cnt, s_base;
   const idx I = big_list[blockIdx.x];
   const idx base_e = eoff[I];
   const idx L = eoff[I + 1] - base_e;
-  idx p = 0;
-  for (idx m = goff[I]; m < goff[I + 1]; ++m) {
-    const idx i = rows[m];
-    const idx lo = arp[i], len = arp[i + 1] - lo;
-    for (idx t = threadIdx.x; t < len; t += blockDim.x) {
-      const idx k = lo + t;
-      gkey[base_e + p + t] = (static_cast<unsigned long long>(assignment[acol[k]]) << 32) |
-                             static_cast<unsigned long long>(p + t);
-      gkk[base_e + p + t] = k;
-      gri[base_e + p + t] = i;
-    }
-    p += len;
+  const bool in_smem = L <= kGalCapBig;
+  unsigned long long* skey = in_smem ? big_smem : gkey + base_e;
+  idx* skk = in_smem ? reinterpret_cast<idx*>(big_smem + kGalCapBig) : gkk + base_e;
+  idx* sri = in_smem ? skk + kGalCapBig : gri + base_e;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    s_cnt = 0;
+    s_base = 0;
   }
-  if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
+  const idx m0 = goff[I], m1 = goff[I + 1];
+  for (idx mb = m0; mb < m1; mb += blockDim.x) {  // member-parallel gather, block scan
+    const idx m = mb + threadIdx.x;
+    idx i = 0, lo = 0, len = 0;
+    if (m < m1) {
+      i = rows[m];
+      lo = arp[i];
+      len = arp[i + 1] - lo;
+    }
+    idx incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const idx t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wtot[warp] = incl;
+    __syncthreads();
+    idx wbase = 0;
+    for (int q = 0; q < warp; ++q) wbase += s_wtot[q];
+    const idx off = s_base + wbase + incl - len;
+    for (idx t = 0; t < len; ++t) {
+      const idx k = lo + t, p = off + t;
+      skey[p] = (static_cast<unsigned long long>(assignment[acol[k]]) << 32) |
+                static_cast<unsigned long long>(p);
+      skk[p] = k;
+      sri[p] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      idx tot = 0;
+      for (int q = 0; q < 8; ++q) tot += s_wtot[q];
+      s_base += tot;
+    }
+    __syncthreads();
+  }
   for (idx q = threadIdx.x; q < L; q += blockDim.x) {
-    const unsigned long long key = gkey[base_e + q];
+    const unsigned long long key = skey[q];
     idx rank = 0;
-    for (idx z = 0; z < L; ++z) rank += (gkey[base_e + z] < key) ? 1 : 0;
-    entry[base_e + rank] = gkk[base_e + q];
-    entry_row[base_e + rank] = gri[base_e + q];
+    for (idx z = 0; z < L; ++z) rank += (skey[z] < key) ? 1 : 0;
+    entry[base_e + rank] = skk[q];
+    entry_row[base_e + rank] = sri[q];
     sorted_j[base_e + rank] = static_cast<idx>(key >> 32);
   }
   __syncthreads();
-  __threadfence_block();
   idx c = 0;
   for (idx r = threadIdx.x; r < L; r += blockDim.x)
     c += (r == 0 || sorted_j[base_e + r] != sorted_j[base_e + r - 1]) ? 1 : 0;
@@ -647,23 +703,23 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg) {
                agg.rows_by_coarse.get(), A.rowptr.get(), nc, ecnt.get());
   const int64_t total = scan_to_offsets(ecnt.get(), eoff.get(), nc);
   require(total == A.nnz, "galerkin: aggregation does not cover the matrix rows");
-  const size_t smem = static_cast<size_t>(kGalWarps) * kGalCap * (8 + 4 + 4 + 4);
-  static bool raised = false;
-  if (!raised) {
-    AGG_CUDA(cudaFuncSetAttribute(k_gal_symbolic, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    raised = true;
-  }
   if (nc > 0)
     AGG_LAUNCH(k_gal_symbolic, static_cast<unsigned>((nc + kGalWarps - 1) / kGalWarps),
-               kGalWarps * 32, smem, agg.agg_row_offsets.get(), agg.rows_by_coarse.get(),
+               kGalWarps * 32, 0, agg.agg_row_offsets.get(), agg.rows_by_coarse.get(),
                A.rowptr.get(), A.col.get(), agg.assignment.get(), nc, eoff.get(), g.entry.get(),
                g.entry_row.get(), sorted_j.get(), cnnz.get(), big_list.get(), big_count.get());
   const int nbig = read_scalar(big_count.get());
   if (nbig > 0) {
+    const size_t smem = static_cast<size_t>(kGalCapBig) * (8 + 4 + 4);
+    static bool raised = false;
+    if (!raised) {
+      AGG_CUDA(cudaFuncSetAttribute(k_gal_symbolic_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      raised = true;
+    }
     DevBuf<unsigned long long> gkey(A.nnz);
     DevBuf<idx> gkk(A.nnz), gri(A.nnz);
-    AGG_LAUNCH(k_gal_symbolic_big, static_cast<unsigned>(nbig), 256, 0, big_list.get(),
+    AGG_LAUNCH(k_gal_symbolic_big, static_cast<unsigned>(nbig), 256, smem, big_list.get(),
                agg.agg_row_offsets.get(), agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(),
                agg.assignment.get(), eoff.get(), gkey.get(), gkk.get(), gri.get(), g.entry.get(),
                g.entry_row.get(), sorted_j.get(), cnnz.get());

@@ -51,7 +51,7 @@ double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t see
   std::vector<DevBuf<double>> V;
   V.emplace_back(n);
   vec_uniform_sym(n, seed, V[0].get());
-  const double qn = std::sqrt(dot_host(V[0].get(), V[0].get(), n));
+  const double qn = std::sqrt(dot_host(V[0].get(), V[0].get(), n, 1));
   require(qn > 0.0, "smoother: degenerate start vector");
   vec_scale(n, 1.0 / qn, V[0].get());
 
@@ -73,7 +73,7 @@ double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t see
       d.a[1] = V[i].get();
       d.b[1] = V[i].get();
       d.np = 2;
-      dot_device(d, n, dots.get());
+      dot_device(d, n, dots.get(), nullptr, 1);
       double hv[2];
       dots.download(hv, 2);
       sync();
@@ -82,7 +82,7 @@ double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t see
       vec_axpy(n, -hij, V[i].get(), w.get());
       h_scale = std::max(h_scale, std::abs(hij));
     }
-    const double hj = std::sqrt(dot_host(w.get(), w.get(), n));
+    const double hj = std::sqrt(dot_host(w.get(), w.get(), n, 1));
     if (hj <= 1e-12 * std::max(h_scale, 1.0)) {
       m_eff = j + 1;
       break;

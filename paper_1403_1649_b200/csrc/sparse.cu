@@ -142,67 +142,87 @@ struct EpiTraits {
   static constexpr int np = (E == Epi::kSpmvDot1) ? 1 : (E == Epi::kSpmvDot2) ? 2 : (E == Epi::kSpmvDot3) ? 3 : 0;
 };
 
+// Persistent CSR-stream kernel: each CTA walks row blocks rb = blockIdx.x, +gridDim.x, ...
+// For every row block, phase 1 streams the block's contiguous nonzero range with 128-bit
+// loads and stages val * x[col] in shared memory; phase 2 sums each row sequentially in
+// storage order and applies the epilogue.  Fused dot products accumulate per thread
+// across row blocks and are reduced once per CTA (fixed grid => deterministic).
 template <Epi E>
 __global__ void __launch_bounds__(kStreamThreads)
     k_csr_stream(const idx* __restrict__ rowptr, const idx* __restrict__ col,
-                 const double* __restrict__ val, int64_t n_rows, int rpb, SpmvArgs a,
-                 double* partials, unsigned* ticket) {
+                 const double* __restrict__ val, int64_t n_rows, int rpb, int64_t nblocks,
+                 SpmvArgs a, double* partials, unsigned* ticket) {
   extern __shared__ double prod[];
   constexpr int NP = EpiTraits<E>::np;
   constexpr int NPX = NP > 0 ? NP : 1;
   __shared__ double red_smem[32 * 3 + 1];
   if (a.pred && !*a.pred) return;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rpb;
-  const int64_t r1 = min(r0 + static_cast<int64_t>(rpb), n_rows);
-  const idx e0 = rowptr[r0], e1 = rowptr[r1];
   const double* __restrict__ x = a.x;
-
-  // Phase 1: stream the block's contiguous nonzero range with 128-bit loads.
-  for (idx e = (e0 & ~3) + 4 * static_cast<idx>(threadIdx.x); e < e1; e += 4 * kStreamThreads) {
-    const int4 c4 = __ldcs(reinterpret_cast<const int4*>(col + e));
-    const double2 v01 = __ldcs(reinterpret_cast<const double2*>(val + e));
-    const double2 v23 = __ldcs(reinterpret_cast<const double2*>(val + e + 2));
-    if (e >= e0) prod[e - e0] = __dmul_rn(v01.x, __ldg(x + c4.x));
-    if (e + 1 >= e0 && e + 1 < e1) prod[e + 1 - e0] = __dmul_rn(v01.y, __ldg(x + c4.y));
-    if (e + 2 >= e0 && e + 2 < e1) prod[e + 2 - e0] = __dmul_rn(v23.x, __ldg(x + c4.z));
-    if (e + 3 >= e0 && e + 3 < e1) prod[e + 3 - e0] = __dmul_rn(v23.y, __ldg(x + c4.w));
-  }
-  __syncthreads();
-
-  // Phase 2: one thread per row, sequential sum in storage order (sparse.cpp:58-61).
-  const int64_t r = r0 + threadIdx.x;
-  const bool active = threadIdx.x < rpb && r < r1;
-  double sum = 0.0;
-  if (active) {
-    const idx s = rowptr[r] - e0, t = rowptr[r + 1] - e0;
-    for (idx k = s; k < t; ++k) sum = __dadd_rn(sum, prod[k]);
-  }
-  if constexpr (E == Epi::kSpmv || NP > 0) {
-    if (active) a.y[r] = sum;
-  } else if constexpr (E == Epi::kResidual) {
-    if (active) a.y[r] = __dsub_rn(a.b[r], sum);
-  } else if constexpr (E == Epi::kJacobi) {
-    if (active) a.y[r] = __dadd_rn(x[r], __dmul_rn(a.d[r], __dsub_rn(a.b[r], sum)));
-  } else if constexpr (E == Epi::kScaleDiag) {
-    if (active) a.y[r] = __dmul_rn(sum, a.d[r]);
-  }
-  if constexpr (NP > 0) {
-    double v[NPX];
+  double v[NPX];
 #pragma unroll
-    for (int k = 0; k < NP; ++k) v[k] = 0.0;
-    if (active) {
-      const double lhs = a.dot_with_x ? x[r] : sum;
-      if constexpr (NP == 1) {
-        v[0] = __dmul_rn(a.u[r], sum);
-      } else if constexpr (NP == 2) {
-        v[0] = __dmul_rn(lhs, sum);     // rho  = v.v (gmres) | c.v (cg)
-        v[1] = __dmul_rn(lhs, a.c[r]);  // alpha = v.rc       | c.rc
+  for (int k = 0; k < NPX; ++k) v[k] = 0.0;
+
+  for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+    const int64_t r0 = rb * rpb;
+    const int64_t r1 = min(r0 + static_cast<int64_t>(rpb), n_rows);
+    const idx e0 = rowptr[r0], e1 = rowptr[r1];
+
+    // Phase 1: stream the row block's nonzeros (4 per thread-step, 128-bit loads).
+    for (idx e = (e0 & ~3) + 4 * static_cast<idx>(threadIdx.x); e < e1; e += 4 * kStreamThreads) {
+      const int4 c4 = __ldcs(reinterpret_cast<const int4*>(col + e));
+      const double2 v01 = __ldcs(reinterpret_cast<const double2*>(val + e));
+      const double2 v23 = __ldcs(reinterpret_cast<const double2*>(val + e + 2));
+      if constexpr (E == Epi::kResidualZero) {
+        // x = 0 + wd .* b evaluated on the fly for the gathered neighbours
+        if (e >= e0) prod[e - e0] = __dmul_rn(v01.x, __dadd_rn(0.0, __dmul_rn(__ldg(a.d + c4.x), __ldg(a.b + c4.x))));
+        if (e + 1 >= e0 && e + 1 < e1) prod[e + 1 - e0] = __dmul_rn(v01.y, __dadd_rn(0.0, __dmul_rn(__ldg(a.d + c4.y), __ldg(a.b + c4.y))));
+        if (e + 2 >= e0 && e + 2 < e1) prod[e + 2 - e0] = __dmul_rn(v23.x, __dadd_rn(0.0, __dmul_rn(__ldg(a.d + c4.z), __ldg(a.b + c4.z))));
+        if (e + 3 >= e0 && e + 3 < e1) prod[e + 3 - e0] = __dmul_rn(v23.y, __dadd_rn(0.0, __dmul_rn(__ldg(a.d + c4.w), __ldg(a.b + c4.w))));
       } else {
-        v[0] = __dmul_rn(lhs, a.u[r]);  // gamma = w.v | d.v
-        v[1] = __dmul_rn(lhs, sum);     // beta  = w.w | d.w
-        v[2] = __dmul_rn(lhs, a.c[r]);  // alpha2 = w.rt | d.rt
+        if (e >= e0) prod[e - e0] = __dmul_rn(v01.x, __ldg(x + c4.x));
+        if (e + 1 >= e0 && e + 1 < e1) prod[e + 1 - e0] = __dmul_rn(v01.y, __ldg(x + c4.y));
+        if (e + 2 >= e0 && e + 2 < e1) prod[e + 2 - e0] = __dmul_rn(v23.x, __ldg(x + c4.z));
+        if (e + 3 >= e0 && e + 3 < e1) prod[e + 3 - e0] = __dmul_rn(v23.y, __ldg(x + c4.w));
       }
     }
+    __syncthreads();
+
+    // Phase 2: one thread per row, sequential sum in storage order (sparse.cpp:58-61).
+    const int64_t r = r0 + threadIdx.x;
+    if (threadIdx.x < rpb && r < r1) {
+      const idx s = rowptr[r] - e0, t = rowptr[r + 1] - e0;
+      double sum = 0.0;
+      for (idx k = s; k < t; ++k) sum = __dadd_rn(sum, prod[k]);
+      if constexpr (E == Epi::kSpmv || NP > 0) {
+        a.y[r] = sum;
+      } else if constexpr (E == Epi::kResidual) {
+        a.y[r] = __dsub_rn(a.b[r], sum);
+      } else if constexpr (E == Epi::kResidualZero) {
+        const double br = a.b[r];
+        a.y[r] = __dsub_rn(br, sum);                                // r = b - A x1
+        a.x_out[r] = __dadd_rn(0.0, __dmul_rn(a.d[r], br));         // x1 = 0 + wd b
+      } else if constexpr (E == Epi::kJacobi) {
+        a.y[r] = __dadd_rn(x[r], __dmul_rn(a.d[r], __dsub_rn(a.b[r], sum)));
+      } else if constexpr (E == Epi::kScaleDiag) {
+        a.y[r] = __dmul_rn(sum, a.d[r]);
+      }
+      if constexpr (NP > 0) {
+        const double lhs = a.dot_with_x ? x[r] : sum;
+        if constexpr (NP == 1) {
+          v[0] = __dadd_rn(v[0], __dmul_rn(a.u[r], sum));
+        } else if constexpr (NP == 2) {
+          v[0] = __dadd_rn(v[0], __dmul_rn(lhs, sum));     // rho  = v.v (gmres) | c.v (cg)
+          v[1] = __dadd_rn(v[1], __dmul_rn(lhs, a.c[r]));  // alpha = v.rc       | c.rc
+        } else {
+          v[0] = __dadd_rn(v[0], __dmul_rn(lhs, a.u[r]));  // gamma = w.v | d.v
+          v[1] = __dadd_rn(v[1], __dmul_rn(lhs, sum));     // beta  = w.w | d.w
+          v[2] = __dadd_rn(v[2], __dmul_rn(lhs, a.c[r]));  // alpha2 = w.rt | d.rt
+        }
+      }
+    }
+    __syncthreads();  // prod is reused by the next row block
+  }
+  if constexpr (NP > 0) {
     block_reduce<NPX>(v, red_smem);
     if (threadIdx.x == 0)
 #pragma unroll
@@ -213,19 +233,27 @@ __global__ void __launch_bounds__(kStreamThreads)
 
 template <Epi E>
 void launch_stream(const DevCsr& A, const SpmvArgs& a) {
-  const int64_t blocks = (A.n_rows + A.rows_per_block - 1) / A.rows_per_block;
+  const int64_t nblocks = (A.n_rows + A.rows_per_block - 1) / A.rows_per_block;
   const size_t smem = sizeof(double) * A.smem_entries;
-  if (smem > 48 * 1024) {
-    static bool raised = false;
-    if (!raised) {
-      AGG_CUDA(cudaFuncSetAttribute(k_csr_stream<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    227 * 1024));
-      raised = true;
-    }
+  static bool raised = false;
+  if (smem > 48 * 1024 && !raised) {
+    AGG_CUDA(cudaFuncSetAttribute(k_csr_stream<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    raised = true;
   }
-  require(blocks < (1 << 20), "spmv: too many row blocks for the reduction scratch");
-  AGG_LAUNCH(k_csr_stream<E>, static_cast<unsigned>(blocks), kStreamThreads, smem, A.rowptr.get(),
-             A.col.get(), A.val.get(), A.n_rows, A.rows_per_block, a, reduce_partials(),
+  // persistent grid: as many CTAs as can be co-resident
+  static size_t cached_smem = 0;
+  static int cached_per_sm = 0;
+  if (cached_smem != smem) {
+    int per_sm = 0;
+    AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_csr_stream<E>,
+                                                           kStreamThreads, smem));
+    cached_per_sm = std::max(1, per_sm);
+    cached_smem = smem;
+  }
+  const int64_t grid = std::min<int64_t>(nblocks, static_cast<int64_t>(cached_per_sm) * sm_count());
+  AGG_LAUNCH(k_csr_stream<E>, static_cast<unsigned>(grid), kStreamThreads, smem, A.rowptr.get(),
+             A.col.get(), A.val.get(), A.n_rows, A.rows_per_block, nblocks, a, reduce_partials(),
              reduce_ticket());
 }
 
@@ -236,6 +264,7 @@ double spmv_bytes(const DevCsr& A, Epi epi) {
   double b = 12.0 * nnz + 4.0 * (n + 1) + 8.0 * static_cast<double>(A.n_cols) + 8.0 * n;
   switch (epi) {
     case Epi::kResidual: b += 8.0 * n; break;
+    case Epi::kResidualZero: b += 8.0 * n + 16.0 * n; break;  // wd gathered, x1 written
     case Epi::kJacobi: b += 16.0 * n; break;
     case Epi::kScaleDiag: b += 8.0 * n; break;
     case Epi::kSpmvDot1: b += 8.0 * n; break;
@@ -252,6 +281,7 @@ void spmv_run(const DevCsr& A, Epi epi, const SpmvArgs& a, int prof_family) {
   switch (epi) {
     case Epi::kSpmv: launch_stream<Epi::kSpmv>(A, a); break;
     case Epi::kResidual: launch_stream<Epi::kResidual>(A, a); break;
+    case Epi::kResidualZero: launch_stream<Epi::kResidualZero>(A, a); break;
     case Epi::kJacobi: launch_stream<Epi::kJacobi>(A, a); break;
     case Epi::kScaleDiag: launch_stream<Epi::kScaleDiag>(A, a); break;
     case Epi::kSpmvDot1: launch_stream<Epi::kSpmvDot1>(A, a); break;

@@ -40,6 +40,7 @@ void download_csr(const DevCsr& A, int64_t* rowptr, int64_t* col, double* val);
 enum class Epi {
   kSpmv,       // y = A x
   kResidual,   // y = b - A x
+  kResidualZero,  // x_out = 0 + wd .* b ; y = b - A x_out  (first sweep from x = 0 fused)
   kJacobi,     // y = x + wd .* (b - A x)          (wd = omega * inv_diag)
   kScaleDiag,  // y = (A x) .* d                   (Arnoldi, smoother.cpp:53-54)
   kSpmvDot2,   // y = A x ; dots (y.y, y.c) [gmres inner] or (x.y, x.c) [cg inner]
@@ -50,6 +51,7 @@ enum class Epi {
 struct SpmvArgs {
   const double* x = nullptr;
   double* y = nullptr;
+  double* x_out = nullptr;     // kResidualZero: the smoothed iterate
   const double* b = nullptr;   // residual / jacobi rhs
   const double* d = nullptr;   // wd (jacobi) or inv_diag (scale)
   const double* c = nullptr;   // second dot operand
