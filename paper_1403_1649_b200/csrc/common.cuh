@@ -41,6 +41,7 @@ inline void require(bool cond, const char* msg) {
 // Launch bookkeeping: every kernel goes through AGG_LAUNCH so the library can
 // report how many of its own kernels ran (bench.py "gpu_launches").
 void note_launch();
+void note_launches(int64_t n);  // graph replays: n kernels launched by one cudaGraphLaunch
 void check_launch(const char* file, int line);
 
 #define AGG_LAUNCH(kernel, grid, block, smem, ...)                                   \

@@ -1,6 +1,8 @@
 // cycles.cu — V-cycle (Alg. 4) and K-cycle (Alg. 5) recursion on device buffers.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include "chunked.cuh"
 #include "cycles.cuh"
@@ -224,7 +226,11 @@ void descend(DevHierarchy& h, int64_t k, const double* b, const double* x_in, do
   ra.y = L.r.get();
   ra.b = b;
   ra.pred = pred;
-  if (!x_in && L.smoother.kind != 2) {
+  // Measured on B200 (profiles/r01_kernel_bench.json): the fused pass gathers wd and b
+  // for every stencil neighbour and loses to jacobi_zero + residual at every level, so it
+  // stays off; the kernel remains available (aggmg_bench_kernel kind 2).
+  constexpr bool kFuseZeroGuess = false;
+  if (kFuseZeroGuess && !x_in && L.smoother.kind != 2) {
     ra.x_out = x_out;
     ra.d = L.smoother.wdiag.get();
     spmv_run(*L.A, Epi::kResidualZero, ra, k == 0 ? kProfSpmvL0 : 0);
@@ -245,8 +251,81 @@ void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in,
 void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
                 const double* x_in, double* x_out, const int* pred);
 
+void inner_cycle_eager(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
+                       double* x_out, const int* pred);
+void subcycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b, double* x_out,
+              const int* pred, bool vee);
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("AGGMG_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// The sub-cycle below level 0 is a fixed kernel sequence over fixed buffers (device
+// predicates steer the K-cycle branches), so it is captured once per (config, level,
+// in/out/predicate buffers) into a CUDA graph and replayed: the ~100 small coarse-level
+// kernels of one preconditioner application then launch back to back from the graph.
+// The first call with a new key runs eagerly (initialising lazily created resources),
+// the second captures.
+void subcycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b, double* x_out,
+              const int* pred, bool vee) {
+  auto eager = [&] {
+    if (vee)
+      vcycle_dev(h, k, b, nullptr, x_out, pred);
+    else
+      inner_cycle_eager(h, cfg, k, b, x_out, pred);
+  };
+  if (k != 1 || !graphs_enabled() || k == h.coarsest()) {
+    eager();
+    return;
+  }
+  char keybuf[256];
+  std::snprintf(keybuf, sizeof(keybuf), "%d/%d/%d/%.17g/%d/%lld/%p/%p/%p", vee ? 1 : 0, cfg.kind,
+                cfg.k_levels, cfg.t, cfg.inner, static_cast<long long>(k),
+                static_cast<const void*>(b), static_cast<void*>(x_out),
+                static_cast<const void*>(pred));
+  const std::string key(keybuf);
+  SubcycleGraph* g = nullptr;
+  for (auto& e : h.graphs)
+    if (e.first == key) g = &e.second;
+  if (!g) {  // first sighting: eager run, remember the key
+    h.graphs.emplace_back(key, SubcycleGraph{});
+    eager();
+    return;
+  }
+  if (!g->exec) {
+    AGG_CUDA(cudaStreamBeginCapture(stream(), cudaStreamCaptureModeThreadLocal));
+    const int64_t before = launch_count();
+    try {
+      eager();
+    } catch (...) {
+      cudaGraph_t junk;
+      cudaStreamEndCapture(stream(), &junk);
+      if (junk) cudaGraphDestroy(junk);
+      throw;
+    }
+    g->kernels = launch_count() - before;
+    note_launches(-g->kernels);  // counted again on every replay
+    cudaGraph_t graph;
+    AGG_CUDA(cudaStreamEndCapture(stream(), &graph));
+    AGG_CUDA(cudaGraphInstantiate(&g->exec, graph, 0));
+    AGG_CUDA(cudaGraphDestroy(graph));
+  }
+  AGG_CUDA(cudaGraphLaunch(g->exec, stream()));
+  note_launches(g->kernels);
+  ++h.graph_uses;
+}
+
 void inner_cycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b, double* x_out,
                  const int* pred) {
+  subcycle(h, cfg, k, b, x_out, pred, false);
+}
+
+void inner_cycle_eager(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
+                       double* x_out, const int* pred) {
   if (accelerated(cfg, k))
     kcycle_dev(h, cfg, k, b, nullptr, x_out, pred);
   else
@@ -264,7 +343,7 @@ void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in,
   if (k + 1 == h.coarsest())
     coarse_solve(h, L.rc.get(), L.xc.get(), pred);
   else
-    vcycle_dev(h, k + 1, L.rc.get(), nullptr, L.xc.get(), pred);
+    subcycle(h, CycleCfg{}, k + 1, L.rc.get(), L.xc.get(), pred, true);
   postsmooth(L, b, x_out, pred, k == 0);
 }
 

@@ -100,6 +100,10 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
 
 // hierarchy.cpp:90-104: numeric half only; aggregates, P and R are untouched.
 void refresh_values(DevHierarchy& h, const double* new_values_dev) {
+  // the smoother arrays are reallocated below: captured sub-cycle graphs become stale
+  for (auto& g : h.graphs)
+    if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+  h.graphs.clear();
   DevLevel& L0 = h.levels[0];
   copy_double(L0.A->val.get(), new_values_dev, L0.A->nnz);
   for (int64_t k = 0; k + 1 < h.n_levels(); ++k) {
@@ -110,6 +114,11 @@ void refresh_values(DevHierarchy& h, const double* new_values_dev) {
                    level_seed(h.cfg.seed, k, kSmootherTag), fine.smoother);
   }
   factor_coarsest(h);
+}
+
+DevHierarchy::~DevHierarchy() {
+  for (auto& g : graphs)
+    if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
 }
 
 void DevHierarchy::ensure_workspace() {

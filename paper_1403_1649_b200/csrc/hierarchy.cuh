@@ -48,8 +48,18 @@ struct DevLevel {
   DevBuf<KScalars> ks;
 };
 
+// Captured CUDA graph of one coarse sub-cycle launch (levels >= 1 are launch-latency
+// bound: ~100 small kernels per preconditioner application).
+struct SubcycleGraph {
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
+};
+
 struct DevHierarchy {
+  ~DevHierarchy();
   std::vector<DevLevel> levels;
+  std::vector<std::pair<std::string, SubcycleGraph>> graphs;  // key -> graph
+  int graph_uses = 0;
   SetupCfg cfg;
   std::vector<std::string> warnings;
   HostLu coarse_lu;

@@ -103,6 +103,7 @@ double* pinned_scratch(int n) {
 }
 
 void note_launch() { launches().fetch_add(1, std::memory_order_relaxed); }
+void note_launches(int64_t n) { launches().fetch_add(n, std::memory_order_relaxed); }
 int64_t launch_count() { return launches().load(); }
 
 void check_launch(const char* file, int line) {

@@ -55,23 +55,50 @@ __global__ void k_max_row(const idx* rowptr, int64_t n, int* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
+// largest staged span (e1 - (e0 & ~1)) over the row blocks of rpb rows
+__global__ void k_max_block_span(const idx* rowptr, int64_t n, int rpb, int* out) {
+  int m = 0;
+  const int64_t nb = (n + rpb - 1) / rpb;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < nb;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r0 = b * rpb, r1 = min(r0 + rpb, n);
+    m = max(m, rowptr[r1] - (rowptr[r0] & ~1));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 }  // namespace
 
 constexpr int kStreamThreads = 256;
-constexpr int kStreamCap = 4096;  // staged products per block in the common case (32 KB)
+constexpr int kStreamTarget = 2048;  // staged products per row block (16 KB)
 
+// Row-block plan: about kStreamTarget nonzeros per block (mean row length), staging
+// sized to the largest actual block span so the shared-memory carve-out leaves L1
+// room for the x gathers of the irregular coarse operators.
 void DevCsr::plan() {
   max_row = 0;
-  if (n_rows > 0) {
-    DevBuf<int> m(1);
+  rows_per_block = 1;
+  smem_entries = 8;
+  if (n_rows == 0) return;
+  DevBuf<int> m(1);
+  m.zero();
+  AGG_LAUNCH(k_max_row, grid_for(n_rows, 256, 4 * sm_count()), 256, 0, rowptr.get(), n_rows, m.get());
+  max_row = read_scalar(m.get());
+  const double mean = std::max(1.0, static_cast<double>(nnz) / static_cast<double>(n_rows));
+  int rpb = static_cast<int>(std::min<double>(kStreamThreads, std::max(1.0, kStreamTarget / mean)));
+  while (true) {
     m.zero();
-    AGG_LAUNCH(k_max_row, grid_for(n_rows, 256, 4 * sm_count()), 256, 0, rowptr.get(), n_rows,
-               m.get());
-    max_row = read_scalar(m.get());
+    AGG_LAUNCH(k_max_block_span, grid_for((n_rows + rpb - 1) / rpb, 256, 4 * sm_count()), 256, 0,
+               rowptr.get(), n_rows, rpb, m.get());
+    const int span = read_scalar(m.get());
+    if (static_cast<int64_t>(span + 4) * 8 <= 200 * 1024 || rpb == 1) {
+      rows_per_block = rpb;
+      smem_entries = span + 4;
+      break;
+    }
+    rpb = std::max(1, rpb / 2);
   }
-  const int mr = std::max(1, max_row);
-  rows_per_block = std::max(1, std::min(kStreamThreads, kStreamCap / mr));
-  smem_entries = rows_per_block * mr + 4;
   // rows longer than the opt-in shared-memory limit (~28k entries) are not supported
   require(static_cast<int64_t>(smem_entries) * 8 <= 227 * 1024,
           "spmv: a row has " + std::to_string(max_row) +
@@ -152,10 +179,10 @@ __global__ void __launch_bounds__(kStreamThreads)
     k_csr_stream(const idx* __restrict__ rowptr, const idx* __restrict__ col,
                  const double* __restrict__ val, int64_t n_rows, int rpb, int64_t nblocks,
                  SpmvArgs a, double* partials, unsigned* ticket) {
-  extern __shared__ double prod[];
+  extern __shared__ __align__(16) double prod[];
   constexpr int NP = EpiTraits<E>::np;
   constexpr int NPX = NP > 0 ? NP : 1;
-  __shared__ double red_smem[32 * 3 + 1];
+  __shared__ __align__(16) double red_smem[32 * 3 + 2];
   if (a.pred && !*a.pred) return;
   const double* __restrict__ x = a.x;
   double v[NPX];
@@ -167,30 +194,50 @@ __global__ void __launch_bounds__(kStreamThreads)
     const int64_t r1 = min(r0 + static_cast<int64_t>(rpb), n_rows);
     const idx e0 = rowptr[r0], e1 = rowptr[r1];
 
-    // Phase 1: stream the row block's nonzeros (4 per thread-step, 128-bit loads).
-    for (idx e = (e0 & ~3) + 4 * static_cast<idx>(threadIdx.x); e < e1; e += 4 * kStreamThreads) {
-      const int4 c4 = __ldcs(reinterpret_cast<const int4*>(col + e));
-      const double2 v01 = __ldcs(reinterpret_cast<const double2*>(val + e));
-      const double2 v23 = __ldcs(reinterpret_cast<const double2*>(val + e + 2));
+    // Phase 1: stream the row block's nonzeros.  Thread t owns entry pairs
+    // (ea + 2t + 512k, +1): 128-bit value loads, 64-bit column loads, both fully
+    // coalesced; two pairs are issued before their gathers to keep 4 gathers in flight.
+    // Products land in shared memory at [e - ea] (pairs 16-byte aligned, so the
+    // 128-bit stores are bank-conflict free); slots outside [e0, e1) are never read.
+    const idx ea = e0 & ~1;
+    for (idx e = ea + 2 * static_cast<idx>(threadIdx.x); e < e1; e += 4 * kStreamThreads) {
+      const idx eb = e + 2 * kStreamThreads;
+      const bool hb = eb < e1;
+      const int2 ca = __ldcs(reinterpret_cast<const int2*>(col + e));
+      const double2 va = __ldcs(reinterpret_cast<const double2*>(val + e));
+      int2 cb = make_int2(0, 0);
+      double2 vb = make_double2(0.0, 0.0);
+      if (hb) {
+        cb = __ldcs(reinterpret_cast<const int2*>(col + eb));
+        vb = __ldcs(reinterpret_cast<const double2*>(val + eb));
+      }
+      const bool a0 = e >= e0, a1 = e + 1 < e1, b1 = hb && eb + 1 < e1;
+      double xa0 = 0.0, xa1 = 0.0, xb0 = 0.0, xb1 = 0.0;
       if constexpr (E == Epi::kResidualZero) {
         // x = 0 + wd .* b evaluated on the fly for the gathered neighbours
-        if (e >= e0) prod[e - e0] = __dmul_rn(v01.x, __dadd_rn(0.0, __dmul_rn(__ldg(a.d + c4.x), __ldg(a.b + c4.x))));
-        if (e + 1 >= e0 && e + 1 < e1) prod[e + 1 - e0] = __dmul_rn(v01.y, __dadd_rn(0.0, __dmul_rn(__ldg(a.d + c4.y), __ldg(a.b + c4.y))));
-        if (e + 2 >= e0 && e + 2 < e1) prod[e + 2 - e0] = __dmul_rn(v23.x, __dadd_rn(0.0, __dmul_rn(__ldg(a.d + c4.z), __ldg(a.b + c4.z))));
-        if (e + 3 >= e0 && e + 3 < e1) prod[e + 3 - e0] = __dmul_rn(v23.y, __dadd_rn(0.0, __dmul_rn(__ldg(a.d + c4.w), __ldg(a.b + c4.w))));
+        auto xz = [&](idx c) { return __dadd_rn(0.0, __dmul_rn(__ldg(a.d + c), __ldg(a.b + c))); };
+        if (a0) xa0 = xz(ca.x);
+        if (a1) xa1 = xz(ca.y);
+        if (hb) xb0 = xz(cb.x);
+        if (b1) xb1 = xz(cb.y);
       } else {
-        if (e >= e0) prod[e - e0] = __dmul_rn(v01.x, __ldg(x + c4.x));
-        if (e + 1 >= e0 && e + 1 < e1) prod[e + 1 - e0] = __dmul_rn(v01.y, __ldg(x + c4.y));
-        if (e + 2 >= e0 && e + 2 < e1) prod[e + 2 - e0] = __dmul_rn(v23.x, __ldg(x + c4.z));
-        if (e + 3 >= e0 && e + 3 < e1) prod[e + 3 - e0] = __dmul_rn(v23.y, __ldg(x + c4.w));
+        if (a0) xa0 = __ldg(x + ca.x);
+        if (a1) xa1 = __ldg(x + ca.y);
+        if (hb) xb0 = __ldg(x + cb.x);
+        if (b1) xb1 = __ldg(x + cb.y);
       }
+      *reinterpret_cast<double2*>(prod + (e - ea)) =
+          make_double2(__dmul_rn(va.x, xa0), __dmul_rn(va.y, xa1));
+      if (hb)
+        *reinterpret_cast<double2*>(prod + (eb - ea)) =
+            make_double2(__dmul_rn(vb.x, xb0), __dmul_rn(vb.y, xb1));
     }
     __syncthreads();
 
     // Phase 2: one thread per row, sequential sum in storage order (sparse.cpp:58-61).
     const int64_t r = r0 + threadIdx.x;
     if (threadIdx.x < rpb && r < r1) {
-      const idx s = rowptr[r] - e0, t = rowptr[r + 1] - e0;
+      const idx s = rowptr[r] - ea, t = rowptr[r + 1] - ea;
       double sum = 0.0;
       for (idx k = s; k < t; ++k) sum = __dadd_rn(sum, prod[k]);
       if constexpr (E == Epi::kSpmv || NP > 0) {

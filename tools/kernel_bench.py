@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--kinds", default="0,1,2,3,4")
+    ap.add_argument("--only", default="", help="e.g. L1.A:0 — run just this matrix:kind")
     args = ap.parse_args()
     lib = M.b200().lib
     assert lib.fn("init")(0) == 0, lib.fn("last_error")()
@@ -40,6 +41,11 @@ def main():
     out = {}
     for name, m in mats.items():
         kinds = [int(k) for k in args.kinds.split(",")] if name.endswith(".A") else [0]
+        if args.only:
+            oname, okind = args.only.split(":")
+            if oname != name:
+                continue
+            kinds = [int(okind)]
         for kind in kinds:
             ms, by = C.c_double(), C.c_double()
             rc = lib.fn("bench_kernel")(m, kind, args.reps, C.byref(ms), C.byref(by))
