@@ -261,7 +261,8 @@ def run_b200(args, world, rank, local):
 
     # ---- timed region: value (inputs resident in HBM) ----
     records = []
-    check(lib.fn("profile_enable")((1 << PROF_SMOOTH) | (1 << PROF_SPMV)))
+    if not args.no_prof:
+        check(lib.fn("profile_enable")((1 << PROF_SMOOTH) | (1 << PROF_SPMV)))
     launches0 = lib.fn("kernel_launches")()
     dist.barrier()
     check(lib.fn("synchronize")())
@@ -364,6 +365,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-prof", action="store_true", help="skip per-launch CUDA-event timing")
     ap.add_argument("--ref-sample", type=int, default=0)
     args = ap.parse_args()
     world, rank, local = dist_env()

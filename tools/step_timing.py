@@ -1,0 +1,39 @@
+#!/usr/bin/env python
+"""Wall-clock split of one bench step (setup / solve / free) on the device path."""
+import ctypes as C
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1403_1649_b200 import _abi  # noqa: E402
+from paper_1403_1649_b200 import aggmg as M  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+lib = M.b200().lib
+assert lib.fn("init")(0) == 0
+dm = C.c_void_p()
+assert lib.fn("dmatrix_poisson")(3, n, n, n, 1.0, -1, C.byref(dm)) == 0
+s = M.SetupConfig(alpha=0.5, reuse_caches=True)._c()
+c = M.CycleConfig()._c()
+v = M.SolverConfig(method=M.PCG, tol=1e-8, max_iters=500)._c()
+hist = np.zeros(600)
+for step in range(4):
+    t0 = time.perf_counter()
+    h = C.c_void_p()
+    assert lib.fn("setup_hierarchy_device")(dm, C.byref(s), C.byref(h)) == 0
+    lib.fn("synchronize")()
+    t1 = time.perf_counter()
+    rep = _abi.SolveReportC()
+    rep.history = hist.ctypes.data_as(_abi.f64p)
+    rep.history_capacity = 600
+    assert lib.fn("solve_device")(h, C.byref(c), C.byref(v), None, C.byref(rep)) == 0
+    lib.fn("synchronize")()
+    t2 = time.perf_counter()
+    lib.fn("hierarchy_free")(h)
+    lib.fn("synchronize")()
+    t3 = time.perf_counter()
+    print(f"step {step}: setup {1e3*(t1-t0):.1f} ms, solve {1e3*(t2-t1):.1f} ms ({rep.iterations} its), "
+          f"free {1e3*(t3-t2):.1f} ms", flush=True)
