@@ -15,7 +15,15 @@ OBJS      := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(CU_SRCS)) \
              $(patsubst $(SRC_DIR)/%.cpp,$(OBJ_DIR)/%.cpp.o,$(CPP_SRCS))
 HDRS      := $(wildcard $(SRC_DIR)/*.cuh) $(wildcard $(SRC_DIR)/*.hpp) include/aggmg_b200.h
 
-all: $(LIB) oracle
+DEMO      := build/cpp_dropin_demo
+
+all: $(LIB) oracle $(DEMO)
+
+# reference-style C++ caller built against the drop-in header include/aggmg/aggmg.hpp
+$(DEMO): tools/cpp_dropin_demo.cpp include/aggmg/aggmg.hpp include/aggmg_b200.h $(LIB)
+	@mkdir -p build
+	$(HOSTCXX) -std=c++20 -O2 -Wall -Iinclude $< -Lpaper_1403_1649_b200/lib -laggmg_b200 \
+	  -Wl,-rpath,'$$ORIGIN/../paper_1403_1649_b200/lib' -o $@
 
 $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p $(OBJ_DIR)
