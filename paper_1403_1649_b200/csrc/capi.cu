@@ -379,11 +379,38 @@ int aggmg_build_transfer(int64_t n, int64_t nc, const int64_t* assignment, const
 int aggmg_galerkin_direct(const aggmg_csr* R, const aggmg_csr* A, const aggmg_csr* P,
                           aggmg_csr* Ac) {
   return guarded([&] {
-    require(R->n_cols == A->n_rows && A->n_cols == P->n_rows,
+    require(R->n_cols == A->n_rows && A->n_cols == P->n_rows && R->n_rows == P->n_cols,
             "galerkin_direct: operand shapes disagree");
-    throw Error("galerkin_direct: the explicit triple product is not provided by the device "
-                "library; use the cached segmented reduce (build/apply_galerkin_cache)");
-    (void)Ac;
+    require(A->n_rows == A->n_cols, "galerkin: matrix must be square");
+    // The device product is specialised to the AMG shape: P one entry per row, R = P^T.
+    const int64_t n = P->n_rows, nc = P->n_cols;
+    std::vector<int64_t> a(n, 0);
+    std::vector<double> pv(n, 0.0);
+    std::vector<int64_t> rcount(nc + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t w = P->row_offsets[i + 1] - P->row_offsets[i];
+      require(w <= 1, "galerkin_direct: the device path needs one entry per row of P");
+      if (w == 1) {
+        a[i] = P->col_indices[P->row_offsets[i]];
+        pv[i] = P->values[P->row_offsets[i]];
+        ++rcount[a[i] + 1];
+      }
+    }
+    for (int64_t J = 0; J < nc; ++J) rcount[J + 1] += rcount[J];
+    bool is_transpose = R->row_offsets[nc] == rcount[nc];
+    for (int64_t J = 0; J <= nc && is_transpose; ++J) is_transpose = R->row_offsets[J] == rcount[J];
+    std::vector<int64_t> cur(rcount.begin(), rcount.end() - 1);
+    for (int64_t i = 0; i < n && is_transpose; ++i) {
+      if (P->row_offsets[i + 1] == P->row_offsets[i]) continue;
+      const int64_t k = cur[a[i]]++;
+      is_transpose = R->col_indices[k] == i && R->values[k] == pv[i];
+    }
+    require(is_transpose, "galerkin_direct: the device path needs R = transpose(P)");
+    auto dA = up(A);
+    AggDev agg = agg_from_host(n, nc, a.data());
+    auto dpv = up_vec(pv.data(), n);
+    auto dAc = galerkin_direct(*dA, agg, dpv.get());
+    down(*dAc, Ac);
   });
 }
 

@@ -75,8 +75,13 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     }
     fine.mis_sweeps = mis.sweeps;
     fine.tr = build_transfer(agg, fine.B.get());
-    fine.gal = build_galerkin_cache(A, agg);
-    DevCsrPtr Ac = apply_galerkin_cache(fine.gal, A, fine.tr.pval.get());
+    DevCsrPtr Ac;
+    if (cfg.reuse_caches) {  // hierarchy.cpp:69-71: cached sort / segmented reduce
+      fine.gal = build_galerkin_cache(A, agg);
+      Ac = apply_galerkin_cache(fine.gal, A, fine.tr.pval.get());
+    } else {  // hierarchy.cpp:73: galerkin_direct, the reference default
+      Ac = galerkin_direct(A, agg, fine.tr.pval.get());
+    }
     setup_smoother(A, cfg.smoother, cfg.arnoldi_m, level_seed(cfg.seed, k, kSmootherTag),
                    fine.smoother);
     fine.has_smoother = true;

@@ -463,6 +463,154 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) cnnz[I] = s_cnt;
 }
 
+// ---- galerkin_direct: R*(A*P) in the reference spmm order (galerkin.cpp:33-36) ----------
+//
+// spmm(R, A) accumulates, for coarse row I, RA_Ij = sum over members i of I (ascending,
+// P row non-empty) of p_i * a_ij, starting from 0 (sparse.cpp:102-120); spmm(RA, P) then
+// accumulates Ac_IJ = sum over j ascending (P row j non-empty, agg(j) = J) of RA_Ij * p_j.
+// Per coarse row we gather (key = J<<32 | j, value = p_i * a_ij) in member/storage order,
+// rank-sort by key with the gather position as tie-break, and walk the sorted run
+// sequentially — the exact association and order of the two CPU products.
+
+// One coarse row's walk over sorted (key, value) arrays; writes (or counts) Ac entries.
+__device__ inline idx gal_direct_walk(const unsigned long long* skey, const double* sval, idx L,
+                                      const double* pval, idx* ccol, double* cval) {
+  idx out = 0;
+  idx p = 0;
+  while (p < L) {
+    const idx J = static_cast<idx>(skey[p] >> 32);
+    double acc = 0.0;
+    while (p < L && static_cast<idx>(skey[p] >> 32) == J) {
+      const idx j = static_cast<idx>(skey[p] & 0xffffffffull);
+      double raij = 0.0;
+      while (p < L && skey[p] == ((static_cast<unsigned long long>(J) << 32) | static_cast<unsigned>(j))) {
+        raij = __dadd_rn(raij, sval[p]);
+        ++p;
+      }
+      acc = __dadd_rn(acc, __dmul_rn(raij, pval[j]));
+    }
+    if (ccol) {
+      ccol[out] = J;
+      cval[out] = acc;
+    }
+    ++out;
+  }
+  return out;
+}
+
+// mode 0: count coarse row lengths into cnnz; mode 1: fill at crp.  Warp per coarse row,
+// rows with more than kGalCap gathered entries are deferred to the CTA kernel.
+constexpr int kGalDirectWarps = 4;  // 4 warps x 256 x 32 B = 32 KB static smem
+__global__ void __launch_bounds__(kGalDirectWarps * 32)
+    k_gal_direct(const idx* goff, const idx* rows, const idx* arp, const idx* acol,
+                 const double* aval, const idx* assignment, const double* pval, int64_t nc,
+                 const idx* eoff, int mode, idx* cnnz, const idx* crp, idx* ccol, double* cval,
+                 idx* big_list, int* big_count) {
+  __shared__ unsigned long long s_key[kGalDirectWarps][kGalCap], s_skey[kGalDirectWarps][kGalCap];
+  __shared__ double s_val[kGalDirectWarps][kGalCap], s_sval[kGalDirectWarps][kGalCap];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t I = static_cast<int64_t>(blockIdx.x) * kGalDirectWarps + w;
+  if (I >= nc) return;
+  if (eoff[I + 1] - eoff[I] > kGalCap) {
+    if (lane == 0) big_list[atomicAdd(big_count, 1)] = static_cast<idx>(I);
+    return;
+  }
+  // gather in (member ascending, storage order), skipping empty P rows on either side
+  idx L = 0;
+  for (idx m = goff[I]; m < goff[I + 1]; ++m) {
+    const idx i = rows[m];
+    const double pi = pval[i];
+    if (pi == 0.0) continue;
+    for (idx k0 = arp[i]; k0 < arp[i + 1]; k0 += 32) {
+      const idx k = k0 + lane;
+      bool keep = false;
+      unsigned long long key = 0;
+      double v = 0.0;
+      if (k < arp[i + 1]) {
+        const idx j = acol[k];
+        if (pval[j] != 0.0) {
+          keep = true;
+          key = (static_cast<unsigned long long>(assignment[j]) << 32) | static_cast<unsigned>(j);
+          v = __dmul_rn(pi, aval[k]);
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const idx pos = L + __popc(bal & ((1u << lane) - 1u));
+        s_key[w][pos] = key;
+        s_val[w][pos] = v;
+      }
+      L += __popc(bal);
+    }
+  }
+  __syncwarp();
+  for (idx q = lane; q < L; q += 32) {  // stable rank: key, then gather position
+    const unsigned long long key = s_key[w][q];
+    idx rank = 0;
+    for (idx z = 0; z < L; ++z) {
+      const unsigned long long kz = s_key[w][z];
+      rank += (kz < key || (kz == key && z < q)) ? 1 : 0;
+    }
+    s_skey[w][rank] = key;
+    s_sval[w][rank] = s_val[w][q];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (mode == 0)
+      cnnz[I] = gal_direct_walk(s_skey[w], s_sval[w], L, pval, nullptr, nullptr);
+    else
+      gal_direct_walk(s_skey[w], s_sval[w], L, pval, ccol + crp[I], cval + crp[I]);
+  }
+}
+
+// CTA per long coarse row, (key, value) staged in global scratch at [eoff[I], eoff[I+1]).
+__global__ void __launch_bounds__(256)
+    k_gal_direct_big(const idx* big_list, const idx* goff, const idx* rows, const idx* arp,
+                     const idx* acol, const double* aval, const idx* assignment,
+                     const double* pval, const idx* eoff, int mode, unsigned long long* gkey,
+                     double* gval, unsigned long long* gskey, double* gsval, idx* cnnz,
+                     const idx* crp, idx* ccol, double* cval) {
+  __shared__ idx s_L;
+  const idx I = big_list[blockIdx.x];
+  const idx base = eoff[I];
+  unsigned long long* key = gkey + base;
+  double* val = gval + base;
+  unsigned long long* skey = gskey + base;
+  double* sval = gsval + base;
+  if (threadIdx.x == 0) {  // sequential gather keeps member/storage order trivially
+    idx L = 0;
+    for (idx m = goff[I]; m < goff[I + 1]; ++m) {
+      const idx i = rows[m];
+      const double pi = pval[i];
+      if (pi == 0.0) continue;
+      for (idx k = arp[i]; k < arp[i + 1]; ++k) {
+        const idx j = acol[k];
+        if (pval[j] == 0.0) continue;
+        key[L] = (static_cast<unsigned long long>(assignment[j]) << 32) | static_cast<unsigned>(j);
+        val[L] = __dmul_rn(pi, aval[k]);
+        ++L;
+      }
+    }
+    s_L = L;
+  }
+  __syncthreads();
+  const idx L = s_L;
+  for (idx q = threadIdx.x; q < L; q += blockDim.x) {
+    const unsigned long long kq = key[q];
+    idx rank = 0;
+    for (idx z = 0; z < L; ++z) rank += (key[z] < kq || (key[z] == kq && z < q)) ? 1 : 0;
+    skey[rank] = kq;
+    sval[rank] = val[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (mode == 0)
+      cnnz[I] = gal_direct_walk(skey, sval, L, pval, nullptr, nullptr);
+    else
+      gal_direct_walk(skey, sval, L, pval, ccol + crp[I], cval + crp[I]);
+  }
+}
+
 // Warp per coarse row: segment boundaries -> coarse columns, segment offsets, slot_of_csr.
 __global__ void k_gal_fill(int64_t nc, const idx* eoff, const idx* sorted_j, const idx* entry,
                            const idx* crp, idx* ccol, idx* seg_off, idx* slot_of_csr) {
@@ -755,6 +903,53 @@ DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const doub
     AGG_LAUNCH(k_gal_numeric, grid_for(g.nnz_coarse, 256), 256, 0, g.nnz_coarse,
                g.segment_offsets.get(), g.entry.get(), g.entry_row.get(), A.col.get(), A.val.get(),
                pval, Ac->val.get());
+  }
+  Ac->plan();
+  return Ac;
+}
+
+DevCsrPtr galerkin_direct(const DevCsr& A, const AggDev& agg, const double* pval) {
+  require(A.n_rows == A.n_cols && agg.n_fine == A.n_rows, "galerkin: aggregation size mismatch");
+  const int64_t nc = agg.n_agg;
+  auto Ac = std::make_shared<DevCsr>();
+  Ac->n_rows = Ac->n_cols = nc;
+  Ac->rowptr.resize(nc + 1);
+  DevBuf<idx> ecnt(nc), eoff(nc + 1), cnnz(nc), big_list(nc > 0 ? nc : 1);
+  DevBuf<int> big_count(1);
+  big_count.zero();
+  if (nc > 0)
+    AGG_LAUNCH(k_group_entry_counts, grid_for(nc, 256), 256, 0, agg.agg_row_offsets.get(),
+               agg.rows_by_coarse.get(), A.rowptr.get(), nc, ecnt.get());
+  scan_to_offsets_async(ecnt.get(), eoff.get(), nc);
+  const unsigned grid = static_cast<unsigned>((nc + kGalDirectWarps - 1) / kGalDirectWarps);
+  DevBuf<unsigned long long> gkey, gskey;
+  DevBuf<double> gval, gsval;
+  for (int mode = 0; mode < 2; ++mode) {
+    big_count.zero();
+    if (nc > 0)
+      AGG_LAUNCH(k_gal_direct, grid, kGalDirectWarps * 32, 0, agg.agg_row_offsets.get(),
+                 agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(), A.val.get(),
+                 agg.assignment.get(), pval, nc, eoff.get(), mode, cnnz.get(), Ac->rowptr.get(),
+                 Ac->col.get(), Ac->val.get(), big_list.get(), big_count.get());
+    const int nbig = read_scalar(big_count.get());
+    if (nbig > 0) {
+      if (gkey.size() == 0) {
+        gkey.resize(A.nnz);
+        gskey.resize(A.nnz);
+        gval.resize(A.nnz);
+        gsval.resize(A.nnz);
+      }
+      AGG_LAUNCH(k_gal_direct_big, static_cast<unsigned>(nbig), 256, 0, big_list.get(),
+                 agg.agg_row_offsets.get(), agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(),
+                 A.val.get(), agg.assignment.get(), pval, eoff.get(), mode, gkey.get(), gval.get(),
+                 gskey.get(), gsval.get(), cnnz.get(), Ac->rowptr.get(), Ac->col.get(),
+                 Ac->val.get());
+    }
+    if (mode == 0) {
+      Ac->nnz = scan_to_offsets(cnnz.get(), Ac->rowptr.get(), nc);
+      Ac->col.resize(Ac->nnz);
+      Ac->val.resize(Ac->nnz);
+    }
   }
   Ac->plan();
   return Ac;

@@ -54,7 +54,8 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg);
 DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const double* pval);
 uint64_t pattern_fingerprint(const DevCsr& A, const idx* assignment);
 
-// galerkin_direct: R*A*P by two row-wise products in the reference spmm order.
-DevCsrPtr spmm(const DevCsr& A, const DevCsr& B);
+// galerkin_direct (galerkin.cpp:33-36): R*(A*P) for P = one entry per row (pval) and
+// R = P^T, summed in the association and order of the reference's two spmm calls.
+DevCsrPtr galerkin_direct(const DevCsr& A, const AggDev& agg, const double* pval);
 
 }  // namespace aggmg_b200
