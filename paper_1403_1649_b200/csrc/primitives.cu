@@ -215,10 +215,75 @@ __global__ void k_segsort(const idx* offsets, int64_t nseg, const idx* kin, idx*
 }
 }  // namespace
 
+namespace {
+constexpr int kSmallSeg = 16;
+// Thread per segment for short segments (insertion sort in registers); longer segments
+// are listed for the warp kernel.
+__global__ void k_segsort_small(const idx* offsets, int64_t nseg, const idx* kin, idx* kout,
+                                const double* vin, double* vout, idx* long_list, int* n_long) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const idx lo = offsets[s], L = offsets[s + 1] - lo;
+  if (L > kSmallSeg) {
+    long_list[atomicAdd(n_long, 1)] = static_cast<idx>(s);
+    return;
+  }
+  idx k[kSmallSeg];
+  double v[kSmallSeg];
+#pragma unroll
+  for (int q = 0; q < kSmallSeg; ++q) {
+    if (q < L) {
+      k[q] = kin[lo + q];
+      if (vout) v[q] = vin[lo + q];
+    }
+  }
+  for (int q = 1; q < L; ++q) {
+    const idx kq = k[q];
+    const double vq = vout ? v[q] : 0.0;
+    int z = q - 1;
+    while (z >= 0 && k[z] > kq) {
+      k[z + 1] = k[z];
+      if (vout) v[z + 1] = v[z];
+      --z;
+    }
+    k[z + 1] = kq;
+    if (vout) v[z + 1] = vq;
+  }
+  for (int q = 0; q < L; ++q) {
+    kout[lo + q] = k[q];
+    if (vout) vout[lo + q] = v[q];
+  }
+}
+
+__global__ void k_segsort_list(const idx* list, const int* n_list, const idx* offsets,
+                               const idx* kin, idx* kout, const double* vin, double* vout) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= *n_list) return;
+  const idx s = list[w];
+  const idx lo = offsets[s], L = offsets[s + 1] - lo;
+  for (idx e = lane; e < L; e += 32) {
+    const idx key = kin[lo + e];
+    idx rank = 0;
+    for (idx q = 0; q < L; ++q) rank += (kin[lo + q] < key) ? 1 : 0;
+    kout[lo + rank] = key;
+    if (vout) vout[lo + rank] = vin[lo + e];
+  }
+}
+}  // namespace
+
 void segmented_sort(const idx* offsets, int64_t nseg, const idx* kin, idx* kout, const double* vin,
                     double* vout) {
   if (nseg <= 0) return;
-  AGG_LAUNCH(k_segsort, grid_for(nseg * 32, 256), 256, 0, offsets, nseg, kin, kout, vin, vout);
+  DevBuf<idx> list(nseg);
+  DevBuf<int> n_long(1);
+  n_long.zero();
+  AGG_LAUNCH(k_segsort_small, grid_for(nseg, 128), 128, 0, offsets, nseg, kin, kout, vin, vout,
+             list.get(), n_long.get());
+  const int nl = read_scalar(n_long.get());
+  if (nl > 0)
+    AGG_LAUNCH(k_segsort_list, grid_for(static_cast<int64_t>(nl) * 32, 256), 256, 0, list.get(),
+               n_long.get(), offsets, kin, kout, vin, vout);
 }
 
 // ---- helpers -----------------------------------------------------------------------
