@@ -13,25 +13,36 @@
 
 namespace aggmg_b200 {
 
-constexpr int kChunk = 8192;       // vector_ops.hpp:18
-constexpr int kChunkThreads = 256;
-// elements per pipeline stage (two stages of NP tiles must fit in 48 KB static smem)
-template <int NP>
-struct ChunkTile {
-  static constexpr int value = NP >= 3 ? 512 : 1024;
-};
+constexpr int kChunk = 8192;  // vector_ops.hpp:18
+// CTA layout: warp 0 is the consumer (lanes 0..NP-1 each run one sequential chain),
+// warps 1..3 produce tiles (elementwise op + products) into a double buffer.
+constexpr int kChunkThreads = 128;
+constexpr int kChunkProducers = kChunkThreads - 32;
+constexpr int kChunkTile = 8 * kChunkProducers;  // 768 elements per stage
 
 // Process-wide switch for the solve-phase reductions: exact (reference order) or tree
 // (default).  The smoother setup and the public dot/norm2 always use the exact order.
 bool exact_reductions();
 void set_exact_reductions(bool on);
 
+__device__ inline void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ inline void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// One CTA per 8192-element chunk.  Producers fill stage b = t & 1 and arrive on FULL[b];
+// the consumer waits on FULL[b], adds the stage sequentially, arrives on EMPTY[b]; the
+// producers wait on EMPTY[b] before refilling it two tiles later.  The chain latency
+// (8192 dependent adds) overlaps the memory traffic, and 16 CTAs per SM put every chunk
+// of a 16.7 M vector in flight at once.
 template <int NP, class Op>
 __global__ void __launch_bounds__(kChunkThreads)
     k_chunked(int64_t n, Op op, double* partials, unsigned* ticket, double* out) {
-  constexpr int kChunkTile = ChunkTile<NP>::value;
-  __shared__ double tile[2][NP][kChunkTile];
+  __shared__ __align__(16) double tile[2][NP][kChunkTile];
   __shared__ bool last;
+  constexpr int kFull0 = 1, kEmpty0 = 3;  // named barrier ids 1,2 (full) and 3,4 (empty)
   if (!op.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) op.inactive();
     return;
@@ -39,44 +50,55 @@ __global__ void __launch_bounds__(kChunkThreads)
   op.init();
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kChunk;
   const int len = static_cast<int>(min(static_cast<int64_t>(kChunk), n - c0));
+  const int ntiles = (len + kChunkTile - 1) / kChunkTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool summer = lane == 0 && warp < NP;
   double acc = 0.0;
-  for (int tb = 0, t = 0; tb < len; tb += kChunkTile, ++t) {
-    double(*buf)[kChunkTile] = tile[t & 1];
+  if (warp > 0) {  // producers
+    const int pt = threadIdx.x - 32;
+    for (int t = 0; t < ntiles; ++t) {
+      const int b = t & 1;
+      if (t >= 2) named_sync(kEmpty0 + b, kChunkThreads);
+      const int tb = t * kChunkTile;
 #pragma unroll
-    for (int j = 0; j < kChunkTile / kChunkThreads; ++j) {
-      const int pos = tb + j * kChunkThreads + threadIdx.x;
-      if (pos < len) {
-        double p[NP];
-        op(c0 + pos, p);
+      for (int j = 0; j < kChunkTile / kChunkProducers; ++j) {
+        const int pos = tb + j * kChunkProducers + pt;
+        if (pos < len) {
+          double p[NP];
+          op(c0 + pos, p);
 #pragma unroll
-        for (int k = 0; k < NP; ++k) buf[k][pos - tb] = p[k];
+          for (int k = 0; k < NP; ++k) tile[b][k][pos - tb] = p[k];
+        }
       }
+      named_arrive(kFull0 + b, kChunkThreads);
     }
-    __syncthreads();
-    if (summer) {
-      const int m = min(kChunkTile, len - tb);
-      const double* src = buf[warp];
-      int q = 0;
-      for (; q + 8 <= m; q += 8) {
-        const double2 a = *reinterpret_cast<const double2*>(src + q);
-        const double2 b = *reinterpret_cast<const double2*>(src + q + 2);
-        const double2 c = *reinterpret_cast<const double2*>(src + q + 4);
-        const double2 d = *reinterpret_cast<const double2*>(src + q + 6);
-        acc = __dadd_rn(acc, a.x);
-        acc = __dadd_rn(acc, a.y);
-        acc = __dadd_rn(acc, b.x);
-        acc = __dadd_rn(acc, b.y);
-        acc = __dadd_rn(acc, c.x);
-        acc = __dadd_rn(acc, c.y);
-        acc = __dadd_rn(acc, d.x);
-        acc = __dadd_rn(acc, d.y);
+  } else {  // consumer warp
+    for (int t = 0; t < ntiles; ++t) {
+      const int b = t & 1;
+      named_sync(kFull0 + b, kChunkThreads);
+      if (lane < NP) {
+        const int m = min(kChunkTile, len - t * kChunkTile);
+        const double* src = tile[b][lane];
+        int q = 0;
+        for (; q + 8 <= m; q += 8) {
+          const double2 a = *reinterpret_cast<const double2*>(src + q);
+          const double2 c = *reinterpret_cast<const double2*>(src + q + 2);
+          const double2 d = *reinterpret_cast<const double2*>(src + q + 4);
+          const double2 e = *reinterpret_cast<const double2*>(src + q + 6);
+          acc = __dadd_rn(acc, a.x);
+          acc = __dadd_rn(acc, a.y);
+          acc = __dadd_rn(acc, c.x);
+          acc = __dadd_rn(acc, c.y);
+          acc = __dadd_rn(acc, d.x);
+          acc = __dadd_rn(acc, d.y);
+          acc = __dadd_rn(acc, e.x);
+          acc = __dadd_rn(acc, e.y);
+        }
+        for (; q < m; ++q) acc = __dadd_rn(acc, src[q]);
       }
-      for (; q < m; ++q) acc = __dadd_rn(acc, src[q]);
+      if (t + 2 < ntiles) named_arrive(kEmpty0 + b, kChunkThreads);
     }
+    if (lane < NP) partials[blockIdx.x * NP + lane] = acc;
   }
-  if (summer) partials[blockIdx.x * NP + warp] = acc;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);

@@ -34,8 +34,25 @@ __global__ void __launch_bounds__(kB) k_pcg_update(int64_t n, PcgSlots* s, int p
   const double alpha = __ddiv_rn(s->q[par][0], s->pAp);
   const double malpha = -alpha;
   double acc[1] = {0.0};
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  // 128-bit loads/stores: pairs (2i, 2i+1); the odd tail element goes to the last pair slot
+  const int64_t npair = n >> 1;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < npair; q += stride) {
+    const double2 pq = reinterpret_cast<const double2*>(p)[q];
+    const double2 aq = reinterpret_cast<const double2*>(Ap)[q];
+    const double2 rq = reinterpret_cast<const double2*>(r)[q];
+    double2 xq = reinterpret_cast<double2*>(x)[q];
+    xq.x = __dadd_rn(xq.x, __dmul_rn(alpha, pq.x));
+    xq.y = __dadd_rn(xq.y, __dmul_rn(alpha, pq.y));
+    reinterpret_cast<double2*>(x)[q] = xq;
+    const double v0 = __dadd_rn(rq.x, __dmul_rn(malpha, aq.x));
+    const double v1 = __dadd_rn(rq.y, __dmul_rn(malpha, aq.y));
+    reinterpret_cast<double2*>(rn)[q] = make_double2(v0, v1);
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(v0, v0));
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(v1, v1));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t i = n - 1;
     x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
     const double v = __dadd_rn(r[i], __dmul_rn(malpha, Ap[i]));
     rn[i] = v;

@@ -127,10 +127,19 @@ __global__ void __launch_bounds__(kRedBlock) k_dot(DotArgs args, int64_t n, doub
 #pragma unroll
   for (int k = 0; k < NP; ++k) v[k] = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+  const int64_t npair = n >> 1;  // 128-bit loads; the odd tail element handled once below
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < npair; q += stride) {
 #pragma unroll
-    for (int k = 0; k < NP; ++k) v[k] = __dadd_rn(v[k], __dmul_rn(args.a[k][i], args.b[k][i]));
+    for (int k = 0; k < NP; ++k) {
+      const double2 a = reinterpret_cast<const double2*>(args.a[k])[q];
+      const double2 b = reinterpret_cast<const double2*>(args.b[k])[q];
+      v[k] = __dadd_rn(v[k], __dmul_rn(a.x, b.x));
+      v[k] = __dadd_rn(v[k], __dmul_rn(a.y, b.y));
+    }
   }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < NP; ++k) v[k] = __dadd_rn(v[k], __dmul_rn(args.a[k][n - 1], args.b[k][n - 1]));
   block_reduce<NP>(v, smem);
   if (threadIdx.x == 0)
 #pragma unroll
