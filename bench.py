@@ -41,9 +41,12 @@ CONFIGS = {
            256, 256, 1.0, 0.5, "pcg"),
     "c3": ("3D anisotropic 7-point (eps=1e-3) 384^3, FGMRES(30) + K-cycle to 1e-8", 3, 384, 384,
            384, 1e-3, 0.5, "fgmres"),
+    "c4": ("3D variable-coefficient jumping diffusion 27-point 256^3 (jump 1e6, 32^3 blocks), "
+           "PCG + K-cycle to 1e-8", 27, 256, 256, 256, 1e6, 0.5, "pcg"),
     "c5": ("3D 7-point Poisson 512^3 (134M unknowns), PCG + K-cycle to 1e-8", 3, 512, 512, 512,
            1.0, 0.5, "pcg"),
 }
+JUMP_BLOCK = 32  # c4: coefficient jump on a checkerboard of 32^3 blocks
 PROF_SMOOTH, PROF_SPMV = 1, 2
 METRIC = "setup+solve DOF/s"
 
@@ -173,7 +176,9 @@ def cpu_reference_run(M, cfg_name, sample_n, threads):
     label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[cfg_name]
     r = M.ref()
     r.lib.fn("set_num_threads")(threads)
-    if dims == 3:
+    if dims == 27:
+        A = M.oracle().generate_jump27(sample_n, sample_n, sample_n, eps, JUMP_BLOCK)
+    elif dims == 3:
         A = r.generate_poisson(3, sample_n, sample_n, sample_n, eps)
     else:
         A = r.generate_poisson(2, sample_n, sample_n, 1, eps)
@@ -192,7 +197,7 @@ def run_reference_arm(args, world, rank):
         return 0
     threads = os.cpu_count() or 1
     dims = CONFIGS[args.config][1]
-    sample_n = args.ref_sample or (96 if dims == 3 else 512)
+    sample_n = args.ref_sample or (512 if dims == 2 else (64 if dims == 27 else 96))
     times, n = [], 0
     for i in range(args.warmup + args.steps):
         n, dt, res = cpu_reference_run(M, args.config, sample_n, threads)
@@ -200,7 +205,7 @@ def run_reference_arm(args, world, rank):
             times.append(dt)
     total = sum(times)
     value = n * len(times) / total
-    sample = (f"{sample_n}^{dims} grid of the same problem class, full setup+solve per step "
+    sample = (f"{sample_n}^{2 if dims == 2 else 3} grid of the same problem class, full setup+solve per step "
               f"(reference default Galerkin path), {res.report.iterations} iterations")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s",
@@ -235,7 +240,10 @@ def run_b200(args, world, rank, local):
     s_c, c_c, v_c = setup._c(), cycle._c(), solver._c()
 
     dm = C.c_void_p()
-    check(lib.fn("dmatrix_poisson")(dims, nx, ny, nz, eps, -1, C.byref(dm)))
+    if dims == 27:
+        check(lib.fn("dmatrix_jump27")(nx, ny, nz, eps, JUMP_BLOCK, C.byref(dm)))
+    else:
+        check(lib.fn("dmatrix_poisson")(dims, nx, ny, nz, eps, -1, C.byref(dm)))
     n_, nnz_ = C.c_int64(), C.c_int64()
     check(lib.fn("dmatrix_size")(dm, C.byref(n_), C.byref(nnz_)))
     n, nnz = n_.value, nnz_.value
@@ -288,7 +296,8 @@ def run_b200(args, world, rank, local):
     # ---- end to end through the host C-ABI (host CSR in, x out) ----
     e2e = None
     if not args.no_e2e:
-        Ah = gpu.generate_poisson(dims, nx, ny, nz, eps)
+        Ah = (gpu.generate_jump27(nx, ny, nz, eps, JUMP_BLOCK) if dims == 27
+              else gpu.generate_poisson(dims, nx, ny, nz, eps))
         b = np.ones(n)
         gpu.setup_and_solve(Ah, b, setup, cycle, solver)  # warm-up
         dist.barrier()
@@ -306,10 +315,10 @@ def run_b200(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and os.path.exists(_abi.REF_LIB):
         threads = os.cpu_count() or 1
-        sample_n = 128 if dims == 3 else 512
+        sample_n = 512 if dims == 2 else (96 if dims == 27 else 128)
         ns, dt, cres = cpu_reference_run(M, args.config, sample_n, threads)
         cpu = {"value": ns / dt, "unit": "DOF/s", "cores": threads, "kind": "reference",
-               "sample": f"one setup+solve of the {sample_n}^{dims} grid (reference default "
+               "sample": f"one setup+solve of the {sample_n}^{2 if dims == 2 else 3} grid (reference default "
                          f"Galerkin path, {cres.report.iterations} its, {dt:.1f} s)"}
 
     peak, peak_src = load_peak()
@@ -332,7 +341,8 @@ def run_b200(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: device-generated Poisson matrix (poisson.cpp semantics), b = B0 = ones, x0 = 0",
+        "data": ("synthetic: device-generated " + ("27-point jumping-coefficient matrix (DESIGN.md §7)"
+                 if dims == 27 else "Poisson matrix (poisson.cpp semantics)") + ", b = B0 = ones, x0 = 0"),
         "config": {"workload": label, "n": n, "nnz": nnz, "levels": r0.get("levels"),
                    "iterations": r0.get("iterations"), "converged": r0.get("converged"),
                    "setup_ms": statistics.median(r["setup_ms"] for r in records),
@@ -340,7 +350,7 @@ def run_b200(args, world, rank, local):
                    "solve_dof_per_s": n / statistics.median(r["solve_s"] for r in records),
                    "level0_spmv_residual_gbs": spmv_gbs,
                    "galerkin": "cached sort/segmented reduce (reference reuse_caches=true order)",
-                   "l2": "inputs larger than L2 (A alone is 1.4 GB at 256^3)",
+                   "l2": f"inputs larger than L2 (A alone is {(12 * nnz + 4 * n) / 1e9:.2f} GB)",
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
         "roofline": roof,
         "cpu_baseline": cpu,
