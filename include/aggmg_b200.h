@@ -261,6 +261,70 @@ int aggmg_hierarchy_level_dmatrix(const aggmg_hierarchy* h, int64_t k, int which
 int aggmg_solve_device(const aggmg_hierarchy* h, const aggmg_cycle_config* cycle,
                        const aggmg_solver_config* cfg, double* x, aggmg_solve_report* report);
 
+/* ---- row-partitioned multi-GPU path (no reference analogue: the reference
+ * is single-process OpenMP, parallel.hpp:40-74) --------------------------------------------
+ * Fine levels are split into contiguous row slabs, one per rank; levels at or below
+ * `agglomerate_rows` are gathered onto rank 0.  Every call below is COLLECTIVE over the
+ * communicator (all ranks call it in the same order).  Setup artefacts equal the one-GPU
+ * hierarchy bit for bit; solve scalars are summed over ranks in rank order. */
+typedef struct aggmg_comm aggmg_comm;
+typedef struct aggmg_dist_matrix aggmg_dist_matrix;
+typedef struct aggmg_dist_hierarchy aggmg_dist_hierarchy;
+
+/* one process per GPU over NCCL: rank 0 creates the id, the launcher broadcasts it;
+ * call aggmg_init(local_device) first */
+int aggmg_comm_nccl_unique_id(char id[128]);
+int aggmg_comm_init_nccl(int rank, int nranks, const char id[128], aggmg_comm** out);
+/* R ranks as R threads of this process (devices[r] per rank, may repeat): fn(comm, rank,
+ * user) runs on every rank thread; returns the first non-zero fn result (or an error). */
+typedef int (*aggmg_rank_fn)(aggmg_comm* comm, int rank, void* user);
+int aggmg_comm_run_threads(int nranks, const int* devices, aggmg_rank_fn fn, void* user);
+int aggmg_comm_rank(const aggmg_comm* c);
+int aggmg_comm_size(const aggmg_comm* c);
+const char* aggmg_comm_kind(const aggmg_comm* c);
+void aggmg_comm_free(aggmg_comm* c);
+
+/* this rank's rows [row0, row0 + rows->n_rows) of an n_global x n_global matrix, global
+ * column ids (canonical rows) */
+int aggmg_dist_matrix_from_host(aggmg_comm* c, int64_t n_global, int64_t row0,
+                                const aggmg_csr* rows, aggmg_dist_matrix** out);
+/* generated in HBM on every rank (even row partition) — poisson.cpp:15-77 / DESIGN.md §7 */
+int aggmg_dist_matrix_poisson(aggmg_comm* c, int dims, int64_t nx, int64_t ny, int64_t nz,
+                              double epsilon, int weak_axis, aggmg_dist_matrix** out);
+int aggmg_dist_matrix_jump27(aggmg_comm* c, int64_t nx, int64_t ny, int64_t nz, double jump,
+                             int64_t block, aggmg_dist_matrix** out);
+int aggmg_dist_matrix_info(const aggmg_dist_matrix* A, int64_t* n_global, int64_t* row0,
+                           int64_t* n_local, int64_t* nnz_local);
+void aggmg_dist_matrix_free(aggmg_dist_matrix* A);
+
+/* setup_hierarchy (hierarchy.hpp:57) over the ranks; B0_local (host, this rank's rows) may be
+ * NULL = ones; agglomerate_rows <= 0 picks the default (max(coarse_size_max, 2^16)) */
+int aggmg_dist_setup(aggmg_comm* c, const aggmg_dist_matrix* A0, const double* B0_local,
+                     const aggmg_setup_config* cfg, int64_t agglomerate_rows,
+                     aggmg_dist_hierarchy** out);
+/* pcg/fgmres (krylov.hpp:43-50) preconditioned by the partitioned cycle, x0 = 0;
+ * b_local (host) NULL = ones; x_local (host) may be NULL */
+int aggmg_dist_solve(aggmg_dist_hierarchy* h, const aggmg_cycle_config* cycle,
+                     const aggmg_solver_config* cfg, const double* b_local, double* x_local,
+                     aggmg_solve_report* report);
+/* z = M r on this rank's rows (apply_preconditioner, cycles.hpp:42) */
+int aggmg_dist_apply_preconditioner(aggmg_dist_hierarchy* h, const aggmg_cycle_config* cycle,
+                                    const double* r_local, double* z_local);
+int aggmg_dist_hierarchy_info(const aggmg_dist_hierarchy* h, int64_t* n_levels,
+                              int64_t* n_distributed, double* setup_ms);
+int aggmg_dist_hierarchy_level_size(const aggmg_dist_hierarchy* h, int64_t k, int64_t* n,
+                                    int64_t* nnz);
+/* level k's artefacts gathered on rank 0 (global numbering; other ranks receive nothing):
+ * operator, aggregation (assignment[n_k], mis sweeps), P values (pval[n_k]), B[n_k], omega */
+int aggmg_dist_hierarchy_level_A(aggmg_dist_hierarchy* h, int64_t k, aggmg_csr* A);
+int aggmg_dist_hierarchy_level_transfer(aggmg_dist_hierarchy* h, int64_t k, int64_t* assignment,
+                                        double* pval, int32_t* mis_sweeps);
+int aggmg_dist_hierarchy_level_B(aggmg_dist_hierarchy* h, int64_t k, double* B);
+int aggmg_dist_hierarchy_level_omega(aggmg_dist_hierarchy* h, int64_t k, double* omega);
+int64_t aggmg_dist_hierarchy_n_warnings(const aggmg_dist_hierarchy* h);
+const char* aggmg_dist_hierarchy_warning(const aggmg_dist_hierarchy* h, int64_t i);
+void aggmg_dist_hierarchy_free(aggmg_dist_hierarchy* h);
+
 /* ---- measurement ------------------------------------------------------------------ */
 
 /* Per-kernel-family CUDA-event timing on the library stream.  mask has bit (1 << f) set

@@ -75,6 +75,8 @@ class SolveReportC(C.Structure):
 
 
 csrp = C.POINTER(CSR)
+# int (*)(aggmg_comm*, int rank, void* user)
+RANK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p)
 I = C.c_int
 L = C.c_int64
 
@@ -156,6 +158,32 @@ SIGNATURES = {
     "timer_start": (I, []),
     "timer_stop": (I, [f64p]),
     "setup_config_default": (None, [C.POINTER(SetupConfigC)]),
+    # row-partitioned multi-GPU path
+    "comm_nccl_unique_id": (I, [C.c_char_p]),
+    "comm_init_nccl": (I, [I, I, C.c_char_p, C.POINTER(vp)]),
+    "comm_run_threads": (I, [I, i32p, vp, vp]),
+    "comm_rank": (I, [vp]),
+    "comm_size": (I, [vp]),
+    "comm_kind": (C.c_char_p, [vp]),
+    "comm_free": (None, [vp]),
+    "dist_matrix_from_host": (I, [vp, L, L, csrp, C.POINTER(vp)]),
+    "dist_matrix_poisson": (I, [vp, I, L, L, L, C.c_double, I, C.POINTER(vp)]),
+    "dist_matrix_jump27": (I, [vp, L, L, L, C.c_double, L, C.POINTER(vp)]),
+    "dist_matrix_info": (I, [vp, i64p, i64p, i64p, i64p]),
+    "dist_matrix_free": (None, [vp]),
+    "dist_setup": (I, [vp, vp, f64p, C.POINTER(SetupConfigC), L, C.POINTER(vp)]),
+    "dist_solve": (I, [vp, C.POINTER(CycleConfigC), C.POINTER(SolverConfigC), f64p, f64p,
+                       C.POINTER(SolveReportC)]),
+    "dist_apply_preconditioner": (I, [vp, C.POINTER(CycleConfigC), f64p, f64p]),
+    "dist_hierarchy_info": (I, [vp, i64p, i64p, f64p]),
+    "dist_hierarchy_level_size": (I, [vp, L, i64p, i64p]),
+    "dist_hierarchy_level_A": (I, [vp, L, csrp]),
+    "dist_hierarchy_level_transfer": (I, [vp, L, i64p, f64p, i32p]),
+    "dist_hierarchy_level_B": (I, [vp, L, f64p]),
+    "dist_hierarchy_level_omega": (I, [vp, L, f64p]),
+    "dist_hierarchy_n_warnings": (L, [vp]),
+    "dist_hierarchy_warning": (C.c_char_p, [vp, L]),
+    "dist_hierarchy_free": (None, [vp]),
     "cycle_config_default": (None, [C.POINTER(CycleConfigC)]),
     "solver_config_default": (None, [C.POINTER(SolverConfigC)]),
 }

@@ -9,8 +9,11 @@
 #include <string>
 #include <vector>
 
+#include <thread>
+
 #include "../../include/aggmg_b200.h"
 #include "chunked.cuh"
+#include "dist_solve.cuh"
 #include "krylov.cuh"
 #include "vecops.cuh"
 
@@ -31,6 +34,18 @@ struct aggmg_galerkin_cache {
 };
 struct aggmg_dmatrix {
   DevCsrPtr A;
+};
+struct aggmg_comm {
+  std::unique_ptr<Comm> comm;
+};
+struct aggmg_dist_matrix {
+  Comm* comm = nullptr;
+  DistCsrPtr A;
+};
+struct aggmg_dist_hierarchy {
+  Comm* comm = nullptr;
+  DistCsrPtr A0;
+  std::unique_ptr<DistHierarchy> h;
 };
 
 namespace {
@@ -204,6 +219,50 @@ const DevLevel& level(const aggmg_hierarchy* h, int64_t k) {
   return h->h->levels[k];
 }
 
+}  // namespace
+
+namespace {
+aggmg_dist_matrix* wrap_rows(aggmg_comm* c, int64_t n_global, int64_t row0, DevCsrPtr rows) {
+  Comm& comm = *c->comm;
+  const std::vector<int64_t> counts = comm.allgather_host({rows->n_rows});
+  const std::vector<int64_t> starts = comm.allgather_host({row0});
+  const Partition part = Partition::from_counts(counts);
+  for (int r = 0; r < comm.size(); ++r)
+    require(starts[r] == part.begin(r), "dist matrix: rank row ranges must be contiguous, in rank order");
+  require(part.n() == n_global, "dist matrix: the ranks' rows do not cover the matrix");
+  auto m = std::make_unique<aggmg_dist_matrix>();
+  m->comm = &comm;
+  m->A = make_dist(comm, part, part, *rows);
+  return m.release();
+}
+int64_t dist_rows_begin(int64_t n, const Comm& comm) {
+  return Partition::even(n, comm.size()).begin(comm.rank());
+}
+int64_t dist_rows_count(int64_t n, const Comm& comm) {
+  return Partition::even(n, comm.size()).count(comm.rank());
+}
+// generic gather of `count` POD values per rank onto rank 0 (rank order)
+template <class T>
+void gather_pod(Comm& comm, const T* local, int64_t count, DevBuf<T>& all) {
+  const std::vector<int64_t> cnt = comm.allgather_host({count});
+  std::vector<CommMsg> s, r;
+  s.push_back({0, const_cast<T*>(local), sizeof(T) * count});
+  if (comm.rank() == 0) {
+    int64_t tot = 0;
+    for (int64_t v : cnt) tot += v;
+    all.resize(tot);
+    int64_t off = 0;
+    for (int q = 0; q < comm.size(); ++q) {
+      r.push_back({q, all.get() + off, sizeof(T) * cnt[q]});
+      off += cnt[q];
+    }
+  }
+  comm.exchange(s, r);
+}
+DistHierarchy& dh(aggmg_dist_hierarchy* h) {
+  require(h && h->h, "null distributed hierarchy");
+  return *h->h;
+}
 }  // namespace
 
 extern "C" {
@@ -893,5 +952,270 @@ int aggmg_bench_kernel(const aggmg_dmatrix* A, int kind, int reps, double* avg_m
     *bytes = spmv_bytes(M, epi);
   });
 }
+
+
+// ---- row-partitioned multi-GPU path -------------------------------------------------------
+
+int aggmg_comm_nccl_unique_id(char id[128]) {
+  return guarded([&] { nccl_unique_id(id); });
+}
+
+int aggmg_comm_init_nccl(int rank, int nranks, const char id[128], aggmg_comm** out) {
+  return guarded([&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "comm: rank out of range");
+    auto c = std::make_unique<aggmg_comm>();
+    c->comm = make_nccl_comm(rank, nranks, id);
+    *out = c.release();
+  });
+}
+
+int aggmg_comm_run_threads(int nranks, const int* devices, aggmg_rank_fn fn, void* user) {
+  return guarded([&] {
+    require(nranks >= 1 && nranks <= 64, "comm: 1..64 ranks");
+    require(fn != nullptr, "comm: null rank function");
+    auto group = ThreadComm::make_group(nranks);
+    std::vector<int> rc(nranks, 0);
+    std::vector<std::string> msg(nranks);
+    std::vector<std::thread> th;
+    for (int r = 0; r < nranks; ++r)
+      th.emplace_back([&, r] {
+        try {
+          init_device(devices ? devices[r] : 0);
+          aggmg_comm c;
+          c.comm = std::make_unique<ThreadComm>(group, r, nranks);
+          rc[r] = fn(&c, r, user);
+          if (rc[r] != 0) {
+            msg[r] = aggmg_last_error();
+            thread_group_abort(*group);
+          }
+          cudaStreamSynchronize(stream());
+        } catch (const std::exception& e) {
+          rc[r] = AGGMG_ERR;
+          msg[r] = e.what();
+          thread_group_abort(*group);
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int r = 0; r < nranks; ++r)
+      if (rc[r] != 0)
+        throw Error("rank " + std::to_string(r) + ": " + (msg[r].empty() ? "failed" : msg[r]));
+  });
+}
+
+int aggmg_comm_rank(const aggmg_comm* c) { return c ? c->comm->rank() : -1; }
+int aggmg_comm_size(const aggmg_comm* c) { return c ? c->comm->size() : 0; }
+const char* aggmg_comm_kind(const aggmg_comm* c) { return c ? c->comm->kind() : ""; }
+void aggmg_comm_free(aggmg_comm* c) { delete c; }
+
+
+int aggmg_dist_matrix_from_host(aggmg_comm* c, int64_t n_global, int64_t row0, const aggmg_csr* rows,
+                                aggmg_dist_matrix** out) {
+  return guarded([&] {
+    require(c && rows, "dist matrix: null argument");
+    require(rows->n_cols == n_global, "dist matrix: rows must use global column ids");
+    DevCsrPtr R = upload_csr(rows->n_rows, rows->n_cols, rows->row_offsets, rows->col_indices,
+                             rows->values, true);
+    *out = wrap_rows(c, n_global, row0, R);
+  });
+}
+
+int aggmg_dist_matrix_poisson(aggmg_comm* c, int dims, int64_t nx, int64_t ny, int64_t nz,
+                              double epsilon, int weak_axis, aggmg_dist_matrix** out) {
+  return guarded([&] {
+    const int64_t n = nx * ny * (dims == 2 ? 1 : nz);
+    DevCsrPtr R = generate_poisson_rows(dims, nx, ny, nz, epsilon, weak_axis,
+                                        dist_rows_begin(n, *c->comm), dist_rows_count(n, *c->comm));
+    *out = wrap_rows(c, n, dist_rows_begin(n, *c->comm), R);
+  });
+}
+
+int aggmg_dist_matrix_jump27(aggmg_comm* c, int64_t nx, int64_t ny, int64_t nz, double jump,
+                             int64_t block, aggmg_dist_matrix** out) {
+  return guarded([&] {
+    const int64_t n = nx * ny * nz;
+    DevCsrPtr R = generate_jump27_rows(nx, ny, nz, jump, block, dist_rows_begin(n, *c->comm),
+                                       dist_rows_count(n, *c->comm));
+    *out = wrap_rows(c, n, dist_rows_begin(n, *c->comm), R);
+  });
+}
+
+int aggmg_dist_matrix_info(const aggmg_dist_matrix* A, int64_t* n_global, int64_t* row0,
+                           int64_t* n_local, int64_t* nnz_local) {
+  return guarded([&] {
+    require(A && A->A, "null dist matrix");
+    const int me = A->comm->rank();
+    if (n_global) *n_global = A->A->rows.n();
+    if (row0) *row0 = A->A->rows.begin(me);
+    if (n_local) *n_local = A->A->A.n_rows;
+    if (nnz_local) *nnz_local = A->A->A.nnz;
+  });
+}
+
+void aggmg_dist_matrix_free(aggmg_dist_matrix* A) { delete A; }
+
+int aggmg_dist_setup(aggmg_comm* c, const aggmg_dist_matrix* A0, const double* B0_local,
+                     const aggmg_setup_config* cfg, int64_t agglomerate_rows,
+                     aggmg_dist_hierarchy** out) {
+  return guarded([&] {
+    require(c && A0 && A0->A, "dist setup: null argument");
+    Comm& comm = *c->comm;
+    DevBuf<double> B;
+    if (B0_local) B = up_vec(B0_local, A0->A->A.n_rows);
+    const SetupCfg s = to_cfg(cfg);
+    if (agglomerate_rows <= 0) agglomerate_rows = std::max<int64_t>(s.coarse_size_max, int64_t{1} << 16);
+    auto h = std::make_unique<aggmg_dist_hierarchy>();
+    h->comm = &comm;
+    h->A0 = A0->A;
+    h->h = dist_setup_hierarchy(comm, A0->A, B0_local ? B.get() : nullptr, s, agglomerate_rows);
+    *out = h.release();
+  });
+}
+
+int aggmg_dist_solve(aggmg_dist_hierarchy* h, const aggmg_cycle_config* cycle,
+                     const aggmg_solver_config* cfg, const double* b_local, double* x_local,
+                     aggmg_solve_report* report) {
+  return guarded([&] {
+    DistHierarchy& H = dh(h);
+    const int64_t n = h->A0->A.n_rows;
+    DevBuf<double> db(n), dx(n);
+    if (b_local)
+      db.upload(b_local, n);
+    else
+      fill_double(db.get(), n, 1.0);
+    dx.zero();
+    SolveOut o = dist_solve(H, *h->A0, to_cfg(cycle), to_cfg(cfg), db.get(), dx.get());
+    if (x_local) {
+      dx.download(x_local, n);
+      sync();
+    }
+    fill_report(o, report);
+  });
+}
+
+int aggmg_dist_apply_preconditioner(aggmg_dist_hierarchy* h, const aggmg_cycle_config* cycle,
+                                    const double* r_local, double* z_local) {
+  return guarded([&] {
+    DistHierarchy& H = dh(h);
+    H.ensure_workspace();
+    const int64_t n = h->A0->A.n_rows;
+    const int64_t cap = H.kd() ? H.levels[0].halo_cap : 0;
+    DevBuf<double> dr(n), dz(n + cap);
+    dr.upload(r_local, n);
+    dist_apply_preconditioner(H, to_cfg(cycle), dr.get(), dz.get());
+    dz.download(z_local, n);
+    sync();
+  });
+}
+
+int aggmg_dist_hierarchy_info(const aggmg_dist_hierarchy* h, int64_t* n_levels, int64_t* n_distributed,
+                              double* setup_ms) {
+  return guarded([&] {
+    require(h && h->h, "null distributed hierarchy");
+    if (n_levels) *n_levels = h->h->n_levels_total;
+    if (n_distributed) *n_distributed = h->h->kd();
+    if (setup_ms) *setup_ms = h->h->setup_ms;
+  });
+}
+
+int aggmg_dist_hierarchy_level_size(const aggmg_dist_hierarchy* h, int64_t k, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    require(h && h->h, "null distributed hierarchy");
+    require(k >= 0 && k < h->h->n_levels_total, "hierarchy: level index out of range");
+    if (n) *n = h->h->level_rows[k];
+    if (nnz) *nnz = h->h->level_nnz[k];
+  });
+}
+
+int aggmg_dist_hierarchy_level_A(aggmg_dist_hierarchy* h, int64_t k, aggmg_csr* A) {
+  return guarded([&] {
+    DistHierarchy& H = dh(h);
+    require(k >= 0 && k < H.n_levels_total, "hierarchy: level index out of range");
+    Comm& comm = *H.comm;
+    A->n_rows = A->n_cols = A->nnz = 0;
+    A->row_offsets = nullptr;
+    A->col_indices = nullptr;
+    A->values = nullptr;
+    if (k < H.kd()) {
+      DevCsrPtr G = gather_to_root(comm, *H.levels[k].A, 0);
+      if (comm.rank() == 0) down(*G, A);
+    } else if (comm.rank() == 0) {
+      down(*H.tail->levels[k - H.kd()].A, A);
+    }
+  });
+}
+
+int aggmg_dist_hierarchy_level_transfer(aggmg_dist_hierarchy* h, int64_t k, int64_t* assignment,
+                                        double* pval, int32_t* mis_sweeps) {
+  return guarded([&] {
+    DistHierarchy& H = dh(h);
+    require(k >= 0 && k + 1 < H.n_levels_total, "hierarchy: level has no transfer");
+    Comm& comm = *H.comm;
+    if (k < H.kd()) {
+      const DistLevel& L = H.levels[k];
+      const int64_t n = L.A->A.n_rows;
+      DevBuf<idx> a_all;
+      DevBuf<double> p_all;
+      gather_pod<idx>(comm, L.agg_global.get(), n, a_all);
+      gather_pod<double>(comm, L.pval.get(), n, p_all);
+      if (comm.rank() == 0) {
+        if (assignment) down_index(a_all, a_all.size(), assignment);
+        if (pval) {
+          p_all.download(pval, p_all.size());
+          sync();
+        }
+        if (mis_sweeps) *mis_sweeps = L.mis_sweeps;
+      }
+    } else if (comm.rank() == 0) {
+      const DevLevel& L = H.tail->levels[k - H.kd()];
+      if (assignment) down_index(L.agg.assignment, L.agg.n_fine, assignment);
+      if (pval) {
+        L.tr.pval.download(pval, L.agg.n_fine);
+        sync();
+      }
+      if (mis_sweeps) *mis_sweeps = L.mis_sweeps;
+    }
+  });
+}
+
+int aggmg_dist_hierarchy_level_B(aggmg_dist_hierarchy* h, int64_t k, double* B) {
+  return guarded([&] {
+    DistHierarchy& H = dh(h);
+    require(k >= 0 && k < H.n_levels_total, "hierarchy: level index out of range");
+    Comm& comm = *H.comm;
+    if (k < H.kd()) {
+      DevBuf<double> all;
+      gather_pod<double>(comm, H.levels[k].B.get(), H.levels[k].A->A.n_rows, all);
+      if (comm.rank() == 0) {
+        all.download(B, all.size());
+        sync();
+      }
+    } else if (comm.rank() == 0) {
+      const DevLevel& L = H.tail->levels[k - H.kd()];
+      L.B.download(B, L.A->n_rows);
+      sync();
+    }
+  });
+}
+
+int aggmg_dist_hierarchy_level_omega(aggmg_dist_hierarchy* h, int64_t k, double* omega) {
+  return guarded([&] {
+    DistHierarchy& H = dh(h);
+    require(k >= 0 && k < H.n_levels_total, "hierarchy: level index out of range");
+    if (k < H.kd())
+      *omega = H.levels[k].smoother.omega;
+    else if (H.comm->rank() == 0)
+      *omega = H.tail->levels[k - H.kd()].smoother.omega;
+  });
+}
+
+int64_t aggmg_dist_hierarchy_n_warnings(const aggmg_dist_hierarchy* h) {
+  return (h && h->h) ? static_cast<int64_t>(h->h->warnings.size()) : 0;
+}
+const char* aggmg_dist_hierarchy_warning(const aggmg_dist_hierarchy* h, int64_t i) {
+  if (!h || !h->h || i < 0 || i >= static_cast<int64_t>(h->h->warnings.size())) return "";
+  return h->h->warnings[i].c_str();
+}
+
+void aggmg_dist_hierarchy_free(aggmg_dist_hierarchy* h) { delete h; }
 
 }  // extern "C"

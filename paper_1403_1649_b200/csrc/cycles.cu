@@ -15,12 +15,18 @@ constexpr int kB = 256;
 unsigned egrid(int64_t n) { return grid_for(n, kB, 8 * static_cast<int64_t>(sm_count())); }
 
 int* warn_bits() {
-  static int* p = nullptr;
-  if (!p) {
-    AGG_CUDA(cudaMalloc(&p, 2 * sizeof(int)));
-    AGG_CUDA(cudaMemset(p, 0, 2 * sizeof(int)));
+  struct Bits {
+    int* p = nullptr;
+    ~Bits() {
+      if (p) cudaFree(p);
+    }
+  };
+  static thread_local Bits b;
+  if (!b.p) {
+    AGG_CUDA(cudaMalloc(&b.p, 2 * sizeof(int)));
+    AGG_CUDA(cudaMemset(b.p, 0, 2 * sizeof(int)));
   }
-  return p;
+  return b.p;
 }
 
 inline __device__ bool on(const int* pred) { return !pred || *pred; }
@@ -253,6 +259,9 @@ void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b
 
 void inner_cycle_eager(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
                        double* x_out, const int* pred);
+CoarseWork work_of(DevLevel& L) {
+  return CoarseWork{L.c.get(), L.v.get(), L.rt.get(), L.d.get(), L.w.get(), L.ks.get()};
+}
 void subcycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b, double* x_out,
               const int* pred, bool vee);
 
@@ -326,7 +335,7 @@ void inner_cycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* 
 
 void inner_cycle_eager(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
                        double* x_out, const int* pred) {
-  if (accelerated(cfg, k))
+  if (accelerated(cfg, k + h.cfg.level_offset))
     kcycle_dev(h, cfg, k, b, nullptr, x_out, pred);
   else
     vcycle_dev(h, k, b, nullptr, x_out, pred);
@@ -340,10 +349,7 @@ void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in,
   }
   DevLevel& L = h.levels[k];
   descend(h, k, b, x_in, x_out, pred);
-  if (k + 1 == h.coarsest())
-    coarse_solve(h, L.rc.get(), L.xc.get(), pred);
-  else
-    subcycle(h, CycleCfg{}, k + 1, L.rc.get(), L.xc.get(), pred, true);
+  coarse_correction(h, CycleCfg{}, false, k + 1, L.rc.get(), L.xc.get(), work_of(L), pred);
   postsmooth(L, b, x_out, pred, k == 0);
 }
 
@@ -355,78 +361,119 @@ void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b
   }
   DevLevel& L = h.levels[k];
   descend(h, k, b, x_in, x_out, pred);
-  if (k + 1 == h.coarsest()) {
-    coarse_solve(h, L.rc.get(), L.xc.get(), pred);
-  } else {
-    const DevCsr& Ac = *h.levels[k + 1].A;
-    const int64_t nc = Ac.n_rows;
-    const bool cg = cfg.inner == 0;
-    inner_cycle(h, cfg, k + 1, L.rc.get(), L.c.get(), pred);
-    SpmvArgs a1;  // v = Ac c ; rho1, alpha1  (cycles.cpp:86-95)
-    a1.x = L.c.get();
-    a1.y = L.v.get();
-    a1.c = L.rc.get();
-    a1.dot_with_x = cg ? 1 : 0;
-    a1.dots_out = &L.ks.get()->rho1;
-    a1.pred = pred;
-    const bool exact = exact_reductions();
-    if (exact) {  // SpMV, then the two dots in the reference's chunk order
-      spmv_run(Ac, Epi::kSpmv, a1);
-      DotOp<2> d;
-      d.a[0] = cg ? L.c.get() : L.v.get();  // rho1 = c.v | v.v
-      d.b[0] = L.v.get();
-      d.a[1] = cg ? L.c.get() : L.v.get();  // alpha1 = c.rc | v.rc
-      d.b[1] = L.rc.get();
-      d.pred = pred;
-      launch_chunked<2>(d, nc, &L.ks.get()->rho1);
-      KStep1Op op;
-      op.ks = L.ks.get();
-      op.tt = cfg.t;
-      op.rc = L.rc.get();
-      op.v = L.v.get();
-      op.rt = L.rt.get();
-      op.pred = pred;
-      op.warn = warn_bits();
-      op.level = static_cast<int>(k + 1);
-      launch_chunked<2>(op, nc, &L.ks.get()->nrt);
-    } else {
-      spmv_run(Ac, Epi::kSpmvDot2, a1);
-      const unsigned g = reduce_grid(nc);
-      AGG_LAUNCH(k_kstep1, g, kB, 0, nc, L.rc.get(), L.v.get(), L.rt.get(), L.ks.get(), cfg.t, pred,
-                 reduce_partials(), reduce_ticket(), warn_bits(), static_cast<int>(k + 1));
-    }
-    const int* p2 = &L.ks.get()->flag2;
-    inner_cycle(h, cfg, k + 1, L.rt.get(), L.d.get(), p2);
-    SpmvArgs a2;  // w = Ac d ; gamma, beta, alpha2  (cycles.cpp:110-121)
-    a2.x = L.d.get();
-    a2.y = L.w.get();
-    a2.u = L.v.get();
-    a2.c = L.rt.get();
-    a2.dot_with_x = cg ? 1 : 0;
-    a2.dots_out = &L.ks.get()->gamma;
-    a2.pred = p2;
-    if (exact) {
-      spmv_run(Ac, Epi::kSpmv, a2);
-      DotOp<3> d;
-      const double* lhs = cg ? L.d.get() : L.w.get();
-      d.a[0] = lhs;  // gamma = d.v | w.v
-      d.b[0] = L.v.get();
-      d.a[1] = lhs;  // beta = d.w | w.w
-      d.b[1] = L.w.get();
-      d.a[2] = lhs;  // alpha2 = d.rt | w.rt
-      d.b[2] = L.rt.get();
-      d.pred = p2;
-      launch_chunked<3>(d, nc, &L.ks.get()->gamma);
-    } else {
-      spmv_run(Ac, Epi::kSpmvDot3, a2);
-    }
-    AGG_LAUNCH(k_kcombine, egrid(nc), kB, 0, nc, L.c.get(), L.d.get(), L.xc.get(), L.ks.get(), pred,
-               warn_bits(), static_cast<int>(k + 1));
-  }
+  coarse_correction(h, cfg, true, k + 1, L.rc.get(), L.xc.get(), work_of(L), pred);
   postsmooth(L, b, x_out, pred, k == 0);
 }
 
 }  // namespace
+
+// The coarse half of a cycle visit: level kc receives rc and returns xc.  kparent: the
+// visiting level runs a K-cycle (two inner cycles combined by the inner CG/GMRES scalars,
+// cycles.cpp:84-132); otherwise a V-cycle (cycles.cpp:58-60).
+void coarse_correction(DevHierarchy& h, const CycleCfg& cfg, bool kparent, int64_t kc,
+                       const double* rc, double* xc, const CoarseWork& W, const int* pred) {
+  if (kc == h.coarsest()) {
+    coarse_solve(h, rc, xc, pred);
+    return;
+  }
+  if (!kparent) {
+    subcycle(h, CycleCfg{}, kc, rc, xc, pred, true);
+    return;
+  }
+  const DevCsr& Ac = *h.levels[kc].A;
+  const int64_t nc = Ac.n_rows;
+  const int level = static_cast<int>(kc + h.cfg.level_offset);
+  const bool cg = cfg.inner == 0;
+  inner_cycle(h, cfg, kc, rc, W.c, pred);
+  SpmvArgs a1;  // v = Ac c ; rho1, alpha1  (cycles.cpp:86-95)
+  a1.x = W.c;
+  a1.y = W.v;
+  a1.c = rc;
+  a1.dot_with_x = cg ? 1 : 0;
+  a1.dots_out = &W.ks->rho1;
+  a1.pred = pred;
+  const bool exact = exact_reductions();
+  if (exact) {  // SpMV, then the two dots in the reference's chunk order
+    spmv_run(Ac, Epi::kSpmv, a1);
+    DotOp<2> d;
+    d.a[0] = cg ? W.c : W.v;  // rho1 = c.v | v.v
+    d.b[0] = W.v;
+    d.a[1] = cg ? W.c : W.v;  // alpha1 = c.rc | v.rc
+    d.b[1] = rc;
+    d.pred = pred;
+    launch_chunked<2>(d, nc, &W.ks->rho1);
+    KStep1Op op;
+    op.ks = W.ks;
+    op.tt = cfg.t;
+    op.rc = rc;
+    op.v = W.v;
+    op.rt = W.rt;
+    op.pred = pred;
+    op.warn = warn_bits();
+    op.level = level;
+    launch_chunked<2>(op, nc, &W.ks->nrt);
+  } else {
+    spmv_run(Ac, Epi::kSpmvDot2, a1);
+    const unsigned g = reduce_grid(nc);
+    AGG_LAUNCH(k_kstep1, g, kB, 0, nc, rc, W.v, W.rt, W.ks, cfg.t, pred, reduce_partials(),
+               reduce_ticket(), warn_bits(), level);
+  }
+  const int* p2 = &W.ks->flag2;
+  inner_cycle(h, cfg, kc, W.rt, W.d, p2);
+  SpmvArgs a2;  // w = Ac d ; gamma, beta, alpha2  (cycles.cpp:110-121)
+  a2.x = W.d;
+  a2.y = W.w;
+  a2.u = W.v;
+  a2.c = W.rt;
+  a2.dot_with_x = cg ? 1 : 0;
+  a2.dots_out = &W.ks->gamma;
+  a2.pred = p2;
+  if (exact) {
+    spmv_run(Ac, Epi::kSpmv, a2);
+    DotOp<3> d;
+    const double* lhs = cg ? W.d : W.w;
+    d.a[0] = lhs;  // gamma = d.v | w.v
+    d.b[0] = W.v;
+    d.a[1] = lhs;  // beta = d.w | w.w
+    d.b[1] = W.w;
+    d.a[2] = lhs;  // alpha2 = d.rt | w.rt
+    d.b[2] = W.rt;
+    d.pred = p2;
+    launch_chunked<3>(d, nc, &W.ks->gamma);
+  } else {
+    spmv_run(Ac, Epi::kSpmvDot3, a2);
+  }
+  AGG_LAUNCH(k_kcombine, egrid(nc), kB, 0, nc, W.c, W.d, xc, W.ks, pred, warn_bits(), level);
+}
+
+// ---- building blocks of the row-partitioned cycle (dist_solve.cu) --------------------
+
+namespace {
+__global__ void k_kflag(KScalars* ks, double tt, const int* pred) {
+  if (!on(pred) || ks->rho1 == 0.0) return;  // k_kstep1 already set flag2 = 0
+  ks->flag2 = (__dsqrt_rn(ks->nrt) <= __dmul_rn(tt, __dsqrt_rn(ks->nrc))) ? 0 : 1;
+}
+}  // namespace
+
+void launch_jacobi_zero(int64_t n, const double* wd, const double* b, double* x, const int* pred) {
+  if (n > 0) AGG_LAUNCH(k_jacobi_zero, egrid(n), kB, 0, n, wd, b, x, pred);
+}
+void launch_prolong(int64_t n, const double* x, const idx* agg, const double* pval, const double* xc,
+                    double* t, const int* pred) {
+  if (n > 0) AGG_LAUNCH(k_prolong, egrid(n), kB, 0, n, x, agg, pval, xc, t, pred);
+}
+void launch_kstep1(int64_t n, const double* rc, const double* v, double* rt, KScalars* ks, double t,
+                   const int* pred, int level) {
+  AGG_LAUNCH(k_kstep1, reduce_grid(std::max<int64_t>(n, 1)), kB, 0, n, rc, v, rt, ks, t, pred,
+             reduce_partials(), reduce_ticket(), warn_bits(), level);
+}
+void launch_kflag(KScalars* ks, double t, const int* pred) { AGG_LAUNCH(k_kflag, 1, 1, 0, ks, t, pred); }
+void launch_kcombine(int64_t n, const double* c, const double* d, double* xc, const KScalars* ks,
+                     const int* pred, int level) {
+  AGG_LAUNCH(k_kcombine, egrid(std::max<int64_t>(n, 1)), kB, 0, n, c, d, xc, ks, pred, warn_bits(),
+             level);
+}
+bool cycle_accelerated(const CycleCfg& cfg, int64_t k) { return accelerated(cfg, k); }
 
 void coarse_solve(DevHierarchy& h, const double* b, double* x, const int* pred) {
   const int64_t n = h.levels.back().A->n_rows;

@@ -28,6 +28,28 @@ void apply_preconditioner(DevHierarchy& h, const CycleCfg& cfg, const double* r,
 // Host-visible warnings raised by device-side branch fallbacks (cycles.cpp:97,124).
 void flush_cycle_warnings();
 
+// Workspace of one coarse correction (vectors of the coarse level).
+struct CoarseWork {
+  double *c, *v, *rt, *d, *w;
+  KScalars* ks;
+};
+// Coarse half of a cycle visit (cycles.cpp:56-132): level kc of h receives rc, returns xc.
+void coarse_correction(DevHierarchy& h, const CycleCfg& cfg, bool kparent, int64_t kc,
+                       const double* rc, double* xc, const CoarseWork& w, const int* pred);
+
+// Building blocks of the row-partitioned cycle (dist_solve.cu).
+void launch_jacobi_zero(int64_t n, const double* wd, const double* b, double* x, const int* pred);
+void launch_prolong(int64_t n, const double* x, const idx* agg, const double* pval, const double* xc,
+                    double* t, const int* pred);
+// rt = rc - s1 v and this rank's ||rt||^2, ||rc||^2 into ks->nrt/nrc
+void launch_kstep1(int64_t n, const double* rc, const double* v, double* rt, KScalars* ks, double t,
+                   const int* pred, int level);
+// second-step flag from the (summed) norms
+void launch_kflag(KScalars* ks, double t, const int* pred);
+void launch_kcombine(int64_t n, const double* c, const double* d, double* xc, const KScalars* ks,
+                     const int* pred, int level);
+bool cycle_accelerated(const CycleCfg& cfg, int64_t k);  // cycles.cpp:16-20
+
 // dense coarse solve x = A_L^{-1} b
 void coarse_solve(DevHierarchy& h, const double* b, double* x, const int* pred);
 

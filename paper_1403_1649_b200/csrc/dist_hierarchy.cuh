@@ -1,0 +1,66 @@
+// dist_hierarchy.cuh — the row-partitioned AMG hierarchy.
+//
+// Levels 0..kd-1 are split into contiguous row slabs across the ranks of a Comm; every
+// setup artefact (strength, MIS(2) states, aggregates, P, R, B, coarse operators) equals the
+// one-GPU hierarchy bit for bit.  Level kd — the first level at or below the agglomeration
+// threshold (or the coarsest / stalled level) — is gathered onto rank 0 and continued there
+// as an ordinary DevHierarchy whose level 0 is global level kd (SetupCfg::level_offset).
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dist.cuh"
+#include "hierarchy.cuh"
+
+namespace aggmg_b200 {
+
+struct DistLevel {
+  DistCsrPtr A;       // this level's operator (rows = cols partition)
+  DevBuf<double> B;   // near-null-space vector, owned rows
+  SmootherDev smoother;
+  int mis_sweeps = 0;
+  // transfer to level k+1 (always present: the last distributed level feeds the tail)
+  DistCsrPtr R;          // rows = owned coarse rows, cols = this level's rows (members)
+  HaloPlan P_halo;       // plan over the coarse space for prolongation
+  DevBuf<idx> agg_local; // coarse id of every owned row in P_halo's local numbering
+  DevBuf<idx> agg_global;
+  DevBuf<double> pval;
+  // cycle workspace: fine vectors carry a halo (max of A's and R's), coarse ones P's
+  int64_t halo_cap = 0;
+  DevBuf<double> r, t;
+  DevBuf<double> rc, xc, c, v, rt, d, w;  // level k+1 vectors (owned + halo)
+  DevBuf<KScalars> ks;
+};
+
+struct DistHierarchy {
+  ~DistHierarchy();
+  Comm* comm = nullptr;
+  SetupCfg cfg;
+  int64_t agglomerate_rows = 0;
+  std::vector<DistLevel> levels;       // distributed levels 0..kd-1
+  Partition tail_rows;                 // row partition of level kd before the gather
+  int64_t tail_halo_cap = 0;           // halo slots the level-kd vectors need (P of level kd-1)
+  std::unique_ptr<DevHierarchy> tail;  // rank 0 only: global levels kd..
+  int64_t n_levels_total = 0;          // global level count (same on every rank)
+  std::vector<int64_t> level_rows, level_nnz;  // global sizes per level
+  std::vector<std::string> warnings;
+  double setup_ms = 0.0;
+  bool workspace_ready = false;
+  // tail-side buffers on rank 0 (gathered rc, xc) and the per-rank tail pieces
+  DevBuf<double> tail_b, tail_x;
+  DevBuf<double> tail_work_c, tail_work_v, tail_work_rt, tail_work_d, tail_work_w;
+  DevBuf<KScalars> tail_ks;
+
+  int64_t kd() const { return static_cast<int64_t>(levels.size()); }
+  void ensure_workspace();
+};
+
+// Collective over comm: every rank passes its own rows [A0.rows.begin(me), ...).
+// B0_local == nullptr means ones.
+std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0,
+                                                    const double* B0_local, const SetupCfg& cfg,
+                                                    int64_t agglomerate_rows);
+
+}  // namespace aggmg_b200

@@ -1,0 +1,903 @@
+// dist_setup.cu — setup of the row-partitioned levels (SURVEY §8(e) "setup collectives").
+//
+// Each step restates the one-GPU kernel of setup.cu (and through it the reference lines it
+// cites) for a slab of rows, plus the exchange the step needs:
+//   strength            row-local                                   (strength.cpp:28-72)
+//   influence           column counts + reverse halo add            (strength.cpp:74-78)
+//   S = C u C^T         transpose pairs shipped to the row owner    (strength.cpp:80-111)
+//   MIS(2)              two tuple halos + one count allreduce/sweep (aggregation.cpp:45-86)
+//   aggregation         state/representative halos, A_ji requests,
+//                       global renumbering by representative node   (aggregation.cpp:88-159)
+//   transfer            members shipped to the aggregate owner,
+//                       summed in ascending global order            (transfer.cpp:15-49)
+//   Galerkin            (I, J, (p_i a_ij) p_j) records shipped to the owner of I in global
+//                       (row, entry) order, stable sort by (I, J), ordered segment sums —
+//                       the reference cache order                   (galerkin.cpp:38-137)
+//   smoother            inverse diagonal + Arnoldi with halo SpMVs  (smoother.cpp:21-99)
+// Integer / index results and coarse values are bit-identical to the one-GPU hierarchy;
+// omega differs only by the order of the Arnoldi dot products (<= 1e-12 relative).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cub/cub.cuh>
+#include <sstream>
+
+#include "dist_hierarchy.cuh"
+#include "primitives.cuh"
+#include "vecops.cuh"
+
+namespace aggmg_b200 {
+
+namespace {
+
+template <class F>
+void cub_call(F&& f) {
+  size_t bytes = 0;
+  AGG_CUDA(f(nullptr, bytes));
+  DevBuf<char> tmp(static_cast<int64_t>(std::max<size_t>(bytes, 1)));
+  AGG_CUDA(f(tmp.get(), bytes));
+}
+
+constexpr int kMaxRanks = 64;
+struct PartDev {
+  int64_t off[kMaxRanks + 1];
+  int nranks;
+};
+PartDev part_dev(const Partition& p) {
+  require(p.off.size() <= kMaxRanks + 1, "distributed path supports at most 64 ranks");
+  PartDev d{};
+  d.nranks = static_cast<int>(p.off.size()) - 1;
+  for (size_t r = 0; r < p.off.size(); ++r) d.off[r] = p.off[r];
+  return d;
+}
+__device__ inline int dev_owner(const PartDev& p, int64_t g) {
+  int lo = 0, hi = p.nranks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (p.off[mid] <= g)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ inline double dmax_ref(double a, double b) { return (a < b) ? b : a; }
+
+// global id of local column c
+__device__ inline idx gcol_of(idx c, int64_t nloc, int64_t c0, const idx* halo) {
+  return c < nloc ? static_cast<idx>(c + c0) : halo[c - nloc];
+}
+
+// value of A(i, gj) for local row i by binary search over the row's global column ids
+__device__ inline double row_at(const idx* rp, const idx* gcol, const double* val, idx i, idx gj) {
+  idx lo = rp[i], hi = rp[i + 1];
+  while (lo < hi) {
+    const idx mid = lo + ((hi - lo) >> 1);
+    if (gcol[mid] < gj)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return (lo < rp[i + 1] && gcol[lo] == gj) ? val[lo] : 0.0;
+}
+
+// ---- influence / symmetrize -----------------------------------------------------------
+__global__ void k_count_cols(const idx* col, int64_t nnz, idx* cnt) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < nnz) atomicAdd(&cnt[col[k]], 1);
+}
+// transpose pairs (row = global column of C, col = global row), destination = owner of row
+__global__ void k_tpairs_count(const idx* rp, const idx* gcol, int64_t n, PartDev p, unsigned long long* cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (idx k = rp[i]; k < rp[i + 1]; ++k) atomicAdd(&cnt[dev_owner(p, gcol[k])], 1ull);
+}
+__global__ void k_tpairs_fill(const idx* rp, const idx* gcol, int64_t n, int64_t row0, PartDev p,
+                              const int64_t* off, unsigned long long* cursor, int2* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+    const int q = dev_owner(p, gcol[k]);
+    const unsigned long long slot = atomicAdd(&cursor[q], 1ull);
+    out[off[q] + slot] = make_int2(gcol[k], static_cast<int>(row0 + i));
+  }
+}
+__global__ void k_tkeys(const int2* pr, int64_t m, int64_t row0, unsigned long long* key) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  key[k] = (static_cast<unsigned long long>(pr[k].x - row0) << 32) | static_cast<unsigned>(pr[k].y);
+}
+__global__ void k_tsplit(const unsigned long long* key, int64_t m, idx* trow_cnt, idx* tcol) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  atomicAdd(&trow_cnt[key[k] >> 32], 1);
+  tcol[k] = static_cast<idx>(key[k] & 0xffffffffull);
+}
+// sorted merge of C row i and C^T row i (strength.cpp:86-103), global ids.  mode 0 counts.
+__global__ void k_merge_rows_g(const idx* crp, const idx* ccol, const idx* trp, const idx* tcol,
+                               int64_t n, int mode, const idx* srp, idx* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  idx a = crp[i], ae = crp[i + 1], b = trp[i], be = trp[i + 1];
+  idx cnt = 0;
+  idx* o = mode ? out + srp[i] : nullptr;
+  while (a < ae || b < be) {
+    idx j;
+    if (b >= be || (a < ae && ccol[a] <= tcol[b])) {
+      j = ccol[a];
+      if (b < be && tcol[b] == j) ++b;
+      ++a;
+    } else {
+      j = tcol[b++];
+    }
+    if (o) o[cnt] = j;
+    ++cnt;
+  }
+  if (!mode) out[i] = cnt;
+}
+
+// ---- MIS(2) ---------------------------------------------------------------------------
+struct __align__(16) Tuple {
+  double v;
+  int i;  // global node id
+  int s;
+};
+__device__ inline bool tuple_less(const Tuple& a, const Tuple& b) {
+  if (a.s != b.s) return a.s < b.s;
+  if (a.v != b.v) return a.v < b.v;
+  return a.i < b.i;
+}
+struct DMisCtl {
+  long long undecided;  // global
+  long long dec;        // decided this sweep (local, then summed)
+  int active;
+  int sweeps;
+};
+__global__ void k_dmis_init(const idx* infl, int64_t n, int64_t row0, uint64_t seed, Tuple* cur,
+                            int8_t* state) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Tuple t;
+  t.v = __dadd_rn(static_cast<double>(infl[i]),
+                  uniform_open01(seed, static_cast<uint64_t>(row0 + i)));
+  t.i = static_cast<int>(row0 + i);
+  t.s = 0;
+  cur[i] = t;
+  state[i] = 0;
+}
+__global__ void k_dmis_pass1(const idx* rp, const idx* col, int64_t n, const Tuple* cur, Tuple* mid,
+                             DMisCtl* ctl) {
+  const long long und = ctl->undecided;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->active = und > 0 ? 1 : 0;
+    if (und > 0) ctl->sweeps += 1;
+  }
+  if (und == 0) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Tuple best = cur[i];
+  for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+    const Tuple t = cur[col[k]];
+    if (tuple_less(best, t)) best = t;
+  }
+  mid[i] = best;
+}
+__global__ void k_dmis_pass2(const idx* rp, const idx* col, int64_t n, int64_t row0, const Tuple* mid,
+                             Tuple* cur, int8_t* state, DMisCtl* ctl) {
+  if (!ctl->active) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int decided = 0;
+  if (i < n && state[i] == 0) {
+    Tuple far = mid[i];
+    for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+      const Tuple t = mid[col[k]];
+      if (tuple_less(far, t)) far = t;
+    }
+    int8_t st = 0;
+    if (far.i == static_cast<int>(row0 + i))
+      st = 1;
+    else if (far.s == 1)
+      st = -1;
+    if (st != 0) {
+      state[i] = st;
+      cur[i].s = st;
+      decided = 1;
+    }
+  }
+  const unsigned ballot = __ballot_sync(0xffffffffu, decided);
+  if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->dec),
+                                                   static_cast<unsigned long long>(__popc(ballot)));
+}
+__global__ void k_dmis_update(DMisCtl* ctl) {
+  if (ctl->active) ctl->undecided -= ctl->dec;
+  ctl->dec = 0;
+}
+
+// ---- aggregation ------------------------------------------------------------------------
+// pass 1: representative (global root id) and the local column of that root (via1)
+__global__ void k_dagg_pass1(const idx* rp, const idx* col, int64_t n, int64_t row0, int64_t nloc,
+                             const idx* halo, const int8_t* state, idx* rep, idx* via) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  idx r = -1, v = -1;
+  if (state[i] == 1) {
+    r = static_cast<idx>(row0 + i);
+  } else {
+    for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+      const idx c = col[k];
+      if (state[c] == 1) {
+        r = gcol_of(c, nloc, row0, halo);
+        v = c;
+        break;
+      }
+    }
+  }
+  rep[i] = r;
+  via[i] = v;
+}
+// S cross entries that pass 2 needs A(j, i) for: rows still unassigned after pass 1
+__global__ void k_dagg_req_count(const idx* srp, const idx* scol, int64_t n, int64_t nloc,
+                                 const idx* rep, idx* cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  idx c = 0;
+  if (rep[i] == -1)
+    for (idx k = srp[i]; k < srp[i + 1]; ++k) c += (scol[k] >= nloc && rep[scol[k]] != -1) ? 1 : 0;
+  cnt[i] = c;
+}
+__global__ void k_dagg_req_fill(const idx* srp, const idx* scol, int64_t n, int64_t row0, int64_t nloc,
+                                const idx* halo, const idx* rep, const idx* off, int2* req, idx* slot) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  idx p = off[i];
+  for (idx k = srp[i]; k < srp[i + 1]; ++k) {
+    slot[k] = -1;
+    if (rep[i] != -1) continue;
+    const idx c = scol[k];
+    if (c >= nloc && rep[c] != -1) {
+      req[p] = make_int2(halo[c - nloc], static_cast<int>(row0 + i));  // A(j, i)
+      slot[k] = p;
+      ++p;
+    }
+  }
+}
+// pass 2 against the pass-1 snapshot (aggregation.cpp:118-136), leftovers singletons
+__global__ void k_dagg_pass2(const idx* srp, const idx* scol, const idx* arp, const idx* agcol,
+                             const double* aval, int64_t n, int64_t row0, int64_t nloc,
+                             const idx* halo, const idx* rep, const idx* slot, const double* tval,
+                             idx* rep2, idx* via2, idx* isrep) {
+  const int64_t ii = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (ii >= n) return;
+  const idx i = static_cast<idx>(ii);
+  const idx gi = static_cast<idx>(row0 + i);
+  idx r = rep[i], v = -1;
+  if (r == -1) {
+    idx best = -1;
+    double best_w = -1.0;
+    for (idx k = srp[i]; k < srp[i + 1]; ++k) {
+      const idx c = scol[k];
+      const idx ja = rep[c];
+      if (ja == -1) continue;
+      const idx gj = gcol_of(c, nloc, row0, halo);
+      const double aij = row_at(arp, agcol, aval, i, gj);
+      const double aji = c < nloc ? row_at(arp, agcol, aval, c, gi) : tval[slot[k]];
+      const double w = dmax_ref(fabs(aij), fabs(aji));
+      if (w > best_w || (w == best_w && ja < best)) {
+        best_w = w;
+        best = ja;
+        v = c;
+      }
+    }
+    r = best == -1 ? gi : best;
+    if (best == -1) v = -1;
+  }
+  rep2[i] = r;
+  via2[i] = v;
+  isrep[i] = (r == gi) ? 1 : 0;
+}
+__global__ void k_dagg_fid_reps(const idx* isrep, const idx* rank, int64_t n, int64_t cbase, idx* fid) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) fid[i] = isrep[i] ? static_cast<idx>(cbase + rank[i]) : -1;
+}
+// phase 1: pass-1 members copy their root's id; phase 2: pass-2 members copy their neighbour's
+__global__ void k_dagg_fid_copy(const idx* via, const idx* rep_or_null, const idx* isrep, int64_t n,
+                                int phase, idx* fid) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || isrep[i]) return;
+  const bool pass1_member = rep_or_null[i] != -1;
+  if ((phase == 1) == pass1_member) fid[i] = fid[via[i]];
+}
+
+// ---- pair requests: A(row_g, col_g) from the owner of row_g ------------------------------
+__global__ void k_req_owner(const int2* req, int64_t m, PartDev p, unsigned* own, idx* perm) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  own[k] = static_cast<unsigned>(dev_owner(p, req[k].x));
+  perm[k] = static_cast<idx>(k);
+}
+__global__ void k_req_gather(const int2* req, const idx* perm, int64_t m, int2* out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) out[k] = req[perm[k]];
+}
+__global__ void k_req_answer(const int2* req, int64_t m, int64_t row0, const idx* arp, const idx* agcol,
+                             const double* aval, double* out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) out[k] = row_at(arp, agcol, aval, static_cast<idx>(req[k].x - row0), req[k].y);
+}
+__global__ void k_scatter_back(const double* in, const idx* perm, int64_t m, double* out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) out[perm[k]] = in[k];
+}
+__global__ void k_count_u(const unsigned* own, int64_t m, long long* cnt) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[own[k]]), 1ull);
+}
+
+// ---- transfer ------------------------------------------------------------------------------
+struct __align__(16) MemberRec {
+  int J;     // global coarse id
+  int gid;   // global fine id
+  double b;  // fine near-null-space value
+};
+__global__ void k_member_recs(const idx* fid, const double* b, int64_t n, int64_t row0, PartDev cp,
+                              MemberRec* rec, unsigned* dest, idx* perm) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  MemberRec r;
+  r.J = fid[i];
+  r.gid = static_cast<int>(row0 + i);
+  r.b = b[i];
+  rec[i] = r;
+  dest[i] = static_cast<unsigned>(dev_owner(cp, fid[i]));
+  perm[i] = static_cast<idx>(i);
+}
+template <class T>
+__global__ void k_gather_rec(const T* in, const idx* perm, int64_t m, T* out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) out[k] = in[perm[k]];
+}
+__global__ void k_member_keys(const MemberRec* rec, int64_t m, int64_t cbase, unsigned long long* key,
+                              idx* perm, idx* cnt) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int64_t Jl = rec[k].J - cbase;
+  key[k] = (static_cast<unsigned long long>(Jl) << 32) | static_cast<unsigned>(rec[k].gid);
+  perm[k] = static_cast<idx>(k);
+  atomicAdd(&cnt[Jl], 1);
+}
+// sq_J over members in ascending global order (transfer.cpp:21-22); R rows
+__global__ void k_dtransfer_norms(const idx* goff, const idx* perm, const MemberRec* rec, int64_t nc,
+                                  double* coarse_b, idx* rcnt, int* bad) {
+  const int64_t J = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (J >= nc) return;
+  double sq = 0.0;
+  idx c = 0;
+  for (idx m = goff[J]; m < goff[J + 1]; ++m) {
+    const double bi = rec[perm[m]].b;
+    sq = __dadd_rn(sq, __dmul_rn(bi, bi));
+    c += (bi != 0.0) ? 1 : 0;
+  }
+  if (!(sq > 0.0)) atomicMin(bad, static_cast<int>(J));
+  coarse_b[J] = __dsqrt_rn(sq);
+  rcnt[J] = c;
+}
+__global__ void k_dtransfer_R(const idx* goff, const idx* perm, const MemberRec* rec, int64_t nc,
+                              const double* coarse_b, const idx* rrp, idx* rcol, double* rval) {
+  const int64_t J = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (J >= nc) return;
+  idx p = rrp[J];
+  for (idx m = goff[J]; m < goff[J + 1]; ++m) {
+    const MemberRec r = rec[perm[m]];
+    if (r.b != 0.0) {
+      rcol[p] = r.gid;
+      rval[p] = __ddiv_rn(r.b, coarse_b[J]);
+      ++p;
+    }
+  }
+}
+__global__ void k_dtransfer_pval(const double* b, const double* cb_of_row, int64_t n, double* pval) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double bi = b[i];
+  pval[i] = (bi != 0.0) ? __ddiv_rn(bi, cb_of_row[i]) : 0.0;
+}
+
+// ---- Galerkin --------------------------------------------------------------------------------
+struct __align__(16) GalRec {
+  int I;  // global coarse row
+  int J;  // global coarse column
+  double v;  // (p_i a_ij) p_j
+};
+__global__ void k_gal_recs(const idx* rp, const idx* col, const double* val, int64_t n,
+                           const idx* fid, const double* pv, PartDev cp, GalRec* rec, unsigned* dest,
+                           idx* perm) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const idx I = fid[i];
+  const unsigned d = static_cast<unsigned>(dev_owner(cp, I));
+  const double pi = pv[i];
+  for (idx e = rp[i]; e < rp[i + 1]; ++e) {
+    GalRec r;
+    r.I = I;
+    r.J = fid[col[e]];
+    r.v = __dmul_rn(__dmul_rn(pi, val[e]), pv[col[e]]);
+    rec[e] = r;
+    dest[e] = d;
+    perm[e] = e;
+  }
+}
+__global__ void k_gal_keys(const GalRec* rec, int64_t m, int64_t cbase, unsigned long long* key, idx* perm) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  key[k] = (static_cast<unsigned long long>(rec[k].I - cbase) << 32) | static_cast<unsigned>(rec[k].J);
+  perm[k] = static_cast<idx>(k);
+}
+__global__ void k_seg_sum(const idx* seg_off, int64_t nseg, const idx* perm, const GalRec* rec,
+                          const unsigned long long* ukey, int64_t cbase, double* out_val, idx* out_col,
+                          idx* row_cnt) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  double acc = 0.0;
+  for (idx p = seg_off[s]; p < seg_off[s + 1]; ++p) acc = __dadd_rn(acc, rec[perm[p]].v);
+  out_val[s] = acc;
+  out_col[s] = static_cast<idx>(ukey[s] & 0xffffffffull);
+  atomicAdd(&row_cnt[ukey[s] >> 32], 1);
+}
+
+__global__ void k_uniform_sym_off(int64_t n, int64_t row0, uint64_t seed, double* x) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = uniform_sym(seed, static_cast<uint64_t>(row0 + i));
+}
+
+// records grouped by destination (stable: original order kept inside each destination)
+template <class T>
+DevBuf<double2> ship_stable(Comm& comm, const T* rec, DevBuf<unsigned>& dest, DevBuf<idx>& perm,
+                            int64_t m, std::vector<int64_t>* recv_cnt) {
+  static_assert(sizeof(T) == sizeof(double2), "records travel as 16-byte units");
+  const int P = comm.size();
+  DevBuf<unsigned> dest_s(m);
+  DevBuf<idx> perm_s(m);
+  DevBuf<long long> cnt_d(P);
+  cnt_d.zero();
+  DevBuf<T> grouped(m);
+  if (m > 0) {
+    AGG_LAUNCH(k_count_u, grid_for(m, 256), 256, 0, dest.get(), m, cnt_d.get());
+    if (P > 1) {
+      const int nbits = std::max(1, 32 - __builtin_clz(static_cast<unsigned>(P)));
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, dest.get(), dest_s.get(), perm.get(),
+                                               perm_s.get(), static_cast<int>(m), 0, nbits, stream());
+      });
+      AGG_LAUNCH(k_gather_rec<T>, grid_for(m, 256), 256, 0, rec, perm_s.get(), m, grouped.get());
+    } else {
+      AGG_CUDA(cudaMemcpyAsync(grouped.get(), rec, sizeof(T) * m, cudaMemcpyDeviceToDevice, stream()));
+    }
+  }
+  std::vector<long long> c(P);
+  cnt_d.download(c.data(), P);
+  sync();
+  std::vector<int64_t> cnt(c.begin(), c.end());
+  return alltoallv<double2>(comm, reinterpret_cast<const double2*>(grouped.get()), cnt, recv_cnt);
+}
+
+double dist_dot(Comm& comm, const double* a, const double* b, int64_t n) {
+  DevBuf<double> d(1);
+  DotArgs args{};
+  args.a[0] = a;
+  args.b[0] = b;
+  args.np = 1;
+  if (n > 0)
+    dot_device(args, n, d.get(), nullptr, 1);
+  else
+    d.zero();
+  comm.allreduce_sum(d.get(), 1);
+  return read_scalar(d.get());
+}
+
+}  // namespace
+
+
+namespace {
+
+struct Coarsened {
+  bool stalled = false;
+  int64_t n_agg_global = 0;
+  DistCsrPtr Ac;
+  DevBuf<double> Bc;
+};
+
+Coarsened coarsen_level(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k) {
+  const int me = comm.rank(), P = comm.size();
+  const DistCsr& A = *L.A;
+  const int64_t nloc = A.A.n_rows, nh = A.halo.nhalo, row0 = A.rows.begin(me);
+  const int64_t ntot = nloc + nh;
+  const int64_t n_glob = A.rows.n();
+  const PartDev rp_dev = part_dev(A.rows);
+  const unsigned g = grid_for(std::max<int64_t>(nloc, 1), 256);
+  Coarsened out;
+
+  // ---- a3 strength, a4 influence ----
+  DevCsrPtr C = strength_rows(A.A, cfg.alpha, 0);
+  DevBuf<idx> infl(ntot);
+  infl.zero();
+  if (C->nnz) AGG_LAUNCH(k_count_cols, grid_for(C->nnz, 256), 256, 0, C->col.get(), C->nnz, infl.get());
+  halo_reverse_add(comm, A.halo, infl.get());
+
+  // ---- a5 S = C u C^T (global ids), then local ids over A's halo ----
+  DevBuf<idx> Cg(C->nnz);
+  globalize_cols(A.halo, C->col.get(), C->nnz, Cg.get());
+  DevBuf<unsigned long long> tcnt(P), tcur(P);
+  tcnt.zero();
+  tcur.zero();
+  if (nloc) AGG_LAUNCH(k_tpairs_count, g, 256, 0, C->rowptr.get(), Cg.get(), nloc, rp_dev, tcnt.get());
+  std::vector<unsigned long long> tc(P);
+  tcnt.download(tc.data(), P);
+  sync();
+  std::vector<int64_t> tsend(P), toff(P + 1, 0);
+  for (int q = 0; q < P; ++q) {
+    tsend[q] = static_cast<int64_t>(tc[q]);
+    toff[q + 1] = toff[q] + tsend[q];
+  }
+  DevBuf<int64_t> toff_d(P + 1);
+  toff_d.upload(toff.data(), P + 1);
+  DevBuf<int2> tpairs(C->nnz);
+  if (nloc)
+    AGG_LAUNCH(k_tpairs_fill, g, 256, 0, C->rowptr.get(), Cg.get(), nloc, row0, rp_dev, toff_d.get(),
+               tcur.get(), tpairs.get());
+  DevBuf<int2> mine = alltoallv<int2>(comm, tpairs.get(), tsend);
+  tpairs.reset();
+  const int64_t mt = mine.size();
+  DevBuf<unsigned long long> tkey(mt), tkey_s(mt);
+  DevBuf<idx> trp(nloc + 1), trow_cnt(nloc), tcol(mt);
+  trow_cnt.zero();
+  if (mt > 0) {
+    AGG_LAUNCH(k_tkeys, grid_for(mt, 256), 256, 0, mine.get(), mt, row0, tkey.get());
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, tkey.get(), tkey_s.get(), static_cast<int>(mt), 0, 64,
+                                            stream());
+    });
+    AGG_LAUNCH(k_tsplit, grid_for(mt, 256), 256, 0, tkey_s.get(), mt, trow_cnt.get(), tcol.get());
+  }
+  scan_to_offsets_async(trow_cnt.get(), trp.get(), nloc);
+  DevBuf<idx> scnt(nloc), srp(nloc + 1);
+  if (nloc)
+    AGG_LAUNCH(k_merge_rows_g, g, 256, 0, C->rowptr.get(), Cg.get(), trp.get(), tcol.get(), nloc, 0,
+               nullptr, scnt.get());
+  const int64_t snnz = scan_to_offsets(scnt.get(), srp.get(), nloc);
+  DevBuf<idx> sg(snnz), scol(snnz);
+  if (nloc && snnz)
+    AGG_LAUNCH(k_merge_rows_g, g, 256, 0, C->rowptr.get(), Cg.get(), trp.get(), tcol.get(), nloc, 1,
+               srp.get(), sg.get());
+  localize_cols(A.halo, sg.get(), snnz, scol.get(),
+                "distributed setup requires a structurally symmetric matrix (strength graph "
+                "reaches a column outside the operator's halo)");
+  C.reset();
+  Cg.reset();
+  sg.reset();
+  mine.reset();
+
+  // ---- a6 MIS(2) ----
+  DevBuf<Tuple> cur(ntot), mid(ntot);
+  DevBuf<int8_t> state(ntot);
+  DevBuf<DMisCtl> ctl(1);
+  DMisCtl h0{static_cast<long long>(n_glob), 0, 0, 0};
+  ctl.upload(&h0, 1);
+  const uint64_t seed = level_seed(cfg.seed, k, kMisTag);
+  if (nloc) AGG_LAUNCH(k_dmis_init, g, 256, 0, infl.get(), nloc, row0, seed, cur.get(), state.get());
+  int batch = 8;
+  while (true) {
+    for (int b = 0; b < batch; ++b) {
+      halo_update<double2>(comm, A.halo, reinterpret_cast<double2*>(cur.get()));
+      AGG_LAUNCH(k_dmis_pass1, g, 256, 0, srp.get(), scol.get(), nloc, cur.get(), mid.get(), ctl.get());
+      halo_update<double2>(comm, A.halo, reinterpret_cast<double2*>(mid.get()));
+      AGG_LAUNCH(k_dmis_pass2, g, 256, 0, srp.get(), scol.get(), nloc, row0, mid.get(), cur.get(),
+                 state.get(), ctl.get());
+      comm.allreduce_sum(reinterpret_cast<int64_t*>(&ctl.get()->dec), 1);
+      AGG_LAUNCH(k_dmis_update, 1, 1, 0, ctl.get());
+    }
+    const DMisCtl h = read_scalar(ctl.get());
+    if (h.sweeps > n_glob) throw Error("mis2: failed to decide all nodes");
+    if (h.undecided == 0) {
+      L.mis_sweeps = h.sweeps;
+      break;
+    }
+    batch = 4;
+  }
+  cur.reset();
+  mid.reset();
+
+  // ---- a7 aggregation ----
+  halo_update<int8_t>(comm, A.halo, state.get());
+  DevBuf<idx> rep(ntot), via1(nloc), rep2(nloc), via2(nloc), isrep(nloc), rank(nloc + 1);
+  if (nloc)
+    AGG_LAUNCH(k_dagg_pass1, g, 256, 0, srp.get(), scol.get(), nloc, row0, nloc, A.halo.halo_gid.get(),
+               state.get(), rep.get(), via1.get());
+  halo_update<idx>(comm, A.halo, rep.get());
+  // A(j, i) for the cross edges pass 2 looks at
+  DevBuf<idx> Ag = global_cols(A);
+  DevBuf<idx> rq_cnt(nloc), rq_off(nloc + 1), slot(snnz);
+  if (nloc)
+    AGG_LAUNCH(k_dagg_req_count, g, 256, 0, srp.get(), scol.get(), nloc, nloc, rep.get(), rq_cnt.get());
+  const int64_t nreq = scan_to_offsets(rq_cnt.get(), rq_off.get(), nloc);
+  DevBuf<int2> req(nreq);
+  if (nloc)
+    AGG_LAUNCH(k_dagg_req_fill, g, 256, 0, srp.get(), scol.get(), nloc, row0, nloc,
+               A.halo.halo_gid.get(), rep.get(), rq_off.get(), req.get(), slot.get());
+  DevBuf<double> tval(nreq);
+  {
+    DevBuf<unsigned> own(nreq);
+    DevBuf<idx> perm(nreq);
+    if (nreq) AGG_LAUNCH(k_req_owner, grid_for(nreq, 256), 256, 0, req.get(), nreq, rp_dev, own.get(), perm.get());
+    // ship_stable returns the requests grouped by source; remember the permutation
+    DevBuf<unsigned> own_s(nreq);
+    DevBuf<idx> perm_s(nreq);
+    DevBuf<long long> cnt_d(P);
+    cnt_d.zero();
+    DevBuf<int2> grouped(nreq);
+    if (nreq) {
+      AGG_LAUNCH(k_count_u, grid_for(nreq, 256), 256, 0, own.get(), nreq, cnt_d.get());
+      const int nbits = std::max(1, 32 - __builtin_clz(static_cast<unsigned>(P)));
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, own.get(), own_s.get(), perm.get(), perm_s.get(),
+                                               static_cast<int>(nreq), 0, nbits, stream());
+      });
+      AGG_LAUNCH(k_req_gather, grid_for(nreq, 256), 256, 0, req.get(), perm_s.get(), nreq, grouped.get());
+    }
+    std::vector<long long> c(P);
+    cnt_d.download(c.data(), P);
+    sync();
+    std::vector<int64_t> cnt(c.begin(), c.end()), rc;
+    DevBuf<int2> incoming = alltoallv<int2>(comm, grouped.get(), cnt, &rc);
+    const int64_t nin = incoming.size();
+    DevBuf<double> ans(nin);
+    if (nin)
+      AGG_LAUNCH(k_req_answer, grid_for(nin, 256), 256, 0, incoming.get(), nin, row0, A.A.rowptr.get(),
+                 Ag.get(), A.A.val.get(), ans.get());
+    DevBuf<double> back = alltoallv<double>(comm, ans.get(), rc);
+    if (nreq) AGG_LAUNCH(k_scatter_back, grid_for(nreq, 256), 256, 0, back.get(), perm_s.get(), nreq, tval.get());
+  }
+  if (nloc)
+    AGG_LAUNCH(k_dagg_pass2, g, 256, 0, srp.get(), scol.get(), A.A.rowptr.get(), Ag.get(),
+               A.A.val.get(), nloc, row0, nloc, A.halo.halo_gid.get(), rep.get(), slot.get(),
+               tval.get(), rep2.get(), via2.get(), isrep.get());
+  const int64_t nrep = scan_to_offsets(isrep.get(), rank.get(), nloc);
+  const std::vector<int64_t> reps_all = comm.allgather_host({nrep});
+  const Partition cpart = Partition::from_counts(reps_all);
+  out.n_agg_global = cpart.n();
+  if (static_cast<double>(out.n_agg_global) >= 0.95 * static_cast<double>(n_glob)) {
+    out.stalled = true;
+    return out;
+  }
+  const int64_t cbase = cpart.begin(me), ncl = cpart.count(me);
+  DevBuf<idx> fid(ntot);
+  if (nloc) AGG_LAUNCH(k_dagg_fid_reps, g, 256, 0, isrep.get(), rank.get(), nloc, cbase, fid.get());
+  halo_update<idx>(comm, A.halo, fid.get());
+  if (nloc) AGG_LAUNCH(k_dagg_fid_copy, g, 256, 0, via1.get(), rep.get(), isrep.get(), nloc, 1, fid.get());
+  halo_update<idx>(comm, A.halo, fid.get());
+  if (nloc) AGG_LAUNCH(k_dagg_fid_copy, g, 256, 0, via2.get(), rep.get(), isrep.get(), nloc, 2, fid.get());
+  halo_update<idx>(comm, A.halo, fid.get());
+  srp.reset();
+  scol.reset();
+
+  // ---- a8 transfer ----
+  const PartDev cp_dev = part_dev(cpart);
+  DevBuf<MemberRec> mrec(nloc);
+  DevBuf<unsigned> mdest(nloc);
+  DevBuf<idx> mperm(nloc);
+  if (nloc)
+    AGG_LAUNCH(k_member_recs, g, 256, 0, fid.get(), L.B.get(), nloc, row0, cp_dev, mrec.get(),
+               mdest.get(), mperm.get());
+  DevBuf<double2> members_buf = ship_stable<MemberRec>(comm, mrec.get(), mdest, mperm, nloc, nullptr);
+  const MemberRec* members = reinterpret_cast<const MemberRec*>(members_buf.get());
+  const int64_t nm = members_buf.size();
+  DevBuf<unsigned long long> mkey(nm), mkey_s(nm);
+  DevBuf<idx> mp(nm), mp_s(nm), gcnt(ncl), goff(ncl + 1);
+  gcnt.zero();
+  if (nm) {
+    AGG_LAUNCH(k_member_keys, grid_for(nm, 256), 256, 0, members, nm, cbase, mkey.get(), mp.get(),
+               gcnt.get());
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, mkey.get(), mkey_s.get(), mp.get(), mp_s.get(),
+                                             static_cast<int>(nm), 0, 64, stream());
+    });
+  }
+  scan_to_offsets_async(gcnt.get(), goff.get(), ncl);
+  out.Bc.resize(ncl);
+  DevBuf<idx> rcnt(ncl);
+  DevBuf<int> bad(1);
+  fill_int(bad.get(), 1, INT32_MAX);
+  if (ncl)
+    AGG_LAUNCH(k_dtransfer_norms, grid_for(ncl, 256), 256, 0, goff.get(), mp_s.get(), members, ncl,
+               out.Bc.get(), rcnt.get(), bad.get());
+  auto Rg = std::make_shared<DevCsr>();
+  Rg->n_rows = ncl;
+  Rg->n_cols = n_glob;
+  Rg->rowptr.resize(ncl + 1);
+  Rg->nnz = scan_to_offsets(rcnt.get(), Rg->rowptr.get(), ncl);
+  {
+    const int b = read_scalar(bad.get());
+    const int64_t worst = comm.allreduce_host_max(b == INT32_MAX ? -1 : cbase + b);
+    if (worst >= 0)
+      throw Error("transfer: near-null-space vector vanishes on aggregate " + std::to_string(worst));
+  }
+  Rg->col.resize(Rg->nnz);
+  Rg->val.resize(Rg->nnz);
+  if (ncl)
+    AGG_LAUNCH(k_dtransfer_R, grid_for(ncl, 256), 256, 0, goff.get(), mp_s.get(), members, ncl,
+               out.Bc.get(), Rg->rowptr.get(), Rg->col.get(), Rg->val.get());
+  L.R = make_dist(comm, cpart, A.rows, *Rg, "restriction: member outside the plan");
+  members_buf.reset();
+  // P: coarse norms of the aggregates of my rows, then p_i = b_i / ||b_J||
+  DevBuf<double> cb_row(nloc);
+  fetch_remote<double>(comm, cpart, out.Bc.get(), fid.get(), nloc, cb_row.get());
+  L.pval.resize(ntot);
+  L.pval.zero();
+  if (nloc) AGG_LAUNCH(k_dtransfer_pval, g, 256, 0, L.B.get(), cb_row.get(), nloc, L.pval.get());
+  build_halo_plan(comm, cpart, fid.get(), nloc, L.P_halo);
+  L.agg_local.resize(nloc);
+  localize_cols(L.P_halo, fid.get(), nloc, L.agg_local.get(), "prolongation: aggregate outside the plan");
+  L.agg_global.resize(nloc);
+  if (nloc)
+    AGG_CUDA(cudaMemcpyAsync(L.agg_global.get(), fid.get(), sizeof(idx) * nloc, cudaMemcpyDeviceToDevice,
+                             stream()));
+
+  // ---- a9/a10 Galerkin in the cache order ----
+  halo_update<double>(comm, A.halo, L.pval.get());
+  const int64_t nnz = A.A.nnz;
+  DevBuf<GalRec> grec(nnz);
+  DevBuf<unsigned> gdest(nnz);
+  DevBuf<idx> gperm(nnz);
+  if (nloc)
+    AGG_LAUNCH(k_gal_recs, g, 256, 0, A.A.rowptr.get(), A.A.col.get(), A.A.val.get(), nloc, fid.get(),
+               L.pval.get(), cp_dev, grec.get(), gdest.get(), gperm.get());
+  DevBuf<double2> ents_buf = ship_stable<GalRec>(comm, grec.get(), gdest, gperm, nnz, nullptr);
+  const GalRec* ents = reinterpret_cast<const GalRec*>(ents_buf.get());
+  grec.reset();
+  gdest.reset();
+  gperm.reset();
+  const int64_t ne = ents_buf.size();
+  DevBuf<unsigned long long> ekey(ne), ekey_s(ne), ukey(ne);
+  DevBuf<idx> ep(ne), ep_s(ne), seg_len(ne), seg_off(ne + 1);
+  DevBuf<int> nseg_d(1);
+  nseg_d.zero();
+  if (ne) {
+    AGG_LAUNCH(k_gal_keys, grid_for(ne, 256), 256, 0, ents, ne, cbase, ekey.get(), ep.get());
+    cub_call([&](void* t, size_t& b) {  // stable: ties keep the global (row, entry) order
+      return cub::DeviceRadixSort::SortPairs(t, b, ekey.get(), ekey_s.get(), ep.get(), ep_s.get(),
+                                             static_cast<int>(ne), 0, 64, stream());
+    });
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRunLengthEncode::Encode(t, b, ekey_s.get(), ukey.get(), seg_len.get(),
+                                                nseg_d.get(), static_cast<int>(ne), stream());
+    });
+  }
+  const int64_t nseg = read_scalar(nseg_d.get());
+  scan_to_offsets_async(seg_len.get(), seg_off.get(), nseg);
+  auto Acg = std::make_shared<DevCsr>();
+  Acg->n_rows = ncl;
+  Acg->n_cols = cpart.n();
+  Acg->nnz = nseg;
+  Acg->rowptr.resize(ncl + 1);
+  Acg->col.resize(nseg);
+  Acg->val.resize(nseg);
+  DevBuf<idx> crow(ncl);
+  crow.zero();
+  if (nseg)
+    AGG_LAUNCH(k_seg_sum, grid_for(nseg, 256), 256, 0, seg_off.get(), nseg, ep_s.get(), ents,
+               ukey.get(), cbase, Acg->val.get(), Acg->col.get(), crow.get());
+  scan_to_offsets_async(crow.get(), Acg->rowptr.get(), ncl);
+  out.Ac = make_dist(comm, cpart, cpart, *Acg);
+  return out;
+}
+
+void dist_smoother(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k) {
+  const DistCsr& A = *L.A;
+  const int me = comm.rank();
+  const int64_t nloc = A.A.n_rows, row0 = A.rows.begin(me);
+  const uint64_t seed = level_seed(cfg.seed, k, kSmootherTag);
+  ArnoldiOps ops;
+  ops.n_alloc = nloc + A.halo.nhalo;
+  ops.n_global = A.rows.n();
+  ops.row0 = row0;
+  ops.start = [&](double* v) {
+    if (nloc) AGG_LAUNCH(k_uniform_sym_off, grid_for(nloc, 256), 256, 0, nloc, row0, seed, v);
+  };
+  ops.before_spmv = [&](double* v) { halo_update<double>(comm, A.halo, v); };
+  ops.dot = [&](const double* a, const double* b) { return dist_dot(comm, a, b, nloc); };
+  // a zero diagonal on any rank must fail every rank
+  std::string err;
+  try {
+    setup_smoother(A.A, cfg.smoother, cfg.arnoldi_m, seed, L.smoother, &ops);
+  } catch (const Error& e) {
+    err = e.what();
+  }
+  if (comm.allreduce_host_sum(err.empty() ? 0 : 1) > 0)
+    throw Error(err.empty() ? "smoother: zero diagonal on another rank" : err);
+}
+
+}  // namespace
+
+DistHierarchy::~DistHierarchy() = default;
+
+std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, const double* B0_local,
+                                                    const SetupCfg& cfg, int64_t agglomerate_rows) {
+  require(A0->rows.n() == A0->cols.n(), "setup: matrix must be square");
+  require(cfg.coarse_size_max >= 1, "setup: coarse_size_max must be at least 1");
+  require(cfg.max_levels >= 1, "setup: max_levels must be at least 1");
+  const int me = comm.rank();
+  comm.barrier();
+  const auto t0 = std::chrono::steady_clock::now();
+  auto h = std::make_unique<DistHierarchy>();
+  h->comm = &comm;
+  h->cfg = cfg;
+  h->agglomerate_rows = std::max<int64_t>(agglomerate_rows, cfg.coarse_size_max);
+
+  DistCsrPtr A = A0;
+  DevBuf<double> B(A->A.n_rows);
+  if (B0_local)
+    copy_double(B.get(), B0_local, A->A.n_rows);
+  else
+    fill_double(B.get(), A->A.n_rows, 1.0);
+  {
+    const double nb = std::sqrt(dist_dot(comm, B.get(), B.get(), A->A.n_rows));
+    require(nb > 0.0, "setup: near-null-space vector is zero");
+  }
+  int64_t k = 0;
+  while (true) {
+    const int64_t n_glob = A->rows.n();
+    if (n_glob <= h->agglomerate_rows || k + 1 >= cfg.max_levels) break;
+    DistLevel L;
+    L.A = A;
+    L.B = std::move(B);
+    Coarsened c = coarsen_level(comm, L, cfg, k);
+    if (c.stalled) {  // the tail re-runs this level and records the reference's warning
+      B = std::move(L.B);
+      break;
+    }
+    dist_smoother(comm, L, cfg, k);
+    A = c.Ac;
+    B = std::move(c.Bc);
+    h->levels.push_back(std::move(L));
+    ++k;
+  }
+  // agglomerate level kd onto rank 0 and continue with the one-GPU setup there
+  h->tail_rows = A->rows;
+  DevCsrPtr Ag = gather_to_root(comm, *A, 0);
+  DevBuf<double> Bg(me == 0 ? A->rows.n() : 0);
+  gather_vector(comm, A->rows, B.get(), Bg.get(), 0);
+  std::vector<int64_t> meta(3, 0);  // tail level count, warnings flag
+  if (me == 0) {
+    SetupCfg tc = cfg;
+    tc.level_offset = k;
+    tc.max_levels = cfg.max_levels - static_cast<int>(k);
+    h->tail = setup_hierarchy(Ag, Bg.get(), tc);
+    meta[0] = h->tail->n_levels();
+  }
+  const std::vector<int64_t> m_all = comm.allgather_host(meta);
+  h->n_levels_total = k + m_all[0];
+  if (me == 0) h->warnings = h->tail->warnings;
+  // global sizes per level (same on every rank)
+  for (auto& L : h->levels) {
+    h->level_rows.push_back(L.A->rows.n());
+    h->level_nnz.push_back(comm.allreduce_host_sum(L.A->A.nnz));
+  }
+  std::vector<int64_t> tail_sizes;
+  if (me == 0)
+    for (auto& L : h->tail->levels) {
+      tail_sizes.push_back(L.A->n_rows);
+      tail_sizes.push_back(L.A->nnz);
+    }
+  tail_sizes.resize(2 * m_all[0], 0);
+  const std::vector<int64_t> ts_all = comm.allgather_host(tail_sizes);
+  for (int64_t l = 0; l < m_all[0]; ++l) {
+    h->level_rows.push_back(ts_all[2 * l]);
+    h->level_nnz.push_back(ts_all[2 * l + 1]);
+  }
+  if (!h->levels.empty()) h->tail_halo_cap = h->levels.back().P_halo.nhalo;
+  comm.barrier();
+  h->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return h;
+}
+
+}  // namespace aggmg_b200

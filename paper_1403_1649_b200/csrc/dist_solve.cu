@@ -1,0 +1,192 @@
+// dist_solve.cu — the solve stage on a row-partitioned hierarchy (SURVEY §8(e) "solve
+// collectives"): halo exchange before every SpMV-family kernel, rank-ordered allreduce of
+// every Krylov / K-cycle scalar, gather of the restricted residual onto rank 0 at the
+// agglomeration level and scatter of the coarse correction back.
+//
+// The kernel sequence per level is the one-GPU sequence of cycles.cu (cycles.cpp:16-146),
+// so on one rank the partitioned solve is bit-identical to the one-GPU solve, and on R
+// ranks it differs only by the summation order of the dot products.
+#include <algorithm>
+
+#include "dist_solve.cuh"
+#include "primitives.cuh"
+
+namespace aggmg_b200 {
+
+void DistHierarchy::ensure_workspace() {
+  if (workspace_ready) return;
+  const int64_t kd_ = kd();
+  // halo capacity per level: A's and R's column halos of the level, P's of the level above
+  std::vector<int64_t> cap(kd_ + 1, 0), nl(kd_ + 1, 0);
+  for (int64_t k = 0; k < kd_; ++k) {
+    DistLevel& L = levels[k];
+    nl[k] = L.A->A.n_rows;
+    cap[k] = std::max(cap[k], std::max(L.A->halo.nhalo, L.R->halo.nhalo));
+    cap[k + 1] = std::max(cap[k + 1], L.P_halo.nhalo);
+  }
+  nl[kd_] = tail_rows.count(comm->rank());
+  for (int64_t k = 0; k < kd_; ++k) {
+    DistLevel& L = levels[k];
+    L.halo_cap = cap[k];
+    L.r.resize(nl[k] + cap[k]);
+    L.t.resize(nl[k] + cap[k]);
+    const int64_t nc = nl[k + 1] + cap[k + 1];
+    L.rc.resize(nc);
+    L.xc.resize(nc);
+    L.c.resize(nc);
+    L.v.resize(nc);
+    L.rt.resize(nc);
+    L.d.resize(nc);
+    L.w.resize(nc);
+    L.ks.resize(1);
+    L.ks.zero();
+  }
+  if (tail) {
+    tail->ensure_workspace();
+    const int64_t n = tail->levels[0].A->n_rows;
+    tail_b.resize(n);
+    tail_x.resize(n);
+    tail_work_c.resize(n);
+    tail_work_v.resize(n);
+    tail_work_rt.resize(n);
+    tail_work_d.resize(n);
+    tail_work_w.resize(n);
+    tail_ks.resize(1);
+    tail_ks.zero();
+  }
+  workspace_ready = true;
+}
+
+namespace {
+
+void dist_cycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, const double* b,
+                double* x, const int* pred);
+
+// coarse half of a visit of distributed level k (cycles.cpp:56-132)
+void dist_coarse(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kparent, const int* pred) {
+  Comm& comm = *h.comm;
+  DistLevel& L = h.levels[k];
+  if (k + 1 == h.kd()) {  // the agglomerated tail on rank 0
+    gather_vector(comm, h.tail_rows, L.rc.get(), h.tail_b.get(), 0);
+    if (comm.rank() == 0) {
+      CoarseWork W{h.tail_work_c.get(), h.tail_work_v.get(), h.tail_work_rt.get(),
+                   h.tail_work_d.get(), h.tail_work_w.get(), h.tail_ks.get()};
+      coarse_correction(*h.tail, cfg, kparent, 0, h.tail_b.get(), h.tail_x.get(), W, pred);
+    }
+    scatter_vector(comm, h.tail_rows, h.tail_x.get(), L.xc.get(), 0);
+    return;
+  }
+  DistLevel& C = h.levels[k + 1];
+  if (!kparent) {  // V-cycle below a V-cycle
+    dist_cycle(h, cfg, k + 1, false, L.rc.get(), L.xc.get(), pred);
+    return;
+  }
+  const int64_t nc = C.A->A.n_rows;
+  const bool cg = cfg.inner == 0;
+  const bool inner_k = cycle_accelerated(cfg, k + 1);
+  const int level = static_cast<int>(k + 1);
+  dist_cycle(h, cfg, k + 1, inner_k, L.rc.get(), L.c.get(), pred);
+  halo_update<double>(comm, C.A->halo, L.c.get());
+  SpmvArgs a1;  // v = Ac c ; rho1, alpha1
+  a1.x = L.c.get();
+  a1.y = L.v.get();
+  a1.c = L.rc.get();
+  a1.dot_with_x = cg ? 1 : 0;
+  a1.dots_out = &L.ks.get()->rho1;
+  a1.pred = pred;
+  spmv_run(C.A->A, Epi::kSpmvDot2, a1);
+  comm.allreduce_sum(&L.ks.get()->rho1, 2);
+  launch_kstep1(nc, L.rc.get(), L.v.get(), L.rt.get(), L.ks.get(), cfg.t, pred, level);
+  comm.allreduce_sum(&L.ks.get()->nrt, 2);
+  launch_kflag(L.ks.get(), cfg.t, pred);
+  const int* p2 = &L.ks.get()->flag2;
+  dist_cycle(h, cfg, k + 1, inner_k, L.rt.get(), L.d.get(), p2);
+  halo_update<double>(comm, C.A->halo, L.d.get());
+  SpmvArgs a2;  // w = Ac d ; gamma, beta, alpha2
+  a2.x = L.d.get();
+  a2.y = L.w.get();
+  a2.u = L.v.get();
+  a2.c = L.rt.get();
+  a2.dot_with_x = cg ? 1 : 0;
+  a2.dots_out = &L.ks.get()->gamma;
+  a2.pred = p2;
+  spmv_run(C.A->A, Epi::kSpmvDot3, a2);
+  comm.allreduce_sum(&L.ks.get()->gamma, 3);
+  launch_kcombine(nc, L.c.get(), L.d.get(), L.xc.get(), L.ks.get(), pred, level);
+}
+
+// x = cycle(k) applied to b from the zero guess; kc: K-cycle (else V-cycle) at level k.
+void dist_cycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, const double* b,
+                double* x, const int* pred) {
+  Comm& comm = *h.comm;
+  DistLevel& L = h.levels[k];
+  const int64_t n = L.A->A.n_rows;
+  const int prof = k == 0 ? kProfSmoothL0 : 0;
+  // pre-smooth from zero, residual, restriction (cycles.cpp:54-57)
+  launch_jacobi_zero(n, L.smoother.wdiag.get(), b, x, pred);
+  halo_update<double>(comm, L.A->halo, x);
+  SpmvArgs ra;
+  ra.x = x;
+  ra.y = L.r.get();
+  ra.b = b;
+  ra.pred = pred;
+  spmv_run(L.A->A, Epi::kResidual, ra, k == 0 ? kProfSpmvL0 : 0);
+  halo_update<double>(comm, L.R->halo, L.r.get());
+  SpmvArgs rr;
+  rr.x = L.r.get();
+  rr.y = L.rc.get();
+  rr.pred = pred;
+  spmv_run(L.R->A, Epi::kSpmv, rr);
+  dist_coarse(h, cfg, k, kc, pred);
+  // prolongation + post-smooth (cycles.cpp:37-44, 59-60)
+  halo_update<double>(comm, L.P_halo, L.xc.get());
+  launch_prolong(n, x, L.agg_local.get(), L.pval.get(), L.xc.get(), L.t.get(), pred);
+  halo_update<double>(comm, L.A->halo, L.t.get());
+  SpmvArgs ja;
+  ja.x = L.t.get();
+  ja.y = x;
+  ja.b = b;
+  ja.d = L.smoother.wdiag.get();
+  ja.pred = pred;
+  spmv_run(L.A->A, Epi::kJacobi, ja, prof);
+}
+
+}  // namespace
+
+void dist_apply_preconditioner(DistHierarchy& h, const CycleCfg& cfg, const double* r, double* z) {
+  h.ensure_workspace();
+  if (h.kd() == 0) {  // everything agglomerated: the one-GPU cycle on rank 0
+    Comm& comm = *h.comm;
+    gather_vector(comm, h.tail_rows, r, h.tail_b.get(), 0);
+    if (comm.rank() == 0) apply_preconditioner(*h.tail, cfg, h.tail_b.get(), h.tail_x.get());
+    scatter_vector(comm, h.tail_rows, h.tail_x.get(), z, 0);
+    return;
+  }
+  dist_cycle(h, cfg, 0, cycle_accelerated(cfg, 0), r, z, nullptr);
+}
+
+SolveOut dist_solve(DistHierarchy& h, const DistCsr& A, const CycleCfg& cyc, const SolverCfg& cfg,
+                    const double* b, double* x) {
+  h.ensure_workspace();
+  Comm& comm = *h.comm;
+  KrylovDist d;
+  d.n_alloc = A.A.n_rows + std::max<int64_t>(A.halo.nhalo, h.kd() ? h.levels[0].halo_cap : 0);
+  d.halo = [&](double* v) { halo_update<double>(comm, A.halo, v); };
+  d.allreduce = [&](double* v, int k) { comm.allreduce_sum(v, k); };
+  d.precond = [&](const double* r, double* z) { dist_apply_preconditioner(h, cyc, r, z); };
+  d.flush_warnings = [&] {
+    if (comm.rank() == 0) flush_cycle_warnings();
+  };
+  Precond M;
+  M.cfg = cyc;
+  // x needs halo room for the residual SpMV: solve in a workspace copy
+  DevBuf<double> xw(d.n_alloc);
+  xw.zero();
+  copy_double(xw.get(), x, A.A.n_rows);
+  SolveOut out = cfg.method == 1 ? pcg(A.A, b, xw.get(), M, cfg, &d) : fgmres(A.A, b, xw.get(), M, cfg, &d);
+  copy_double(x, xw.get(), A.A.n_rows);
+  sync();
+  return out;
+}
+
+}  // namespace aggmg_b200

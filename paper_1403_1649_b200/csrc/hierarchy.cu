@@ -62,13 +62,13 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     DevCsrPtr S;
     influence_and_symmetrize(*C, influence, S);
     C.reset();
-    Mis2Dev mis = mis2(*S, influence.get(), level_seed(cfg.seed, k, kMisTag));
+    Mis2Dev mis = mis2(*S, influence.get(), level_seed(cfg.seed, k + cfg.level_offset, kMisTag));
     AggDev agg = aggregate(*S, A, mis.state.get());
     S.reset();
 
     if (static_cast<double>(agg.n_agg) >= 0.95 * static_cast<double>(n)) {
       std::ostringstream msg;
-      msg << "coarsening stalled at level " << k << " (" << n << " -> " << agg.n_agg
+      msg << "coarsening stalled at level " << k + cfg.level_offset << " (" << n << " -> " << agg.n_agg
           << " aggregates); solving this level directly";
       h->warnings.push_back(msg.str());
       break;
@@ -82,7 +82,7 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     } else {  // hierarchy.cpp:73: galerkin_direct, the reference default
       Ac = galerkin_direct(A, agg, fine.tr.pval.get());
     }
-    setup_smoother(A, cfg.smoother, cfg.arnoldi_m, level_seed(cfg.seed, k, kSmootherTag),
+    setup_smoother(A, cfg.smoother, cfg.arnoldi_m, level_seed(cfg.seed, k + cfg.level_offset, kSmootherTag),
                    fine.smoother);
     fine.has_smoother = true;
     fine.agg = std::move(agg);
@@ -116,7 +116,7 @@ void refresh_values(DevHierarchy& h, const double* new_values_dev) {
     DevCsrPtr Ac = apply_galerkin_cache(fine.gal, *fine.A, fine.tr.pval.get());
     copy_double(h.levels[k + 1].A->val.get(), Ac->val.get(), Ac->nnz);
     setup_smoother(*fine.A, h.cfg.smoother, h.cfg.arnoldi_m,
-                   level_seed(h.cfg.seed, k, kSmootherTag), fine.smoother);
+                   level_seed(h.cfg.seed, k + h.cfg.level_offset, kSmootherTag), fine.smoother);
   }
   factor_coarsest(h);
 }

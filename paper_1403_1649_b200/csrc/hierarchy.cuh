@@ -19,6 +19,9 @@ struct SetupCfg {
   int arnoldi_m = 5;
   int reuse_caches = 0;
   uint64_t seed = 42;
+  // Global index of this hierarchy's level 0 (> 0 for the agglomerated tail of a
+  // row-partitioned hierarchy): seeds, K-cycle level policy and messages use k + offset.
+  int64_t level_offset = 0;
 };
 
 // K-cycle scalars of one level, resident in device memory (cycles.cpp:88-132).

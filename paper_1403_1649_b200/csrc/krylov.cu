@@ -153,14 +153,17 @@ __global__ void k_multi_axpy(int64_t n, AxpyList L, double* __restrict__ x) {
 
 unsigned egrid(int64_t n) { return grid_for(n, kB, 8 * static_cast<int64_t>(sm_count())); }
 
-void apply_M(const Precond& M, const double* r, double* z, int64_t n) {
-  if (M.h)
+void apply_M(const Precond& M, const double* r, double* z, int64_t n, const KrylovDist* dist) {
+  if (dist && dist->precond)
+    dist->precond(r, z);
+  else if (M.h)
     apply_preconditioner(*M.h, M.cfg, r, z);
   else
     copy_double(z, r, n);
 }
 
-void residual(const DevCsr& A, const double* b, const double* x, double* r) {
+void residual(const DevCsr& A, const double* b, const double* x, double* r, const KrylovDist* dist) {
+  if (dist) dist->halo(const_cast<double*>(x));
   SpmvArgs a;
   a.x = x;
   a.y = r;
@@ -168,7 +171,23 @@ void residual(const DevCsr& A, const double* b, const double* x, double* r) {
   spmv_run(A, Epi::kResidual, a);
 }
 
-double norm_host(const double* v, int64_t n) { return std::sqrt(dot_host(v, v, n)); }
+double norm_host(const double* v, int64_t n, const KrylovDist* dist = nullptr) {
+  if (!dist) return std::sqrt(dot_host(v, v, n));
+  DevBuf<double> d(1);
+  DotArgs a{};
+  a.a[0] = v;
+  a.b[0] = v;
+  a.np = 1;
+  if (n > 0)
+    dot_device(a, n, d.get(), nullptr, 0);
+  else
+    d.zero();
+  dist->allreduce(d.get(), 1);
+  return std::sqrt(read_scalar(d.get()));
+}
+void reduce(const KrylovDist* dist, double* v, int k) {
+  if (dist) dist->allreduce(v, k);
+}
 
 double seconds_since(Clock::time_point t0) {
   return std::chrono::duration<double>(Clock::now() - t0).count();
@@ -176,13 +195,14 @@ double seconds_since(Clock::time_point t0) {
 
 }  // namespace
 
-SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, const SolverCfg& cfg) {
-  require(A.n_rows == A.n_cols, "pcg: matrix must be square");
+SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, const SolverCfg& cfg,
+             const KrylovDist* dist) {
+  require(dist || A.n_rows == A.n_cols, "pcg: matrix must be square");
   require(cfg.tol > 0.0, "pcg: tol must be positive");
   const auto t0 = Clock::now();
   const int64_t n = A.n_rows;
   SolveOut out;
-  const double norm_b = norm_host(b, n);
+  const double norm_b = norm_host(b, n, dist);
   if (norm_b == 0.0) {
     fill_double(x, n, 0.0);
     out.converged = true;
@@ -192,16 +212,17 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     return out;
   }
   const double target = cfg.tol * norm_b;
-  const bool exact = exact_reductions();
-  DevBuf<double> rA(n), rB(n), z(n), p(n), Ap(n);
+  const bool exact = exact_reductions() && !dist;
+  const int64_t n_alloc = dist ? dist->n_alloc : n;  // SpMV inputs and cycle outputs carry a halo
+  DevBuf<double> rA(n), rB(n), z(n_alloc), p(n_alloc), Ap(n);
   DevBuf<PcgSlots> slots(1);
   slots.zero();
   double* r = rA.get();
   double* rn = rB.get();
-  residual(A, b, x, r);
-  double res = norm_host(r, n);
+  residual(A, b, x, r, dist);
+  double res = norm_host(r, n, dist);
   out.history.push_back(res);
-  apply_M(M, r, z.get(), n);
+  apply_M(M, r, z.get(), n, dist);
   copy_double(p.get(), z.get(), n);
   {
     DotArgs d{};
@@ -209,6 +230,7 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     d.b[0] = z.get();
     d.np = 1;
     dot_device(d, n, &slots.get()->q[0][0]);
+    reduce(dist, &slots.get()->q[0][0], 1);
   }
   double* pinned = pinned_scratch(8);
   int par = 0;  // q[par][0] holds the current r.z
@@ -218,6 +240,7 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     a.y = Ap.get();
     a.u = p.get();
     a.dots_out = &slots.get()->pAp;
+    if (dist) dist->halo(p.get());
     if (exact) {
       spmv_run(A, Epi::kSpmv, a, kProfSpmvL0);
       DotOp<1> d1;
@@ -236,8 +259,10 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
       launch_chunked<1>(u, n, &slots.get()->res2);
     } else {
       spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
+      reduce(dist, &slots.get()->pAp, 1);
       AGG_LAUNCH(k_pcg_update, reduce_grid(n), kB, 0, n, slots.get(), par, p.get(), Ap.get(), r, x,
                  rn, reduce_partials(), reduce_ticket());
+      reduce(dist, &slots.get()->res2, 1);
     }
     AGG_CUDA(cudaMemcpyAsync(pinned, slots.get(), 2 * sizeof(double), cudaMemcpyDeviceToHost,
                              stream()));
@@ -249,7 +274,7 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     out.history.push_back(res);
     std::swap(r, rn);  // r = new residual, rn = r_old
     if (res <= target) break;
-    apply_M(M, r, z.get(), n);
+    apply_M(M, r, z.get(), n, dist);
     DotArgs d{};
     d.a[0] = r;
     d.b[0] = z.get();
@@ -258,10 +283,14 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     d.np = 2;
     const int cur = par ^ 1;
     dot_device(d, n, &slots.get()->q[cur][0]);  // {r.z, r_old.z}
+    reduce(dist, &slots.get()->q[cur][0], 2);
     AGG_LAUNCH(k_pcg_p, egrid(n), kB, 0, n, slots.get(), cur, z.get(), p.get());
     par = cur;
   }
-  if (M.h) flush_cycle_warnings();
+  if (dist && dist->flush_warnings)
+    dist->flush_warnings();
+  else if (M.h)
+    flush_cycle_warnings();
   out.converged = res <= target;
   sync();
   out.solve_seconds = seconds_since(t0);
@@ -269,15 +298,15 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
 }
 
 SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
-                const SolverCfg& cfg) {
-  require(A.n_rows == A.n_cols, "fgmres: matrix must be square");
+                const SolverCfg& cfg, const KrylovDist* dist) {
+  require(dist || A.n_rows == A.n_cols, "fgmres: matrix must be square");
   require(cfg.tol > 0.0, "fgmres: tol must be positive");
   require(cfg.restart >= 1, "fgmres: restart must be at least 1");
   const auto t0 = Clock::now();
   const int64_t n = A.n_rows;
   const int m = cfg.restart;
   SolveOut out;
-  const double norm_b = norm_host(b, n);
+  const double norm_b = norm_host(b, n, dist);
   if (norm_b == 0.0) {
     fill_double(x, n, 0.0);
     out.converged = true;
@@ -287,11 +316,12 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
     return out;
   }
   const double target = cfg.tol * norm_b;
-  const bool exact = exact_reductions();
+  const bool exact = exact_reductions() && !dist;
+  const int64_t nz_alloc = dist ? dist->n_alloc : n;
   DevBuf<double> r(n), w(n), hcol(m + 2);
   std::vector<DevBuf<double>> V, Z;
-  residual(A, b, x, r.get());
-  double beta = norm_host(r.get(), n);
+  residual(A, b, x, r.get(), dist);
+  double beta = norm_host(r.get(), n, dist);
   out.history.push_back(beta);
   std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0);  // column-major, ld m+1
   auto h = [&](int i, int j) -> double& { return H[static_cast<size_t>(j) * (m + 1) + i]; };
@@ -306,8 +336,9 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
     std::fill(H.begin(), H.end(), 0.0);
     int j = 0;
     for (; j < m && out.iterations < cfg.max_iters; ++j) {
-      if (static_cast<int>(Z.size()) <= j) Z.emplace_back(n);
-      apply_M(M, V[j].get(), Z[j].get(), n);
+      if (static_cast<int>(Z.size()) <= j) Z.emplace_back(nz_alloc);
+      apply_M(M, V[j].get(), Z[j].get(), n, dist);
+      if (dist) dist->halo(Z[j].get());
       SpmvArgs a;  // w = A Z_j ; h(0,j) = V_0 . w
       a.x = Z[j].get();
       a.y = w.get();
@@ -322,6 +353,7 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
         launch_chunked<1>(d1, n, hcol.get());
       } else {
         spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
+        reduce(dist, hcol.get(), 1);
       }
       for (int i = 0; i <= j; ++i) {
         const double* vnext = (i < j) ? V[i + 1].get() : nullptr;
@@ -336,6 +368,7 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
         } else {
           AGG_LAUNCH(k_mgs_step, reduce_grid(n), kB, 0, n, hcol.get(), i, V[i].get(), vnext,
                      w.get(), hcol.get() + i + 1, reduce_partials(), reduce_ticket());
+          reduce(dist, hcol.get() + i + 1, 1);
         }
       }
       AGG_CUDA(cudaMemcpyAsync(pinned, hcol.get(), sizeof(double) * (j + 2),
@@ -387,14 +420,17 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
       }
       AGG_LAUNCH(k_multi_axpy, egrid(n), kB, 0, n, L, x);
     }
-    residual(A, b, x, r.get());
-    beta = norm_host(r.get(), n);
+    residual(A, b, x, r.get(), dist);
+    beta = norm_host(r.get(), n, dist);
     out.history.back() = beta;
     if (beta > target && beta >= prev_outer && j == m)
       out.note = "stagnation: no residual decrease over a full restart cycle";
     prev_outer = beta;
   }
-  if (M.h) flush_cycle_warnings();
+  if (dist && dist->flush_warnings)
+    dist->flush_warnings();
+  else if (M.h)
+    flush_cycle_warnings();
   out.converged = beta <= target;
   sync();
   out.solve_seconds = seconds_since(t0);

@@ -2,6 +2,7 @@
 // vectors in HBM.  The host keeps only the scalar recurrences it must branch on.
 #pragma once
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -30,9 +31,22 @@ struct Precond {
   CycleCfg cfg;
 };
 
-// x (device, n) holds x0 on entry and the solution on exit.
-SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, const SolverCfg& cfg);
+// Hooks for a row-partitioned operator (dist_solve.cu): A is this rank's rows with local
+// column ids, vectors that feed an SpMV carry n_alloc >= n entries (owned + halo), every
+// dot product written to device memory is summed over ranks in rank order, and the
+// preconditioner is the partitioned cycle.  nullptr = the one-GPU path.
+struct KrylovDist {
+  int64_t n_alloc = 0;
+  std::function<void(double*)> halo;                 // fill the halo of an SpMV input
+  std::function<void(double*, int)> allreduce;       // device scalars, in place
+  std::function<void(const double*, double*)> precond;
+  std::function<void()> flush_warnings;
+};
+
+// x (device, n; n_alloc with dist) holds x0 on entry and the solution on exit.
+SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, const SolverCfg& cfg,
+             const KrylovDist* dist = nullptr);
 SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
-                const SolverCfg& cfg);
+                const SolverCfg& cfg, const KrylovDist* dist = nullptr);
 
 }  // namespace aggmg_b200

@@ -106,9 +106,13 @@ struct RedScratch {
   double* partials = nullptr;
   unsigned* ticket = nullptr;
   int cap = 0;
+  ~RedScratch() {
+    if (partials) cudaFree(partials);
+    if (ticket) cudaFree(ticket);
+  }
 };
 RedScratch& red() {
-  static RedScratch r;
+  static thread_local RedScratch r;
   if (!r.partials) {
     r.cap = 1 << 20;
     AGG_CUDA(cudaMalloc(&r.partials, sizeof(double) * 3 * r.cap));

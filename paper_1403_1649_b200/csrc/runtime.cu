@@ -16,10 +16,18 @@ struct Context {
   cudaStream_t stream = nullptr;
   double* pinned = nullptr;
   int pinned_n = 0;
+  ~Context() {  // rank threads exit: release their stream and staging
+    if (!ready) return;
+    if (stream) cudaStreamDestroy(stream);
+    if (pinned) cudaFreeHost(pinned);
+  }
 };
 
+// One context per host thread: the library's default user (the C-ABI caller) and every
+// rank thread of an in-process distributed run (comm.cu ThreadGroup) get their own stream,
+// pinned staging and reduction scratch, so ranks never share ordering state.
 Context& ctx() {
-  static Context c;
+  static thread_local Context c;
   return c;
 }
 std::mutex& ctx_mutex() {
@@ -40,15 +48,15 @@ struct ProfState {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
 };
 ProfState& prof() {
-  static ProfState p;
+  static thread_local ProfState p;
   return p;
 }
 
 }  // namespace
 
 void init_device(int device) {
-  std::lock_guard<std::mutex> lk(ctx_mutex());
   Context& c = ctx();
+  std::lock_guard<std::mutex> lk(ctx_mutex());
   if (c.ready) return;
   int count = 0;
   cudaError_t e = cudaGetDeviceCount(&count);
@@ -82,6 +90,10 @@ cudaStream_t stream() {
 int sm_count() {
   ensure_init();
   return ctx().sms;
+}
+int current_device() {
+  ensure_init();
+  return ctx().device;
 }
 
 void* dev_alloc(size_t bytes) {

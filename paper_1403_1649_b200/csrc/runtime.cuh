@@ -12,6 +12,8 @@
 namespace aggmg_b200 {
 
 void ensure_init();
+void init_device(int device);  // creates the calling thread's context on `device`
+int current_device();
 void* dev_alloc(size_t bytes);
 void dev_free(void* p);
 

@@ -680,10 +680,17 @@ __global__ void k_fingerprint(const idx* rowptr, int64_t n, const idx* col, int6
 
 DevCsrPtr classic_strength(const DevCsr& A, double alpha, int zero_diag_policy) {
   require(A.n_rows == A.n_cols, "strength: matrix must be square");
+  return strength_rows(A, alpha, zero_diag_policy);
+}
+
+// Rows of a (possibly row-partitioned) operator whose owned columns are 0..n_rows-1 in
+// local ids: the diagonal of row i is column i, halo columns never are.
+DevCsrPtr strength_rows(const DevCsr& A, double alpha, int zero_diag_policy) {
   require(alpha > 0.0 && alpha < 1.0, "strength: alpha must be in (0, 1)");
   const int64_t n = A.n_rows;
   auto C = std::make_shared<DevCsr>();
-  C->n_rows = C->n_cols = n;
+  C->n_rows = n;
+  C->n_cols = A.n_cols;
   C->rowptr.resize(n + 1);
   DevBuf<idx> cnt(n);
   DevBuf<int> bad(1);
@@ -859,7 +866,7 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg) {
   const int nbig = read_scalar(big_count.get());
   if (nbig > 0) {
     const size_t smem = static_cast<size_t>(kGalCapBig) * (8 + 4 + 4);
-    static bool raised = false;
+    static thread_local bool raised = false;
     if (!raised) {
       AGG_CUDA(cudaFuncSetAttribute(k_gal_symbolic_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));

@@ -10,6 +10,8 @@ namespace aggmg_b200 {
 
 // a3: classic strength (strength.cpp:28-72).  Pattern only (values not stored on device).
 DevCsrPtr classic_strength(const DevCsr& A, double alpha, int zero_diag_policy);
+// Same kernel on the local rows of a row-partitioned operator (local column ids).
+DevCsrPtr strength_rows(const DevCsr& A, double alpha, int zero_diag_policy);
 // a4 + a5: influence counts (column counts of C) and S = pattern(C u C^T).
 void influence_and_symmetrize(const DevCsr& C, DevBuf<idx>& influence, DevCsrPtr& S);
 

@@ -45,13 +45,21 @@ __global__ void k_sgs(const idx* rp, const idx* col, const double* val, int64_t 
   }
 }
 
-double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t seed) {
+double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t seed,
+                    const ArnoldiOps* ops) {
   const int64_t n = A.n_rows;
-  m = static_cast<int>(std::min<int64_t>(m, n));
+  const int64_t n_alloc = ops ? ops->n_alloc : n;
+  m = static_cast<int>(std::min<int64_t>(m, ops ? ops->n_global : n));
+  auto dot = [&](const double* a, const double* b) {
+    return ops ? ops->dot(a, b) : dot_host(a, b, n, 1);
+  };
   std::vector<DevBuf<double>> V;
-  V.emplace_back(n);
-  vec_uniform_sym(n, seed, V[0].get());
-  const double qn = std::sqrt(dot_host(V[0].get(), V[0].get(), n, 1));
+  V.emplace_back(n_alloc);
+  if (ops)
+    ops->start(V[0].get());
+  else
+    vec_uniform_sym(n, seed, V[0].get());
+  const double qn = std::sqrt(dot(V[0].get(), V[0].get()));
   require(qn > 0.0, "smoother: degenerate start vector");
   vec_scale(n, 1.0 / qn, V[0].get());
 
@@ -60,6 +68,7 @@ double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t see
   int m_eff = m;
   DevBuf<double> w(n), dots(2);
   for (int j = 0; j < m; ++j) {
+    if (ops) ops->before_spmv(V[j].get());  // halo of the Krylov vector
     SpmvArgs a;
     a.x = V[j].get();
     a.y = w.get();
@@ -67,29 +76,34 @@ double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t see
     spmv_run(A, Epi::kScaleDiag, a);
     double h_scale = 0.0;
     for (int i = 0; i <= j; ++i) {
-      DotArgs d{};
-      d.a[0] = V[i].get();
-      d.b[0] = w.get();
-      d.a[1] = V[i].get();
-      d.b[1] = V[i].get();
-      d.np = 2;
-      dot_device(d, n, dots.get(), nullptr, 1);
       double hv[2];
-      dots.download(hv, 2);
-      sync();
+      if (ops) {
+        hv[0] = ops->dot(V[i].get(), w.get());
+        hv[1] = ops->dot(V[i].get(), V[i].get());
+      } else {
+        DotArgs d{};
+        d.a[0] = V[i].get();
+        d.b[0] = w.get();
+        d.a[1] = V[i].get();
+        d.b[1] = V[i].get();
+        d.np = 2;
+        dot_device(d, n, dots.get(), nullptr, 1);
+        dots.download(hv, 2);
+        sync();
+      }
       const double hij = hv[0] / hv[1];
       h(i, j) = hij;
       vec_axpy(n, -hij, V[i].get(), w.get());
       h_scale = std::max(h_scale, std::abs(hij));
     }
-    const double hj = std::sqrt(dot_host(w.get(), w.get(), n, 1));
+    const double hj = std::sqrt(dot(w.get(), w.get()));
     if (hj <= 1e-12 * std::max(h_scale, 1.0)) {
       m_eff = j + 1;
       break;
     }
     h(j + 1, j) = hj;
     if (j + 1 < m) {
-      V.emplace_back(n);
+      V.emplace_back(n_alloc);
       vec_scale_into(n, 1.0 / hj, w.get(), V.back().get());
     }
   }
@@ -109,8 +123,9 @@ __global__ void k_scale_diag(const double* inv, double omega, int64_t n, double*
 
 }  // namespace
 
-void setup_smoother(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, SmootherDev& s) {
-  require(A.n_rows == A.n_cols, "smoother: matrix must be square");
+void setup_smoother(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, SmootherDev& s,
+                    const ArnoldiOps* ops) {
+  require(ops || A.n_rows == A.n_cols, "smoother: matrix must be square");
   require(arnoldi_m >= 1 && arnoldi_m <= 5, "smoother: arnoldi_m must be in [1, 5]");
   const int64_t n = A.n_rows;
   s.kind = kind;
@@ -122,11 +137,12 @@ void setup_smoother(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, Smo
     AGG_LAUNCH(k_inv_diag, grid_for(n, 256), 256, 0, A.rowptr.get(), A.col.get(), A.val.get(), n,
                s.inv_diag.get(), bad.get());
   const int b = read_scalar(bad.get());
-  if (b != INT32_MAX) throw Error("smoother: zero diagonal at row " + std::to_string(b));
+  if (b != INT32_MAX)
+    throw Error("smoother: zero diagonal at row " + std::to_string(b + (ops ? ops->row0 : 0)));
   s.omega = 1.0;
   s.rho_est = 1.0;
   if (kind == 1) {  // damped Jacobi
-    s.rho_est = estimate_rho(A, s.inv_diag.get(), arnoldi_m, seed);
+    s.rho_est = estimate_rho(A, s.inv_diag.get(), arnoldi_m, seed, ops);
     s.omega = (4.0 / 3.0) / s.rho_est;
   }
   const double w = (kind == 0) ? 1.0 : s.omega;  // smoother.cpp:120

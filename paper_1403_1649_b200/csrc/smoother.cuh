@@ -1,6 +1,8 @@
 // smoother.cuh — smoother setup (a12) and sweeps (a15).
 #pragma once
 
+#include <functional>
+
 #include "sparse.cuh"
 
 namespace aggmg_b200 {
@@ -14,9 +16,20 @@ struct SmootherDev {
   int arnoldi_m = 5;
 };
 
+// Hooks that run the Arnoldi estimate on a row-partitioned operator: the Krylov vectors
+// carry a halo (n_alloc entries), the start vector uses global indices, dots are summed
+// over ranks.  nullptr = the one-GPU path.
+struct ArnoldiOps {
+  int64_t n_alloc = 0, n_global = 0, row0 = 0;
+  std::function<void(double*)> start;
+  std::function<void(double*)> before_spmv;
+  std::function<double(const double*, const double*)> dot;
+};
+
 // smoother.cpp:86-99 (inverse diagonal with "zero diagonal at row i"; Arnoldi rho for
 // damped Jacobi with start vector uniform_sym(seed, i)).
-void setup_smoother(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, SmootherDev& s);
+void setup_smoother(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, SmootherDev& s,
+                    const ArnoldiOps* ops = nullptr);
 
 // One sweep on device vectors (smoother.cpp:101-124): jacobi/damped Jacobi out of place
 // into x_out (x_out may not alias x); sgs in place on x.

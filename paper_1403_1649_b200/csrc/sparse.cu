@@ -282,15 +282,15 @@ template <Epi E>
 void launch_stream(const DevCsr& A, const SpmvArgs& a) {
   const int64_t nblocks = (A.n_rows + A.rows_per_block - 1) / A.rows_per_block;
   const size_t smem = sizeof(double) * A.smem_entries;
-  static bool raised = false;
+  static thread_local bool raised = false;
   if (smem > 48 * 1024 && !raised) {
     AGG_CUDA(cudaFuncSetAttribute(k_csr_stream<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   227 * 1024));
     raised = true;
   }
   // persistent grid: as many CTAs as can be co-resident
-  static size_t cached_smem = 0;
-  static int cached_per_sm = 0;
+  static thread_local size_t cached_smem = 0;
+  static thread_local int cached_per_sm = 0;
   if (cached_smem != smem) {
     int per_sm = 0;
     AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_csr_stream<E>,
@@ -385,18 +385,24 @@ DevCsrPtr transpose(const DevCsr& A) {
 namespace {
 
 // Same stencil, ordering and arithmetic as poisson.cpp:32-75.
-__global__ void k_poisson_count(int64_t nx, int64_t ny, int64_t nz, idx* cnt) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= nx * ny * nz) return;
+// Rows [row0, row0 + nrows) of the grid operator (the whole matrix: row0 = 0, nrows = n);
+// output row t = global row row0 + t, columns global.
+__global__ void k_poisson_count(int64_t nx, int64_t ny, int64_t nz, int64_t row0, int64_t nrows,
+                                idx* cnt) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+  const int64_t r = row0 + t;
   const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
-  cnt[r] = 1 + (i > 0) + (i + 1 < nx) + (j > 0) + (j + 1 < ny) + (k > 0) + (k + 1 < nz);
+  cnt[t] = 1 + (i > 0) + (i + 1 < nx) + (j > 0) + (j + 1 < ny) + (k > 0) + (k + 1 < nz);
 }
-__global__ void k_poisson_fill(int64_t nx, int64_t ny, int64_t nz, double cx, double cy, double cz,
-                               double diag, const idx* rowptr, idx* col, double* val) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= nx * ny * nz) return;
+__global__ void k_poisson_fill(int64_t nx, int64_t ny, int64_t nz, int64_t row0, int64_t nrows,
+                               double cx, double cy, double cz, double diag, const idx* rowptr,
+                               idx* col, double* val) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+  const int64_t r = row0 + t;
   const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
-  idx p = rowptr[r];
+  idx p = rowptr[t];
   auto put = [&](int64_t c, double v) {
     col[p] = static_cast<idx>(c);
     val[p] = v;
@@ -415,26 +421,29 @@ __device__ inline double jump_kappa(int64_t x, int64_t y, int64_t z, int64_t blo
   return (((x / block) + (y / block) + (z / block)) & 1) ? jump : 1.0;
 }
 
-__global__ void k_jump27_count(int64_t nx, int64_t ny, int64_t nz, idx* cnt) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= nx * ny * nz) return;
+__global__ void k_jump27_count(int64_t nx, int64_t ny, int64_t nz, int64_t row0, int64_t nrows,
+                               idx* cnt) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+  const int64_t r = row0 + t;
   const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
   const int cxn = 1 + (i > 0) + (i + 1 < nx), cyn = 1 + (j > 0) + (j + 1 < ny),
             czn = 1 + (k > 0) + (k + 1 < nz);
-  cnt[r] = cxn * cyn * czn;
+  cnt[t] = cxn * cyn * czn;
 }
 
 // 27-point variable-coefficient operator: off-diagonal -kappa_ij with
 // kappa_ij = 2 k_i k_j / (k_i + k_j); diagonal = sum over the 26 neighbour slots of
 // kappa_ij (kappa_i for Dirichlet-eliminated slots), accumulated in slot order.
-__global__ void k_jump27_fill(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,
-                              const idx* rowptr, idx* col, double* val) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= nx * ny * nz) return;
+__global__ void k_jump27_fill(int64_t nx, int64_t ny, int64_t nz, int64_t row0, int64_t nrows,
+                              double jump, int64_t block, const idx* rowptr, idx* col, double* val) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+  const int64_t r = row0 + t;
   const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
   const double ki = jump_kappa(i, j, k, block, jump);
   double diag = 0.0;
-  idx p = rowptr[r];
+  idx p = rowptr[t];
   idx pdiag = -1;
   for (int dz = -1; dz <= 1; ++dz)
     for (int dy = -1; dy <= 1; ++dy)
@@ -463,8 +472,8 @@ __global__ void k_jump27_fill(int64_t nx, int64_t ny, int64_t nz, double jump, i
 
 }  // namespace
 
-DevCsrPtr generate_poisson_device(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
-                                  int weak_axis) {
+DevCsrPtr generate_poisson_rows(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
+                                int weak_axis, int64_t row0, int64_t nrows) {
   require(dims == 2 || dims == 3, "poisson: dims must be 2 or 3");
   if (dims == 2) nz = 1;
   require(nx >= 1 && ny >= 1 && nz >= 1, "poisson: grid extents must be positive");
@@ -473,39 +482,59 @@ DevCsrPtr generate_poisson_device(int dims, int64_t nx, int64_t ny, int64_t nz, 
   require(weak < dims, "poisson: weak axis " + std::to_string(weak) + " out of range for " +
                            std::to_string(dims) + "D");
   const int64_t n = nx * ny * nz;
+  if (nrows < 0) nrows = n - row0;
+  require(row0 >= 0 && row0 + nrows <= n, "poisson: row range outside the grid");
   const double cx = weak == 0 ? -eps : -1.0, cy = weak == 1 ? -eps : -1.0,
                cz = weak == 2 ? -eps : -1.0;
   const double diag = -2.0 * (cx + cy + (dims == 3 ? cz : 0.0));
   auto A = std::make_shared<DevCsr>();
-  A->n_rows = A->n_cols = n;
-  A->rowptr.resize(n + 1);
-  DevBuf<idx> cnt(n);
-  AGG_LAUNCH(k_poisson_count, grid_for(n, 256), 256, 0, nx, ny, nz, cnt.get());
-  A->nnz = scan_to_offsets(cnt.get(), A->rowptr.get(), n);
+  A->n_rows = nrows;
+  A->n_cols = n;
+  A->rowptr.resize(nrows + 1);
+  DevBuf<idx> cnt(nrows);
+  if (nrows > 0)
+    AGG_LAUNCH(k_poisson_count, grid_for(nrows, 256), 256, 0, nx, ny, nz, row0, nrows, cnt.get());
+  A->nnz = scan_to_offsets(cnt.get(), A->rowptr.get(), nrows);
   A->col.resize(A->nnz);
   A->val.resize(A->nnz);
-  AGG_LAUNCH(k_poisson_fill, grid_for(n, 256), 256, 0, nx, ny, nz, cx, cy, cz, diag,
-             A->rowptr.get(), A->col.get(), A->val.get());
+  if (nrows > 0)
+    AGG_LAUNCH(k_poisson_fill, grid_for(nrows, 256), 256, 0, nx, ny, nz, row0, nrows, cx, cy, cz,
+               diag, A->rowptr.get(), A->col.get(), A->val.get());
+  A->plan();
+  return A;
+}
+
+DevCsrPtr generate_poisson_device(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
+                                  int weak_axis) {
+  return generate_poisson_rows(dims, nx, ny, nz, eps, weak_axis, 0, -1);
+}
+
+DevCsrPtr generate_jump27_rows(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,
+                               int64_t row0, int64_t nrows) {
+  require(nx >= 1 && ny >= 1 && nz >= 1 && block >= 1, "jump27: extents must be positive");
+  require(jump > 0.0, "jump27: jump must be positive");
+  const int64_t n = nx * ny * nz;
+  if (nrows < 0) nrows = n - row0;
+  require(row0 >= 0 && row0 + nrows <= n, "jump27: row range outside the grid");
+  auto A = std::make_shared<DevCsr>();
+  A->n_rows = nrows;
+  A->n_cols = n;
+  A->rowptr.resize(nrows + 1);
+  DevBuf<idx> cnt(nrows);
+  if (nrows > 0)
+    AGG_LAUNCH(k_jump27_count, grid_for(nrows, 256), 256, 0, nx, ny, nz, row0, nrows, cnt.get());
+  A->nnz = scan_to_offsets(cnt.get(), A->rowptr.get(), nrows);
+  A->col.resize(A->nnz);
+  A->val.resize(A->nnz);
+  if (nrows > 0)
+    AGG_LAUNCH(k_jump27_fill, grid_for(nrows, 256), 256, 0, nx, ny, nz, row0, nrows, jump, block,
+               A->rowptr.get(), A->col.get(), A->val.get());
   A->plan();
   return A;
 }
 
 DevCsrPtr generate_jump27_device(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block) {
-  require(nx >= 1 && ny >= 1 && nz >= 1 && block >= 1, "jump27: extents must be positive");
-  require(jump > 0.0, "jump27: jump must be positive");
-  const int64_t n = nx * ny * nz;
-  auto A = std::make_shared<DevCsr>();
-  A->n_rows = A->n_cols = n;
-  A->rowptr.resize(n + 1);
-  DevBuf<idx> cnt(n);
-  AGG_LAUNCH(k_jump27_count, grid_for(n, 256), 256, 0, nx, ny, nz, cnt.get());
-  A->nnz = scan_to_offsets(cnt.get(), A->rowptr.get(), n);
-  A->col.resize(A->nnz);
-  A->val.resize(A->nnz);
-  AGG_LAUNCH(k_jump27_fill, grid_for(n, 256), 256, 0, nx, ny, nz, jump, block, A->rowptr.get(),
-             A->col.get(), A->val.get());
-  A->plan();
-  return A;
+  return generate_jump27_rows(nx, ny, nz, jump, block, 0, -1);
 }
 
 }  // namespace aggmg_b200

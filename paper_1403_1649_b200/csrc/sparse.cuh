@@ -78,6 +78,11 @@ DevCsrPtr transpose(const DevCsr& A);
 DevCsrPtr generate_poisson_device(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
                                   int weak_axis);
 DevCsrPtr generate_jump27_device(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block);
+// Rows [row0, row0 + nrows) only (nrows < 0: to the end), global column ids; n_cols = n.
+DevCsrPtr generate_poisson_rows(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
+                                int weak_axis, int64_t row0, int64_t nrows);
+DevCsrPtr generate_jump27_rows(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,
+                               int64_t row0, int64_t nrows);
 
 double spmv_bytes(const DevCsr& A, Epi epi);
 
