@@ -16,8 +16,12 @@ quoted on (configs[1]: 3-D 7-point Poisson 256^3, PCG + hybrid K-cycle, fp64).
           bytes per launch / CUDA-event launch time vs MEASURED_PEAKS.json hbm_gbs.
   cpu_baseline  the unmodified reference (oracle/_ref) on all host cores, bounded sample.
 
-Multi-GPU (torchrun): every rank solves its own copy of the workload (replicas; the
-row-partitioned solve is future work), scaling "weak".
+Multi-GPU (torchrun, --gpus N > 1): the ROW-PARTITIONED solver: the grid of
+the config is stacked N times along its slowest axis (weak scaling, the config's problem per
+GPU), each rank generates and owns one slab, setup and solve exchange halos and scalars over
+NCCL, coarse levels are agglomerated on rank 0.  --mode replicas instead runs N independent
+copies; --emulate-ranks R runs the partitioned path as R rank threads on one GPU (a
+transport/overhead diagnostic, not a scaling number).
 --impl reference times the reference CPU implementation on the host cores instead.
 """
 import argparse
@@ -365,6 +369,186 @@ def run_b200(args, world, rank, local):
     return 0
 
 
+def dist_grid(dims, nx, ny, nz, world):
+    """Weak scaling: the config's grid per rank, stacked along the slowest axis."""
+    if dims == 2:
+        return nx, ny * world, 1
+    return nx, ny, nz * world
+
+
+def rank_bench(comm, rank, local, args, sync_max, sync_sum):
+    """One rank of the partitioned benchmark (NCCL process or emulated rank thread).
+    sync_max / sync_sum reduce a float over the ranks (host)."""
+    from paper_1403_1649_b200 import aggmg as M
+    from paper_1403_1649_b200 import dist as D
+
+    lib = M.b200().lib
+    world = comm.size
+    label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[args.config]
+    gx, gy, gz = dist_grid(dims, nx, ny, nz, world)
+    setup, cycle, solver = configs_c(M, alpha, method)
+    if dims == 27:
+        dA = D.DistMatrix.jump27(comm, gx, gy, gz, eps, JUMP_BLOCK)
+    else:
+        dA = D.DistMatrix.poisson(comm, dims, gx, gy, gz, eps)
+    n_glob, row0, nloc, nnz_loc = dA.info()
+    nnz_glob = sync_sum(float(nnz_loc))
+
+    def step(record):
+        h = D.setup(comm, dA, setup, agglomerate_rows=args.agglomerate)
+        res = h.solve(solver, cycle)
+        if record is not None:
+            nl, nd, sms = h.info()
+            record.append({"setup_ms": sms, "solve_s": res.report.solve_seconds,
+                           "iterations": res.report.iterations, "converged": res.report.converged,
+                           "levels": nl, "distributed_levels": nd})
+        h.free()
+
+    for _ in range(args.warmup):
+        step(None)
+    records = []
+    if rank == 0 and not args.no_prof:
+        lib.fn("profile_enable")((1 << PROF_SMOOTH) | (1 << PROF_SPMV))
+    launches0 = lib.fn("kernel_launches")()
+    comm.barrier()
+    with ClockSampler(local) as clk:
+        lib.fn("timer_start")()
+        for _ in range(args.steps):
+            step(records)
+        ms = C.c_double()
+        lib.fn("timer_stop")(C.byref(ms))
+    comm.barrier()
+    launches = lib.fn("kernel_launches")() - launches0
+    elapsed_ms = sync_max(ms.value)
+    value = n_glob * args.steps / (elapsed_ms / 1e3)
+    fam = {}
+    if rank == 0:
+        for f, name in ((PROF_SMOOTH, "jacobi_l0"), (PROF_SPMV, "spmv_l0")):
+            t, cnt, by = C.c_double(), C.c_int64(), C.c_double()
+            lib.fn("profile_read")(f, C.byref(t), C.byref(cnt), C.byref(by))
+            fam[name] = (t.value, cnt.value, by.value)
+        lib.fn("profile_enable")(0)
+
+    # end to end: this rank's host slab in, its part of x out
+    e2e = None
+    if not args.no_e2e:
+        kind = "jump27" if dims == 27 else "poisson"
+        rows = D.host_rows(kind, row0, nloc, gx, gy, gz, eps, dims=2 if dims == 2 else 3,
+                           jump=eps, block=JUMP_BLOCK)
+        b = np.ones(nloc)
+        comm.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            A2 = D.DistMatrix.from_rows(comm, n_glob, row0, rows)
+            h = D.setup(comm, A2, setup, agglomerate_rows=args.agglomerate)
+            res = h.solve(solver, cycle, b_local=b, n_local=nloc)
+            h.free()
+            A2.free()
+        comm.barrier()
+        dt = sync_max(time.perf_counter() - t0)
+        h2d = rows.row_offsets.nbytes + rows.col_indices.nbytes + rows.values.nbytes + b.nbytes
+        e2e = {"value": n_glob * args.e2e_steps / dt, "unit": "DOF/s",
+               "h2d_bytes_per_step": int(sync_sum(float(h2d))),
+               "d2h_bytes_per_step": int(n_glob * 8), "iterations": res.report.iterations}
+    dA.free()
+    if rank != 0:
+        return None
+    peak, peak_src = load_peak()
+    roof = None
+    jt, jc, jb = fam.get("jacobi_l0", (0, 0, 0))
+    if jc > 0:
+        achieved = (jb / jc) / ((jt / jc) / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "k_csr_stream<Epi::kJacobi> on level 0 (rank 0's slab)",
+                "bytes_per_launch": jb / jc, "avg_launch_ms": jt / jc, "launches": jc,
+                "peak_source": peak_src, "share_of_step": jt / elapsed_ms}
+    r0 = records[0] if records else {}
+    return {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": ("synthetic: device-generated " + ("27-point jumping-coefficient matrix"
+                 if dims == 27 else "Poisson matrix (poisson.cpp semantics)")
+                 + ", one row slab per rank, b = B0 = ones, x0 = 0"),
+        "config": {"workload": label + f" per GPU, stacked x{world} along the slowest axis",
+                   "grid": [gx, gy, gz], "n": n_glob, "nnz": int(nnz_glob),
+                   "levels": r0.get("levels"), "distributed_levels": r0.get("distributed_levels"),
+                   "agglomerate_rows": args.agglomerate,
+                   "iterations": r0.get("iterations"), "converged": r0.get("converged"),
+                   "setup_ms": statistics.median(r["setup_ms"] for r in records),
+                   "solve_ms": 1e3 * statistics.median(r["solve_s"] for r in records),
+                   "galerkin": "cached sort/segmented reduce order (bit-identical to one GPU)",
+                   "l2": "inputs larger than L2",
+                   "parallelism": f"row-partitioned x{world} ({comm.kind})"},
+        "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+
+def run_dist(args, world, rank, local):
+    """torchrun: one process per GPU, NCCL transport."""
+    import torch
+    import torch.distributed as tdist
+
+    from paper_1403_1649_b200 import dist as D
+
+    torch.cuda.set_device(local)
+    tdist.init_process_group("gloo")
+    obj = [D.nccl_unique_id() if rank == 0 else None]
+    tdist.broadcast_object_list(obj, src=0)
+    comm = D.nccl_comm(rank, world, obj[0], local)
+
+    def red(v, op):
+        t = torch.tensor([v], dtype=torch.float64)
+        tdist.all_reduce(t, op=op)
+        return float(t.item())
+
+    line = rank_bench(comm, rank, local, args, lambda v: red(v, tdist.ReduceOp.MAX),
+                      lambda v: red(v, tdist.ReduceOp.SUM))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    comm.close()
+    tdist.destroy_process_group()
+    return 0
+
+
+def run_emulated(args):
+    """R rank threads on one GPU (in-process transport): overhead diagnostic."""
+    import threading
+
+    from paper_1403_1649_b200 import dist as D
+
+    R = args.emulate_ranks
+    vals, lock, out = {}, threading.Lock(), {}
+    bar = threading.Barrier(R)
+
+    def reducer(op):
+        def f(v):
+            with lock:
+                vals.setdefault(op, []).append(v)
+            bar.wait()
+            res = max(vals[op]) if op == "max" else sum(vals[op])
+            bar.wait()
+            with lock:
+                vals.pop(op, None)
+            bar.wait()
+            return res
+        return f
+
+    def fn(comm, rank):
+        line = rank_bench(comm, rank, 0, args, reducer("max"), reducer("sum"))
+        if rank == 0:
+            out["line"] = line
+
+    D.run_threads(R, fn)
+    line = out["line"]
+    line["config"]["parallelism"] = f"row-partitioned x{R} rank threads emulated on ONE GPU"
+    line["n_gpus"] = 1
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -377,10 +561,27 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-prof", action="store_true", help="skip per-launch CUDA-event timing")
     ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--mode", default="auto", choices=["auto", "single", "dist", "replicas"],
+                    help="auto: one GPU -> single, torchrun N>1 -> dist (row-partitioned)")
+    ap.add_argument("--agglomerate", type=int, default=0,
+                    help="rows at or below which a level is gathered on rank 0 (0 = default)")
+    ap.add_argument("--emulate-ranks", type=int, default=0)
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference_arm(args, world, rank)
+    if args.emulate_ranks > 0:
+        return run_emulated(args)
+    mode = args.mode
+    if mode == "auto":
+        mode = "dist" if world > 1 else "single"
+    if mode == "dist":
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        return run_dist(args, world, rank, local)
     return run_b200(args, world, rank, local)
 
 

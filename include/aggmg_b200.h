@@ -279,6 +279,7 @@ int aggmg_comm_init_nccl(int rank, int nranks, const char id[128], aggmg_comm** 
  * user) runs on every rank thread; returns the first non-zero fn result (or an error). */
 typedef int (*aggmg_rank_fn)(aggmg_comm* comm, int rank, void* user);
 int aggmg_comm_run_threads(int nranks, const int* devices, aggmg_rank_fn fn, void* user);
+int aggmg_comm_barrier(aggmg_comm* c);  /* host + device barrier over the ranks */
 int aggmg_comm_rank(const aggmg_comm* c);
 int aggmg_comm_size(const aggmg_comm* c);
 const char* aggmg_comm_kind(const aggmg_comm* c);
@@ -288,6 +289,12 @@ void aggmg_comm_free(aggmg_comm* c);
  * column ids (canonical rows) */
 int aggmg_dist_matrix_from_host(aggmg_comm* c, int64_t n_global, int64_t row0,
                                 const aggmg_csr* rows, aggmg_dist_matrix** out);
+/* host rows [row0, row0 + nrows) of the generator matrices (global column ids): one rank's
+ * slab as a host input for aggmg_dist_matrix_from_host */
+int aggmg_generate_poisson_rows(int dims, int64_t nx, int64_t ny, int64_t nz, double epsilon,
+                                int weak_axis, int64_t row0, int64_t nrows, aggmg_csr* A);
+int aggmg_generate_jump27_rows(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,
+                               int64_t row0, int64_t nrows, aggmg_csr* A);
 /* generated in HBM on every rank (even row partition) — poisson.cpp:15-77 / DESIGN.md §7 */
 int aggmg_dist_matrix_poisson(aggmg_comm* c, int dims, int64_t nx, int64_t ny, int64_t nz,
                               double epsilon, int weak_axis, aggmg_dist_matrix** out);

@@ -162,10 +162,13 @@ SIGNATURES = {
     "comm_nccl_unique_id": (I, [C.c_char_p]),
     "comm_init_nccl": (I, [I, I, C.c_char_p, C.POINTER(vp)]),
     "comm_run_threads": (I, [I, i32p, vp, vp]),
+    "comm_barrier": (I, [vp]),
     "comm_rank": (I, [vp]),
     "comm_size": (I, [vp]),
     "comm_kind": (C.c_char_p, [vp]),
     "comm_free": (None, [vp]),
+    "generate_poisson_rows": (I, [I, L, L, L, C.c_double, I, L, L, csrp]),
+    "generate_jump27_rows": (I, [L, L, L, C.c_double, L, L, L, csrp]),
     "dist_matrix_from_host": (I, [vp, L, L, csrp, C.POINTER(vp)]),
     "dist_matrix_poisson": (I, [vp, I, L, L, L, C.c_double, I, C.POINTER(vp)]),
     "dist_matrix_jump27": (I, [vp, L, L, L, C.c_double, L, C.POINTER(vp)]),

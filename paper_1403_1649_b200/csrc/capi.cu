@@ -816,10 +816,22 @@ int aggmg_setup_and_solve(const aggmg_csr* A, const double* b, const double* B0,
 
 static void host_to_out(const HostCsr& H, aggmg_csr* A) {
   const int64_t nnz = static_cast<int64_t>(H.col.size());
-  alloc_csr(A, H.n, H.n, nnz);
+  alloc_csr(A, H.n, H.ncols, nnz);
   std::memcpy(A->row_offsets, H.rp.data(), sizeof(int64_t) * (H.n + 1));
   std::memcpy(A->col_indices, H.col.data(), sizeof(int64_t) * nnz);
   std::memcpy(A->values, H.val.data(), sizeof(double) * nnz);
+}
+
+int aggmg_generate_poisson_rows(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
+                                int weak_axis, int64_t row0, int64_t nrows, aggmg_csr* A) {
+  return guarded([&] {
+    host_to_out(generate_poisson_host(dims, nx, ny, nz, eps, weak_axis, row0, nrows), A);
+  });
+}
+
+int aggmg_generate_jump27_rows(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,
+                               int64_t row0, int64_t nrows, aggmg_csr* A) {
+  return guarded([&] { host_to_out(generate_jump27_host(nx, ny, nz, jump, block, row0, nrows), A); });
 }
 
 int aggmg_generate_poisson(int dims, int64_t nx, int64_t ny, int64_t nz, double eps, int weak_axis,
@@ -999,6 +1011,14 @@ int aggmg_comm_run_threads(int nranks, const int* devices, aggmg_rank_fn fn, voi
     for (int r = 0; r < nranks; ++r)
       if (rc[r] != 0)
         throw Error("rank " + std::to_string(r) + ": " + (msg[r].empty() ? "failed" : msg[r]));
+  });
+}
+
+int aggmg_comm_barrier(aggmg_comm* c) {
+  return guarded([&] {
+    require(c != nullptr, "null comm");
+    c->comm->barrier();
+    sync();
   });
 }
 

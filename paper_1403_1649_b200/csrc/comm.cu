@@ -36,14 +36,14 @@ __global__ void k_sum_ranks_i64(const int64_t* all, int n, int nranks, int64_t* 
 // ---- helpers --------------------------------------------------------------------
 
 void Comm::allreduce_sum(double* v, int n) {
-  if (n <= 0) return;
+  if (n <= 0 || size_ == 1) return;  // one rank: the sum of one partial is the partial
   DevBuf<double> all(static_cast<int64_t>(n) * size_);
   allgather(v, all.get(), sizeof(double) * n);
   AGG_LAUNCH(k_sum_ranks_f64, grid_for(n, 128), 128, 0, all.get(), n, size_, v);
 }
 
 void Comm::allreduce_sum(int64_t* v, int n) {
-  if (n <= 0) return;
+  if (n <= 0 || size_ == 1) return;
   DevBuf<int64_t> all(static_cast<int64_t>(n) * size_);
   allgather(v, all.get(), sizeof(int64_t) * n);
   AGG_LAUNCH(k_sum_ranks_i64, grid_for(n, 128), 128, 0, all.get(), n, size_, v);

@@ -186,6 +186,9 @@ __global__ void k_gemv(int64_t n, const double* __restrict__ M, const double* __
   if (lane == 0) x[row] = s;
 }
 
+// the global finest level (profiling families time level 0 only)
+bool finest(const DevHierarchy& h, int64_t k) { return k + h.cfg.level_offset == 0; }
+
 bool accelerated(const CycleCfg& c, int64_t k) {  // cycles.cpp:16-20
   if (c.kind == 1) return true;
   if (c.kind == 2) return k < c.k_levels;
@@ -239,11 +242,11 @@ void descend(DevHierarchy& h, int64_t k, const double* b, const double* x_in, do
   if (kFuseZeroGuess && !x_in && L.smoother.kind != 2) {
     ra.x_out = x_out;
     ra.d = L.smoother.wdiag.get();
-    spmv_run(*L.A, Epi::kResidualZero, ra, k == 0 ? kProfSpmvL0 : 0);
+    spmv_run(*L.A, Epi::kResidualZero, ra, finest(h, k) ? kProfSpmvL0 : 0);
   } else {
-    presmooth(L, b, x_in, x_out, pred, k == 0);
+    presmooth(L, b, x_in, x_out, pred, finest(h, k));
     ra.x = x_out;
-    spmv_run(*L.A, Epi::kResidual, ra, k == 0 ? kProfSpmvL0 : 0);  // cycles.cpp:30-35
+    spmv_run(*L.A, Epi::kResidual, ra, finest(h, k) ? kProfSpmvL0 : 0);  // cycles.cpp:30-35
   }
   SpmvArgs rr;
   rr.x = L.r.get();
@@ -350,7 +353,7 @@ void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in,
   DevLevel& L = h.levels[k];
   descend(h, k, b, x_in, x_out, pred);
   coarse_correction(h, CycleCfg{}, false, k + 1, L.rc.get(), L.xc.get(), work_of(L), pred);
-  postsmooth(L, b, x_out, pred, k == 0);
+  postsmooth(L, b, x_out, pred, finest(h, k));
 }
 
 void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
@@ -362,7 +365,7 @@ void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b
   DevLevel& L = h.levels[k];
   descend(h, k, b, x_in, x_out, pred);
   coarse_correction(h, cfg, true, k + 1, L.rc.get(), L.xc.get(), work_of(L), pred);
-  postsmooth(L, b, x_out, pred, k == 0);
+  postsmooth(L, b, x_out, pred, finest(h, k));
 }
 
 }  // namespace

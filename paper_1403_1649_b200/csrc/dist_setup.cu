@@ -20,6 +20,8 @@
 #include <chrono>
 #include <cmath>
 #include <cub/cub.cuh>
+#include <cstdio>
+#include <cstdlib>
 #include <sstream>
 
 #include "dist_hierarchy.cuh"
@@ -88,32 +90,6 @@ __global__ void k_count_cols(const idx* col, int64_t nnz, idx* cnt) {
   if (k < nnz) atomicAdd(&cnt[col[k]], 1);
 }
 // transpose pairs (row = global column of C, col = global row), destination = owner of row
-__global__ void k_tpairs_count(const idx* rp, const idx* gcol, int64_t n, PartDev p, unsigned long long* cnt) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  for (idx k = rp[i]; k < rp[i + 1]; ++k) atomicAdd(&cnt[dev_owner(p, gcol[k])], 1ull);
-}
-__global__ void k_tpairs_fill(const idx* rp, const idx* gcol, int64_t n, int64_t row0, PartDev p,
-                              const int64_t* off, unsigned long long* cursor, int2* out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  for (idx k = rp[i]; k < rp[i + 1]; ++k) {
-    const int q = dev_owner(p, gcol[k]);
-    const unsigned long long slot = atomicAdd(&cursor[q], 1ull);
-    out[off[q] + slot] = make_int2(gcol[k], static_cast<int>(row0 + i));
-  }
-}
-__global__ void k_tkeys(const int2* pr, int64_t m, int64_t row0, unsigned long long* key) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= m) return;
-  key[k] = (static_cast<unsigned long long>(pr[k].x - row0) << 32) | static_cast<unsigned>(pr[k].y);
-}
-__global__ void k_tsplit(const unsigned long long* key, int64_t m, idx* trow_cnt, idx* tcol) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= m) return;
-  atomicAdd(&trow_cnt[key[k] >> 32], 1);
-  tcol[k] = static_cast<idx>(key[k] & 0xffffffffull);
-}
 // sorted merge of C row i and C^T row i (strength.cpp:86-103), global ids.  mode 0 counts.
 __global__ void k_merge_rows_g(const idx* crp, const idx* ccol, const idx* trp, const idx* tcol,
                                int64_t n, int mode, const idx* srp, idx* out) {
@@ -334,151 +310,16 @@ __global__ void k_count_u(const unsigned* own, int64_t m, long long* cnt) {
   if (k < m) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[own[k]]), 1ull);
 }
 
-// ---- transfer ------------------------------------------------------------------------------
+// ---- transfer: an exported member row (global aggregate id, global row id, b_i) ----------
 struct __align__(16) MemberRec {
-  int J;     // global coarse id
-  int gid;   // global fine id
-  double b;  // fine near-null-space value
+  int J;
+  int gid;
+  double b;
 };
-__global__ void k_member_recs(const idx* fid, const double* b, int64_t n, int64_t row0, PartDev cp,
-                              MemberRec* rec, unsigned* dest, idx* perm) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  MemberRec r;
-  r.J = fid[i];
-  r.gid = static_cast<int>(row0 + i);
-  r.b = b[i];
-  rec[i] = r;
-  dest[i] = static_cast<unsigned>(dev_owner(cp, fid[i]));
-  perm[i] = static_cast<idx>(i);
-}
-template <class T>
-__global__ void k_gather_rec(const T* in, const idx* perm, int64_t m, T* out) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k < m) out[k] = in[perm[k]];
-}
-__global__ void k_member_keys(const MemberRec* rec, int64_t m, int64_t cbase, unsigned long long* key,
-                              idx* perm, idx* cnt) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= m) return;
-  const int64_t Jl = rec[k].J - cbase;
-  key[k] = (static_cast<unsigned long long>(Jl) << 32) | static_cast<unsigned>(rec[k].gid);
-  perm[k] = static_cast<idx>(k);
-  atomicAdd(&cnt[Jl], 1);
-}
-// sq_J over members in ascending global order (transfer.cpp:21-22); R rows
-__global__ void k_dtransfer_norms(const idx* goff, const idx* perm, const MemberRec* rec, int64_t nc,
-                                  double* coarse_b, idx* rcnt, int* bad) {
-  const int64_t J = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (J >= nc) return;
-  double sq = 0.0;
-  idx c = 0;
-  for (idx m = goff[J]; m < goff[J + 1]; ++m) {
-    const double bi = rec[perm[m]].b;
-    sq = __dadd_rn(sq, __dmul_rn(bi, bi));
-    c += (bi != 0.0) ? 1 : 0;
-  }
-  if (!(sq > 0.0)) atomicMin(bad, static_cast<int>(J));
-  coarse_b[J] = __dsqrt_rn(sq);
-  rcnt[J] = c;
-}
-__global__ void k_dtransfer_R(const idx* goff, const idx* perm, const MemberRec* rec, int64_t nc,
-                              const double* coarse_b, const idx* rrp, idx* rcol, double* rval) {
-  const int64_t J = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (J >= nc) return;
-  idx p = rrp[J];
-  for (idx m = goff[J]; m < goff[J + 1]; ++m) {
-    const MemberRec r = rec[perm[m]];
-    if (r.b != 0.0) {
-      rcol[p] = r.gid;
-      rval[p] = __ddiv_rn(r.b, coarse_b[J]);
-      ++p;
-    }
-  }
-}
-__global__ void k_dtransfer_pval(const double* b, const double* cb_of_row, int64_t n, double* pval) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double bi = b[i];
-  pval[i] = (bi != 0.0) ? __ddiv_rn(bi, cb_of_row[i]) : 0.0;
-}
-
-// ---- Galerkin --------------------------------------------------------------------------------
-struct __align__(16) GalRec {
-  int I;  // global coarse row
-  int J;  // global coarse column
-  double v;  // (p_i a_ij) p_j
-};
-__global__ void k_gal_recs(const idx* rp, const idx* col, const double* val, int64_t n,
-                           const idx* fid, const double* pv, PartDev cp, GalRec* rec, unsigned* dest,
-                           idx* perm) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const idx I = fid[i];
-  const unsigned d = static_cast<unsigned>(dev_owner(cp, I));
-  const double pi = pv[i];
-  for (idx e = rp[i]; e < rp[i + 1]; ++e) {
-    GalRec r;
-    r.I = I;
-    r.J = fid[col[e]];
-    r.v = __dmul_rn(__dmul_rn(pi, val[e]), pv[col[e]]);
-    rec[e] = r;
-    dest[e] = d;
-    perm[e] = e;
-  }
-}
-__global__ void k_gal_keys(const GalRec* rec, int64_t m, int64_t cbase, unsigned long long* key, idx* perm) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= m) return;
-  key[k] = (static_cast<unsigned long long>(rec[k].I - cbase) << 32) | static_cast<unsigned>(rec[k].J);
-  perm[k] = static_cast<idx>(k);
-}
-__global__ void k_seg_sum(const idx* seg_off, int64_t nseg, const idx* perm, const GalRec* rec,
-                          const unsigned long long* ukey, int64_t cbase, double* out_val, idx* out_col,
-                          idx* row_cnt) {
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= nseg) return;
-  double acc = 0.0;
-  for (idx p = seg_off[s]; p < seg_off[s + 1]; ++p) acc = __dadd_rn(acc, rec[perm[p]].v);
-  out_val[s] = acc;
-  out_col[s] = static_cast<idx>(ukey[s] & 0xffffffffull);
-  atomicAdd(&row_cnt[ukey[s] >> 32], 1);
-}
 
 __global__ void k_uniform_sym_off(int64_t n, int64_t row0, uint64_t seed, double* x) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) x[i] = uniform_sym(seed, static_cast<uint64_t>(row0 + i));
-}
-
-// records grouped by destination (stable: original order kept inside each destination)
-template <class T>
-DevBuf<double2> ship_stable(Comm& comm, const T* rec, DevBuf<unsigned>& dest, DevBuf<idx>& perm,
-                            int64_t m, std::vector<int64_t>* recv_cnt) {
-  static_assert(sizeof(T) == sizeof(double2), "records travel as 16-byte units");
-  const int P = comm.size();
-  DevBuf<unsigned> dest_s(m);
-  DevBuf<idx> perm_s(m);
-  DevBuf<long long> cnt_d(P);
-  cnt_d.zero();
-  DevBuf<T> grouped(m);
-  if (m > 0) {
-    AGG_LAUNCH(k_count_u, grid_for(m, 256), 256, 0, dest.get(), m, cnt_d.get());
-    if (P > 1) {
-      const int nbits = std::max(1, 32 - __builtin_clz(static_cast<unsigned>(P)));
-      cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, dest.get(), dest_s.get(), perm.get(),
-                                               perm_s.get(), static_cast<int>(m), 0, nbits, stream());
-      });
-      AGG_LAUNCH(k_gather_rec<T>, grid_for(m, 256), 256, 0, rec, perm_s.get(), m, grouped.get());
-    } else {
-      AGG_CUDA(cudaMemcpyAsync(grouped.get(), rec, sizeof(T) * m, cudaMemcpyDeviceToDevice, stream()));
-    }
-  }
-  std::vector<long long> c(P);
-  cnt_d.download(c.data(), P);
-  sync();
-  std::vector<int64_t> cnt(c.begin(), c.end());
-  return alltoallv<double2>(comm, reinterpret_cast<const double2*>(grouped.get()), cnt, recv_cnt);
 }
 
 double dist_dot(Comm& comm, const double* a, const double* b, int64_t n) {
@@ -499,6 +340,234 @@ double dist_dot(Comm& comm, const double* a, const double* b, int64_t n) {
 
 
 namespace {
+
+
+
+// ---- C^T pieces ------------------------------------------------------------------------------
+__global__ void k_cross_count(const idx* rp, const idx* col, const idx* gcol, int64_t n, int64_t nloc,
+                              PartDev p, unsigned long long* cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (idx k = rp[i]; k < rp[i + 1]; ++k)
+    if (col[k] >= nloc) atomicAdd(&cnt[dev_owner(p, gcol[k])], 1ull);
+}
+__global__ void k_cross_fill(const idx* rp, const idx* col, const idx* gcol, int64_t n, int64_t nloc,
+                             int64_t row0, PartDev p, const int64_t* off, unsigned long long* cursor,
+                             int2* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+    if (col[k] < nloc) continue;
+    const int q = dev_owner(p, gcol[k]);
+    const unsigned long long slot = atomicAdd(&cursor[q], 1ull);
+    out[off[q] + slot] = make_int2(gcol[k], static_cast<int>(row0 + i));
+  }
+}
+__global__ void k_tcount_local(const idx* rp, const idx* col, int64_t n, int64_t nloc, idx* cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (idx k = rp[i]; k < rp[i + 1]; ++k)
+    if (col[k] < nloc) atomicAdd(&cnt[col[k]], 1);
+}
+__global__ void k_tcount_remote(const int2* pr, int64_t m, int64_t row0, idx* cnt) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) atomicAdd(&cnt[pr[k].x - row0], 1);
+}
+__global__ void k_tfill_local(const idx* rp, const idx* col, int64_t n, int64_t nloc, int64_t row0,
+                              const idx* trp, idx* cur, idx* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+    const idx c = col[k];
+    if (c < nloc) out[trp[c] + atomicAdd(&cur[c], 1)] = static_cast<idx>(row0 + i);
+  }
+}
+__global__ void k_tfill_remote(const int2* pr, int64_t m, int64_t row0, const idx* trp, idx* cur, idx* out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int64_t r = pr[k].x - row0;
+  out[trp[r] + atomicAdd(&cur[r], 1)] = pr[k].y;
+}
+
+// ---- extended row set (transfer / Galerkin across ranks) ------------------------------------
+struct __align__(16) EntRec {
+  double a;    // entry value
+  double pvc;  // P weight of the entry's column
+};
+static_assert(sizeof(EntRec) == 16, "EntRec travels as a 16-byte unit");
+__global__ void k_agg_owner(const idx* fid, int64_t n, PartDev cp, int me, unsigned* dest, idx* ex) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int o = dev_owner(cp, fid[i]);
+  dest[i] = static_cast<unsigned>(o);
+  ex[i] = (o != me) ? 1 : 0;
+}
+__global__ void k_export_list(const idx* ex, const idx* pos, const unsigned* dest, int64_t n, idx* rows,
+                              unsigned* d) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || !ex[i]) return;
+  rows[pos[i]] = static_cast<idx>(i);
+  d[pos[i]] = dest[i];
+}
+__global__ void k_export_members(const idx* rows, int64_t m, const idx* fid, const double* b, int64_t row0,
+                                 MemberRec* out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const idx i = rows[k];
+  MemberRec r;
+  r.J = fid[i];
+  r.gid = static_cast<int>(row0 + i);
+  r.b = b[i];
+  out[k] = r;
+}
+__global__ void k_ext_rows(const double* b, int64_t nloc, int64_t ntot, int64_t row0, const MemberRec* imp,
+                           int64_t m, double* b_ext, idx* gid_ext) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nloc) {
+    b_ext[i] = b[i];
+    gid_ext[i] = static_cast<idx>(row0 + i);
+  } else if (i < ntot) {
+    gid_ext[i] = -1;
+  } else if (i < ntot + m) {
+    const MemberRec r = imp[i - ntot];
+    b_ext[i] = r.b;
+    gid_ext[i] = r.gid;
+  }
+}
+__global__ void k_group_count(const idx* fid, const idx* ex, int64_t nloc, const MemberRec* imp, int64_t m,
+                              int64_t cbase, idx* cnt) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < nloc) {
+    if (!ex[t]) atomicAdd(&cnt[fid[t] - cbase], 1);
+  } else if (t < nloc + m) {
+    atomicAdd(&cnt[imp[t - nloc].J - cbase], 1);
+  }
+}
+// keys = global row id (unique), payload = extended row index (exact as a double)
+__global__ void k_group_fill(const idx* fid, const idx* ex, int64_t nloc, int64_t ntot, int64_t row0,
+                             const MemberRec* imp, int64_t m, int64_t cbase, const idx* off, idx* cur,
+                             idx* keys, double* pay) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t Jl, gid, ext;
+  if (t < nloc) {
+    if (ex[t]) return;
+    Jl = fid[t] - cbase;
+    gid = row0 + t;
+    ext = t;
+  } else if (t < nloc + m) {
+    Jl = imp[t - nloc].J - cbase;
+    gid = imp[t - nloc].gid;
+    ext = ntot + (t - nloc);
+  } else {
+    return;
+  }
+  const idx p = off[Jl] + atomicAdd(&cur[Jl], 1);
+  keys[p] = static_cast<idx>(gid);
+  pay[p] = static_cast<double>(ext);
+}
+__global__ void k_payload_to_idx(const double* pay, int64_t n, idx* out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = static_cast<idx>(pay[t]);
+}
+__global__ void k_export_J(const idx* rows, int64_t m, const idx* fid, idx* q) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) q[k] = fid[rows[k]];
+}
+// p_i = b_i / ||b_J|| (transfer.cpp:42-45) for local rows of owned aggregates and imports
+__global__ void k_ext_pval(const double* b_ext, const idx* fid, const idx* ex, int64_t nloc, int64_t ntot,
+                           const MemberRec* imp, int64_t m, int64_t cbase, const double* cb, double* pv) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nloc) {
+    if (ex[i]) return;
+    const double bi = b_ext[i];
+    pv[i] = (bi != 0.0) ? __ddiv_rn(bi, cb[fid[i] - cbase]) : 0.0;
+  } else if (i >= ntot && i < ntot + m) {
+    const double bi = b_ext[i];
+    pv[i] = (bi != 0.0) ? __ddiv_rn(bi, cb[imp[i - ntot].J - cbase]) : 0.0;
+  }
+}
+__global__ void k_export_pval(const idx* rows, const double* cb, const double* b, int64_t m, double* pv) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const idx i = rows[k];
+  const double bi = b[i];
+  pv[i] = (bi != 0.0) ? __ddiv_rn(bi, cb[k]) : 0.0;
+}
+__global__ void k_map_idx(idx* x, int64_t n, const idx* map) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) x[k] = map[x[k]];
+}
+__global__ void k_export_len(const idx* rows, int64_t m, const idx* rp, idx* len) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) len[k] = rp[rows[k] + 1] - rp[rows[k]];
+}
+__global__ void k_export_entries(const idx* rows, int64_t m, const idx* off, const idx* rp, const idx* col,
+                                 const double* val, const idx* fid, const double* pv, EntRec* out,
+                                 idx* jc) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const idx i = rows[k];
+  idx p = off[k];
+  for (idx e = rp[i]; e < rp[i + 1]; ++e, ++p) {
+    EntRec r;
+    r.a = val[e];
+    r.pvc = pv[col[e]];
+    out[p] = r;
+    jc[p] = fid[col[e]];
+  }
+}
+__global__ void k_ext_entries(const EntRec* ent, const idx* jc, int64_t nie, int64_t base, int64_t next,
+                              idx* col, double* val, idx* asg, double* pvc) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nie) return;
+  col[base + t] = static_cast<idx>(next + t);
+  val[base + t] = ent[t].a;
+  asg[next + t] = jc[t];
+  pvc[next + t] = ent[t].pvc;
+}
+__global__ void k_ext_len(const idx* rp, int64_t nloc, int64_t ntot, const idx* ilen, int64_t m, idx* len) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nloc)
+    len[i] = rp[i + 1] - rp[i];
+  else if (i < ntot)
+    len[i] = 0;
+  else if (i < ntot + m)
+    len[i] = ilen[i - ntot];
+}
+
+// AGGMG_DIST_TIMING=1: per-phase wall time of the distributed setup on rank 0 (stderr).
+struct PhaseTimer {
+  bool on = false;
+  int rank = 0;
+  std::chrono::steady_clock::time_point t;
+  std::vector<std::pair<std::string, double>> acc;
+  PhaseTimer() {
+    const char* e = std::getenv("AGGMG_DIST_TIMING");
+    on = e && e[0] == '1';
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    sync();
+    const auto now = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+    t = now;
+    for (auto& a : acc)
+      if (a.first == name) {
+        a.second += ms;
+        return;
+      }
+    acc.emplace_back(name, ms);
+  }
+  void report() {
+    if (!on || rank != 0) return;
+    for (auto& a : acc) std::fprintf(stderr, "[dist setup] %-12s %8.2f ms\n", a.first.c_str(), a.second);
+  }
+};
+thread_local PhaseTimer* g_phase = nullptr;
+void phase(const char* name) {
+  if (g_phase) g_phase->mark(name);
+}
 
 struct Coarsened {
   bool stalled = false;
@@ -523,14 +592,19 @@ Coarsened coarsen_level(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k
   infl.zero();
   if (C->nnz) AGG_LAUNCH(k_count_cols, grid_for(C->nnz, 256), 256, 0, C->col.get(), C->nnz, infl.get());
   halo_reverse_add(comm, A.halo, infl.get());
+  phase("strength");
 
   // ---- a5 S = C u C^T (global ids), then local ids over A's halo ----
   DevBuf<idx> Cg(C->nnz);
   globalize_cols(A.halo, C->col.get(), C->nnz, Cg.get());
+  // C^T: entries with an owned column are transposed locally; the cross entries travel to
+  // the owner of their column as (row, col) pairs (global ids)
   DevBuf<unsigned long long> tcnt(P), tcur(P);
   tcnt.zero();
   tcur.zero();
-  if (nloc) AGG_LAUNCH(k_tpairs_count, g, 256, 0, C->rowptr.get(), Cg.get(), nloc, rp_dev, tcnt.get());
+  if (nloc)
+    AGG_LAUNCH(k_cross_count, g, 256, 0, C->rowptr.get(), C->col.get(), Cg.get(), nloc, nloc, rp_dev,
+               tcnt.get());
   std::vector<unsigned long long> tc(P);
   tcnt.download(tc.data(), P);
   sync();
@@ -541,25 +615,28 @@ Coarsened coarsen_level(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k
   }
   DevBuf<int64_t> toff_d(P + 1);
   toff_d.upload(toff.data(), P + 1);
-  DevBuf<int2> tpairs(C->nnz);
-  if (nloc)
-    AGG_LAUNCH(k_tpairs_fill, g, 256, 0, C->rowptr.get(), Cg.get(), nloc, row0, rp_dev, toff_d.get(),
-               tcur.get(), tpairs.get());
+  DevBuf<int2> tpairs(toff[P]);
+  if (nloc && toff[P])
+    AGG_LAUNCH(k_cross_fill, g, 256, 0, C->rowptr.get(), C->col.get(), Cg.get(), nloc, nloc, row0, rp_dev,
+               toff_d.get(), tcur.get(), tpairs.get());
   DevBuf<int2> mine = alltoallv<int2>(comm, tpairs.get(), tsend);
   tpairs.reset();
   const int64_t mt = mine.size();
-  DevBuf<unsigned long long> tkey(mt), tkey_s(mt);
-  DevBuf<idx> trp(nloc + 1), trow_cnt(nloc), tcol(mt);
+  DevBuf<idx> trp(nloc + 1), trow_cnt(nloc), tcur2(nloc), ttmp(C->nnz + mt), tcol(C->nnz + mt);
   trow_cnt.zero();
-  if (mt > 0) {
-    AGG_LAUNCH(k_tkeys, grid_for(mt, 256), 256, 0, mine.get(), mt, row0, tkey.get());
-    cub_call([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, tkey.get(), tkey_s.get(), static_cast<int>(mt), 0, 64,
-                                            stream());
-    });
-    AGG_LAUNCH(k_tsplit, grid_for(mt, 256), 256, 0, tkey_s.get(), mt, trow_cnt.get(), tcol.get());
-  }
+  tcur2.zero();
+  if (nloc)
+    AGG_LAUNCH(k_tcount_local, g, 256, 0, C->rowptr.get(), C->col.get(), nloc, nloc, trow_cnt.get());
+  if (mt) AGG_LAUNCH(k_tcount_remote, grid_for(mt, 256), 256, 0, mine.get(), mt, row0, trow_cnt.get());
   scan_to_offsets_async(trow_cnt.get(), trp.get(), nloc);
+  if (nloc)
+    AGG_LAUNCH(k_tfill_local, g, 256, 0, C->rowptr.get(), C->col.get(), nloc, nloc, row0, trp.get(),
+               tcur2.get(), ttmp.get());
+  if (mt)
+    AGG_LAUNCH(k_tfill_remote, grid_for(mt, 256), 256, 0, mine.get(), mt, row0, trp.get(), tcur2.get(),
+               ttmp.get());
+  segmented_sort(trp.get(), nloc, ttmp.get(), tcol.get());
+  ttmp.reset();
   DevBuf<idx> scnt(nloc), srp(nloc + 1);
   if (nloc)
     AGG_LAUNCH(k_merge_rows_g, g, 256, 0, C->rowptr.get(), Cg.get(), trp.get(), tcol.get(), nloc, 0,
@@ -576,6 +653,7 @@ Coarsened coarsen_level(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k
   Cg.reset();
   sg.reset();
   mine.reset();
+  phase("symmetrize");
 
   // ---- a6 MIS(2) ----
   DevBuf<Tuple> cur(ntot), mid(ntot);
@@ -606,6 +684,7 @@ Coarsened coarsen_level(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k
   }
   cur.reset();
   mid.reset();
+  phase("mis2");
 
   // ---- a7 aggregation ----
   halo_update<int8_t>(comm, A.halo, state.get());
@@ -629,7 +708,7 @@ Coarsened coarsen_level(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k
     DevBuf<unsigned> own(nreq);
     DevBuf<idx> perm(nreq);
     if (nreq) AGG_LAUNCH(k_req_owner, grid_for(nreq, 256), 256, 0, req.get(), nreq, rp_dev, own.get(), perm.get());
-    // ship_stable returns the requests grouped by source; remember the permutation
+    // requests grouped (stably) by owner; the permutation routes the answers back
     DevBuf<unsigned> own_s(nreq);
     DevBuf<idx> perm_s(nreq);
     DevBuf<long long> cnt_d(P);
@@ -679,61 +758,119 @@ Coarsened coarsen_level(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k
   halo_update<idx>(comm, A.halo, fid.get());
   srp.reset();
   scol.reset();
+  phase("aggregate");
 
-  // ---- a8 transfer ----
+  // ---- a8 transfer / a9-a10 Galerkin over the EXTENDED row set ----
+  // Rows whose aggregate lives on another rank are exported to the aggregate's owner.  The
+  // owner's extended row space is [0, nloc) local rows, [nloc, ntot) halo (empty rows),
+  // [ntot, ntot + m) imported rows; member groups are ordered by global row id, so the
+  // one-GPU group kernels (ascending-member norms, R rows, the Galerkin sort / ordered
+  // segment sums) run unchanged and reproduce the reference order across ranks.
   const PartDev cp_dev = part_dev(cpart);
-  DevBuf<MemberRec> mrec(nloc);
-  DevBuf<unsigned> mdest(nloc);
-  DevBuf<idx> mperm(nloc);
+  DevBuf<unsigned> odest(nloc);
+  DevBuf<idx> exflag(nloc), expos(nloc + 1);
   if (nloc)
-    AGG_LAUNCH(k_member_recs, g, 256, 0, fid.get(), L.B.get(), nloc, row0, cp_dev, mrec.get(),
-               mdest.get(), mperm.get());
-  DevBuf<double2> members_buf = ship_stable<MemberRec>(comm, mrec.get(), mdest, mperm, nloc, nullptr);
-  const MemberRec* members = reinterpret_cast<const MemberRec*>(members_buf.get());
-  const int64_t nm = members_buf.size();
-  DevBuf<unsigned long long> mkey(nm), mkey_s(nm);
-  DevBuf<idx> mp(nm), mp_s(nm), gcnt(ncl), goff(ncl + 1);
-  gcnt.zero();
-  if (nm) {
-    AGG_LAUNCH(k_member_keys, grid_for(nm, 256), 256, 0, members, nm, cbase, mkey.get(), mp.get(),
-               gcnt.get());
-    cub_call([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, mkey.get(), mkey_s.get(), mp.get(), mp_s.get(),
-                                             static_cast<int>(nm), 0, 64, stream());
+    AGG_LAUNCH(k_agg_owner, g, 256, 0, fid.get(), nloc, cp_dev, me, odest.get(), exflag.get());
+  const int64_t nexp = scan_to_offsets(exflag.get(), expos.get(), nloc);
+  // exported rows in row order, grouped (stably) by destination
+  DevBuf<idx> exrow(nexp), exrow_s(nexp);
+  DevBuf<unsigned> exdest(nexp), exdest_s(nexp);
+  std::vector<int64_t> ecnt(P, 0);
+  if (nexp) {
+    AGG_LAUNCH(k_export_list, g, 256, 0, exflag.get(), expos.get(), odest.get(), nloc, exrow.get(),
+               exdest.get());
+    DevBuf<long long> cnt_d(P);
+    cnt_d.zero();
+    AGG_LAUNCH(k_count_u, grid_for(nexp, 256), 256, 0, exdest.get(), nexp, cnt_d.get());
+    const int nbits = std::max(1, 32 - __builtin_clz(static_cast<unsigned>(P)));
+    cub_call([&](void* t, size_t& bb) {
+      return cub::DeviceRadixSort::SortPairs(t, bb, exdest.get(), exdest_s.get(), exrow.get(),
+                                             exrow_s.get(), static_cast<int>(nexp), 0, nbits, stream());
     });
+    std::vector<long long> c(P);
+    cnt_d.download(c.data(), P);
+    sync();
+    for (int q = 0; q < P; ++q) ecnt[q] = c[q];
   }
+  // round 1: (gid, J, b) of every exported row
+  DevBuf<MemberRec> mrec(nexp);
+  if (nexp)
+    AGG_LAUNCH(k_export_members, grid_for(nexp, 256), 256, 0, exrow_s.get(), nexp, fid.get(),
+               L.B.get(), row0, mrec.get());
+  std::vector<int64_t> icnt;
+  DevBuf<double2> imp_buf = alltoallv<double2>(comm, reinterpret_cast<const double2*>(mrec.get()), ecnt, &icnt);
+  const MemberRec* imp = reinterpret_cast<const MemberRec*>(imp_buf.get());
+  const int64_t m = imp_buf.size();
+  const int64_t next = ntot + m;  // extended row space
+  DevBuf<double> b_ext(next);
+  DevBuf<idx> gid_ext(next);
+  b_ext.zero();
+  if (next)
+    AGG_LAUNCH(k_ext_rows, grid_for(next, 256), 256, 0, L.B.get(), nloc, ntot, row0, imp, m,
+               b_ext.get(), gid_ext.get());
+  // member groups of the owned aggregates, ascending global row id
+  DevBuf<idx> gcnt(ncl), goff(ncl + 1), gcur(ncl), gkeys(nloc + m), gsorted(nloc + m);
+  DevBuf<double> gpay(nloc + m), gpay_s(nloc + m);
+  gcnt.zero();
+  gcur.zero();
+  if (nloc + m)
+    AGG_LAUNCH(k_group_count, grid_for(nloc + m, 256), 256, 0, fid.get(), exflag.get(), nloc, imp, m,
+               cbase, gcnt.get());
   scan_to_offsets_async(gcnt.get(), goff.get(), ncl);
+  if (nloc + m)
+    AGG_LAUNCH(k_group_fill, grid_for(nloc + m, 256), 256, 0, fid.get(), exflag.get(), nloc, ntot,
+               row0, imp, m, cbase, goff.get(), gcur.get(), gkeys.get(), gpay.get());
+  segmented_sort(goff.get(), ncl, gkeys.get(), gsorted.get(), gpay.get(), gpay_s.get());
+  DevBuf<idx> rows_ext(nloc + m);
+  if (nloc + m)
+    AGG_LAUNCH(k_payload_to_idx, grid_for(nloc + m, 256), 256, 0, gpay_s.get(), nloc + m, rows_ext.get());
+  gkeys.reset();
+  gpay.reset();
+  gpay_s.reset();
+  gsorted.reset();
+  // coarse norms (transfer.cpp:21-29) and R rows
   out.Bc.resize(ncl);
   DevBuf<idx> rcnt(ncl);
-  DevBuf<int> bad(1);
-  fill_int(bad.get(), 1, INT32_MAX);
-  if (ncl)
-    AGG_LAUNCH(k_dtransfer_norms, grid_for(ncl, 256), 256, 0, goff.get(), mp_s.get(), members, ncl,
-               out.Bc.get(), rcnt.get(), bad.get());
+  {
+    const int64_t bad = transfer_norms_groups(goff.get(), rows_ext.get(), b_ext.get(), ncl,
+                                              out.Bc.get(), rcnt.get());
+    const int64_t worst = comm.allreduce_host_max(bad < 0 ? -1 : cbase + bad);
+    if (worst >= 0)
+      throw Error("transfer: near-null-space vector vanishes on aggregate " + std::to_string(worst));
+  }
+  // P values: owned aggregates here, the others from their owners' norms
+  DevBuf<idx> fq(nexp);
+  DevBuf<double> fcb(nexp);
+  if (nexp)
+    AGG_LAUNCH(k_export_J, grid_for(nexp, 256), 256, 0, exrow.get(), nexp, fid.get(), fq.get());
+  fetch_remote<double>(comm, cpart, out.Bc.get(), fq.get(), nexp, fcb.get());
+  DevBuf<double> pv_ext(next);
+  pv_ext.zero();
+  if (next)
+    AGG_LAUNCH(k_ext_pval, grid_for(next, 256), 256, 0, b_ext.get(), fid.get(), exflag.get(), nloc,
+               ntot, imp, m, cbase, out.Bc.get(), pv_ext.get());
+  if (nexp)
+    AGG_LAUNCH(k_export_pval, grid_for(nexp, 256), 256, 0, exrow.get(), fcb.get(), L.B.get(), nexp,
+               pv_ext.get());
   auto Rg = std::make_shared<DevCsr>();
   Rg->n_rows = ncl;
   Rg->n_cols = n_glob;
   Rg->rowptr.resize(ncl + 1);
   Rg->nnz = scan_to_offsets(rcnt.get(), Rg->rowptr.get(), ncl);
-  {
-    const int b = read_scalar(bad.get());
-    const int64_t worst = comm.allreduce_host_max(b == INT32_MAX ? -1 : cbase + b);
-    if (worst >= 0)
-      throw Error("transfer: near-null-space vector vanishes on aggregate " + std::to_string(worst));
-  }
   Rg->col.resize(Rg->nnz);
   Rg->val.resize(Rg->nnz);
-  if (ncl)
-    AGG_LAUNCH(k_dtransfer_R, grid_for(ncl, 256), 256, 0, goff.get(), mp_s.get(), members, ncl,
-               out.Bc.get(), Rg->rowptr.get(), Rg->col.get(), Rg->val.get());
+  transfer_R_groups(goff.get(), rows_ext.get(), pv_ext.get(), ncl, Rg->rowptr.get(), Rg->col.get(),
+                    Rg->val.get());
+  if (Rg->nnz)
+    AGG_LAUNCH(k_map_idx, grid_for(Rg->nnz, 256), 256, 0, Rg->col.get(), Rg->nnz, gid_ext.get());
   L.R = make_dist(comm, cpart, A.rows, *Rg, "restriction: member outside the plan");
-  members_buf.reset();
-  // P: coarse norms of the aggregates of my rows, then p_i = b_i / ||b_J||
-  DevBuf<double> cb_row(nloc);
-  fetch_remote<double>(comm, cpart, out.Bc.get(), fid.get(), nloc, cb_row.get());
+  // P on this rank's rows: coarse id (local numbering over the P plan) and value
   L.pval.resize(ntot);
-  L.pval.zero();
-  if (nloc) AGG_LAUNCH(k_dtransfer_pval, g, 256, 0, L.B.get(), cb_row.get(), nloc, L.pval.get());
+  AGG_CUDA(cudaMemcpyAsync(L.pval.get(), pv_ext.get(), sizeof(double) * ntot, cudaMemcpyDeviceToDevice,
+                           stream()));
+  halo_update<double>(comm, A.halo, L.pval.get());
+  AGG_CUDA(cudaMemcpyAsync(pv_ext.get(), L.pval.get(), sizeof(double) * ntot, cudaMemcpyDeviceToDevice,
+                           stream()));  // halo columns' weights for the Galerkin products
   build_halo_plan(comm, cpart, fid.get(), nloc, L.P_halo);
   L.agg_local.resize(nloc);
   localize_cols(L.P_halo, fid.get(), nloc, L.agg_local.get(), "prolongation: aggregate outside the plan");
@@ -741,53 +878,77 @@ Coarsened coarsen_level(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k
   if (nloc)
     AGG_CUDA(cudaMemcpyAsync(L.agg_global.get(), fid.get(), sizeof(idx) * nloc, cudaMemcpyDeviceToDevice,
                              stream()));
+  phase("transfer");
 
-  // ---- a9/a10 Galerkin in the cache order ----
-  halo_update<double>(comm, A.halo, L.pval.get());
-  const int64_t nnz = A.A.nnz;
-  DevBuf<GalRec> grec(nnz);
-  DevBuf<unsigned> gdest(nnz);
-  DevBuf<idx> gperm(nnz);
-  if (nloc)
-    AGG_LAUNCH(k_gal_recs, g, 256, 0, A.A.rowptr.get(), A.A.col.get(), A.A.val.get(), nloc, fid.get(),
-               L.pval.get(), cp_dev, grec.get(), gdest.get(), gperm.get());
-  DevBuf<double2> ents_buf = ship_stable<GalRec>(comm, grec.get(), gdest, gperm, nnz, nullptr);
-  const GalRec* ents = reinterpret_cast<const GalRec*>(ents_buf.get());
-  grec.reset();
-  gdest.reset();
-  gperm.reset();
-  const int64_t ne = ents_buf.size();
-  DevBuf<unsigned long long> ekey(ne), ekey_s(ne), ukey(ne);
-  DevBuf<idx> ep(ne), ep_s(ne), seg_len(ne), seg_off(ne + 1);
-  DevBuf<int> nseg_d(1);
-  nseg_d.zero();
-  if (ne) {
-    AGG_LAUNCH(k_gal_keys, grid_for(ne, 256), 256, 0, ents, ne, cbase, ekey.get(), ep.get());
-    cub_call([&](void* t, size_t& b) {  // stable: ties keep the global (row, entry) order
-      return cub::DeviceRadixSort::SortPairs(t, b, ekey.get(), ekey_s.get(), ep.get(), ep_s.get(),
-                                             static_cast<int>(ne), 0, 64, stream());
-    });
-    cub_call([&](void* t, size_t& b) {
-      return cub::DeviceRunLengthEncode::Encode(t, b, ekey_s.get(), ukey.get(), seg_len.get(),
-                                                nseg_d.get(), static_cast<int>(ne), stream());
-    });
+  // round 2: the exported rows' entries (coarse column, value, column weight)
+  DevBuf<idx> exlen(nexp), exoff(nexp + 1);
+  if (nexp)
+    AGG_LAUNCH(k_export_len, grid_for(nexp, 256), 256, 0, exrow_s.get(), nexp, A.A.rowptr.get(), exlen.get());
+  const int64_t nent = scan_to_offsets(exlen.get(), exoff.get(), nexp);
+  DevBuf<EntRec> erec(nent);
+  DevBuf<idx> ejc(nent);
+  if (nexp)
+    AGG_LAUNCH(k_export_entries, grid_for(nexp, 256), 256, 0, exrow_s.get(), nexp, exoff.get(),
+               A.A.rowptr.get(), A.A.col.get(), A.A.val.get(), fid.get(), L.pval.get(), erec.get(),
+               ejc.get());
+  std::vector<int64_t> ent_cnt(P, 0);
+  {
+    std::vector<int64_t> rowc(P, 0), pos(P + 1, 0);
+    for (int q = 0; q < P; ++q) pos[q + 1] = pos[q] + ecnt[q];
+    std::vector<idx> off_h(nexp + 1);
+    if (nexp) {
+      exoff.download(off_h.data(), nexp + 1);
+      sync();
+    }
+    for (int q = 0; q < P; ++q) ent_cnt[q] = nexp ? off_h[pos[q + 1]] - off_h[pos[q]] : 0;
   }
-  const int64_t nseg = read_scalar(nseg_d.get());
-  scan_to_offsets_async(seg_len.get(), seg_off.get(), nseg);
-  auto Acg = std::make_shared<DevCsr>();
-  Acg->n_rows = ncl;
+  DevBuf<idx> ilen = alltoallv<idx>(comm, exlen.get(), ecnt);
+  DevBuf<double2> ient_buf = alltoallv<double2>(comm, reinterpret_cast<const double2*>(erec.get()), ent_cnt);
+  DevBuf<idx> ijc = alltoallv<idx>(comm, ejc.get(), ent_cnt);
+  const EntRec* ient = reinterpret_cast<const EntRec*>(ient_buf.get());
+  const int64_t nie = ient_buf.size();
+  // extended CSR: local rows, empty halo rows, imported rows; imported columns get private
+  // slots [next, next + nie) carrying their coarse id and weight
+  auto Aext = std::make_shared<DevCsr>();
+  Aext->n_rows = next;
+  Aext->n_cols = next + nie;
+  Aext->nnz = A.A.nnz + nie;
+  Aext->rowptr.resize(next + 1);
+  Aext->col.resize(Aext->nnz);
+  Aext->val.resize(Aext->nnz);
+  {
+    DevBuf<idx> len(next);
+    if (next)
+      AGG_LAUNCH(k_ext_len, grid_for(next, 256), 256, 0, A.A.rowptr.get(), nloc, ntot, ilen.get(), m,
+                 len.get());
+    scan_to_offsets(len.get(), Aext->rowptr.get(), next);
+  }
+  if (A.A.nnz) {
+    AGG_CUDA(cudaMemcpyAsync(Aext->col.get(), A.A.col.get(), sizeof(idx) * A.A.nnz,
+                             cudaMemcpyDeviceToDevice, stream()));
+    AGG_CUDA(cudaMemcpyAsync(Aext->val.get(), A.A.val.get(), sizeof(double) * A.A.nnz,
+                             cudaMemcpyDeviceToDevice, stream()));
+  }
+  DevBuf<idx> asg_ext(next + nie);
+  DevBuf<double> pvc_ext(next + nie);
+  AGG_CUDA(cudaMemcpyAsync(asg_ext.get(), fid.get(), sizeof(idx) * ntot, cudaMemcpyDeviceToDevice, stream()));
+  AGG_CUDA(cudaMemcpyAsync(pvc_ext.get(), pv_ext.get(), sizeof(double) * next, cudaMemcpyDeviceToDevice,
+                           stream()));
+  if (nie)
+    AGG_LAUNCH(k_ext_entries, grid_for(nie, 256), 256, 0, ient, ijc.get(), nie, A.A.nnz, next,
+               Aext->col.get(), Aext->val.get(), asg_ext.get(), pvc_ext.get());
+  AggDev gx;
+  gx.n_fine = next;
+  gx.n_agg = ncl;
+  gx.assignment = std::move(asg_ext);
+  gx.agg_row_offsets = std::move(goff);
+  gx.rows_by_coarse = std::move(rows_ext);
+  GalerkinDev gal = build_galerkin_cache(*Aext, gx, true);
+  DevCsrPtr Acg = apply_galerkin_cache(gal, *Aext, pvc_ext.get());
   Acg->n_cols = cpart.n();
-  Acg->nnz = nseg;
-  Acg->rowptr.resize(ncl + 1);
-  Acg->col.resize(nseg);
-  Acg->val.resize(nseg);
-  DevBuf<idx> crow(ncl);
-  crow.zero();
-  if (nseg)
-    AGG_LAUNCH(k_seg_sum, grid_for(nseg, 256), 256, 0, seg_off.get(), nseg, ep_s.get(), ents,
-               ukey.get(), cbase, Acg->val.get(), Acg->col.get(), crow.get());
-  scan_to_offsets_async(crow.get(), Acg->rowptr.get(), ncl);
+  phase("galerkin");
   out.Ac = make_dist(comm, cpart, cpart, *Acg);
+  phase("coarse-plan");
   return out;
 }
 
@@ -805,6 +966,22 @@ void dist_smoother(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k) {
   };
   ops.before_spmv = [&](double* v) { halo_update<double>(comm, A.halo, v); };
   ops.dot = [&](const double* a, const double* b) { return dist_dot(comm, a, b, nloc); };
+  DevBuf<double> d2(2);
+  ops.dot2 = [&](const double* a, const double* b, const double* c, const double* e, double* out) {
+    DotArgs args{};
+    args.a[0] = a;
+    args.b[0] = b;
+    args.a[1] = c;
+    args.b[1] = e;
+    args.np = 2;
+    if (nloc > 0)
+      dot_device(args, nloc, d2.get(), nullptr, 1);
+    else
+      d2.zero();
+    comm.allreduce_sum(d2.get(), 2);
+    d2.download(out, 2);
+    sync();
+  };
   // a zero diagonal on any rank must fail every rank
   std::string err;
   try {
@@ -828,6 +1005,9 @@ std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, c
   const int me = comm.rank();
   comm.barrier();
   const auto t0 = std::chrono::steady_clock::now();
+  PhaseTimer timer;
+  timer.rank = me;
+  g_phase = timer.on ? &timer : nullptr;
   auto h = std::make_unique<DistHierarchy>();
   h->comm = &comm;
   h->cfg = cfg;
@@ -856,11 +1036,13 @@ std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, c
       break;
     }
     dist_smoother(comm, L, cfg, k);
+    phase("smoother");
     A = c.Ac;
     B = std::move(c.Bc);
     h->levels.push_back(std::move(L));
     ++k;
   }
+  phase("levels");
   // agglomerate level kd onto rank 0 and continue with the one-GPU setup there
   h->tail_rows = A->rows;
   DevCsrPtr Ag = gather_to_root(comm, *A, 0);
@@ -895,6 +1077,9 @@ std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, c
     h->level_nnz.push_back(ts_all[2 * l + 1]);
   }
   if (!h->levels.empty()) h->tail_halo_cap = h->levels.back().P_halo.nhalo;
+  phase("tail");
+  timer.report();
+  g_phase = nullptr;
   comm.barrier();
   h->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return h;

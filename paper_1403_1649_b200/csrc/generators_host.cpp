@@ -11,7 +11,7 @@
 namespace aggmg_b200 {
 
 HostCsr generate_poisson_host(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
-                              int weak_axis) {
+                              int weak_axis, int64_t row0, int64_t nrows) {
   require(dims == 2 || dims == 3, "poisson: dims must be 2 or 3");
   if (dims == 2) nz = 1;
   require(nx >= 1 && ny >= 1 && nz >= 1, "poisson: grid extents must be positive");
@@ -23,11 +23,14 @@ HostCsr generate_poisson_host(int dims, int64_t nx, int64_t ny, int64_t nz, doub
                cz = weak == 2 ? -eps : -1.0;
   const double diag = -2.0 * (cx + cy + (dims == 3 ? cz : 0.0));
   HostCsr A;
-  A.n = nx * ny * nz;
+  A.ncols = nx * ny * nz;
+  if (nrows < 0) nrows = A.ncols - row0;
+  require(row0 >= 0 && row0 + nrows <= A.ncols, "poisson: row range outside the grid");
+  A.n = nrows;
   A.rp.assign(A.n + 1, 0);
   A.col.reserve(static_cast<size_t>(A.n) * (dims == 3 ? 7 : 5));
   A.val.reserve(A.col.capacity());
-  for (int64_t r = 0; r < A.n; ++r) {
+  for (int64_t r = row0; r < row0 + A.n; ++r) {
     const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
     auto put = [&](int64_t c, double v) {
       A.col.push_back(c);
@@ -40,21 +43,25 @@ HostCsr generate_poisson_host(int dims, int64_t nx, int64_t ny, int64_t nz, doub
     if (i + 1 < nx) put(r + 1, cx);
     if (j + 1 < ny) put(r + nx, cy);
     if (k + 1 < nz) put(r + nx * ny, cz);
-    A.rp[r + 1] = static_cast<int64_t>(A.col.size());
+    A.rp[r - row0 + 1] = static_cast<int64_t>(A.col.size());
   }
   return A;
 }
 
-HostCsr generate_jump27_host(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block) {
+HostCsr generate_jump27_host(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,
+                             int64_t row0, int64_t nrows) {
   require(nx >= 1 && ny >= 1 && nz >= 1 && block >= 1, "jump27: extents must be positive");
   require(jump > 0.0, "jump27: jump must be positive");
   auto kappa = [&](int64_t x, int64_t y, int64_t z) {
     return (((x / block) + (y / block) + (z / block)) & 1) ? jump : 1.0;
   };
   HostCsr A;
-  A.n = nx * ny * nz;
+  A.ncols = nx * ny * nz;
+  if (nrows < 0) nrows = A.ncols - row0;
+  require(row0 >= 0 && row0 + nrows <= A.ncols, "jump27: row range outside the grid");
+  A.n = nrows;
   A.rp.assign(A.n + 1, 0);
-  for (int64_t r = 0; r < A.n; ++r) {
+  for (int64_t r = row0; r < row0 + A.n; ++r) {
     const int64_t i = r % nx, j = (r / nx) % ny, k = r / (nx * ny);
     const double ki = kappa(i, j, k);
     double diag = 0.0;
@@ -81,7 +88,7 @@ HostCsr generate_jump27_host(int64_t nx, int64_t ny, int64_t nz, double jump, in
           A.val.push_back(-kij);
         }
     A.val[pdiag] = diag;
-    A.rp[r + 1] = static_cast<int64_t>(A.col.size());
+    A.rp[r - row0 + 1] = static_cast<int64_t>(A.col.size());
   }
   return A;
 }

@@ -839,8 +839,8 @@ TransferDev build_transfer(const AggDev& agg, const double* fine_b) {
   return t;
 }
 
-GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg) {
-  require(A.n_rows == A.n_cols, "galerkin: matrix must be square");
+GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial) {
+  require(partial || A.n_rows == A.n_cols, "galerkin: matrix must be square");
   require(agg.n_fine == A.n_rows, "galerkin: aggregation size mismatch");
   const int64_t nc = agg.n_agg;
   GalerkinDev g;
@@ -857,7 +857,7 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg) {
     AGG_LAUNCH(k_group_entry_counts, grid_for(nc, 256), 256, 0, agg.agg_row_offsets.get(),
                agg.rows_by_coarse.get(), A.rowptr.get(), nc, ecnt.get());
   const int64_t total = scan_to_offsets(ecnt.get(), eoff.get(), nc);
-  require(total == A.nnz, "galerkin: aggregation does not cover the matrix rows");
+  require(partial || total == A.nnz, "galerkin: aggregation does not cover the matrix rows");
   if (nc > 0)
     AGG_LAUNCH(k_gal_symbolic, static_cast<unsigned>((nc + kGalWarps - 1) / kGalWarps),
                kGalWarps * 32, 0, agg.agg_row_offsets.get(), agg.rows_by_coarse.get(),
@@ -887,11 +887,11 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg) {
     AGG_LAUNCH(k_gal_fill, grid_for(nc * 32, 256), 256, 0, nc, eoff.get(), sorted_j.get(),
                g.entry.get(), g.coarse_rowptr.get(), g.coarse_col.get(), g.segment_offsets.get(),
                g.slot_of_csr.get());
-  const idx nnz32 = static_cast<idx>(A.nnz);
+  const idx nnz32 = static_cast<idx>(total);  // == A.nnz unless partial
   AGG_CUDA(cudaMemcpyAsync(g.segment_offsets.get() + g.nnz_coarse, &nnz32, sizeof(idx),
                            cudaMemcpyHostToDevice, stream()));
   sync();  // nnz32 lives on the host stack
-  g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
+  if (!partial) g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
   return g;
 }
 
@@ -913,6 +913,22 @@ DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const doub
   }
   Ac->plan();
   return Ac;
+}
+
+int64_t transfer_norms_groups(const idx* goff, const idx* rows, const double* b, int64_t nc,
+                              double* coarse_b, idx* rcnt) {
+  DevBuf<int> bad(1);
+  fill_int(bad.get(), 1, INT32_MAX);
+  if (nc > 0)
+    AGG_LAUNCH(k_transfer_norms, grid_for(nc, 256), 256, 0, goff, rows, b, nc, coarse_b, rcnt, bad.get());
+  const int v = read_scalar(bad.get());
+  return v == INT32_MAX ? -1 : v;
+}
+
+void transfer_R_groups(const idx* goff, const idx* rows, const double* pval, int64_t nc,
+                       const idx* rrp, idx* rcol, double* rval) {
+  if (nc > 0)
+    AGG_LAUNCH(k_transfer_R, grid_for(nc, 256), 256, 0, goff, rows, pval, nc, rrp, rcol, rval);
 }
 
 DevCsrPtr galerkin_direct(const DevCsr& A, const AggDev& agg, const double* pval) {

@@ -43,6 +43,12 @@ struct TransferDev {
   int64_t p_nnz = 0;
 };
 TransferDev build_transfer(const AggDev& agg, const double* fine_b);
+// The same kernels over explicit member groups (goff / rows index b and pval): returns the
+// first aggregate whose norm vanishes, or -1.
+int64_t transfer_norms_groups(const idx* goff, const idx* rows, const double* b, int64_t nc,
+                              double* coarse_b, idx* rcnt);
+void transfer_R_groups(const idx* goff, const idx* rows, const double* pval, int64_t nc,
+                       const idx* rrp, idx* rcol, double* rval);
 
 // a9/a10: Galerkin cache and numeric reduce (galerkin.cpp:38-137).
 struct GalerkinDev {
@@ -51,7 +57,9 @@ struct GalerkinDev {
   DevBuf<idx> entry, entry_row, segment_offsets, slot_of_csr;
   uint64_t pattern_hash = 0;
 };
-GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg);
+// partial: the groups cover only some rows of A (rows of other groups, and halo rows, are
+// skipped; the row-partitioned setup's extended row set) — no coverage check, no fingerprint.
+GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial = false);
 // Ac values for the cached pattern.  pval: per fine row P weight.
 DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const double* pval);
 uint64_t pattern_fingerprint(const DevCsr& A, const idx* assignment);

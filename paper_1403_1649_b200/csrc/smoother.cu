@@ -78,8 +78,7 @@ double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t see
     for (int i = 0; i <= j; ++i) {
       double hv[2];
       if (ops) {
-        hv[0] = ops->dot(V[i].get(), w.get());
-        hv[1] = ops->dot(V[i].get(), V[i].get());
+        ops->dot2(V[i].get(), w.get(), V[i].get(), V[i].get(), hv);
       } else {
         DotArgs d{};
         d.a[0] = V[i].get();

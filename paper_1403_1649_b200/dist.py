@@ -49,6 +49,9 @@ class Comm:
     def kind(self) -> str:
         return _lib().fn("comm_kind")(self._h).decode()
 
+    def barrier(self):
+        _check(_lib().fn("comm_barrier")(self._h))
+
     def close(self):
         if self._owned and self._h:
             _lib().fn("comm_free")(self._h)
@@ -96,6 +99,15 @@ def run_threads(nranks: int, fn: Callable[[Comm, int], None],
                 break
         raise first
     _check(rc)
+
+
+def host_rows(kind: str, row0: int, nrows: int, nx: int, ny: int, nz: int = 1,
+              epsilon: float = 1.0, dims: int = 3, jump: float = 1e6, block: int = 32) -> SparseMatrix:
+    """Host slab [row0, row0 + nrows) of a generator matrix (global column ids)."""
+    b = b200()
+    if kind == "jump27":
+        return b._csr_out("generate_jump27_rows", nx, ny, nz, jump, block, row0, nrows)
+    return b._csr_out("generate_poisson_rows", dims, nx, ny, nz, epsilon, -1, row0, nrows)
 
 
 class DistMatrix:
