@@ -105,17 +105,31 @@ __global__ void __launch_bounds__(kChunkThreads)
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < NP) {
-    const volatile double* vp = partials;
-    double s;
-    if (gridDim.x == 1) {
-      s = vp[threadIdx.x];  // single chunk: the reference returns the chunk sum itself
-    } else {
-      s = 0.0;
-      for (unsigned c = 0; c < gridDim.x; ++c) s = __dadd_rn(s, vp[c * NP + threadIdx.x]);
+  // Chunk partials in chunk order.  All threads stage tiles of partials into shared memory
+  // (coalesced, in flight together); lanes 0..NP-1 walk each tile sequentially, so the
+  // dependent chain pays the add latency, not a global-load latency per chunk.
+  double s = 0.0;
+  const unsigned nc = gridDim.x;
+  double* stage = &tile[0][0][0];  // reuse: 2 * NP * kChunkTile >= NP * kFinalTile
+  constexpr int kFinalTile = kChunkTile;
+  for (unsigned base = 0; base < nc; base += kFinalTile) {
+    const int cnt = static_cast<int>(min(static_cast<unsigned>(kFinalTile), nc - base));
+    __syncthreads();
+    for (int q = threadIdx.x; q < cnt * NP; q += kChunkThreads) {
+      const int c = q / NP, k = q - c * NP;
+      stage[k * kFinalTile + c] = __ldcg(partials + (base + c) * NP + k);
     }
-    out[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < NP) {
+      const double* src = stage + threadIdx.x * kFinalTile;
+      if (nc == 1) {
+        s = src[0];  // single chunk: the reference returns the chunk sum itself
+      } else {
+        for (int c = 0; c < cnt; ++c) s = __dadd_rn(s, src[c]);
+      }
+    }
   }
+  if (threadIdx.x < NP) out[threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
     *ticket = 0u;

@@ -1,6 +1,7 @@
 // sparse.cu — device CSR, upload/validation, CSR-stream SpMV family, transpose and
 // the device-side problem generators.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "sparse.cuh"
@@ -86,7 +87,12 @@ void DevCsr::plan() {
   AGG_LAUNCH(k_max_row, grid_for(n_rows, 256, 4 * sm_count()), 256, 0, rowptr.get(), n_rows, m.get());
   max_row = read_scalar(m.get());
   const double mean = std::max(1.0, static_cast<double>(nnz) / static_cast<double>(n_rows));
-  int rpb = static_cast<int>(std::min<double>(kStreamThreads, std::max(1.0, kStreamTarget / mean)));
+  // AGGMG_STREAM_TARGET overrides the staged-products target (tuning experiments)
+  static const double target = [] {
+    const char* e = std::getenv("AGGMG_STREAM_TARGET");
+    return e ? std::max(64.0, std::atof(e)) : static_cast<double>(kStreamTarget);
+  }();
+  int rpb = static_cast<int>(std::min<double>(kStreamThreads, std::max(1.0, target / mean)));
   while (true) {
     m.zero();
     AGG_LAUNCH(k_max_block_span, grid_for((n_rows + rpb - 1) / rpb, 256, 4 * sm_count()), 256, 0,

@@ -23,13 +23,18 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--kinds", default="0,1,2,3,4")
     ap.add_argument("--only", default="", help="e.g. L1.A:0 — run just this matrix:kind")
+    ap.add_argument("--problem", default="c2", choices=["c2", "c4"],
+                    help="c2: 7-point Poisson n^3; c4: 27-point jump 1e6 (32^3 blocks) n^3")
     args = ap.parse_args()
     lib = M.b200().lib
     assert lib.fn("init")(0) == 0, lib.fn("last_error")()
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json")))["hbm_gbs"]
     dm = C.c_void_p()
-    assert lib.fn("dmatrix_poisson")(3, args.n, args.n, args.n, 1.0, -1, C.byref(dm)) == 0
+    if args.problem == "c4":
+        assert lib.fn("dmatrix_jump27")(args.n, args.n, args.n, 1e6, 32, C.byref(dm)) == 0
+    else:
+        assert lib.fn("dmatrix_poisson")(3, args.n, args.n, args.n, 1.0, -1, C.byref(dm)) == 0
     cfg = M.SetupConfig(alpha=0.5, reuse_caches=True)._c()
     h = C.c_void_p()
     assert lib.fn("setup_hierarchy_device")(dm, C.byref(cfg), C.byref(h)) == 0
