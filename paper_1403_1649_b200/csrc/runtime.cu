@@ -1,6 +1,11 @@
 // runtime.cu — process-wide device context for the library.
+#include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "runtime.cuh"
@@ -16,10 +21,19 @@ struct Context {
   cudaStream_t stream = nullptr;
   double* pinned = nullptr;
   int pinned_n = 0;
+  // pinned staging ring for large host <-> device copies
+  static constexpr int kStages = 4;
+  static constexpr size_t kStageBytes = size_t{32} << 20;
+  char* stage[kStages] = {};
+  cudaEvent_t stage_ev[kStages] = {};
   ~Context() {  // rank threads exit: release their stream and staging
     if (!ready) return;
     if (stream) cudaStreamDestroy(stream);
     if (pinned) cudaFreeHost(pinned);
+    for (int b = 0; b < kStages; ++b) {
+      if (stage[b]) cudaFreeHost(stage[b]);
+      if (stage_ev[b]) cudaEventDestroy(stage_ev[b]);
+    }
   }
 };
 
@@ -107,6 +121,223 @@ void dev_free(void* p) {
 }
 
 void sync() { AGG_CUDA(cudaStreamSynchronize(stream())); }
+
+namespace {
+
+constexpr size_t kStagedMin = size_t{8} << 20;  // below this a pageable copy is as fast
+
+// Persistent host worker pool for the staging copies (spawning threads per 32 MB chunk
+// costs more than the copy).  run(n, f) calls f(0..n-1) on the workers and the caller.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+  template <class F>
+  void run(int n, F&& f) {
+    if (n <= 1 || workers_.empty()) {
+      for (int i = 0; i < n; ++i) f(i);
+      return;
+    }
+    std::lock_guard<std::mutex> serial(run_mutex_);  // one parallel region at a time
+    std::function<void(int)> job(std::ref(f));
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      job_ = &job;
+      n_ = n;
+      next_.store(0);
+      pending_ = n;
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(m_);
+    job_ = nullptr;  // late wakers see no job; workers still inside drain() are counted
+    done_cv_.wait(lk, [&] { return pending_ == 0 && active_ == 0; });
+  }
+  int size() const { return static_cast<int>(workers_.size()) + 1; }
+
+ private:
+  HostPool() {
+    const unsigned hc = std::max(2u, std::thread::hardware_concurrency());
+    const int nw = static_cast<int>(std::min(16u, hc)) - 1;
+    for (int t = 0; t < nw; ++t)
+      workers_.emplace_back([this] {
+        uint64_t seen = 0;
+        while (true) {
+          {
+            std::unique_lock<std::mutex> lk(m_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+          }
+          drain();
+        }
+      });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void drain() {
+    std::function<void(int)>* job;
+    int n;
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      job = job_;
+      n = n_;
+      if (!job) return;
+      ++active_;
+    }
+    int done = 0;
+    for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) {
+      (*job)(i);
+      ++done;
+    }
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      pending_ -= done;
+      --active_;
+      if (pending_ == 0 && active_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_, run_mutex_;
+  std::condition_variable cv_, done_cv_;
+  std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, pending_ = 0, active_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// memcpy over the pool in 1 MB pieces (large pageable sources are bandwidth-bound per core)
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPiece = size_t{1} << 20;
+  const int pieces = static_cast<int>((bytes + kPiece - 1) / kPiece);
+  HostPool::get().run(pieces, [&](int p) {
+    const size_t lo = kPiece * p, hi = std::min(bytes, lo + kPiece);
+    std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+  });
+}
+
+Context& staged() {
+  Context& c = ctx();
+  if (!c.stage[0])
+    for (int b = 0; b < Context::kStages; ++b) {
+      AGG_CUDA(cudaMallocHost(&c.stage[b], Context::kStageBytes));
+      AGG_CUDA(cudaEventCreateWithFlags(&c.stage_ev[b], cudaEventDisableTiming));
+      AGG_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));
+    }
+  return c;
+}
+
+}  // namespace
+
+void host_to_device(void* dst, const void* src, size_t bytes) {
+  ensure_init();
+  if (bytes < kStagedMin) {
+    AGG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream()));
+    return;
+  }
+  Context& c = staged();
+  size_t off = 0;
+  for (int k = 0; off < bytes; ++k) {
+    const int b = k % Context::kStages;
+    const size_t len = std::min(Context::kStageBytes, bytes - off);
+    AGG_CUDA(cudaEventSynchronize(c.stage_ev[b]));  // the DMA that last read this stage is done
+    par_memcpy(c.stage[b], static_cast<const char*>(src) + off, len);
+    AGG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, c.stage[b], len, cudaMemcpyHostToDevice,
+                             c.stream));
+    AGG_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));
+    off += len;
+  }
+}
+
+void host_to_device_narrow(int32_t* dst, const int64_t* src, size_t n, int64_t lo, int64_t hi,
+                           int64_t* first_bad) {
+  ensure_init();
+  std::atomic<int64_t> bad{INT64_MAX};
+  // narrow [a, b) of src into out over the pool; remember the first index outside [lo, hi)
+  auto narrow = [&](int32_t* out, size_t a, size_t b) {
+    constexpr size_t kPiece = size_t{1} << 18;
+    const int pieces = static_cast<int>((b - a + kPiece - 1) / kPiece);
+    HostPool::get().run(pieces, [&](int p) {
+      const size_t s0 = a + kPiece * p, s1 = std::min(b, s0 + kPiece);
+      bool any_bad = false;
+      for (size_t k = s0; k < s1; ++k) {
+        const int64_t v = src[k];
+        any_bad |= (v < lo) | (v >= hi);
+        out[k - a] = static_cast<int32_t>(v);
+      }
+      if (any_bad) {
+        int64_t fb = INT64_MAX;
+        for (size_t k = s0; k < s1 && fb == INT64_MAX; ++k)
+          if (src[k] < lo || src[k] >= hi) fb = static_cast<int64_t>(k);
+        int64_t cur = bad.load();
+        while (fb < cur && !bad.compare_exchange_weak(cur, fb)) {
+        }
+      }
+    });
+  };
+  if (n * sizeof(int32_t) < kStagedMin) {
+    std::vector<int32_t> tmp(n);
+    narrow(tmp.data(), 0, n);
+    if (n) {
+      AGG_CUDA(cudaMemcpyAsync(dst, tmp.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, stream()));
+      AGG_CUDA(cudaStreamSynchronize(stream()));  // tmp dies here
+    }
+  } else {
+    Context& c = staged();
+    const size_t per_chunk = Context::kStageBytes / sizeof(int32_t);
+    size_t off = 0;
+    for (int k = 0; off < n; ++k) {
+      const int b = k % Context::kStages;
+      const size_t len = std::min(per_chunk, n - off);
+      AGG_CUDA(cudaEventSynchronize(c.stage_ev[b]));
+      narrow(reinterpret_cast<int32_t*>(c.stage[b]), off, off + len);
+      AGG_CUDA(cudaMemcpyAsync(dst + off, c.stage[b], len * sizeof(int32_t), cudaMemcpyHostToDevice,
+                               c.stream));
+      AGG_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));
+      off += len;
+    }
+  }
+  *first_bad = bad.load() == INT64_MAX ? -1 : bad.load();
+}
+
+void device_to_host(void* dst, const void* src, size_t bytes) {
+  ensure_init();
+  if (bytes < kStagedMin) {
+    AGG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream()));
+    return;
+  }
+  Context& c = staged();
+  // issue the DMAs of the first stages, then drain in order while refilling
+  const size_t nchunks = (bytes + Context::kStageBytes - 1) / Context::kStageBytes;
+  auto issue = [&](size_t k) {
+    const int b = static_cast<int>(k % Context::kStages);
+    const size_t off = k * Context::kStageBytes, len = std::min(Context::kStageBytes, bytes - off);
+    AGG_CUDA(cudaEventSynchronize(c.stage_ev[b]));
+    AGG_CUDA(cudaMemcpyAsync(c.stage[b], static_cast<const char*>(src) + off, len,
+                             cudaMemcpyDeviceToHost, c.stream));
+    AGG_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));
+  };
+  size_t issued = 0;
+  for (; issued < nchunks && issued < static_cast<size_t>(Context::kStages); ++issued) issue(issued);
+  for (size_t k = 0; k < nchunks; ++k) {
+    const int b = static_cast<int>(k % Context::kStages);
+    const size_t off = k * Context::kStageBytes, len = std::min(Context::kStageBytes, bytes - off);
+    AGG_CUDA(cudaEventSynchronize(c.stage_ev[b]));
+    par_memcpy(static_cast<char*>(dst) + off, c.stage[b], len);
+    AGG_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));  // stage free again (host done with it)
+    if (issued < nchunks) issue(issued++);
+  }
+}
 
 double* pinned_scratch(int n) {
   ensure_init();

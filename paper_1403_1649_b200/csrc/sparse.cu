@@ -12,34 +12,23 @@ namespace aggmg_b200 {
 
 namespace {
 
-__global__ void k_convert_rowptr(const int64_t* in, idx* out, int64_t n_rows, int64_t nnz,
-                                 int* bad_row) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i > n_rows) return;
-  const int64_t v = in[i];
-  out[i] = static_cast<idx>(v);
-  if (i < n_rows) {
-    const int64_t nx = in[i + 1];
-    if (nx < v || v < 0 || nx > nnz) atomicMin(bad_row, static_cast<int>(i));
-  }
-}
-
-// One thread per row: columns in range and strictly increasing.
-__global__ void k_convert_cols(const int64_t* rp, const int64_t* in, idx* out, int64_t n_rows,
-                               int64_t n_cols, int* bad_row, int check) {
+// Ordering checks on narrowed arrays (ranges were checked while narrowing on the host):
+// row offsets non-decreasing and within [0, nnz]; columns strictly increasing per row.
+__global__ void k_check_rows(const idx* rp, const idx* col, int64_t n_rows, int64_t nnz, int* bad_row,
+                             int check_cols) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_rows) return;
-  const int64_t lo = rp[i], hi = rp[i + 1];
-  if (hi < lo || lo < 0) return;  // reported by k_convert_rowptr
-  int64_t prev = -1;
-  bool bad = false;
-  for (int64_t k = lo; k < hi; ++k) {
-    const int64_t c = in[k];
-    out[k] = static_cast<idx>(c);
-    if (check && (c < 0 || c >= n_cols || (k > lo && prev >= c))) bad = true;
-    prev = c;
+  const idx lo = rp[i], hi = rp[i + 1];
+  if (hi < lo || lo < 0 || hi > nnz) {
+    atomicMin(bad_row, static_cast<int>(i));
+    return;
   }
-  if (bad) atomicMin(bad_row, static_cast<int>(i));
+  if (!check_cols) return;
+  for (idx k = lo + 1; k < hi; ++k)
+    if (col[k - 1] >= col[k]) {
+      atomicMin(bad_row, static_cast<int>(i));
+      return;
+    }
 }
 
 __global__ void k_widen(const idx* in, int64_t* out, int64_t n) {
@@ -128,18 +117,24 @@ DevCsrPtr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, cons
   A->rowptr.resize(n_rows + 1);
   A->col.resize(nnz);
   A->val.resize(nnz);
-  DevBuf<int64_t> rp64(n_rows + 1), c64(nnz);
+  // indices are narrowed to int32 on the host while staging; range checks ride along,
+  // ordering checks run on the device over the narrowed arrays
   DevBuf<int> bad(1);
   fill_int(bad.get(), 1, INT32_MAX);
-  rp64.upload(rowptr, n_rows + 1);
-  c64.upload(col, nnz);
+  int64_t bad_rp = -1, bad_col = -1;
+  host_to_device_narrow(A->rowptr.get(), rowptr, static_cast<size_t>(n_rows + 1), 0, nnz + 1, &bad_rp);
+  host_to_device_narrow(A->col.get(), col, static_cast<size_t>(nnz), 0, validate ? n_cols : INT32_MAX,
+                        &bad_col);
   A->val.upload(val, nnz);
-  AGG_LAUNCH(k_convert_rowptr, grid_for(n_rows + 1, 256), 256, 0, rp64.get(), A->rowptr.get(),
-             n_rows, nnz, bad.get());
   if (n_rows > 0)
-    AGG_LAUNCH(k_convert_cols, grid_for(n_rows, 256), 256, 0, rp64.get(), c64.get(), A->col.get(),
-               n_rows, n_cols, bad.get(), validate ? 1 : 0);
-  const int bad_row = read_scalar(bad.get());
+    AGG_LAUNCH(k_check_rows, grid_for(n_rows, 256), 256, 0, A->rowptr.get(), A->col.get(), n_rows,
+               nnz, bad.get(), validate ? 1 : 0);
+  int bad_row = read_scalar(bad.get());
+  if (bad_rp >= 0) bad_row = std::min<int64_t>(bad_row, std::max<int64_t>(0, bad_rp - 1));
+  if (bad_col >= 0 && bad_row != 0) {  // the row holding the first out-of-range column
+    const int64_t r = std::upper_bound(rowptr, rowptr + n_rows + 1, bad_col) - rowptr - 1;
+    bad_row = static_cast<int>(std::min<int64_t>(bad_row, std::max<int64_t>(0, r)));
+  }
   if (bad_row != INT32_MAX) {
     // Reproduce the reference's first failing check for that row (sparse.cpp:29-38).
     const int64_t i = bad_row;
