@@ -334,7 +334,8 @@ def run_b200(args, world, rank, local):
         traffic = load_traffic().get(args.config, {}).get("jacobi_l0_dram_bytes_per_launch")
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k_csr_stream<Epi::kJacobi> on level 0 (fused damped-Jacobi sweep)",
+                "kernel": ("k_csr_stream<Epi::kJacobiDot2> on level 0: the fused damped-Jacobi "
+                           "post-smoothing sweep that also produces PCG's (r.z, r_old.z)"),
                 "bytes_per_launch": jb / jc, "avg_launch_ms": jt / jc, "launches": jc,
                 "peak_source": peak_src,
                 "share_of_step": jt / elapsed_ms if world == 1 else None}

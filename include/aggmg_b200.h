@@ -305,7 +305,8 @@ int aggmg_dist_matrix_info(const aggmg_dist_matrix* A, int64_t* n_global, int64_
 void aggmg_dist_matrix_free(aggmg_dist_matrix* A);
 
 /* setup_hierarchy (hierarchy.hpp:57) over the ranks; B0_local (host, this rank's rows) may be
- * NULL = ones; agglomerate_rows <= 0 picks the default (max(coarse_size_max, 2^16)) */
+ * NULL = ones; agglomerate_rows <= 0 picks the default (max(coarse_size_max, 2^20): coarse levels below ~1 M rows are
+ * latency-bound, one GPU runs them faster than exchanging halos for them) */
 int aggmg_dist_setup(aggmg_comm* c, const aggmg_dist_matrix* A0, const double* B0_local,
                      const aggmg_setup_config* cfg, int64_t agglomerate_rows,
                      aggmg_dist_hierarchy** out);
@@ -345,7 +346,8 @@ int aggmg_timer_stop(double* ms);
 /* SpMV micro-benchmark on a device matrix: average ms per launch over `reps` launches */
 int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* bytes);
 /* same for one CSR-stream variant: 0 spmv, 1 residual, 2 fused zero-guess Jacobi+residual,
- * 3 damped-Jacobi sweep, 4 spmv + dot, 5 spmv scaled by the inverse diagonal */
+ * 3 damped-Jacobi sweep, 4 spmv + dot, 5 spmv scaled by the inverse diagonal,
+ * 6 damped-Jacobi sweep + the two fused PCG dots */
 int aggmg_bench_kernel(const aggmg_dmatrix* A, int kind, int reps, double* avg_ms, double* bytes);
 
 #ifdef __cplusplus

@@ -932,13 +932,15 @@ int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* b
 int aggmg_bench_kernel(const aggmg_dmatrix* A, int kind, int reps, double* avg_ms, double* bytes) {
   return guarded([&] {
     const DevCsr& M = *A->A;
-    require(kind >= 0 && kind <= 5, "bench_kernel: kind must be 0..5");
-    const Epi epis[6] = {Epi::kSpmv, Epi::kResidual, Epi::kResidualZero, Epi::kJacobi,
-                         Epi::kSpmvDot1, Epi::kScaleDiag};
+    require(kind >= 0 && kind <= 6, "bench_kernel: kind must be 0..6");
+    const Epi epis[7] = {Epi::kSpmv, Epi::kResidual, Epi::kResidualZero, Epi::kJacobi,
+                         Epi::kSpmvDot1, Epi::kScaleDiag, Epi::kJacobiDot2};
     const Epi epi = epis[kind];
-    DevBuf<double> x(M.n_cols), y(M.n_rows), b(M.n_rows), d(M.n_rows), xo(M.n_rows), dots(4);
+    DevBuf<double> x(M.n_cols), y(M.n_rows), b(M.n_rows), d(M.n_rows), xo(M.n_rows), dots(4),
+        cv(M.n_rows);
     fill_double(x.get(), M.n_cols, 1.0);
     fill_double(b.get(), M.n_rows, 1.0);
+    fill_double(cv.get(), M.n_rows, 0.5);
     fill_double(d.get(), M.n_rows, 0.1);
     SpmvArgs a;
     a.x = x.get();
@@ -946,6 +948,7 @@ int aggmg_bench_kernel(const aggmg_dmatrix* A, int kind, int reps, double* avg_m
     a.b = b.get();
     a.d = d.get();
     a.u = x.get();
+    a.c = cv.get();
     a.x_out = xo.get();
     a.dots_out = dots.get();
     spmv_run(M, epi, a);
@@ -1082,7 +1085,7 @@ int aggmg_dist_setup(aggmg_comm* c, const aggmg_dist_matrix* A0, const double* B
     DevBuf<double> B;
     if (B0_local) B = up_vec(B0_local, A0->A->A.n_rows);
     const SetupCfg s = to_cfg(cfg);
-    if (agglomerate_rows <= 0) agglomerate_rows = std::max<int64_t>(s.coarse_size_max, int64_t{1} << 16);
+    if (agglomerate_rows <= 0) agglomerate_rows = std::max<int64_t>(s.coarse_size_max, int64_t{1} << 20);
     auto h = std::make_unique<aggmg_dist_hierarchy>();
     h->comm = &comm;
     h->A0 = A0->A;

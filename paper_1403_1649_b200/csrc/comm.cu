@@ -123,8 +123,10 @@ ThreadComm::ThreadComm(std::shared_ptr<ThreadGroupState> g, int rank, int size) 
   size_ = size;
 }
 
-void ThreadComm::exchange(const std::vector<CommMsg>& sends, const std::vector<CommMsg>& recvs) {
+void ThreadComm::exchange(const std::vector<CommMsg>& sends, const std::vector<CommMsg>& recvs,
+                          cudaStream_t st) {
   ThreadGroupState& g = *g_;
+  if (!st) st = stream();
   const int me = rank_;
   // self messages: matched in order, plain stream-ordered copies
   std::vector<const CommMsg*> self_send, self_recv;
@@ -136,14 +138,14 @@ void ThreadComm::exchange(const std::vector<CommMsg>& sends, const std::vector<C
   for (size_t k = 0; k < self_send.size(); ++k) {
     require(self_send[k]->bytes == self_recv[k]->bytes, "exchange: self message size mismatch");
     AGG_CUDA(cudaMemcpyAsync(self_recv[k]->ptr, self_send[k]->ptr, self_send[k]->bytes,
-                             cudaMemcpyDeviceToDevice, stream()));
+                             cudaMemcpyDeviceToDevice, st));
   }
   std::vector<std::tuple<int, int, int64_t>> my_posts;
   for (const auto& s : sends) {
     if (s.peer == me || !s.bytes) continue;
     cudaEvent_t ev;
     AGG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    AGG_CUDA(cudaEventRecord(ev, stream()));
+    AGG_CUDA(cudaEventRecord(ev, st));
     std::lock_guard<std::mutex> lk(g.m);
     const auto key = std::make_tuple(me, s.peer, g.send_seq[me * g.size + s.peer]++);
     ThreadGroupState::Post p;
@@ -169,11 +171,11 @@ void ThreadComm::exchange(const std::vector<CommMsg>& sends, const std::vector<C
     const void* src = p.ptr;
     cudaEvent_t ready = p.ready;
     lk.unlock();
-    AGG_CUDA(cudaStreamWaitEvent(stream(), ready, 0));
-    AGG_CUDA(cudaMemcpyAsync(r.ptr, src, r.bytes, cudaMemcpyDeviceToDevice, stream()));
+    AGG_CUDA(cudaStreamWaitEvent(st, ready, 0));
+    AGG_CUDA(cudaMemcpyAsync(r.ptr, src, r.bytes, cudaMemcpyDeviceToDevice, st));
     cudaEvent_t done;
     AGG_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    AGG_CUDA(cudaEventRecord(done, stream()));
+    AGG_CUDA(cudaEventRecord(done, st));
     lk.lock();
     ThreadGroupState::Post& q = g.posts[key];
     q.done = done;
@@ -186,7 +188,7 @@ void ThreadComm::exchange(const std::vector<CommMsg>& sends, const std::vector<C
     ThreadGroupState::Post p = g.posts[key];
     g.posts.erase(key);
     lk.unlock();
-    AGG_CUDA(cudaStreamWaitEvent(stream(), p.done, 0));
+    AGG_CUDA(cudaStreamWaitEvent(st, p.done, 0));
     cudaEventDestroy(p.done);
     cudaEventDestroy(p.ready);
   }
@@ -269,7 +271,9 @@ class NcclComm : public Comm {
   ~NcclComm() override {
     if (comm_ && nccl().comm_destroy) nccl().comm_destroy(comm_);
   }
-  void exchange(const std::vector<CommMsg>& sends, const std::vector<CommMsg>& recvs) override {
+  void exchange(const std::vector<CommMsg>& sends, const std::vector<CommMsg>& recvs,
+                cudaStream_t st = nullptr) override {
+    if (!st) st = stream();
     std::vector<const CommMsg*> self_send, self_recv;
     for (const auto& s : sends)
       if (s.peer == rank_ && s.bytes) self_send.push_back(&s);
@@ -278,14 +282,14 @@ class NcclComm : public Comm {
     require(self_send.size() == self_recv.size(), "exchange: unmatched self message");
     for (size_t k = 0; k < self_send.size(); ++k)
       AGG_CUDA(cudaMemcpyAsync(self_recv[k]->ptr, self_send[k]->ptr, self_send[k]->bytes,
-                               cudaMemcpyDeviceToDevice, stream()));
+                               cudaMemcpyDeviceToDevice, st));
     nccl_check(nccl().group_start(), "ncclGroupStart");
     for (const auto& s : sends)
       if (s.peer != rank_ && s.bytes)
-        nccl_check(nccl().send(s.ptr, s.bytes, kNcclInt8, s.peer, comm_, stream()), "ncclSend");
+        nccl_check(nccl().send(s.ptr, s.bytes, kNcclInt8, s.peer, comm_, st), "ncclSend");
     for (const auto& r : recvs)
       if (r.peer != rank_ && r.bytes)
-        nccl_check(nccl().recv(r.ptr, r.bytes, kNcclInt8, r.peer, comm_, stream()), "ncclRecv");
+        nccl_check(nccl().recv(r.ptr, r.bytes, kNcclInt8, r.peer, comm_, st), "ncclRecv");
     nccl_check(nccl().group_end(), "ncclGroupEnd");
   }
   void allgather(const void* in, void* out, size_t bytes) override {

@@ -40,7 +40,9 @@ class Comm {
   // Point-to-point: every send must be matched by the peer's recv of the same size in
   // the same call order.  Stream-ordered on the calling thread's library stream; the
   // send buffers may be overwritten by later stream work.
-  virtual void exchange(const std::vector<CommMsg>& sends, const std::vector<CommMsg>& recvs) = 0;
+  // st == nullptr: the calling thread's library stream.
+  virtual void exchange(const std::vector<CommMsg>& sends, const std::vector<CommMsg>& recvs,
+                        cudaStream_t st = nullptr) = 0;
   // out[r * bytes, (r+1) * bytes) = in of rank r (device buffers), stream-ordered.
   virtual void allgather(const void* in, void* out, size_t bytes) = 0;
   virtual const char* kind() const = 0;
@@ -64,7 +66,8 @@ struct ThreadGroupState;
 class ThreadComm : public Comm {
  public:
   ThreadComm(std::shared_ptr<ThreadGroupState> g, int rank, int size);
-  void exchange(const std::vector<CommMsg>& sends, const std::vector<CommMsg>& recvs) override;
+  void exchange(const std::vector<CommMsg>& sends, const std::vector<CommMsg>& recvs,
+                cudaStream_t st = nullptr) override;
   void allgather(const void* in, void* out, size_t bytes) override;
   const char* kind() const override { return "threads"; }
   static std::shared_ptr<ThreadGroupState> make_group(int size);

@@ -212,13 +212,25 @@ void presmooth(DevLevel& L, const double* b, const double* x_in, double* x_out, 
     AGG_LAUNCH(k_jacobi_zero, egrid(n), kB, 0, n, L.smoother.wdiag.get(), b, x_out, pred);
 }
 
-void postsmooth(DevLevel& L, const double* b, double* x, const int* pred, bool top) {
+void postsmooth(DevHierarchy& h, DevLevel& L, const double* b, double* x, const int* pred, bool top) {
   const int64_t n = L.A->n_rows;
   AGG_LAUNCH(k_prolong, egrid(n), kB, 0, n, x, L.agg.assignment.get(), L.tr.pval.get(),
              L.xc.get(), L.t.get(), pred);
   if (L.smoother.kind == 2) {
     AGG_LAUNCH(k_copy, egrid(n), kB, 0, n, L.t.get(), x, pred);
     smooth_sgs(L.smoother, *L.A, b, x);
+    return;
+  }
+  if (top && !pred && h.top_dot_out) {  // PCG's (r.z, r_old.z) ride on the last sweep
+    SpmvArgs a;
+    a.x = L.t.get();
+    a.y = x;
+    a.b = b;
+    a.d = L.smoother.wdiag.get();
+    a.c = h.top_dot_c;
+    a.dots_out = h.top_dot_out;
+    spmv_run(*L.A, Epi::kJacobiDot2, a, kProfSmoothL0);
+    h.top_dot_done = true;
     return;
   }
   smooth_sweep(L.smoother, *L.A, b, L.t.get(), x, pred, top ? kProfSmoothL0 : 0);
@@ -353,7 +365,7 @@ void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in,
   DevLevel& L = h.levels[k];
   descend(h, k, b, x_in, x_out, pred);
   coarse_correction(h, CycleCfg{}, false, k + 1, L.rc.get(), L.xc.get(), work_of(L), pred);
-  postsmooth(L, b, x_out, pred, finest(h, k));
+  postsmooth(h, L, b, x_out, pred, finest(h, k));
 }
 
 void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
@@ -365,7 +377,7 @@ void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b
   DevLevel& L = h.levels[k];
   descend(h, k, b, x_in, x_out, pred);
   coarse_correction(h, cfg, true, k + 1, L.rc.get(), L.xc.get(), work_of(L), pred);
-  postsmooth(L, b, x_out, pred, finest(h, k));
+  postsmooth(h, L, b, x_out, pred, finest(h, k));
 }
 
 }  // namespace

@@ -145,6 +145,28 @@ __global__ void k_count_owner(const unsigned* own, int64_t m, int64_t* cnt) {
   if (k < m) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[own[k]]), 1ull);
 }
 
+// rows holding a halo column (col >= nloc); lo = 1 + last such row below mid, hi = first at or
+// above mid
+__global__ void k_interior_bounds(const idx* rp, const idx* col, int64_t n, int64_t nloc,
+                                  int64_t mid, unsigned long long* lo_hi) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool halo = false;
+  for (idx k = rp[i]; k < rp[i + 1] && !halo; ++k) halo = col[k] >= nloc;
+  if (!halo) return;
+  if (i < mid)
+    atomicMax(&lo_hi[0], static_cast<unsigned long long>(i + 1));
+  else
+    atomicMin(&lo_hi[1], static_cast<unsigned long long>(i));
+}
+__global__ void k_sum_parts(const double* parts, int np, int nparts, double* out) {
+  const int k = threadIdx.x;
+  if (k >= np) return;
+  double s = parts[k];
+  for (int p = 1; p < nparts; ++p) s = __dadd_rn(s, parts[p * 3 + k]);
+  out[k] = s;
+}
+
 template <class F>
 void cub_call(F&& f) {  // two-phase CUB call with a pooled temporary
   size_t bytes = 0;
@@ -257,18 +279,27 @@ void globalize_cols(const HaloPlan& plan, const idx* lcols, int64_t m, idx* gcol
 }
 
 template <class T>
-void halo_update(Comm& comm, const HaloPlan& plan, T* x) {
+void halo_update_on(Comm& comm, const HaloPlan& plan, T* x, cudaStream_t st) {
   static_assert(sizeof(T) <= 16, "halo element too large");
   if (comm.size() == 1) return;
   T* buf = reinterpret_cast<T*>(plan.sendbuf.get());
-  if (plan.nsend > 0)
-    AGG_LAUNCH(k_pack<T>, grid_for(plan.nsend, 256), 256, 0, x, plan.send_idx.get(), plan.nsend, buf);
+  if (plan.nsend > 0) {
+    k_pack<T><<<grid_for(plan.nsend, 256), 256, 0, st>>>(x, plan.send_idx.get(), plan.nsend, buf);
+    note_launch();
+    check_launch(__FILE__, __LINE__);
+  }
   std::vector<CommMsg> sends, recvs;
   for (size_t k = 0; k < plan.send_peer.size(); ++k)
     sends.push_back({plan.send_peer[k], buf + plan.send_off[k], sizeof(T) * plan.send_cnt[k]});
   for (size_t k = 0; k < plan.recv_peer.size(); ++k)
     recvs.push_back({plan.recv_peer[k], x + plan.nloc + plan.recv_off[k], sizeof(T) * plan.recv_cnt[k]});
-  comm.exchange(sends, recvs);
+  comm.exchange(sends, recvs, st);
+}
+template void halo_update_on<double>(Comm&, const HaloPlan&, double*, cudaStream_t);
+
+template <class T>
+void halo_update(Comm& comm, const HaloPlan& plan, T* x) {
+  halo_update_on<T>(comm, plan, x, stream());
 }
 template void halo_update<double>(Comm&, const HaloPlan&, double*);
 template void halo_update<idx>(Comm&, const HaloPlan&, idx*);
@@ -375,7 +406,69 @@ DistCsrPtr make_dist(Comm& comm, const Partition& rows, const Partition& cols, D
   localize_cols(M->halo, gA.col.get(), gA.nnz, M->A.col.get(), err);
   gA.col.reset();
   M->A.plan();
+  // overlap window: rows without halo columns around the middle of the slab
+  const int64_t n = M->A.n_rows;
+  M->int_lo = M->int_hi = 0;
+  if (M->halo.nhalo > 0 && n > 0) {
+    DevBuf<unsigned long long> lh(2);
+    const unsigned long long init[2] = {0ull, static_cast<unsigned long long>(n)};
+    lh.upload(init, 2);
+    AGG_LAUNCH(k_interior_bounds, grid_for(n, 256), 256, 0, M->A.rowptr.get(), M->A.col.get(), n,
+               M->halo.nloc, n / 2, lh.get());
+    unsigned long long h[2];
+    lh.download(h, 2);
+    sync();
+    const int64_t rpb = std::max(1, M->A.rows_per_block);
+    const int64_t lo = (static_cast<int64_t>(h[0]) + rpb - 1) / rpb * rpb;
+    const int64_t hi = static_cast<int64_t>(h[1]) / rpb * rpb;
+    if (hi - lo >= std::max<int64_t>(rpb, n / 8)) {  // worth a split
+      M->int_lo = lo;
+      M->int_hi = hi;
+    }
+  }
   return M;
+}
+
+void dist_spmv(Comm& comm, const DistCsr& M, Epi epi, const SpmvArgs& a, int prof) {
+  if (comm.size() == 1 || M.int_hi <= M.int_lo) {
+    halo_update<double>(comm, M.halo, const_cast<double*>(a.x));
+    spmv_run(M.A, epi, a, prof);
+    return;
+  }
+  // exchange on the side stream, ordered after everything that produced a.x
+  cudaStream_t side = side_stream();
+  cudaEvent_t ready, landed;
+  AGG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  AGG_CUDA(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming));
+  AGG_CUDA(cudaEventRecord(ready, stream()));
+  AGG_CUDA(cudaStreamWaitEvent(side, ready, 0));
+  halo_update_on<double>(comm, M.halo, const_cast<double*>(a.x), side);
+  AGG_CUDA(cudaEventRecord(landed, side));
+  const bool dots = a.dots_out != nullptr;
+  DevBuf<double> parts(dots ? 9 : 0);
+  // one timing scope over all parts: the effective time of the operator incl. any halo wait
+  ProfileScope scope(prof, prof ? spmv_bytes(M.A, epi) : 0.0);
+  auto part = [&](int64_t base, int64_t count, int slot) {
+    if (count <= 0) {
+      if (dots) AGG_CUDA(cudaMemsetAsync(parts.get() + 3 * slot, 0, 3 * sizeof(double), stream()));
+      return;
+    }
+    SpmvArgs s = a;
+    s.row_base = base;
+    s.row_count = count;
+    if (dots) s.dots_out = parts.get() + 3 * slot;
+    spmv_run(M.A, epi, s);
+  };
+  part(M.int_lo, M.int_hi - M.int_lo, 0);  // interior: no halo column
+  AGG_CUDA(cudaStreamWaitEvent(stream(), landed, 0));
+  part(0, M.int_lo, 1);
+  part(M.int_hi, M.A.n_rows - M.int_hi, 2);
+  if (dots) {
+    const int np = epi == Epi::kSpmvDot1 ? 1 : epi == Epi::kSpmvDot3 ? 3 : 2;
+    AGG_LAUNCH(k_sum_parts, 1, 32, 0, parts.get(), np, 3, a.dots_out);
+  }
+  cudaEventDestroy(ready);
+  cudaEventDestroy(landed);
 }
 
 DevBuf<idx> global_cols(const DistCsr& M) {

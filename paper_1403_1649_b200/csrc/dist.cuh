@@ -53,6 +53,8 @@ void globalize_cols(const HaloPlan& plan, const idx* lcols, int64_t m, idx* gcol
 // x[nloc + h] <- owner's x for every halo slot (x has nloc + nhalo entries).
 template <class T>
 void halo_update(Comm& comm, const HaloPlan& plan, T* x);
+template <class T>
+void halo_update_on(Comm& comm, const HaloPlan& plan, T* x, cudaStream_t st);
 // owner's x[i] += x[nloc + h] for every halo slot h that refers to i (integer counts).
 void halo_reverse_add(Comm& comm, const HaloPlan& plan, idx* x);
 
@@ -68,11 +70,19 @@ DevBuf<T> alltoallv(Comm& comm, const T* sendbuf, const std::vector<int64_t>& cn
                     std::vector<int64_t>* recv_cnt = nullptr);
 
 // Row-partitioned CSR (square operators, R and P): local rows, local column ids.
+// [int_lo, int_hi) is a run of rows without halo columns, aligned to the CSR-stream row
+// blocks: those rows are computed while the halo exchange is in flight (empty: no overlap).
 struct DistCsr {
   Partition rows, cols;
   DevCsr A;  // n_rows = rows.count(me), n_cols = nloc_cols + nhalo
   HaloPlan halo;
+  int64_t int_lo = 0, int_hi = 0;
 };
+
+// y-side of a CSR-stream kernel on a row-partitioned operator: the halo of a.x is exchanged
+// on a side stream while the interior rows run, then the boundary rows; fused dots are
+// combined as interior + low + high partials (deterministic).
+void dist_spmv(Comm& comm, const DistCsr& M, Epi epi, const SpmvArgs& a, int prof = 0);
 using DistCsrPtr = std::shared_ptr<DistCsr>;
 
 // Wraps rows [row0, row0 + nloc) given with GLOBAL column ids (gA.col) into a DistCsr.

@@ -52,6 +52,10 @@ struct DistHierarchy {
   DevBuf<double> tail_b, tail_x;
   DevBuf<double> tail_work_c, tail_work_v, tail_work_rt, tail_work_d, tail_work_w;
   DevBuf<KScalars> tail_ks;
+  // PCG hook (see DevHierarchy::top_dot_*): fused (r.z, r_old.z) on the last level-0 sweep
+  const double* top_dot_c = nullptr;
+  double* top_dot_out = nullptr;
+  bool top_dot_done = false;
 
   int64_t kd() const { return static_cast<int64_t>(levels.size()); }
   void ensure_workspace();

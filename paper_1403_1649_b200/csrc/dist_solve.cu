@@ -86,7 +86,6 @@ void dist_coarse(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kparent,
   const bool inner_k = cycle_accelerated(cfg, k + 1);
   const int level = static_cast<int>(k + 1);
   dist_cycle(h, cfg, k + 1, inner_k, L.rc.get(), L.c.get(), pred);
-  halo_update<double>(comm, C.A->halo, L.c.get());
   SpmvArgs a1;  // v = Ac c ; rho1, alpha1
   a1.x = L.c.get();
   a1.y = L.v.get();
@@ -94,14 +93,13 @@ void dist_coarse(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kparent,
   a1.dot_with_x = cg ? 1 : 0;
   a1.dots_out = &L.ks.get()->rho1;
   a1.pred = pred;
-  spmv_run(C.A->A, Epi::kSpmvDot2, a1);
+  dist_spmv(comm, *C.A, Epi::kSpmvDot2, a1);
   comm.allreduce_sum(&L.ks.get()->rho1, 2);
   launch_kstep1(nc, L.rc.get(), L.v.get(), L.rt.get(), L.ks.get(), cfg.t, pred, level);
   comm.allreduce_sum(&L.ks.get()->nrt, 2);
   launch_kflag(L.ks.get(), cfg.t, pred);
   const int* p2 = &L.ks.get()->flag2;
   dist_cycle(h, cfg, k + 1, inner_k, L.rt.get(), L.d.get(), p2);
-  halo_update<double>(comm, C.A->halo, L.d.get());
   SpmvArgs a2;  // w = Ac d ; gamma, beta, alpha2
   a2.x = L.d.get();
   a2.y = L.w.get();
@@ -110,7 +108,7 @@ void dist_coarse(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kparent,
   a2.dot_with_x = cg ? 1 : 0;
   a2.dots_out = &L.ks.get()->gamma;
   a2.pred = p2;
-  spmv_run(C.A->A, Epi::kSpmvDot3, a2);
+  dist_spmv(comm, *C.A, Epi::kSpmvDot3, a2);
   comm.allreduce_sum(&L.ks.get()->gamma, 3);
   launch_kcombine(nc, L.c.get(), L.d.get(), L.xc.get(), L.ks.get(), pred, level);
 }
@@ -124,31 +122,36 @@ void dist_cycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, const
   const int prof = k == 0 ? kProfSmoothL0 : 0;
   // pre-smooth from zero, residual, restriction (cycles.cpp:54-57)
   launch_jacobi_zero(n, L.smoother.wdiag.get(), b, x, pred);
-  halo_update<double>(comm, L.A->halo, x);
   SpmvArgs ra;
   ra.x = x;
   ra.y = L.r.get();
   ra.b = b;
   ra.pred = pred;
-  spmv_run(L.A->A, Epi::kResidual, ra, k == 0 ? kProfSpmvL0 : 0);
-  halo_update<double>(comm, L.R->halo, L.r.get());
+  dist_spmv(comm, *L.A, Epi::kResidual, ra, k == 0 ? kProfSpmvL0 : 0);
   SpmvArgs rr;
   rr.x = L.r.get();
   rr.y = L.rc.get();
   rr.pred = pred;
-  spmv_run(L.R->A, Epi::kSpmv, rr);
+  dist_spmv(comm, *L.R, Epi::kSpmv, rr);
   dist_coarse(h, cfg, k, kc, pred);
   // prolongation + post-smooth (cycles.cpp:37-44, 59-60)
   halo_update<double>(comm, L.P_halo, L.xc.get());
   launch_prolong(n, x, L.agg_local.get(), L.pval.get(), L.xc.get(), L.t.get(), pred);
-  halo_update<double>(comm, L.A->halo, L.t.get());
   SpmvArgs ja;
   ja.x = L.t.get();
   ja.y = x;
   ja.b = b;
   ja.d = L.smoother.wdiag.get();
   ja.pred = pred;
-  spmv_run(L.A->A, Epi::kJacobi, ja, prof);
+  if (k == 0 && !pred && h.top_dot_out) {  // PCG's (r.z, r_old.z) ride on the last sweep
+    ja.c = h.top_dot_c;
+    ja.dots_out = h.top_dot_out;
+    dist_spmv(comm, *L.A, Epi::kJacobiDot2, ja, prof);
+    comm.allreduce_sum(h.top_dot_out, 2);
+    h.top_dot_done = true;
+    return;
+  }
+  dist_spmv(comm, *L.A, Epi::kJacobi, ja, prof);
 }
 
 }  // namespace
@@ -171,9 +174,18 @@ SolveOut dist_solve(DistHierarchy& h, const DistCsr& A, const CycleCfg& cyc, con
   Comm& comm = *h.comm;
   KrylovDist d;
   d.n_alloc = A.A.n_rows + std::max<int64_t>(A.halo.nhalo, h.kd() ? h.levels[0].halo_cap : 0);
-  d.halo = [&](double* v) { halo_update<double>(comm, A.halo, v); };
+  d.spmv = [&](Epi epi, const SpmvArgs& a, int prof) { dist_spmv(comm, A, epi, a, prof); };
   d.allreduce = [&](double* v, int k) { comm.allreduce_sum(v, k); };
   d.precond = [&](const double* r, double* z) { dist_apply_preconditioner(h, cyc, r, z); };
+  d.precond_dots = [&](const double* r, const double* rold, double* z, double* q) {
+    h.top_dot_c = rold;
+    h.top_dot_out = q;
+    h.top_dot_done = false;
+    dist_apply_preconditioner(h, cyc, r, z);
+    h.top_dot_c = nullptr;
+    h.top_dot_out = nullptr;
+    return h.top_dot_done;
+  };
   d.flush_warnings = [&] {
     if (comm.rank() == 0) flush_cycle_warnings();
   };

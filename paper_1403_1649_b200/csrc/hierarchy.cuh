@@ -69,6 +69,12 @@ struct DevHierarchy {
   DevBuf<double> coarse_inv;  // explicit inverse of the coarsest operator (row-major)
   double setup_ms = 0.0;
   bool workspace_ready = false;
+  // PCG hook: the finest level's last damped-Jacobi sweep of a preconditioner application
+  // also produces (r . z, top_dot_c . z) into top_dot_out (set by pcg, cleared after use);
+  // top_dot_done reports whether the fused path ran.
+  const double* top_dot_c = nullptr;
+  double* top_dot_out = nullptr;
+  bool top_dot_done = false;
 
   int64_t n_levels() const { return static_cast<int64_t>(levels.size()); }
   int64_t coarsest() const { return n_levels() - 1; }

@@ -163,12 +163,14 @@ void apply_M(const Precond& M, const double* r, double* z, int64_t n, const Kryl
 }
 
 void residual(const DevCsr& A, const double* b, const double* x, double* r, const KrylovDist* dist) {
-  if (dist) dist->halo(const_cast<double*>(x));
   SpmvArgs a;
   a.x = x;
   a.y = r;
   a.b = b;
-  spmv_run(A, Epi::kResidual, a);
+  if (dist)
+    dist->spmv(Epi::kResidual, a, 0);  // halo exchange overlapped with the interior rows
+  else
+    spmv_run(A, Epi::kResidual, a);
 }
 
 double norm_host(const double* v, int64_t n, const KrylovDist* dist = nullptr) {
@@ -222,16 +224,38 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
   residual(A, b, x, r, dist);
   double res = norm_host(r, n, dist);
   out.history.push_back(res);
-  apply_M(M, r, z.get(), n, dist);
+  // (r.z, r_old.z) fused into the preconditioner's last level-0 sweep when possible
+  const bool fuse = !exact && (dist ? static_cast<bool>(dist->precond_dots) : M.h != nullptr);
+  auto precond_dots = [&](const double* rr, const double* rold, double* q, int np) {
+    bool fused = false;
+    if (fuse && dist) {
+      fused = dist->precond_dots(rr, rold, z.get(), q);
+    } else {
+      if (fuse) {
+        M.h->top_dot_c = rold;
+        M.h->top_dot_out = q;
+        M.h->top_dot_done = false;
+      }
+      apply_M(M, rr, z.get(), n, dist);
+      fused = fuse && M.h->top_dot_done;
+      if (fuse) {
+        M.h->top_dot_c = nullptr;
+        M.h->top_dot_out = nullptr;
+      }
+    }
+    if (!fused) {
+      DotArgs d{};
+      d.a[0] = rr;
+      d.b[0] = z.get();
+      d.a[1] = rold;
+      d.b[1] = z.get();
+      d.np = np;
+      dot_device(d, n, q);
+      reduce(dist, q, np);
+    }
+  };
+  precond_dots(r, r, &slots.get()->q[0][0], 1);
   copy_double(p.get(), z.get(), n);
-  {
-    DotArgs d{};
-    d.a[0] = r;
-    d.b[0] = z.get();
-    d.np = 1;
-    dot_device(d, n, &slots.get()->q[0][0]);
-    reduce(dist, &slots.get()->q[0][0], 1);
-  }
   double* pinned = pinned_scratch(8);
   int par = 0;  // q[par][0] holds the current r.z
   while (res > target && out.iterations < cfg.max_iters) {
@@ -240,7 +264,6 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     a.y = Ap.get();
     a.u = p.get();
     a.dots_out = &slots.get()->pAp;
-    if (dist) dist->halo(p.get());
     if (exact) {
       spmv_run(A, Epi::kSpmv, a, kProfSpmvL0);
       DotOp<1> d1;
@@ -258,7 +281,10 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
       u.rn = rn;
       launch_chunked<1>(u, n, &slots.get()->res2);
     } else {
-      spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
+      if (dist)
+        dist->spmv(Epi::kSpmvDot1, a, kProfSpmvL0);
+      else
+        spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
       reduce(dist, &slots.get()->pAp, 1);
       AGG_LAUNCH(k_pcg_update, reduce_grid(n), kB, 0, n, slots.get(), par, p.get(), Ap.get(), r, x,
                  rn, reduce_partials(), reduce_ticket());
@@ -274,16 +300,8 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     out.history.push_back(res);
     std::swap(r, rn);  // r = new residual, rn = r_old
     if (res <= target) break;
-    apply_M(M, r, z.get(), n, dist);
-    DotArgs d{};
-    d.a[0] = r;
-    d.b[0] = z.get();
-    d.a[1] = rn;
-    d.b[1] = z.get();
-    d.np = 2;
     const int cur = par ^ 1;
-    dot_device(d, n, &slots.get()->q[cur][0]);  // {r.z, r_old.z}
-    reduce(dist, &slots.get()->q[cur][0], 2);
+    precond_dots(r, rn, &slots.get()->q[cur][0], 2);  // {r.z, r_old.z}
     AGG_LAUNCH(k_pcg_p, egrid(n), kB, 0, n, slots.get(), cur, z.get(), p.get());
     par = cur;
   }
@@ -338,7 +356,6 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
     for (; j < m && out.iterations < cfg.max_iters; ++j) {
       if (static_cast<int>(Z.size()) <= j) Z.emplace_back(nz_alloc);
       apply_M(M, V[j].get(), Z[j].get(), n, dist);
-      if (dist) dist->halo(Z[j].get());
       SpmvArgs a;  // w = A Z_j ; h(0,j) = V_0 . w
       a.x = Z[j].get();
       a.y = w.get();
@@ -352,7 +369,10 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
         d1.pred = nullptr;
         launch_chunked<1>(d1, n, hcol.get());
       } else {
-        spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
+        if (dist)
+          dist->spmv(Epi::kSpmvDot1, a, kProfSpmvL0);
+        else
+          spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
         reduce(dist, hcol.get(), 1);
       }
       for (int i = 0; i <= j; ++i) {

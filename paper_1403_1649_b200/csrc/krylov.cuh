@@ -37,9 +37,11 @@ struct Precond {
 // preconditioner is the partitioned cycle.  nullptr = the one-GPU path.
 struct KrylovDist {
   int64_t n_alloc = 0;
-  std::function<void(double*)> halo;                 // fill the halo of an SpMV input
+  std::function<void(Epi, const SpmvArgs&, int)> spmv;  // halo exchange + SpMV on the rows
   std::function<void(double*, int)> allreduce;       // device scalars, in place
   std::function<void(const double*, double*)> precond;
+  // precond + (rr . z, rold . z) summed over ranks into q; false = dots not produced
+  std::function<bool(const double*, const double*, double*, double*)> precond_dots;
   std::function<void()> flush_warnings;
 };
 

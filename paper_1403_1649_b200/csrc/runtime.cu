@@ -19,6 +19,7 @@ struct Context {
   int device = 0;
   int sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // halo exchanges that overlap interior rows (dist path)
   double* pinned = nullptr;
   int pinned_n = 0;
   // pinned staging ring for large host <-> device copies
@@ -29,6 +30,7 @@ struct Context {
   ~Context() {  // rank threads exit: release their stream and staging
     if (!ready) return;
     if (stream) cudaStreamDestroy(stream);
+    if (side) cudaStreamDestroy(side);
     if (pinned) cudaFreeHost(pinned);
     for (int b = 0; b < kStages; ++b) {
       if (stage[b]) cudaFreeHost(stage[b]);
@@ -104,6 +106,12 @@ cudaStream_t stream() {
 int sm_count() {
   ensure_init();
   return ctx().sms;
+}
+cudaStream_t side_stream() {
+  ensure_init();
+  Context& c = ctx();
+  if (!c.side) AGG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+  return c.side;
 }
 int current_device() {
   ensure_init();

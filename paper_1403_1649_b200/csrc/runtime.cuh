@@ -24,6 +24,7 @@ void host_to_device_narrow(int32_t* dst, const int64_t* src, size_t n, int64_t l
                            int64_t* first_bad);
 void init_device(int device);  // creates the calling thread's context on `device`
 int current_device();
+cudaStream_t side_stream();  // a second stream of the calling thread (overlapped exchanges)
 void* dev_alloc(size_t bytes);
 void dev_free(void* p);
 

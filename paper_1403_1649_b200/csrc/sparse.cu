@@ -167,7 +167,9 @@ namespace {
 
 template <Epi E>
 struct EpiTraits {
-  static constexpr int np = (E == Epi::kSpmvDot1) ? 1 : (E == Epi::kSpmvDot2) ? 2 : (E == Epi::kSpmvDot3) ? 3 : 0;
+  static constexpr int np = (E == Epi::kSpmvDot1) ? 1
+                            : (E == Epi::kSpmvDot2 || E == Epi::kJacobiDot2) ? 2
+                            : (E == Epi::kSpmvDot3) ? 3 : 0;
 };
 
 // Persistent CSR-stream kernel: each CTA walks row blocks rb = blockIdx.x, +gridDim.x, ...
@@ -239,32 +241,40 @@ __global__ void __launch_bounds__(kStreamThreads)
     const int64_t r = r0 + threadIdx.x;
     if (threadIdx.x < rpb && r < r1) {
       const idx s = rowptr[r] - ea, t = rowptr[r + 1] - ea;
+      const int64_t rg = r + a.row_base;  // row index of the epilogue vectors
       double sum = 0.0;
       for (idx k = s; k < t; ++k) sum = __dadd_rn(sum, prod[k]);
-      if constexpr (E == Epi::kSpmv || NP > 0) {
-        a.y[r] = sum;
+      double yv = sum;
+      if constexpr (E == Epi::kJacobiDot2) {
+        yv = __dadd_rn(x[rg], __dmul_rn(a.d[rg], __dsub_rn(a.b[rg], sum)));
+        a.y[rg] = yv;
+      } else if constexpr (E == Epi::kSpmv || NP > 0) {
+        a.y[rg] = sum;
       } else if constexpr (E == Epi::kResidual) {
-        a.y[r] = __dsub_rn(a.b[r], sum);
+        a.y[rg] = __dsub_rn(a.b[rg], sum);
       } else if constexpr (E == Epi::kResidualZero) {
-        const double br = a.b[r];
-        a.y[r] = __dsub_rn(br, sum);                                // r = b - A x1
-        a.x_out[r] = __dadd_rn(0.0, __dmul_rn(a.d[r], br));         // x1 = 0 + wd b
+        const double br = a.b[rg];
+        a.y[rg] = __dsub_rn(br, sum);                                // r = b - A x1
+        a.x_out[rg] = __dadd_rn(0.0, __dmul_rn(a.d[rg], br));         // x1 = 0 + wd b
       } else if constexpr (E == Epi::kJacobi) {
-        a.y[r] = __dadd_rn(x[r], __dmul_rn(a.d[r], __dsub_rn(a.b[r], sum)));
+        a.y[rg] = __dadd_rn(x[rg], __dmul_rn(a.d[rg], __dsub_rn(a.b[rg], sum)));
       } else if constexpr (E == Epi::kScaleDiag) {
-        a.y[r] = __dmul_rn(sum, a.d[r]);
+        a.y[rg] = __dmul_rn(sum, a.d[rg]);
       }
-      if constexpr (NP > 0) {
-        const double lhs = a.dot_with_x ? x[r] : sum;
+      if constexpr (E == Epi::kJacobiDot2) {
+        v[0] = __dadd_rn(v[0], __dmul_rn(a.b[rg], yv));  // r . z
+        v[1] = __dadd_rn(v[1], __dmul_rn(a.c[rg], yv));  // r_old . z
+      } else if constexpr (NP > 0) {
+        const double lhs = a.dot_with_x ? x[rg] : sum;
         if constexpr (NP == 1) {
-          v[0] = __dadd_rn(v[0], __dmul_rn(a.u[r], sum));
+          v[0] = __dadd_rn(v[0], __dmul_rn(a.u[rg], sum));
         } else if constexpr (NP == 2) {
           v[0] = __dadd_rn(v[0], __dmul_rn(lhs, sum));     // rho  = v.v (gmres) | c.v (cg)
-          v[1] = __dadd_rn(v[1], __dmul_rn(lhs, a.c[r]));  // alpha = v.rc       | c.rc
+          v[1] = __dadd_rn(v[1], __dmul_rn(lhs, a.c[rg]));  // alpha = v.rc       | c.rc
         } else {
-          v[0] = __dadd_rn(v[0], __dmul_rn(lhs, a.u[r]));  // gamma = w.v | d.v
+          v[0] = __dadd_rn(v[0], __dmul_rn(lhs, a.u[rg]));  // gamma = w.v | d.v
           v[1] = __dadd_rn(v[1], __dmul_rn(lhs, sum));     // beta  = w.w | d.w
-          v[2] = __dadd_rn(v[2], __dmul_rn(lhs, a.c[r]));  // alpha2 = w.rt | d.rt
+          v[2] = __dadd_rn(v[2], __dmul_rn(lhs, a.c[rg]));  // alpha2 = w.rt | d.rt
         }
       }
     }
@@ -281,7 +291,9 @@ __global__ void __launch_bounds__(kStreamThreads)
 
 template <Epi E>
 void launch_stream(const DevCsr& A, const SpmvArgs& a) {
-  const int64_t nblocks = (A.n_rows + A.rows_per_block - 1) / A.rows_per_block;
+  const int64_t nrows = a.row_count >= 0 ? a.row_count : A.n_rows - a.row_base;
+  if (nrows <= 0) return;
+  const int64_t nblocks = (nrows + A.rows_per_block - 1) / A.rows_per_block;
   const size_t smem = sizeof(double) * A.smem_entries;
   static thread_local bool raised = false;
   if (smem > 48 * 1024 && !raised) {
@@ -300,9 +312,9 @@ void launch_stream(const DevCsr& A, const SpmvArgs& a) {
     cached_smem = smem;
   }
   const int64_t grid = std::min<int64_t>(nblocks, static_cast<int64_t>(cached_per_sm) * sm_count());
-  AGG_LAUNCH(k_csr_stream<E>, static_cast<unsigned>(grid), kStreamThreads, smem, A.rowptr.get(),
-             A.col.get(), A.val.get(), A.n_rows, A.rows_per_block, nblocks, a, reduce_partials(),
-             reduce_ticket());
+  AGG_LAUNCH(k_csr_stream<E>, static_cast<unsigned>(grid), kStreamThreads, smem,
+             A.rowptr.get() + a.row_base, A.col.get(), A.val.get(), nrows, A.rows_per_block, nblocks,
+             a, reduce_partials(), reduce_ticket());
 }
 
 }  // namespace
@@ -318,6 +330,7 @@ double spmv_bytes(const DevCsr& A, Epi epi) {
     case Epi::kSpmvDot1: b += 8.0 * n; break;
     case Epi::kSpmvDot2: b += 8.0 * n; break;
     case Epi::kSpmvDot3: b += 16.0 * n; break;
+    case Epi::kJacobiDot2: b += 24.0 * n; break;
     default: break;
   }
   return b;
@@ -335,6 +348,7 @@ void spmv_run(const DevCsr& A, Epi epi, const SpmvArgs& a, int prof_family) {
     case Epi::kSpmvDot1: launch_stream<Epi::kSpmvDot1>(A, a); break;
     case Epi::kSpmvDot2: launch_stream<Epi::kSpmvDot2>(A, a); break;
     case Epi::kSpmvDot3: launch_stream<Epi::kSpmvDot3>(A, a); break;
+    case Epi::kJacobiDot2: launch_stream<Epi::kJacobiDot2>(A, a); break;
   }
 }
 

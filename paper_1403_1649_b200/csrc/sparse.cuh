@@ -46,6 +46,7 @@ enum class Epi {
   kSpmvDot2,   // y = A x ; dots (y.y, y.c) [gmres inner] or (x.y, x.c) [cg inner]
   kSpmvDot3,   // y = A x ; dots (y.u, y.y, y.c) [gmres] or (x.u, x.y, x.c) [cg]
   kSpmvDot1,   // y = A x ; dot (u . y)
+  kJacobiDot2, // y = x + wd .* (b - A x) ; dots (b . y, c . y)  (PCG's r.z, r_old.z fused)
 };
 
 struct SpmvArgs {
@@ -59,6 +60,10 @@ struct SpmvArgs {
   int dot_with_x = 0;          // cg-style inner products use x instead of y
   double* dots_out = nullptr;  // device slots for the dot results
   const int* pred = nullptr;   // device predicate: skip the launch body when *pred == 0
+  // rows [row_base, row_base + row_count) only (row_count < 0: to the end); row_base must be a
+  // multiple of A.rows_per_block so the row blocks coincide with the plan's
+  int64_t row_base = 0;
+  int64_t row_count = -1;
 };
 
 void spmv_run(const DevCsr& A, Epi epi, const SpmvArgs& a, int prof_family = 0);

@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1403_1649_b200 import aggmg as M  # noqa: E402
 
 KINDS = {0: "spmv", 1: "residual", 2: "jacobi_zero+residual", 3: "jacobi", 4: "spmv+dot",
-         5: "spmv*invdiag"}
+         5: "spmv*invdiag", 6: "jacobi+dot2"}
 
 
 def main():
