@@ -310,6 +310,7 @@ __global__ void k_group_entry_counts(const idx* goff, const idx* rows, const idx
 constexpr int kGalWarps = 8;
 constexpr int kGalCap = 256;     // tier 1: fine entries per coarse row, one warp, shared memory
 constexpr int kGalCapBig = 4096; // tier 2: one CTA per coarse row, shared memory (80 KB)
+constexpr int kGalHash = 512;    // tier 2: distinct coarse columns per row (hash table slots)
 
 // Member-parallel gather of coarse row I's fine entries into (key, k, row) slots:
 // lanes own member rows, a warp scan of the row lengths gives each member its slot
@@ -388,79 +389,246 @@ __global__ void __launch_bounds__(kGalWarps * 32)
   if (lane == 0) cnnz[I] = cnt;
 }
 
-// Tier 2 — one CTA (256 threads) per long coarse row.  Slots live in shared memory when
-// L <= kGalCapBig, else in the global scratch arrays at [base_e, base_e + L).
+// Tier 2 — one CTA (256 threads) per long coarse row (L > kGalCap gathered entries).
+// Per-entry slots (J, k, row, hash slot, scratch) live in shared memory when L <= cap (the
+// launch's largest L, at most kGalCapBig), else in global scratch at [base_e, base_e + L).
+//  1. gather: entry-parallel over a member table (offsets by warp scan), so all 256 threads
+//     load acol / assignment;
+//  2. distinct coarse columns J in a shared hash table with per-J counts; ranks of the
+//     distinct J; offsets by a warp scan;
+//  3. one warp scatters the entries in gather order (match_any groups equal J, the group
+//     leader advances the J's cursor) — the stable sort by (J, position) of
+//     galerkin.cpp:52-62, in O(L).
+// Fallback (hash overflow or more than kGalMembers members): the O(L^2) rank sort.
+constexpr int kGalMembers = 512;
 __global__ void __launch_bounds__(256)
     k_gal_symbolic_big(const idx* big_list, const idx* goff, const idx* rows, const idx* arp,
-                       const idx* acol, const idx* assignment, const idx* eoff,
-                       unsigned long long* gkey, idx* gkk, idx* gri, idx* entry, idx* entry_row,
-                       idx* sorted_j, idx* cnnz) {
-  extern __shared__ unsigned long long big_smem[];
-  __shared__ idx s_wtot[8];
-  __shared__ idx s_cnt, s_base;
+                       const idx* acol, const idx* assignment, const idx* eoff, int cap,
+                       idx* gscratch, idx* entry, idx* entry_row, idx* sorted_j, idx* cnnz) {
+  extern __shared__ idx big_smem[];
+  __shared__ idx m_off[kGalMembers + 1], m_lo[kGalMembers], m_row[kGalMembers];
+  __shared__ idx h_j[kGalHash], h_cnt[kGalHash], h_cur[kGalHash], d_slot[kGalHash];
+  __shared__ idx s_wsum[32];
+  __shared__ int s_nd, s_over;
   const idx I = big_list[blockIdx.x];
   const idx base_e = eoff[I];
   const idx L = eoff[I + 1] - base_e;
-  const bool in_smem = L <= kGalCapBig;
-  unsigned long long* skey = in_smem ? big_smem : gkey + base_e;
-  idx* skk = in_smem ? reinterpret_cast<idx*>(big_smem + kGalCapBig) : gkk + base_e;
-  idx* sri = in_smem ? skk + kGalCapBig : gri + base_e;
+  const bool in_smem = L <= cap;
+  idx* base = in_smem ? big_smem : gscratch + 5 * static_cast<int64_t>(base_e);
+  const idx stride = in_smem ? cap : L;
+  idx* sJ = base;
+  idx* skk = base + stride;
+  idx* sri = base + 2 * stride;
+  idx* sslot = base + 3 * stride;
+  idx* stmp = base + 4 * stride;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const idx m0 = goff[I], m1 = goff[I + 1], nm = m1 - m0;
+
+  // ---- 1. gather (gather position p = member ascending, storage order) ----
+  if (nm <= kGalMembers) {
+    for (idx m = threadIdx.x; m < nm; m += blockDim.x) {
+      const idx i = rows[m0 + m];
+      m_lo[m] = arp[i];
+      m_row[m] = i;
+      m_off[m + 1] = arp[i + 1] - arp[i];
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the member lengths: lane owns a contiguous run
+      const idx per = (nm + 31) / 32;
+      const idx b0 = lane * per, b1 = min(nm, b0 + per);
+      idx loc = 0;
+      for (idx m = b0; m < b1; ++m) loc += m_off[m + 1];
+      idx incl = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const idx t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      idx run = incl - loc;
+      for (idx m = b0; m < b1; ++m) {
+        const idx len = m_off[m + 1];
+        m_off[m] = run;  // m_off[m] becomes the start (m_off[m + 1] is read before written)
+        run += len;
+      }
+      __syncwarp();
+      if (lane == 31) m_off[nm] = incl;
+    }
+    __syncthreads();
+    for (idx p = threadIdx.x; p < L; p += blockDim.x) {
+      idx lo = 0, hi = nm;  // last member with m_off[m] <= p
+      while (hi - lo > 1) {
+        const idx mid = (lo + hi) >> 1;
+        if (m_off[mid] <= p)
+          lo = mid;
+        else
+          hi = mid;
+      }
+      const idx k = m_lo[lo] + (p - m_off[lo]);
+      sJ[p] = assignment[acol[k]];
+      skk[p] = k;
+      sri[p] = m_row[lo];
+    }
+  } else {  // many members: member-parallel gather, block scan per batch
+    __shared__ idx s_base;
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    for (idx mb = m0; mb < m1; mb += blockDim.x) {
+      const idx m = mb + threadIdx.x;
+      idx i = 0, lo = 0, len = 0;
+      if (m < m1) {
+        i = rows[m];
+        lo = arp[i];
+        len = arp[i + 1] - lo;
+      }
+      idx incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const idx t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      idx wbase = 0;
+      for (int q = 0; q < warp; ++q) wbase += s_wsum[q];
+      const idx off = s_base + wbase + incl - len;
+      for (idx t = 0; t < len; ++t) {
+        const idx k = lo + t, p = off + t;
+        sJ[p] = assignment[acol[k]];
+        skk[p] = k;
+        sri[p] = i;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        idx tot = 0;
+        for (int q = 0; q < 8; ++q) tot += s_wsum[q];
+        s_base += tot;
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- 2. distinct J and their counts ----
+  for (int q = threadIdx.x; q < kGalHash; q += blockDim.x) {
+    h_j[q] = -1;
+    h_cnt[q] = 0;
+  }
   if (threadIdx.x == 0) {
-    s_cnt = 0;
-    s_base = 0;
+    s_nd = 0;
+    s_over = 0;
   }
   __syncthreads();
-  const idx m0 = goff[I], m1 = goff[I + 1];
-  for (idx mb = m0; mb < m1; mb += blockDim.x) {  // member-parallel gather, block scan
-    const idx m = mb + threadIdx.x;
-    idx i = 0, lo = 0, len = 0;
-    if (m < m1) {
-      i = rows[m];
-      lo = arp[i];
-      len = arp[i + 1] - lo;
+  for (idx p = threadIdx.x; p < L; p += blockDim.x) {
+    const idx J = sJ[p];
+    unsigned h = (static_cast<unsigned>(J) * 2654435761u) & (kGalHash - 1);
+    int probes = 0;
+    while (true) {
+      const idx old = atomicCAS(&h_j[h], -1, J);
+      if (old == -1 || old == J) break;
+      h = (h + 1) & (kGalHash - 1);
+      if (++probes >= kGalHash) break;
     }
-    idx incl = len;
+    if (probes >= kGalHash) {
+      s_over = 1;
+    } else {
+      atomicAdd(&h_cnt[h], 1);
+      sslot[p] = static_cast<idx>(h);
+    }
+  }
+  __syncthreads();
+  if (s_over) {  // fallback: rank sort by (J, p)
+    for (idx q = threadIdx.x; q < L; q += blockDim.x) {
+      const idx Jq = sJ[q];
+      idx rank = 0;
+      for (idx z = 0; z < L; ++z) {
+        const idx Jz = sJ[z];
+        rank += (Jz < Jq || (Jz == Jq && z < q)) ? 1 : 0;
+      }
+      entry[base_e + rank] = skk[q];
+      entry_row[base_e + rank] = sri[q];
+      sorted_j[base_e + rank] = Jq;
+    }
+    __syncthreads();
+    idx c = 0;
+    for (idx r = threadIdx.x; r < L; r += blockDim.x)
+      c += (r == 0 || sorted_j[base_e + r] != sorted_j[base_e + r - 1]) ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if (lane == 0) s_wsum[warp] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      idx t = 0;
+      for (int q = 0; q < 8; ++q) t += s_wsum[q];
+      cnnz[I] = t;
+    }
+    return;
+  }
+  for (int q = threadIdx.x; q < kGalHash; q += blockDim.x)
+    if (h_j[q] != -1) d_slot[atomicAdd(&s_nd, 1)] = q;
+  __syncthreads();
+  const int nd = s_nd;
+  // rank of every distinct J (ascending): h_cur[rank] = slot
+  for (int q = threadIdx.x; q < nd; q += blockDim.x) {
+    const idx J = h_j[d_slot[q]];
+    int r = 0;
+    for (int z = 0; z < nd; ++z) r += (h_j[d_slot[z]] < J) ? 1 : 0;
+    h_cur[r] = d_slot[q];
+  }
+  __syncthreads();
+  if (warp == 0) {  // offsets in rank order -> d_slot[rank] = start; h_cnt[slot] = start
+    const int per = (nd + 31) / 32;
+    const int b0 = lane * per, b1 = min(nd, b0 + per);
+    idx loc = 0;
+    for (int r = b0; r < b1; ++r) loc += h_cnt[h_cur[r]];
+    idx incl = loc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const idx t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
-    if (lane == 31) s_wtot[warp] = incl;
-    __syncthreads();
-    idx wbase = 0;
-    for (int q = 0; q < warp; ++q) wbase += s_wtot[q];
-    const idx off = s_base + wbase + incl - len;
-    for (idx t = 0; t < len; ++t) {
-      const idx k = lo + t, p = off + t;
-      skey[p] = (static_cast<unsigned long long>(assignment[acol[k]]) << 32) |
-                static_cast<unsigned long long>(p);
-      skk[p] = k;
-      sri[p] = i;
+    idx run = incl - loc;
+    for (int r = b0; r < b1; ++r) {
+      const idx sl = h_cur[r];
+      const idx cnt = h_cnt[sl];
+      d_slot[r] = run;  // start of run r
+      h_cnt[sl] = run;  // cursor of slot sl
+      run += cnt;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      idx tot = 0;
-      for (int q = 0; q < 8; ++q) tot += s_wtot[q];
-      s_base += tot;
-    }
-    __syncthreads();
   }
+  __syncthreads();
+  // ---- 3. stable scatter: one warp walks the entries in gather order; lanes with the same
+  //         J take consecutive positions (match_any), the group leader advances the cursor ----
+  if (warp == 0) {
+    for (idx c = 0; c < L; c += 32) {
+      const idx p = c + lane;
+      const bool ok = p < L;
+      const idx sl = ok ? sslot[p] : -1 - lane;
+      const unsigned grp = __match_any_sync(0xffffffffu, sl);
+      const int rk = __popc(grp & ((1u << lane) - 1u));
+      idx pos = 0;
+      if (ok) pos = h_cnt[sl] + rk;
+      __syncwarp();
+      if (ok && rk == 0) h_cnt[sl] += __popc(grp);
+      if (ok) stmp[pos] = p;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
   for (idx q = threadIdx.x; q < L; q += blockDim.x) {
-    const unsigned long long key = skey[q];
-    idx rank = 0;
-    for (idx z = 0; z < L; ++z) rank += (skey[z] < key) ? 1 : 0;
-    entry[base_e + rank] = skk[q];
-    entry_row[base_e + rank] = sri[q];
-    sorted_j[base_e + rank] = static_cast<idx>(key >> 32);
+    const idx p = stmp[q];
+    entry[base_e + q] = skk[p];
+    entry_row[base_e + q] = sri[p];
+    sorted_j[base_e + q] = sJ[p];
   }
-  __syncthreads();
-  idx c = 0;
-  for (idx r = threadIdx.x; r < L; r += blockDim.x)
-    c += (r == 0 || sorted_j[base_e + r] != sorted_j[base_e + r - 1]) ? 1 : 0;
-  atomicAdd(&s_cnt, c);
-  __syncthreads();
-  if (threadIdx.x == 0) cnnz[I] = s_cnt;
+  if (threadIdx.x == 0) cnnz[I] = nd;
+}
+
+__global__ void k_max_big_len(const idx* big_list, int nbig, const idx* eoff, int* out) {
+  int m = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nbig; t += gridDim.x * blockDim.x) {
+    const idx I = big_list[t];
+    m = max(m, eoff[I + 1] - eoff[I]);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 // ---- galerkin_direct: R*(A*P) in the reference spmm order (galerkin.cpp:33-36) ----------
@@ -865,19 +1033,23 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
                g.entry_row.get(), sorted_j.get(), cnnz.get(), big_list.get(), big_count.get());
   const int nbig = read_scalar(big_count.get());
   if (nbig > 0) {
-    const size_t smem = static_cast<size_t>(kGalCapBig) * (8 + 4 + 4);
-    static thread_local bool raised = false;
+    DevBuf<int> maxlen(1);
+    maxlen.zero();
+    AGG_LAUNCH(k_max_big_len, grid_for(nbig, 256, 4 * sm_count()), 256, 0, big_list.get(), nbig,
+               eoff.get(), maxlen.get());
+    const int cap = std::min(kGalCapBig, read_scalar(maxlen.get()));
+    const size_t smem = static_cast<size_t>(cap) * 5 * sizeof(idx);
+    static thread_local bool raised = false;  // one value for every thread: the attribute is global
     if (!raised) {
       AGG_CUDA(cudaFuncSetAttribute(k_gal_symbolic_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
+                                    kGalCapBig * 5 * static_cast<int>(sizeof(idx))));
       raised = true;
     }
-    DevBuf<unsigned long long> gkey(A.nnz);
-    DevBuf<idx> gkk(A.nnz), gri(A.nnz);
+    DevBuf<idx> scratch(cap < kGalCapBig ? 1 : 5 * A.nnz);  // only rows longer than kGalCapBig
     AGG_LAUNCH(k_gal_symbolic_big, static_cast<unsigned>(nbig), 256, smem, big_list.get(),
                agg.agg_row_offsets.get(), agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(),
-               agg.assignment.get(), eoff.get(), gkey.get(), gkk.get(), gri.get(), g.entry.get(),
-               g.entry_row.get(), sorted_j.get(), cnnz.get());
+               agg.assignment.get(), eoff.get(), cap, scratch.get(), g.entry.get(), g.entry_row.get(),
+               sorted_j.get(), cnnz.get());
   }
   g.coarse_rowptr.resize(nc + 1);
   g.nnz_coarse = scan_to_offsets(cnnz.get(), g.coarse_rowptr.get(), nc);
