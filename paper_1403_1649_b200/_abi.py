@@ -192,7 +192,9 @@ SIGNATURES = {
 }
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PRODUCT_LIB = os.path.join(REPO, "paper_1403_1649_b200", "lib", "libaggmg_b200.so")
+# AGGMG_LIB: an alternative build of the product library (kernel-variant experiments)
+PRODUCT_LIB = os.environ.get("AGGMG_LIB") or os.path.join(REPO, "paper_1403_1649_b200", "lib",
+                                                          "libaggmg_b200.so")
 ORACLE_LIB = os.path.join(REPO, "oracle", "liboracle.so")
 REF_LIB = os.path.join(REPO, "oracle", "_ref", "libaggmg_ref.so")
 
