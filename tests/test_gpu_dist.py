@@ -157,3 +157,61 @@ def test_dist_errors_propagate(gpu):
     cfg = M.SetupConfig(alpha=0.25, reuse_caches=True, coarse_size_max=4)
     with pytest.raises(M.Error, match="structurally symmetric|rank"):
         run_dist(A, 2, cfg, agglomerate=5)
+
+
+def test_dist_aniso_fgmres_three_ranks_uneven(gpu):
+    A = gpu.generate_poisson(3, 22, 18, 16, 1e-3)
+    cfg = M.SetupConfig(alpha=0.5, reuse_caches=True, coarse_size_max=50)
+    sc = M.SolverConfig(method=M.FGMRES, tol=1e-8, max_iters=300, restart=30)
+    hg = gpu.setup_hierarchy(A, None, cfg)
+    rg = gpu.fgmres(A, np.ones(A.n_rows), None, hg, M.CycleConfig(), sc)
+    n = A.n_rows
+    part = [0, n // 5, n // 2 + 17, n]
+    res = run_dist(A, 3, cfg, agglomerate=300, solver=sc, cycle=M.CycleConfig(), part=part)
+    compare_hierarchy(hg, res, "aniso P=3")
+    s0 = res[0]["solve"]
+    assert s0.report.iterations == rg.report.iterations
+    hd, hs = np.array(s0.report.residual_history), np.array(rg.report.residual_history)
+    assert np.max(np.abs(hd - hs)) <= 1e-10 * hs[0]
+
+
+def test_dist_jump27_pcg_two_ranks(gpu):
+    A = gpu.generate_jump27(14, 13, 12, 1e6, 4)
+    cfg = M.SetupConfig(alpha=0.5, reuse_caches=True, coarse_size_max=40)
+    sc = M.SolverConfig(method=M.PCG, tol=1e-8, max_iters=300)
+    hg = gpu.setup_hierarchy(A, None, cfg)
+    rg = gpu.pcg(A, np.ones(A.n_rows), None, hg, M.CycleConfig(), sc)
+    res = run_dist(A, 2, cfg, agglomerate=150, solver=sc, cycle=M.CycleConfig())
+    compare_hierarchy(hg, res, "jump27 P=2")
+    s0 = res[0]["solve"]
+    assert s0.report.iterations == rg.report.iterations
+    hd, hs = np.array(s0.report.residual_history), np.array(rg.report.residual_history)
+    assert np.max(np.abs(hd - hs)) <= 1e-10 * hs[0]
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_dist_preconditioner_matches_one_gpu(gpu, P):
+    A = gpu.generate_poisson(3, 20, 20, 20)
+    cfg = M.SetupConfig(alpha=0.5, reuse_caches=True, coarse_size_max=40)
+    hg = gpu.setup_hierarchy(A, None, cfg)
+    r = np.random.default_rng(9).uniform(-1, 1, A.n_rows)
+    zg = gpu.apply_preconditioner(hg, M.CycleConfig(), r)
+    n = A.n_rows
+    out = {}
+
+    def fn(comm, k):
+        dA = D.DistMatrix.from_global(comm, A)
+        h = D.setup(comm, dA, cfg, agglomerate_rows=100)
+        _, row0, nloc, _ = dA.info()
+        out[k] = (row0, h.apply_preconditioner(r[row0:row0 + nloc]))
+        h.free()
+        dA.free()
+
+    D.run_threads(P, fn)
+    z = np.zeros(n)
+    for row0, zl in out.values():
+        z[row0:row0 + zl.shape[0]] = zl
+    if P == 1:
+        assert np.array_equal(z.view(np.uint64), zg.view(np.uint64))
+    else:
+        assert np.max(np.abs(z - zg)) <= 1e-12 * np.max(np.abs(zg))
