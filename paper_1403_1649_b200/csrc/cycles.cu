@@ -4,7 +4,11 @@
 #include <cstdlib>
 #include <string>
 
+#include <tuple>
+#include <vector>
+
 #include "chunked.cuh"
+
 #include "cycles.cuh"
 
 namespace aggmg_b200 {
@@ -356,8 +360,42 @@ void inner_cycle_eager(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const do
     vcycle_dev(h, k, b, nullptr, x_out, pred);
 }
 
+// AGGMG_LEVEL_TIMING=1 (with AGGMG_GRAPHS=0): inclusive GPU time of every level visit,
+// summed per level and printed by flush_cycle_warnings() — the per-level cost breakdown.
+struct LevelTimer {
+  bool on = false;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> rec;
+  LevelTimer() {
+    const char* e = std::getenv("AGGMG_LEVEL_TIMING");
+    on = e && e[0] == '1';
+  }
+};
+LevelTimer& ltimer() {
+  static thread_local LevelTimer t;
+  return t;
+}
+struct LevelScope {
+  cudaEvent_t b_ = nullptr, e_ = nullptr;
+  int level_;
+  explicit LevelScope(int level) : level_(level) {
+    if (!ltimer().on) return;
+    cudaStreamCaptureStatus st;
+    cudaStreamIsCapturing(stream(), &st);
+    if (st != cudaStreamCaptureStatusNone) return;
+    cudaEventCreate(&b_);
+    cudaEventCreate(&e_);
+    cudaEventRecord(b_, stream());
+  }
+  ~LevelScope() {
+    if (!b_) return;
+    cudaEventRecord(e_, stream());
+    ltimer().rec.emplace_back(level_, b_, e_);
+  }
+};
+
 void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in, double* x_out,
                 const int* pred) {
+  LevelScope ls(static_cast<int>(k + h.cfg.level_offset));
   if (k == h.coarsest()) {
     coarse_solve(h, b, x_out, pred);
     return;
@@ -370,6 +408,7 @@ void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in,
 
 void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b,
                 const double* x_in, double* x_out, const int* pred) {
+  LevelScope ls(static_cast<int>(k + h.cfg.level_offset));
   if (k == h.coarsest()) {
     coarse_solve(h, b, x_out, pred);
     return;
@@ -511,6 +550,25 @@ void apply_preconditioner(DevHierarchy& h, const CycleCfg& cfg, const double* r,
 }
 
 void flush_cycle_warnings() {
+  if (ltimer().on && !ltimer().rec.empty()) {
+    sync();
+    double inc[32] = {0};
+    int visits[32] = {0};
+    for (auto& r : ltimer().rec) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, std::get<1>(r), std::get<2>(r));
+      const int l = std::min(31, std::get<0>(r));
+      inc[l] += ms;
+      ++visits[l];
+      cudaEventDestroy(std::get<1>(r));
+      cudaEventDestroy(std::get<2>(r));
+    }
+    ltimer().rec.clear();
+    for (int l = 0; l < 32; ++l)
+      if (visits[l])
+        std::fprintf(stderr, "[level timing] level %d: %d visits, inclusive %.3f ms, exclusive %.3f ms\n",
+                     l, visits[l], inc[l], inc[l] - (l + 1 < 32 ? inc[l + 1] : 0.0));
+  }
   int w[2];
   AGG_CUDA(cudaMemcpyAsync(w, warn_bits(), sizeof(w), cudaMemcpyDeviceToHost, stream()));
   AGG_CUDA(cudaStreamSynchronize(stream()));

@@ -76,6 +76,7 @@ struct DevHierarchy {
   double* top_dot_out = nullptr;
   bool top_dot_done = false;
 
+
   int64_t n_levels() const { return static_cast<int64_t>(levels.size()); }
   int64_t coarsest() const { return n_levels() - 1; }
   void ensure_workspace();
