@@ -289,6 +289,17 @@ void aggmg_comm_free(aggmg_comm* c);
  * column ids (canonical rows) */
 int aggmg_dist_matrix_from_host(aggmg_comm* c, int64_t n_global, int64_t row0,
                                 const aggmg_csr* rows, aggmg_dist_matrix** out);
+/* ---- Matrix Market I/O (matrix_market.hpp:23-35) ----------------------------------------
+ * Reader: the reference's file semantics and error messages ("matrix market: line L: ...");
+ * data lines parsed on all host cores, CSR assembled on the device.  Writers: 17 significant
+ * digits, byte-identical to the reference's. */
+int aggmg_read_matrix_market_file(const char* path, int allow_pattern, aggmg_csr* A);
+int aggmg_read_matrix_market(const char* text, int64_t size, int allow_pattern, aggmg_csr* A);
+int aggmg_write_matrix_market_file(const char* path, const aggmg_csr* A);
+/* x may be NULL to query the length n */
+int aggmg_read_vector_market_file(const char* path, double* x, int64_t capacity, int64_t* n);
+int aggmg_write_vector_market_file(const char* path, const double* x, int64_t n);
+
 /* host rows [row0, row0 + nrows) of the generator matrices (global column ids): one rank's
  * slab as a host input for aggmg_dist_matrix_from_host */
 int aggmg_generate_poisson_rows(int dims, int64_t nx, int64_t ny, int64_t nz, double epsilon,

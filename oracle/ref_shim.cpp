@@ -4,6 +4,7 @@
 // signatures as include/aggmg_b200.h, prefixed aggmg_ref_, so the parity tests and the
 // bench's CPU arm can call the reference and the B200 library side by side.  Nothing in
 // the product links or loads this file.
+#include <sstream>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -12,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "aggmg/matrix_market.hpp"
 #include "aggmg/aggregation.hpp"
 #include "aggmg/cycles.hpp"
 #include "aggmg/dense.hpp"
@@ -145,6 +147,39 @@ int aggmg_ref_generate_poisson(int dims, int64_t nx, int64_t ny, int64_t nz, dou
     ps.weak_axis = weak;
     from_ref(aggmg::generate_poisson(ps), A);
   });
+}
+
+// Matrix Market I/O of the unmodified reference (matrix_market.hpp:23-35)
+int aggmg_ref_read_matrix_market_file(const char* path, int allow_pattern, aggmg_csr* A) {
+  return guarded([&] {
+    aggmg::MmOptions o;
+    o.allow_pattern = allow_pattern != 0;
+    from_ref(aggmg::read_matrix_market_file(path, o), A);
+  });
+}
+int aggmg_ref_read_matrix_market(const char* text, int64_t size, int allow_pattern, aggmg_csr* A) {
+  return guarded([&] {
+    aggmg::MmOptions o;
+    o.allow_pattern = allow_pattern != 0;
+    std::istringstream in(std::string(text, static_cast<size_t>(size)));
+    from_ref(aggmg::read_matrix_market(in, o), A);
+  });
+}
+int aggmg_ref_write_matrix_market_file(const char* path, const aggmg_csr* A) {
+  return guarded([&] { aggmg::write_matrix_market_file(path, to_ref(A)); });
+}
+int aggmg_ref_read_vector_market_file(const char* path, double* x, int64_t capacity, int64_t* n) {
+  return guarded([&] {
+    const aggmg::Vector v = aggmg::read_vector_market_file(path);
+    *n = static_cast<int64_t>(v.size());
+    if (x) {
+      if (capacity < *n) throw aggmg::Error("vector market: output buffer too small");
+      std::copy(v.begin(), v.end(), x);
+    }
+  });
+}
+int aggmg_ref_write_vector_market_file(const char* path, const double* x, int64_t n) {
+  return guarded([&] { aggmg::write_vector_market_file(path, aggmg::Vector(x, x + n)); });
 }
 
 int aggmg_ref_spmv(const aggmg_csr* A, const double* x, double* y) {

@@ -167,6 +167,11 @@ SIGNATURES = {
     "comm_size": (I, [vp]),
     "comm_kind": (C.c_char_p, [vp]),
     "comm_free": (None, [vp]),
+    "read_matrix_market_file": (I, [C.c_char_p, I, csrp]),
+    "read_matrix_market": (I, [C.c_char_p, L, I, csrp]),
+    "write_matrix_market_file": (I, [C.c_char_p, csrp]),
+    "read_vector_market_file": (I, [C.c_char_p, f64p, L, i64p]),
+    "write_vector_market_file": (I, [C.c_char_p, f64p, L]),
     "generate_poisson_rows": (I, [I, L, L, L, C.c_double, I, L, L, csrp]),
     "generate_jump27_rows": (I, [L, L, L, C.c_double, L, L, L, csrp]),
     "dist_matrix_from_host": (I, [vp, L, L, csrp, C.POINTER(vp)]),

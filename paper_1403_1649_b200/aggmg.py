@@ -583,6 +583,30 @@ class Backend:
                                           hist[: rep.history_length].tolist(), rep.setup_seconds,
                                           rep.solve_seconds, rep.note.decode()))
 
+    # -- Matrix Market (matrix_market.hpp:23-35) --
+    def read_matrix_market(self, path: str, allow_pattern: bool = False) -> SparseMatrix:
+        return self._csr_out("read_matrix_market_file", str(path).encode(), int(allow_pattern))
+
+    def read_matrix_market_text(self, text, allow_pattern: bool = False) -> SparseMatrix:
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        return self._csr_out("read_matrix_market", data, len(data), int(allow_pattern))
+
+    def write_matrix_market(self, path: str, A: SparseMatrix) -> None:
+        ca = A._c()
+        self._call("write_matrix_market_file", str(path).encode(), C.byref(ca))
+
+    def read_vector_market(self, path: str) -> np.ndarray:
+        n = C.c_int64()
+        self._call("read_vector_market_file", str(path).encode(), None, 0, C.byref(n))
+        x = np.zeros(n.value)
+        self._call("read_vector_market_file", str(path).encode(), _p(x, _abi.f64p), n.value,
+                   C.byref(n))
+        return x
+
+    def write_vector_market(self, path: str, x) -> None:
+        x = _f64(x)
+        self._call("write_vector_market_file", str(path).encode(), _p(x, _abi.f64p), x.shape[0])
+
     # -- inputs (poisson.hpp) --
     def generate_poisson(self, dims: int, nx: int, ny: int, nz: int = 1, epsilon: float = 1.0,
                          weak_axis: int = -1) -> SparseMatrix:

@@ -14,6 +14,7 @@
 #include "../../include/aggmg_b200.h"
 #include "chunked.cuh"
 #include "dist_solve.cuh"
+#include "mm.cuh"
 #include "krylov.cuh"
 #include "vecops.cuh"
 
@@ -820,6 +821,40 @@ static void host_to_out(const HostCsr& H, aggmg_csr* A) {
   std::memcpy(A->row_offsets, H.rp.data(), sizeof(int64_t) * (H.n + 1));
   std::memcpy(A->col_indices, H.col.data(), sizeof(int64_t) * nnz);
   std::memcpy(A->values, H.val.data(), sizeof(double) * nnz);
+}
+
+// ---- Matrix Market (matrix_market.hpp:23-35) ------------------------------------------------
+
+int aggmg_read_matrix_market_file(const char* path, int allow_pattern, aggmg_csr* A) {
+  return guarded([&] { host_to_out(read_matrix_market_file(path, allow_pattern != 0), A); });
+}
+
+int aggmg_read_matrix_market(const char* text, int64_t size, int allow_pattern, aggmg_csr* A) {
+  return guarded([&] {
+    host_to_out(read_matrix_market_text(text, static_cast<size_t>(size), allow_pattern != 0), A);
+  });
+}
+
+int aggmg_write_matrix_market_file(const char* path, const aggmg_csr* A) {
+  return guarded([&] {
+    require(A != nullptr, "null matrix");
+    write_matrix_market_file(path, A->n_rows, A->n_cols, A->row_offsets, A->col_indices, A->values);
+  });
+}
+
+int aggmg_read_vector_market_file(const char* path, double* x, int64_t capacity, int64_t* n) {
+  return guarded([&] {
+    const std::vector<double> v = read_vector_market_file(path);
+    *n = static_cast<int64_t>(v.size());
+    if (x) {
+      require(capacity >= *n, "vector market: output buffer too small");
+      std::memcpy(x, v.data(), sizeof(double) * v.size());
+    }
+  });
+}
+
+int aggmg_write_vector_market_file(const char* path, const double* x, int64_t n) {
+  return guarded([&] { write_vector_market_file(path, x, n); });
 }
 
 int aggmg_generate_poisson_rows(int dims, int64_t nx, int64_t ny, int64_t nz, double eps,
