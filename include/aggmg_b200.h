@@ -354,6 +354,8 @@ int aggmg_profile_read(int family, double* total_ms, int64_t* launches, double* 
 /* device time on the library stream between the two calls (ms) */
 int aggmg_timer_start(void);
 int aggmg_timer_stop(double* ms);
+/* dot_device micro-benchmark: np products over n elements, exact = reference chunk order */
+int aggmg_bench_dot(int64_t n, int np, int exact, int reps, double* avg_ms);
 /* SpMV micro-benchmark on a device matrix: average ms per launch over `reps` launches */
 int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* bytes);
 /* same for one CSR-stream variant: 0 spmv, 1 residual, 2 fused zero-guess Jacobi+residual,

@@ -151,6 +151,7 @@ SIGNATURES = {
     "profile_enable": (I, [I]),
     "profile_read": (I, [I, f64p, i64p, f64p]),
     "bench_spmv": (I, [vp, I, f64p, f64p]),
+    "bench_dot": (I, [L, I, I, I, f64p]),
     "bench_kernel": (I, [vp, I, I, f64p, f64p]),
     "hierarchy_level_dmatrix": (I, [vp, L, I, C.POINTER(vp)]),
     "set_exact_reductions": (None, [I]),

@@ -960,6 +960,34 @@ int aggmg_profile_read(int family, double* total_ms, int64_t* launches, double* 
   return guarded([&] { profile_read(family, total_ms, launches, bytes); });
 }
 
+int aggmg_bench_dot(int64_t n, int np, int exact, int reps, double* avg_ms) {
+  return guarded([&] {
+    require(np >= 1 && np <= 3, "bench_dot: np must be 1..3");
+    DevBuf<double> a(n), b(n), out(4);
+    fill_double(a.get(), n, 0.5);
+    fill_double(b.get(), n, 0.25);
+    DotArgs d{};
+    for (int k = 0; k < np; ++k) {
+      d.a[k] = a.get();
+      d.b[k] = b.get();
+    }
+    d.np = np;
+    dot_device(d, n, out.get(), nullptr, exact);
+    cudaEvent_t e0, e1;
+    AGG_CUDA(cudaEventCreate(&e0));
+    AGG_CUDA(cudaEventCreate(&e1));
+    AGG_CUDA(cudaEventRecord(e0, stream()));
+    for (int r = 0; r < reps; ++r) dot_device(d, n, out.get(), nullptr, exact);
+    AGG_CUDA(cudaEventRecord(e1, stream()));
+    AGG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    AGG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *avg_ms = ms / reps;
+  });
+}
+
 int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* bytes) {
   return aggmg_bench_kernel(A, 0, reps, avg_ms, bytes);
 }

@@ -25,11 +25,26 @@ constexpr int kChunkTile = 8 * kChunkProducers;  // 768 elements per stage
 bool exact_reductions();
 void set_exact_reductions(bool on);
 
-__device__ inline void named_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+// Shared-memory mbarriers for the producer/consumer hand-off.  (Named barriers did the same
+// job but a CTA holding four of them caps residency at four CTAs per SM — 3.5 waves of chunk
+// chains for a 16.7 M vector; mbarriers carry no such limit.)
+__device__ inline unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ inline void named_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+__device__ inline void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ inline void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ inline void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "MBAR_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // One CTA per 8192-element chunk.  Producers fill stage b = t & 1 and arrive on FULL[b];
@@ -42,11 +57,19 @@ __global__ void __launch_bounds__(kChunkThreads)
     k_chunked(int64_t n, Op op, double* partials, unsigned* ticket, double* out) {
   __shared__ __align__(16) double tile[2][NP][kChunkTile];
   __shared__ bool last;
-  constexpr int kFull0 = 1, kEmpty0 = 3;  // named barrier ids 1,2 (full) and 3,4 (empty)
+  __shared__ unsigned long long full[2], empty[2];
   if (!op.active()) {
     if (blockIdx.x == 0 && threadIdx.x == 0) op.inactive();
     return;
   }
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], kChunkProducers);
+    mbar_init(&full[1], kChunkProducers);
+    mbar_init(&empty[0], 1);
+    mbar_init(&empty[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   op.init();
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kChunk;
   const int len = static_cast<int>(min(static_cast<int64_t>(kChunk), n - c0));
@@ -57,7 +80,7 @@ __global__ void __launch_bounds__(kChunkThreads)
     const int pt = threadIdx.x - 32;
     for (int t = 0; t < ntiles; ++t) {
       const int b = t & 1;
-      if (t >= 2) named_sync(kEmpty0 + b, kChunkThreads);
+      if (t >= 2) mbar_wait(&empty[b], ((t >> 1) - 1) & 1);  // consumer freed use t-2
       const int tb = t * kChunkTile;
 #pragma unroll
       for (int j = 0; j < kChunkTile / kChunkProducers; ++j) {
@@ -69,12 +92,12 @@ __global__ void __launch_bounds__(kChunkThreads)
           for (int k = 0; k < NP; ++k) tile[b][k][pos - tb] = p[k];
         }
       }
-      named_arrive(kFull0 + b, kChunkThreads);
+      mbar_arrive(&full[b]);
     }
   } else {  // consumer warp
     for (int t = 0; t < ntiles; ++t) {
       const int b = t & 1;
-      named_sync(kFull0 + b, kChunkThreads);
+      mbar_wait(&full[b], (t >> 1) & 1);
       if (lane < NP) {
         const int m = min(kChunkTile, len - t * kChunkTile);
         const double* src = tile[b][lane];
@@ -95,7 +118,8 @@ __global__ void __launch_bounds__(kChunkThreads)
         }
         for (; q < m; ++q) acc = __dadd_rn(acc, src[q]);
       }
-      if (t + 2 < ntiles) named_arrive(kEmpty0 + b, kChunkThreads);
+      __syncwarp();
+      if (lane == 0 && t + 2 < ntiles) mbar_arrive(&empty[b]);
     }
     if (lane < NP) partials[blockIdx.x * NP + lane] = acc;
   }

@@ -966,22 +966,7 @@ void dist_smoother(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k) {
   };
   ops.before_spmv = [&](double* v) { halo_update<double>(comm, A.halo, v); };
   ops.dot = [&](const double* a, const double* b) { return dist_dot(comm, a, b, nloc); };
-  DevBuf<double> d2(2);
-  ops.dot2 = [&](const double* a, const double* b, const double* c, const double* e, double* out) {
-    DotArgs args{};
-    args.a[0] = a;
-    args.b[0] = b;
-    args.a[1] = c;
-    args.b[1] = e;
-    args.np = 2;
-    if (nloc > 0)
-      dot_device(args, nloc, d2.get(), nullptr, 1);
-    else
-      d2.zero();
-    comm.allreduce_sum(d2.get(), 2);
-    d2.download(out, 2);
-    sync();
-  };
+  ops.allreduce_dev = [&](double* v, int k) { comm.allreduce_sum(v, k); };
   // a zero diagonal on any rank must fail every rank
   std::string err;
   try {

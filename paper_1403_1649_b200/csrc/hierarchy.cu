@@ -1,5 +1,8 @@
 // hierarchy.cu — Algorithm 1 setup loop on the device (hierarchy.cpp:34-104).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <sstream>
 
@@ -9,6 +12,40 @@
 namespace aggmg_b200 {
 
 constexpr int64_t kDenseSolveCap = 5000;  // hierarchy.cpp:23
+
+namespace {
+// AGGMG_SETUP_TIMING=1: per-phase GPU-synchronised wall time of setup_hierarchy (stderr)
+struct SetupTimer {
+  bool on = false;
+  std::chrono::steady_clock::time_point t;
+  std::vector<std::pair<std::string, double>> acc;
+  SetupTimer() {
+    const char* e = std::getenv("AGGMG_SETUP_TIMING");
+    on = e && e[0] == '1';
+    if (on) {
+      sync();
+      t = std::chrono::steady_clock::now();
+    }
+  }
+  void mark(const std::string& name) {
+    if (!on) return;
+    sync();
+    const auto now = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+    t = now;
+    for (auto& a : acc)
+      if (a.first == name) {
+        a.second += ms;
+        return;
+      }
+    acc.emplace_back(name, ms);
+  }
+  ~SetupTimer() {
+    if (!on) return;
+    for (auto& a : acc) std::fprintf(stderr, "[setup] %-14s %8.3f ms\n", a.first.c_str(), a.second);
+  }
+};
+}  // namespace
 
 void factor_coarsest(DevHierarchy& h) {
   DevLevel& L = h.levels.back();
@@ -50,6 +87,7 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
   const double nb = std::sqrt(dot_host(h->levels[0].B.get(), h->levels[0].B.get(), A0->n_rows));
   require(nb > 0.0, "setup: near-null-space vector is zero");
 
+  SetupTimer st;
   while (h->levels.back().A->n_rows > cfg.coarse_size_max &&
          static_cast<int>(h->levels.size()) < cfg.max_levels) {
     const int64_t k = h->coarsest();
@@ -57,14 +95,19 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     const DevCsr& A = *fine.A;
     const int64_t n = A.n_rows;
 
+    const std::string lv = "L" + std::to_string(k) + " ";
     DevCsrPtr C = classic_strength(A, cfg.alpha, 0);
+    st.mark(lv + "strength");
     DevBuf<idx> influence;
     DevCsrPtr S;
     influence_and_symmetrize(*C, influence, S);
     C.reset();
+    st.mark(lv + "symmetrize");
     Mis2Dev mis = mis2(*S, influence.get(), level_seed(cfg.seed, k + cfg.level_offset, kMisTag));
+    st.mark(lv + "mis2");
     AggDev agg = aggregate(*S, A, mis.state.get());
     S.reset();
+    st.mark(lv + "aggregate");
 
     if (static_cast<double>(agg.n_agg) >= 0.95 * static_cast<double>(n)) {
       std::ostringstream msg;
@@ -75,6 +118,7 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     }
     fine.mis_sweeps = mis.sweeps;
     fine.tr = build_transfer(agg, fine.B.get());
+    st.mark(lv + "transfer");
     DevCsrPtr Ac;
     if (cfg.reuse_caches) {  // hierarchy.cpp:69-71: cached sort / segmented reduce
       fine.gal = build_galerkin_cache(A, agg);
@@ -82,8 +126,10 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     } else {  // hierarchy.cpp:73: galerkin_direct, the reference default
       Ac = galerkin_direct(A, agg, fine.tr.pval.get());
     }
+    st.mark(lv + "galerkin");
     setup_smoother(A, cfg.smoother, cfg.arnoldi_m, level_seed(cfg.seed, k + cfg.level_offset, kSmootherTag),
                    fine.smoother);
+    st.mark(lv + "smoother");
     fine.has_smoother = true;
     fine.agg = std::move(agg);
     fine.has_next = true;
@@ -93,6 +139,7 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     h->levels.push_back(std::move(next));
   }
   factor_coarsest(*h);
+  st.mark("coarsest LU");
   AGG_CUDA(cudaEventRecord(e1, stream()));
   AGG_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;

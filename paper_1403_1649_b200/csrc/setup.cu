@@ -404,7 +404,8 @@ constexpr int kGalMembers = 512;
 __global__ void __launch_bounds__(256)
     k_gal_symbolic_big(const idx* big_list, const idx* goff, const idx* rows, const idx* arp,
                        const idx* acol, const idx* assignment, const idx* eoff, int cap,
-                       idx* gscratch, idx* entry, idx* entry_row, idx* sorted_j, idx* cnnz) {
+                       const int64_t* goff_big, idx* gscratch, idx* entry, idx* entry_row,
+                       idx* sorted_j, idx* cnnz) {
   extern __shared__ idx big_smem[];
   __shared__ idx m_off[kGalMembers + 1], m_lo[kGalMembers], m_row[kGalMembers];
   __shared__ idx h_j[kGalHash], h_cnt[kGalHash], h_cur[kGalHash], d_slot[kGalHash];
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(256)
   const idx base_e = eoff[I];
   const idx L = eoff[I + 1] - base_e;
   const bool in_smem = L <= cap;
-  idx* base = in_smem ? big_smem : gscratch + 5 * static_cast<int64_t>(base_e);
+  idx* base = in_smem ? big_smem : gscratch + 5 * goff_big[blockIdx.x];
   const idx stride = in_smem ? cap : L;
   idx* sJ = base;
   idx* skk = base + stride;
@@ -619,6 +620,16 @@ __global__ void __launch_bounds__(256)
     sorted_j[base_e + q] = sJ[p];
   }
   if (threadIdx.x == 0) cnnz[I] = nd;
+}
+
+// scratch offsets of the rows that do not fit in shared memory (exclusive scan input)
+__global__ void k_big_scratch_len(const idx* big_list, int nbig, const idx* eoff, int cap,
+                                  int64_t* len) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nbig) return;
+  const idx I = big_list[t];
+  const idx L = eoff[I + 1] - eoff[I];
+  len[t] = L > cap ? L : 0;
 }
 
 __global__ void k_max_big_len(const idx* big_list, int nbig, const idx* eoff, int* out) {
@@ -1045,11 +1056,25 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
                                     kGalCapBig * 5 * static_cast<int>(sizeof(idx))));
       raised = true;
     }
-    DevBuf<idx> scratch(cap < kGalCapBig ? 1 : 5 * A.nnz);  // only rows longer than kGalCapBig
+    // global scratch only for the rows longer than the shared-memory capacity
+    DevBuf<int64_t> blen(nbig), boff(nbig + 1);
+    AGG_LAUNCH(k_big_scratch_len, grid_for(nbig, 256), 256, 0, big_list.get(), nbig, eoff.get(), cap,
+               blen.get());
+    int64_t big_total = 0;
+    {
+      std::vector<int64_t> h(nbig);
+      blen.download(h.data(), nbig);
+      sync();
+      std::vector<int64_t> o(nbig + 1, 0);
+      for (int t = 0; t < nbig; ++t) o[t + 1] = o[t] + h[t];
+      big_total = o[nbig];
+      boff.upload(o.data(), nbig + 1);
+    }
+    DevBuf<idx> scratch(std::max<int64_t>(1, 5 * big_total));
     AGG_LAUNCH(k_gal_symbolic_big, static_cast<unsigned>(nbig), 256, smem, big_list.get(),
                agg.agg_row_offsets.get(), agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(),
-               agg.assignment.get(), eoff.get(), cap, scratch.get(), g.entry.get(), g.entry_row.get(),
-               sorted_j.get(), cnnz.get());
+               agg.assignment.get(), eoff.get(), cap, boff.get(), scratch.get(), g.entry.get(),
+               g.entry_row.get(), sorted_j.get(), cnnz.get());
   }
   g.coarse_rowptr.resize(nc + 1);
   g.nnz_coarse = scan_to_offsets(cnnz.get(), g.coarse_rowptr.get(), nc);

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <vector>
 
+#include "chunked.cuh"
 #include "dense_host.hpp"
 #include "smoother.cuh"
 #include "vecops.cuh"
@@ -45,6 +46,40 @@ __global__ void k_sgs(const idx* rp, const idx* col, const double* val, int64_t 
   }
 }
 
+// One fused MGS step of the Arnoldi column on the device, in the reference's chunked dot
+// order: w = w + (-h) V_i (skipped for the column's first step), then (V_next . w,
+// V_next . V_next) — or (w . w, 0) after the last basis vector.  The host path this replaces
+// ran dot2 (sync) + axpy per coefficient; the fused form makes one pass per coefficient and
+// one host read per column, with bit-identical coefficients (same operations, same order).
+struct ArnoldiStepOp {
+  const double* hsrc;  // device coefficient h to subtract with (nullptr: first step)
+  const double* vi;
+  double* w;
+  const double* vn;  // next basis vector (nullptr: last step, out = w . w)
+  double mh;
+  __device__ bool active() const { return true; }
+  __device__ void inactive() const {}
+  __device__ void init() { mh = hsrc ? -*hsrc : 0.0; }
+  __device__ void operator()(int64_t t, double* p) const {
+    double wt = w[t];
+    if (hsrc) {
+      wt = __dadd_rn(wt, __dmul_rn(mh, vi[t]));  // vec_axpy(-h, V_i, w)
+      w[t] = wt;
+    }
+    if (vn) {
+      const double v = vn[t];
+      p[0] = __dmul_rn(v, wt);
+      p[1] = __dmul_rn(v, v);
+    } else {
+      p[0] = __dmul_rn(wt, wt);
+      p[1] = 0.0;
+    }
+  }
+  __device__ void finalize(double*) const {}
+};
+
+__global__ void k_hdiv(const double* s, double* h) { *h = s[0] / s[1]; }
+
 double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t seed,
                     const ArnoldiOps* ops) {
   const int64_t n = A.n_rows;
@@ -66,7 +101,9 @@ double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t see
   std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0);  // row-major (m+1) x m
   auto h = [&](int i, int j) -> double& { return H[static_cast<size_t>(i) * m + j]; };
   int m_eff = m;
-  DevBuf<double> w(n), dots(2);
+  // device copies: column j's coefficients Hc[i] (i <= j), step slots, the final ||w||^2
+  DevBuf<double> w(n), Hc(m + 1), slots(2);
+  double* pin = pinned_scratch(m + 2);
   for (int j = 0; j < m; ++j) {
     if (ops) ops->before_spmv(V[j].get());  // halo of the Krylov vector
     SpmvArgs a;
@@ -74,28 +111,30 @@ double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t see
     a.y = w.get();
     a.d = inv_diag;
     spmv_run(A, Epi::kScaleDiag, a);
+    for (int i = -1; i <= j; ++i) {  // i = -1: the first dots, no axpy
+      ArnoldiStepOp op;
+      op.hsrc = i >= 0 ? Hc.get() + i : nullptr;
+      op.vi = i >= 0 ? V[i].get() : nullptr;
+      op.w = w.get();
+      op.vn = i < j ? V[i + 1].get() : nullptr;
+      if (n > 0)
+        launch_chunked<2>(op, n, slots.get());
+      else
+        slots.zero();
+      if (ops) ops->allreduce_dev(slots.get(), 2);
+      if (i < j)
+        AGG_LAUNCH(k_hdiv, 1, 1, 0, slots.get(), Hc.get() + i + 1);  // h(i+1, j)
+    }
+    // one read per column: h(0..j, j) and ||w||^2
+    AGG_CUDA(cudaMemcpyAsync(pin, Hc.get(), sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, stream()));
+    AGG_CUDA(cudaMemcpyAsync(pin + j + 1, slots.get(), sizeof(double), cudaMemcpyDeviceToHost, stream()));
+    sync();
     double h_scale = 0.0;
     for (int i = 0; i <= j; ++i) {
-      double hv[2];
-      if (ops) {
-        ops->dot2(V[i].get(), w.get(), V[i].get(), V[i].get(), hv);
-      } else {
-        DotArgs d{};
-        d.a[0] = V[i].get();
-        d.b[0] = w.get();
-        d.a[1] = V[i].get();
-        d.b[1] = V[i].get();
-        d.np = 2;
-        dot_device(d, n, dots.get(), nullptr, 1);
-        dots.download(hv, 2);
-        sync();
-      }
-      const double hij = hv[0] / hv[1];
-      h(i, j) = hij;
-      vec_axpy(n, -hij, V[i].get(), w.get());
-      h_scale = std::max(h_scale, std::abs(hij));
+      h(i, j) = pin[i];
+      h_scale = std::max(h_scale, std::abs(pin[i]));
     }
-    const double hj = std::sqrt(dot(w.get(), w.get()));
+    const double hj = std::sqrt(pin[j + 1]);
     if (hj <= 1e-12 * std::max(h_scale, 1.0)) {
       m_eff = j + 1;
       break;

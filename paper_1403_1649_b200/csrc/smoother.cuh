@@ -24,8 +24,7 @@ struct ArnoldiOps {
   std::function<void(double*)> start;
   std::function<void(double*)> before_spmv;
   std::function<double(const double*, const double*)> dot;
-  // (a.b, c.d) in one pass and one readback
-  std::function<void(const double*, const double*, const double*, const double*, double*)> dot2;
+  std::function<void(double*, int)> allreduce_dev;  // device scalars summed over ranks
 };
 
 // smoother.cpp:86-99 (inverse diagonal with "zero diagonal at row i"; Arnoldi rho for

@@ -12,10 +12,14 @@ from paper_1403_1649_b200 import _abi  # noqa: E402
 from paper_1403_1649_b200 import aggmg as M  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+kind = sys.argv[2] if len(sys.argv) > 2 else "poisson"
 lib = M.b200().lib
 assert lib.fn("init")(0) == 0
 dm = C.c_void_p()
-assert lib.fn("dmatrix_poisson")(3, n, n, n, 1.0, -1, C.byref(dm)) == 0
+if kind == "jump27":
+    assert lib.fn("dmatrix_jump27")(n, n, n, 1e6, 32, C.byref(dm)) == 0
+else:
+    assert lib.fn("dmatrix_poisson")(3, n, n, n, 1.0, -1, C.byref(dm)) == 0
 s = M.SetupConfig(alpha=0.5, reuse_caches=True)._c()
 c = M.CycleConfig()._c()
 v = M.SolverConfig(method=M.PCG, tol=1e-8, max_iters=500)._c()
