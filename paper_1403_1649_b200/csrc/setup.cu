@@ -140,7 +140,9 @@ __global__ void k_mis_pass1(const idx* __restrict__ rp, const idx* __restrict__ 
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   Tuple best = load_tuple(cur + i);
-  for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+  const idx k0 = rp[i], k1 = rp[i + 1];
+#pragma unroll 8
+  for (idx k = k0; k < k1; ++k) {  // unrolled: the gathers of a row issue together
     const Tuple t = load_tuple(cur + col[k]);
     if (tuple_less(best, t)) best = t;
   }
@@ -155,7 +157,9 @@ __global__ void k_mis_pass2(const idx* __restrict__ rp, const idx* __restrict__ 
   int decided = 0;
   if (i < n && state[i] == 0) {
     Tuple far = load_tuple(mid + i);
-    for (idx k = rp[i]; k < rp[i + 1]; ++k) {
+    const idx k0 = rp[i], k1 = rp[i + 1];
+#pragma unroll 8
+    for (idx k = k0; k < k1; ++k) {
       const Tuple t = load_tuple(mid + col[k]);
       if (tuple_less(far, t)) far = t;
     }
