@@ -326,6 +326,10 @@ int aggmg_dist_setup(aggmg_comm* c, const aggmg_dist_matrix* A0, const double* B
 int aggmg_dist_solve(aggmg_dist_hierarchy* h, const aggmg_cycle_config* cycle,
                      const aggmg_solver_config* cfg, const double* b_local, double* x_local,
                      aggmg_solve_report* report);
+/* refresh_values (hierarchy.hpp:64) over the ranks: new values of this rank's level-0 rows
+ * (same pattern); needs a hierarchy set up with reuse_caches */
+int aggmg_dist_refresh_values(aggmg_dist_hierarchy* h, const double* new_values_local,
+                              int64_t count);
 /* z = M r on this rank's rows (apply_preconditioner, cycles.hpp:42) */
 int aggmg_dist_apply_preconditioner(aggmg_dist_hierarchy* h, const aggmg_cycle_config* cycle,
                                     const double* r_local, double* z_local);

@@ -183,6 +183,7 @@ SIGNATURES = {
     "dist_setup": (I, [vp, vp, f64p, C.POINTER(SetupConfigC), L, C.POINTER(vp)]),
     "dist_solve": (I, [vp, C.POINTER(CycleConfigC), C.POINTER(SolverConfigC), f64p, f64p,
                        C.POINTER(SolveReportC)]),
+    "dist_refresh_values": (I, [vp, f64p, L]),
     "dist_apply_preconditioner": (I, [vp, C.POINTER(CycleConfigC), f64p, f64p]),
     "dist_hierarchy_info": (I, [vp, i64p, i64p, f64p]),
     "dist_hierarchy_level_size": (I, [vp, L, i64p, i64p]),

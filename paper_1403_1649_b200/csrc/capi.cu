@@ -1178,6 +1178,16 @@ int aggmg_dist_solve(aggmg_dist_hierarchy* h, const aggmg_cycle_config* cycle,
   });
 }
 
+int aggmg_dist_refresh_values(aggmg_dist_hierarchy* h, const double* new_values_local, int64_t count) {
+  return guarded([&] {
+    DistHierarchy& H = dh(h);
+    require(count == h->A0->A.nnz, "refresh_values: value count does not match this rank's rows");
+    DevBuf<double> v(count);
+    v.upload(new_values_local, count);
+    dist_refresh_values(H, v.get());
+  });
+}
+
 int aggmg_dist_apply_preconditioner(aggmg_dist_hierarchy* h, const aggmg_cycle_config* cycle,
                                     const double* r_local, double* z_local) {
   return guarded([&] {

@@ -16,6 +16,17 @@
 
 namespace aggmg_b200 {
 
+// What refresh_values needs to redo this level's Galerkin product with new values: the cached
+// sort over the extended row set, its column weights, and which local entries travel where.
+struct DistGalerkin {
+  GalerkinDev gal;
+  DevCsrPtr Aext;
+  DevBuf<double> pvc;
+  DevBuf<idx> exrow, exoff;  // exported rows (destination order) and their entry offsets
+  int64_t nexp = 0, nie = 0;
+  std::vector<int64_t> ent_cnt;  // exported entries per destination rank
+};
+
 struct DistLevel {
   DistCsrPtr A;       // this level's operator (rows = cols partition)
   DevBuf<double> B;   // near-null-space vector, owned rows
@@ -32,6 +43,7 @@ struct DistLevel {
   DevBuf<double> r, t;
   DevBuf<double> rc, xc, c, v, rt, d, w;  // level k+1 vectors (owned + halo)
   DevBuf<KScalars> ks;
+  std::unique_ptr<DistGalerkin> galc;  // kept when SetupConfig::reuse_caches
 };
 
 struct DistHierarchy {
@@ -41,6 +53,7 @@ struct DistHierarchy {
   int64_t agglomerate_rows = 0;
   std::vector<DistLevel> levels;       // distributed levels 0..kd-1
   Partition tail_rows;                 // row partition of level kd before the gather
+  DistCsrPtr tail_A;                   // level kd's rows on this rank (refresh_values)
   int64_t tail_halo_cap = 0;           // halo slots the level-kd vectors need (P of level kd-1)
   std::unique_ptr<DevHierarchy> tail;  // rank 0 only: global levels kd..
   int64_t n_levels_total = 0;          // global level count (same on every rank)
@@ -63,6 +76,10 @@ struct DistHierarchy {
 
 // Collective over comm: every rank passes its own rows [A0.rows.begin(me), ...).
 // B0_local == nullptr means ones.
+// refresh_values (hierarchy.cpp:90-104) on the ranks: new values of level 0's local rows, the
+// cached Galerkin products and smoothers redone level by level (needs reuse_caches).
+void dist_refresh_values(DistHierarchy& h, const double* new_values_local);
+
 std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0,
                                                     const double* B0_local, const SetupCfg& cfg,
                                                     int64_t agglomerate_rows);

@@ -525,6 +525,14 @@ __global__ void k_ext_entries(const EntRec* ent, const idx* jc, int64_t nie, int
   asg[next + t] = jc[t];
   pvc[next + t] = ent[t].pvc;
 }
+__global__ void k_pack_row_values(const idx* rows, int64_t m, const idx* off, const idx* rp,
+                                  const double* val, double* out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const idx i = rows[k];
+  idx p = off[k];
+  for (idx e = rp[i]; e < rp[i + 1]; ++e) out[p++] = val[e];
+}
 __global__ void k_ext_len(const idx* rp, int64_t nloc, int64_t ntot, const idx* ilen, int64_t m, idx* len) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < nloc)
@@ -946,6 +954,18 @@ Coarsened coarsen_level(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k
   GalerkinDev gal = build_galerkin_cache(*Aext, gx, true);
   DevCsrPtr Acg = apply_galerkin_cache(gal, *Aext, pvc_ext.get());
   Acg->n_cols = cpart.n();
+  if (cfg.reuse_caches) {  // keep what refresh_values needs (galerkin.cpp:98-137 reuse)
+    auto gc = std::make_unique<DistGalerkin>();
+    gc->gal = std::move(gal);
+    gc->Aext = Aext;
+    gc->pvc = std::move(pvc_ext);
+    gc->exrow = std::move(exrow_s);
+    gc->exoff = std::move(exoff);
+    gc->nexp = nexp;
+    gc->nie = nie;
+    gc->ent_cnt = ent_cnt;
+    L.galc = std::move(gc);
+  }
   phase("galerkin");
   out.Ac = make_dist(comm, cpart, cpart, *Acg);
   phase("coarse-plan");
@@ -1030,6 +1050,7 @@ std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, c
   phase("levels");
   // agglomerate level kd onto rank 0 and continue with the one-GPU setup there
   h->tail_rows = A->rows;
+  h->tail_A = A;
   DevCsrPtr Ag = gather_to_root(comm, *A, 0);
   DevBuf<double> Bg(me == 0 ? A->rows.n() : 0);
   gather_vector(comm, A->rows, B.get(), Bg.get(), 0);
@@ -1068,6 +1089,60 @@ std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, c
   comm.barrier();
   h->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return h;
+}
+
+}  // namespace aggmg_b200
+
+namespace aggmg_b200 {
+
+void dist_refresh_values(DistHierarchy& h, const double* new_values_local) {
+  Comm& comm = *h.comm;
+  require(h.cfg.reuse_caches, "refresh_values: hierarchy was built without caches; rebuild it");
+  DistCsr& A0 = h.kd() ? *h.levels[0].A : *h.tail_A;
+  copy_double(A0.A.val.get(), new_values_local, A0.A.nnz);
+  for (int64_t k = 0; k < h.kd(); ++k) {
+    DistLevel& L = h.levels[k];
+    DistGalerkin& g = *L.galc;
+    const DevCsr& A = L.A->A;
+    // the exported rows' new values travel to their aggregates' owners, as in setup
+    int64_t nent = 0;
+    for (int64_t c : g.ent_cnt) nent += c;
+    DevBuf<double> send(std::max<int64_t>(nent, 1));
+    if (g.nexp)
+      AGG_LAUNCH(k_pack_row_values, grid_for(g.nexp, 256), 256, 0, g.exrow.get(), g.nexp, g.exoff.get(),
+                 A.rowptr.get(), A.val.get(), send.get());
+    DevBuf<double> recv = alltoallv<double>(comm, send.get(), g.ent_cnt);
+    require(recv.size() == g.nie, "refresh_values: imported entry count changed");
+    if (A.nnz)
+      AGG_CUDA(cudaMemcpyAsync(g.Aext->val.get(), A.val.get(), sizeof(double) * A.nnz,
+                               cudaMemcpyDeviceToDevice, stream()));
+    if (g.nie)
+      AGG_CUDA(cudaMemcpyAsync(g.Aext->val.get() + A.nnz, recv.get(), sizeof(double) * g.nie,
+                               cudaMemcpyDeviceToDevice, stream()));
+    DevCsrPtr Ac = apply_galerkin_cache(g.gal, *g.Aext, g.pvc.get());
+    DistCsr& next = (k + 1 < h.kd()) ? *h.levels[k + 1].A : *h.tail_A;
+    require(Ac->nnz == next.A.nnz, "refresh_values: coarse pattern changed");
+    copy_double(next.A.val.get(), Ac->val.get(), Ac->nnz);
+    dist_smoother(comm, L, h.cfg, k);
+  }
+  // the agglomerated tail: gather level kd's new values (row order = rank order) to rank 0
+  const std::vector<int64_t> cnt = comm.allgather_host({h.tail_A->A.nnz});
+  DevBuf<double> all;
+  std::vector<CommMsg> s, r;
+  s.push_back({0, h.tail_A->A.val.get(), sizeof(double) * h.tail_A->A.nnz});
+  if (comm.rank() == 0) {
+    int64_t tot = 0;
+    for (int64_t c : cnt) tot += c;
+    all.resize(tot);
+    int64_t off = 0;
+    for (int q = 0; q < comm.size(); ++q) {
+      r.push_back({q, all.get() + off, sizeof(double) * cnt[q]});
+      off += cnt[q];
+    }
+  }
+  comm.exchange(s, r);
+  if (comm.rank() == 0) refresh_values(*h.tail, all.get());
+  comm.barrier();
 }
 
 }  // namespace aggmg_b200

@@ -230,6 +230,11 @@ class DistHierarchy:
                                           hist[: rep.history_length].tolist(), 0.0,
                                           rep.solve_seconds, rep.note.decode()))
 
+    def refresh_values(self, new_values_local) -> None:
+        """refresh_values (hierarchy.hpp:64): new values of this rank's level-0 rows."""
+        v = _f64(new_values_local)
+        _check(_lib().fn("dist_refresh_values")(self._h, _p(v, _abi.f64p), v.shape[0]))
+
     def apply_preconditioner(self, r_local, cycle: Optional[CycleConfig] = None) -> np.ndarray:
         r = _f64(r_local)
         z = np.zeros_like(r)

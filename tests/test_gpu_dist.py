@@ -215,3 +215,34 @@ def test_dist_preconditioner_matches_one_gpu(gpu, P):
         assert np.array_equal(z.view(np.uint64), zg.view(np.uint64))
     else:
         assert np.max(np.abs(z - zg)) <= 1e-12 * np.max(np.abs(zg))
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_dist_refresh_values_matches_one_gpu(gpu, P):
+    """refresh_values on the ranks == refresh_values on one GPU (hierarchy.cpp:90-104)."""
+    A = gpu.generate_poisson(3, 18, 17, 16, 0.3)
+    cfg = M.SetupConfig(alpha=0.5, reuse_caches=True, coarse_size_max=40)
+    rng = np.random.default_rng(4)
+    newv = A.values * rng.uniform(0.5, 1.5, A.values.shape[0])  # same pattern, new values
+    Anew = M.SparseMatrix(A.n_rows, A.n_cols, A.row_offsets, A.col_indices, newv)
+    hg = gpu.setup_hierarchy(A, None, cfg)
+    hg = gpu.refresh_values(hg, newv)
+    out = {}
+
+    def fn(comm, r):
+        dA = D.DistMatrix.from_global(comm, A)
+        h = D.setup(comm, dA, cfg, agglomerate_rows=120)
+        _, row0, nloc, _ = dA.info()
+        lo, hi = A.row_offsets[row0], A.row_offsets[row0 + nloc]
+        h.refresh_values(newv[lo:hi])
+        res = {"levels": []}
+        for k in range(h.n_levels()):
+            res["levels"].append((h.level_A(k), h.level_transfer(k) if k + 1 < h.n_levels() else None,
+                                  h.level_B(k), h.level_omega(k)))
+        out[r] = res
+        h.free()
+        dA.free()
+
+    D.run_threads(P, fn)
+    compare_hierarchy(hg, out, f"refresh P={P}")
+    del Anew
