@@ -568,6 +568,8 @@ def main():
                     help="rows at or below which a level is gathered on rank 0 (0 = default)")
     ap.add_argument("--emulate-ranks", type=int, default=0)
     args = ap.parse_args()
+    # NCCL writes its banner/debug lines to stdout by default; keep stdout for the JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference_arm(args, world, rank)
