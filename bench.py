@@ -568,8 +568,13 @@ def main():
                     help="rows at or below which a level is gathered on rank 0 (0 = default)")
     ap.add_argument("--emulate-ranks", type=int, default=0)
     args = ap.parse_args()
-    # NCCL writes its banner/debug lines to stdout by default; keep stdout for the JSON line
+    # Native libraries (NCCL's version banner, driver messages) write to fd 1; point fd 1 at
+    # stderr and keep the real stdout for the JSON line alone.
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    sys.stdout.flush()
+    real_stdout = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(real_stdout, "w", buffering=1)
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference_arm(args, world, rank)
