@@ -316,7 +316,7 @@ int aggmg_dist_matrix_info(const aggmg_dist_matrix* A, int64_t* n_global, int64_
 void aggmg_dist_matrix_free(aggmg_dist_matrix* A);
 
 /* setup_hierarchy (hierarchy.hpp:57) over the ranks; B0_local (host, this rank's rows) may be
- * NULL = ones; agglomerate_rows <= 0 picks the default (max(coarse_size_max, 2^20): coarse levels below ~1 M rows are
+ * NULL = ones; agglomerate_rows <= 0 picks the default (max(coarse_size_max, 2^22): coarse levels below ~4 M rows are
  * latency-bound, one GPU runs them faster than exchanging halos for them) */
 int aggmg_dist_setup(aggmg_comm* c, const aggmg_dist_matrix* A0, const double* B0_local,
                      const aggmg_setup_config* cfg, int64_t agglomerate_rows,

@@ -1148,7 +1148,7 @@ int aggmg_dist_setup(aggmg_comm* c, const aggmg_dist_matrix* A0, const double* B
     DevBuf<double> B;
     if (B0_local) B = up_vec(B0_local, A0->A->A.n_rows);
     const SetupCfg s = to_cfg(cfg);
-    if (agglomerate_rows <= 0) agglomerate_rows = std::max<int64_t>(s.coarse_size_max, int64_t{1} << 20);
+    if (agglomerate_rows <= 0) agglomerate_rows = std::max<int64_t>(s.coarse_size_max, int64_t{1} << 22);
     auto h = std::make_unique<aggmg_dist_hierarchy>();
     h->comm = &comm;
     h->A0 = A0->A;
