@@ -284,13 +284,18 @@ CoarseWork work_of(DevLevel& L) {
 void subcycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b, double* x_out,
               const int* pred, bool vee);
 
-bool graphs_enabled() {
+}  // namespace
+
+bool cycle_graphs_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("AGGMG_GRAPHS");
     return !(e && e[0] == '0');
   }();
   return on;
 }
+
+namespace {
+bool graphs_enabled() { return cycle_graphs_enabled(); }
 
 // The sub-cycle below level 0 is a fixed kernel sequence over fixed buffers (device
 // predicates steer the K-cycle branches), so it is captured once per (config, level,
@@ -306,7 +311,10 @@ void subcycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b, 
     else
       inner_cycle_eager(h, cfg, k, b, x_out, pred);
   };
-  if (k != 1 || !graphs_enabled() || k == h.coarsest()) {
+  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+  AGG_CUDA(cudaStreamIsCapturing(stream(), &capturing));
+  // (inside a caller's capture — the partitioned cycle's graphs — run eagerly: it is recorded)
+  if (k != 1 || !graphs_enabled() || k == h.coarsest() || capturing != cudaStreamCaptureStatusNone) {
     eager();
     return;
   }

@@ -49,6 +49,7 @@ void launch_kflag(KScalars* ks, double t, const int* pred);
 void launch_kcombine(int64_t n, const double* c, const double* d, double* xc, const KScalars* ks,
                      const int* pred, int level);
 bool cycle_accelerated(const CycleCfg& cfg, int64_t k);  // cycles.cpp:16-20
+bool cycle_graphs_enabled();  // AGGMG_GRAPHS != 0
 
 // dense coarse solve x = A_L^{-1} b
 void coarse_solve(DevHierarchy& h, const double* b, double* x, const int* pred);

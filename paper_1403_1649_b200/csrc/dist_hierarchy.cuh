@@ -7,6 +7,7 @@
 // as an ordinary DevHierarchy whose level 0 is global level kd (SetupCfg::level_offset).
 #pragma once
 
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -65,6 +66,9 @@ struct DistHierarchy {
   DevBuf<double> tail_b, tail_x;
   DevBuf<double> tail_work_c, tail_work_v, tail_work_rt, tail_work_d, tail_work_w;
   DevBuf<KScalars> tail_ks;
+  // captured sub-cycles of the distributed levels (NCCL or one rank: no host rendezvous)
+  std::vector<std::pair<std::string, cudaGraphExec_t>> graphs;
+  std::map<std::string, int64_t> graph_kernels;
   // PCG hook (see DevHierarchy::top_dot_*): fused (r.z, r_old.z) on the last level-0 sweep
   const double* top_dot_c = nullptr;
   double* top_dot_out = nullptr;
@@ -72,6 +76,7 @@ struct DistHierarchy {
 
   int64_t kd() const { return static_cast<int64_t>(levels.size()); }
   void ensure_workspace();
+  void drop_graphs();
 };
 
 // Collective over comm: every rank passes its own rows [A0.rows.begin(me), ...).

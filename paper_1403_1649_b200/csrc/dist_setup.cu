@@ -1000,7 +1000,14 @@ void dist_smoother(Comm& comm, DistLevel& L, const SetupCfg& cfg, int64_t k) {
 
 }  // namespace
 
-DistHierarchy::~DistHierarchy() = default;
+DistHierarchy::~DistHierarchy() { drop_graphs(); }
+
+void DistHierarchy::drop_graphs() {
+  for (auto& g : graphs)
+    if (g.second) cudaGraphExecDestroy(g.second);
+  graphs.clear();
+  graph_kernels.clear();
+}
 
 std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, const double* B0_local,
                                                     const SetupCfg& cfg, int64_t agglomerate_rows) {
@@ -1098,6 +1105,7 @@ namespace aggmg_b200 {
 void dist_refresh_values(DistHierarchy& h, const double* new_values_local) {
   Comm& comm = *h.comm;
   require(h.cfg.reuse_caches, "refresh_values: hierarchy was built without caches; rebuild it");
+  h.drop_graphs();  // the smoother arrays are rebuilt below; captured pointers would dangle
   DistCsr& A0 = h.kd() ? *h.levels[0].A : *h.tail_A;
   copy_double(A0.A.val.get(), new_values_local, A0.A.nnz);
   for (int64_t k = 0; k < h.kd(); ++k) {

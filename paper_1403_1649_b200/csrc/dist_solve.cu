@@ -7,6 +7,8 @@
 // so on one rank the partitioned solve is bit-identical to the one-GPU solve, and on R
 // ranks it differs only by the summation order of the dot products.
 #include <algorithm>
+#include <cstdio>
+#include <string>
 
 #include "dist_solve.cuh"
 #include "primitives.cuh"
@@ -61,6 +63,56 @@ namespace {
 
 void dist_cycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, const double* b,
                 double* x, const int* pred);
+void dist_subcycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, const double* b,
+                   double* x, const int* pred);
+
+// A sub-cycle of a distributed level, captured into a CUDA graph on its second use and replayed
+// afterwards (first use eager), keyed by level, cycle kind and buffers.  Only when no exchange
+// needs the host: one rank, or NCCL (its send/recv/allgather capture as graph nodes);
+// in-process rank threads rendezvous on the host and stay eager.
+void dist_subcycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, const double* b,
+                   double* x, const int* pred) {
+  Comm& comm = *h.comm;
+  const bool capturable = cycle_graphs_enabled() && (comm.size() == 1 || std::string(comm.kind()) == "nccl");
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  AGG_CUDA(cudaStreamIsCapturing(stream(), &cap));
+  if (!capturable || cap != cudaStreamCaptureStatusNone) {
+    dist_cycle(h, cfg, k, kc, b, x, pred);
+    return;
+  }
+  char keybuf[256];
+  std::snprintf(keybuf, sizeof(keybuf), "%d/%d/%d/%.17g/%d/%lld/%p/%p/%p", kc ? 1 : 0, cfg.kind,
+                cfg.k_levels, cfg.t, cfg.inner, static_cast<long long>(k), static_cast<const void*>(b),
+                static_cast<void*>(x), static_cast<const void*>(pred));
+  const std::string key(keybuf);
+  for (auto& g : h.graphs)
+    if (g.first == key) {
+      if (!g.second) {  // second use: capture
+        AGG_CUDA(cudaStreamBeginCapture(stream(), cudaStreamCaptureModeThreadLocal));
+        const int64_t before = launch_count();
+        try {
+          dist_cycle(h, cfg, k, kc, b, x, pred);
+        } catch (...) {
+          cudaGraph_t junk = nullptr;
+          cudaStreamEndCapture(stream(), &junk);
+          if (junk) cudaGraphDestroy(junk);
+          throw;
+        }
+        const int64_t kernels = launch_count() - before;
+        cudaGraph_t graph;
+        AGG_CUDA(cudaStreamEndCapture(stream(), &graph));
+        AGG_CUDA(cudaGraphInstantiate(&g.second, graph, 0));
+        AGG_CUDA(cudaGraphDestroy(graph));
+        note_launches(-kernels);  // counted again on every replay below
+        h.graph_kernels[key] = kernels;
+      }
+      AGG_CUDA(cudaGraphLaunch(g.second, stream()));
+      note_launches(h.graph_kernels[key]);
+      return;
+    }
+  h.graphs.emplace_back(key, nullptr);  // first use: eager
+  dist_cycle(h, cfg, k, kc, b, x, pred);
+}
 
 // coarse half of a visit of distributed level k (cycles.cpp:56-132)
 void dist_coarse(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kparent, const int* pred) {
@@ -78,14 +130,14 @@ void dist_coarse(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kparent,
   }
   DistLevel& C = h.levels[k + 1];
   if (!kparent) {  // V-cycle below a V-cycle
-    dist_cycle(h, cfg, k + 1, false, L.rc.get(), L.xc.get(), pred);
+    dist_subcycle(h, cfg, k + 1, false, L.rc.get(), L.xc.get(), pred);
     return;
   }
   const int64_t nc = C.A->A.n_rows;
   const bool cg = cfg.inner == 0;
   const bool inner_k = cycle_accelerated(cfg, k + 1);
   const int level = static_cast<int>(k + 1);
-  dist_cycle(h, cfg, k + 1, inner_k, L.rc.get(), L.c.get(), pred);
+  dist_subcycle(h, cfg, k + 1, inner_k, L.rc.get(), L.c.get(), pred);
   SpmvArgs a1;  // v = Ac c ; rho1, alpha1
   a1.x = L.c.get();
   a1.y = L.v.get();
@@ -99,7 +151,7 @@ void dist_coarse(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kparent,
   comm.allreduce_sum(&L.ks.get()->nrt, 2);
   launch_kflag(L.ks.get(), cfg.t, pred);
   const int* p2 = &L.ks.get()->flag2;
-  dist_cycle(h, cfg, k + 1, inner_k, L.rt.get(), L.d.get(), p2);
+  dist_subcycle(h, cfg, k + 1, inner_k, L.rt.get(), L.d.get(), p2);
   SpmvArgs a2;  // w = Ac d ; gamma, beta, alpha2
   a2.x = L.d.get();
   a2.y = L.w.get();

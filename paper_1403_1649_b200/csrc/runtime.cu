@@ -156,7 +156,9 @@ size_t size_class(size_t b) {  // 1 MB granularity keeps near-equal requests in 
 void* dev_alloc(size_t bytes) {
   ensure_init();
   BlockCache& c = bcache();
-  if (c.enabled && bytes >= kCacheMin) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream(), &cap);  // a captured allocation must stay a graph node
+  if (c.enabled && bytes >= kCacheMin && cap == cudaStreamCaptureStatusNone) {
     const size_t sc = size_class(bytes);
     auto it = c.free_by_size.find(sc);
     if (it != c.free_by_size.end() && !it->second.empty()) {
