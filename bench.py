@@ -331,7 +331,7 @@ def run_b200(args, world, rank, local):
     roof = None
     if jc > 0:
         achieved = (jb / jc) / ((jt / jc) / 1e3) / 1e9
-        traffic = load_traffic().get(args.config, {}).get("jacobi_l0_dram_bytes_per_launch")
+        traffic = load_traffic().get(args.config, {}).get("jacobidot2_l0_dram_bytes_per_launch")
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": ("k_csr_stream<Epi::kJacobiDot2> on level 0: the fused damped-Jacobi "
