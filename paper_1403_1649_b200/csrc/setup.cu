@@ -178,6 +178,60 @@ __global__ void k_mis_pass2(const idx* __restrict__ rp, const idx* __restrict__ 
   if ((threadIdx.x & 31) == 0 && ballot) atomicSub(&ctl->undecided, __popc(ballot));
 }
 
+// ---- MIS(2) late sweeps on the undecided set -----------------------------------------------
+// After the first sweeps most nodes are decided, but the two full passes still visit every
+// row.  far_i = max over j in {i} u N(i) of max over l in {j} u N(j) of T_l, so an undecided
+// node can read its two-hop neighbourhood directly; once fewer than a quarter of the nodes are
+// undecided the sweeps run over a compact list of them: decide (reading the sweep's snapshot),
+// then apply and re-compact.  Same decisions, same sweep count.
+struct MisList {
+  int count;      // entries in the current list
+  int next;       // entries appended to the next list
+  int undecided;  // global undecided count (== count between sweeps)
+  int sweeps;
+};
+__global__ void k_mis_list_init(const int8_t* state, int64_t n, idx* list, MisList* ml) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && state[i] == 0) list[atomicAdd(&ml->count, 1)] = static_cast<idx>(i);
+}
+__global__ void k_mis_2hop(const idx* __restrict__ rp, const idx* __restrict__ col,
+                           const Tuple* cur, const idx* list, const MisList* ml, int8_t* dec) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ml->undecided == 0 || t >= ml->count) return;
+  const idx i = list[t];
+  Tuple far = load_tuple(cur + i);
+  for (idx a = rp[i] - 1; a < rp[i + 1]; ++a) {  // j = i, then the neighbours
+    const idx j = a < rp[i] ? i : col[a];
+    const Tuple tj = load_tuple(cur + j);
+    if (tuple_less(far, tj)) far = tj;
+    for (idx k = rp[j]; k < rp[j + 1]; ++k) {
+      const Tuple tl = load_tuple(cur + col[k]);
+      if (tuple_less(far, tl)) far = tl;
+    }
+  }
+  dec[t] = (far.i == static_cast<int>(i)) ? 1 : (far.s == 1 ? -1 : 0);
+}
+__global__ void k_mis_list_apply(const idx* list, MisList* ml, const int8_t* dec, Tuple* cur,
+                                 int8_t* state, idx* next_list) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ml->undecided == 0 || t >= ml->count) return;
+  const idx i = list[t];
+  const int8_t d = dec[t];
+  if (d != 0) {
+    state[i] = d;
+    cur[i].s = d;
+  } else {
+    next_list[atomicAdd(&ml->next, 1)] = i;
+  }
+}
+__global__ void k_mis_list_swap(MisList* ml) {
+  if (ml->undecided == 0) return;
+  ml->sweeps += 1;
+  ml->count = ml->next;
+  ml->undecided = ml->next;
+  ml->next = 0;
+}
+
 // ---- a7 aggregation ------------------------------------------------------------------------
 // rep[i] = representative node of i's aggregate after pass 1 (roots: themselves).
 __global__ void k_agg_pass1(const idx* rp, const idx* col, int64_t n, const int8_t* state,
@@ -946,9 +1000,37 @@ Mis2Dev mis2(const DevCsr& S, const idx* influence, uint64_t seed) {
     if (h.sweeps > n) throw Error("mis2: failed to decide all nodes");
     if (h.undecided == 0) {
       res.sweeps = h.sweeps;
-      break;
+      return res;
     }
     batch = 4;
+    if (static_cast<double>(h.undecided) < 0.25 * static_cast<double>(n)) {
+      // late sweeps over the compact undecided list
+      DevBuf<idx> la(h.undecided), lb(h.undecided);
+      DevBuf<int8_t> dec(h.undecided);
+      DevBuf<MisList> ml(1);
+      MisList m0{0, 0, h.undecided, h.sweeps};
+      ml.upload(&m0, 1);
+      AGG_LAUNCH(k_mis_list_init, g, 256, 0, res.state.get(), n, la.get(), ml.get());
+      const unsigned gl = grid_for(h.undecided, 128);
+      idx* cur_list = la.get();
+      idx* nxt_list = lb.get();
+      while (true) {
+        for (int b = 0; b < batch; ++b) {
+          AGG_LAUNCH(k_mis_2hop, gl, 128, 0, S.rowptr.get(), S.col.get(), cur.get(), cur_list, ml.get(),
+                     dec.get());
+          AGG_LAUNCH(k_mis_list_apply, gl, 128, 0, cur_list, ml.get(), dec.get(), cur.get(),
+                     res.state.get(), nxt_list);
+          AGG_LAUNCH(k_mis_list_swap, 1, 1, 0, ml.get());
+          std::swap(cur_list, nxt_list);
+        }
+        const MisList hm = read_scalar(ml.get());
+        if (hm.sweeps > n) throw Error("mis2: failed to decide all nodes");
+        if (hm.undecided == 0) {
+          res.sweeps = hm.sweeps;
+          return res;
+        }
+      }
+    }
   }
   return res;
 }
