@@ -18,7 +18,7 @@ constexpr int kChunk = 8192;  // vector_ops.hpp:18
 // warps 1..3 produce tiles (elementwise op + products) into a double buffer.
 constexpr int kChunkThreads = 128;
 constexpr int kChunkProducers = kChunkThreads - 32;
-constexpr int kChunkTile = 8 * kChunkProducers;  // 768 elements per stage
+constexpr int kChunkTile = 4 * kChunkProducers;  // 384 elements per stage: 12 KB, 16 CTAs per SM
 
 // Process-wide switch for the solve-phase reductions: exact (reference order) or tree
 // (default).  The smoother setup and the public dot/norm2 always use the exact order.
@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(kChunkThreads)
       if (lane < NP) {
         const int m = min(kChunkTile, len - t * kChunkTile);
         const double* src = tile[b][lane];
+        // (the chain is bound by the fp64 add latency, ~10 cycles: 8192 adds ~ 45 us per
+        // chunk; software-pipelining the smem loads measured no faster)
         int q = 0;
         for (; q + 8 <= m; q += 8) {
           const double2 a = *reinterpret_cast<const double2*>(src + q);
