@@ -1104,7 +1104,7 @@ TransferDev build_transfer(const AggDev& agg, const double* fine_b) {
   return t;
 }
 
-GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial) {
+GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial, bool fingerprint) {
   require(partial || A.n_rows == A.n_cols, "galerkin: matrix must be square");
   require(agg.n_fine == A.n_rows, "galerkin: aggregation size mismatch");
   const int64_t nc = agg.n_agg;
@@ -1174,7 +1174,7 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
   AGG_CUDA(cudaMemcpyAsync(g.segment_offsets.get() + g.nnz_coarse, &nnz32, sizeof(idx),
                            cudaMemcpyHostToDevice, stream()));
   sync();  // nnz32 lives on the host stack
-  if (!partial) g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
+  if (!partial && fingerprint) g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
   return g;
 }
 

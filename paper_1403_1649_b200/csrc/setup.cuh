@@ -59,7 +59,10 @@ struct GalerkinDev {
 };
 // partial: the groups cover only some rows of A (rows of other groups, and halo rows, are
 // skipped; the row-partitioned setup's extended row set) — no coverage check, no fingerprint.
-GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial = false);
+// fingerprint: the pattern hash apply_galerkin_cache checks for a caller-supplied A (galerkin.cpp:
+// 18-29, 101-103); a hierarchy applies its cache to its own stored operator and skips it.
+GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial = false,
+                                 bool fingerprint = true);
 // Ac values for the cached pattern.  pval: per fine row P weight.
 DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const double* pval);
 uint64_t pattern_fingerprint(const DevCsr& A, const idx* assignment);
