@@ -364,7 +364,8 @@ int aggmg_bench_dot(int64_t n, int np, int exact, int reps, double* avg_ms);
 int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* bytes);
 /* same for one CSR-stream variant: 0 spmv, 1 residual, 2 fused zero-guess Jacobi+residual,
  * 3 damped-Jacobi sweep, 4 spmv + dot, 5 spmv scaled by the inverse diagonal,
- * 6 damped-Jacobi sweep + the two fused PCG dots */
+ * 6 damped-Jacobi sweep + the two fused PCG dots, 7 one level-scheduled symmetric Gauss-Seidel
+ * smooth (forward + backward) */
 int aggmg_bench_kernel(const aggmg_dmatrix* A, int kind, int reps, double* avg_ms, double* bytes);
 
 #ifdef __cplusplus

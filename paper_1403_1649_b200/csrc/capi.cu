@@ -576,6 +576,7 @@ int aggmg_smooth(int kind, const double* inv_diag, double omega, const aggmg_csr
     vec_scale_into(n, kind == AGGMG_SMOOTHER_JACOBI ? 1.0 : omega, s.inv_diag.get(), s.wdiag.get());
     auto db = up_vec(b, n), dx = up_vec(x, n);
     if (kind == AGGMG_SMOOTHER_SGS) {
+      build_sgs_schedule(*dA, s);
       smooth_sgs(s, *dA, db.get(), dx.get());
       dx.download(x, n);
     } else {
@@ -995,7 +996,32 @@ int aggmg_bench_spmv(const aggmg_dmatrix* A, int reps, double* avg_ms, double* b
 int aggmg_bench_kernel(const aggmg_dmatrix* A, int kind, int reps, double* avg_ms, double* bytes) {
   return guarded([&] {
     const DevCsr& M = *A->A;
-    require(kind >= 0 && kind <= 6, "bench_kernel: kind must be 0..6");
+    require(kind >= 0 && kind <= 7, "bench_kernel: kind must be 0..7");
+    if (kind == 7) {  // one symmetric Gauss-Seidel smooth (both directions, level-scheduled)
+      SmootherDev s;
+      s.kind = AGGMG_SMOOTHER_SGS;
+      s.inv_diag.resize(M.n_rows);
+      fill_double(s.inv_diag.get(), M.n_rows, 0.25);
+      build_sgs_schedule(M, s);
+      DevBuf<double> b(M.n_rows), x(M.n_rows);
+      fill_double(b.get(), M.n_rows, 1.0);
+      fill_double(x.get(), M.n_rows, 0.0);
+      smooth_sgs(s, M, b.get(), x.get());
+      cudaEvent_t e0, e1;
+      AGG_CUDA(cudaEventCreate(&e0));
+      AGG_CUDA(cudaEventCreate(&e1));
+      AGG_CUDA(cudaEventRecord(e0, stream()));
+      for (int r = 0; r < reps; ++r) smooth_sgs(s, M, b.get(), x.get());
+      AGG_CUDA(cudaEventRecord(e1, stream()));
+      AGG_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      AGG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      *avg_ms = ms / reps;
+      *bytes = 2.0 * (12.0 * M.nnz + 40.0 * M.n_rows);  // per direction: A + b, inv, x in/out
+      return;
+    }
     const Epi epis[7] = {Epi::kSpmv, Epi::kResidual, Epi::kResidualZero, Epi::kJacobi,
                          Epi::kSpmvDot1, Epi::kScaleDiag, Epi::kJacobiDot2};
     const Epi epi = epis[kind];

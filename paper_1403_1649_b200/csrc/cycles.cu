@@ -207,7 +207,7 @@ void presmooth(DevLevel& L, const double* b, const double* x_in, double* x_out, 
       AGG_LAUNCH(k_copy, egrid(n), kB, 0, n, x_in, x_out, pred);
     else
       fill_double(x_out, n, 0.0);
-    smooth_sgs(L.smoother, *L.A, b, x_out);
+    smooth_sgs(L.smoother, *L.A, b, x_out, pred);
     return;
   }
   if (x_in)
@@ -222,7 +222,7 @@ void postsmooth(DevHierarchy& h, DevLevel& L, const double* b, double* x, const 
              L.xc.get(), L.t.get(), pred);
   if (L.smoother.kind == 2) {
     AGG_LAUNCH(k_copy, egrid(n), kB, 0, n, L.t.get(), x, pred);
-    smooth_sgs(L.smoother, *L.A, b, x);
+    smooth_sgs(L.smoother, *L.A, b, x, pred);
     return;
   }
   if (top && !pred && h.top_dot_out) {  // PCG's (r.z, r_old.z) ride on the last sweep

@@ -1014,6 +1014,10 @@ std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, c
   require(A0->rows.n() == A0->cols.n(), "setup: matrix must be square");
   require(cfg.coarse_size_max >= 1, "setup: coarse_size_max must be at least 1");
   require(cfg.max_levels >= 1, "setup: max_levels must be at least 1");
+  // sgs is one global sequential sweep (smoother.cpp:105-119): no row partition reproduces it
+  require(cfg.smoother != 2,
+          "setup: the sgs smoother is a global sequential sweep; a row-partitioned hierarchy "
+          "supports jacobi and damped_jacobi");
   const int me = comm.rank();
   comm.barrier();
   const auto t0 = std::chrono::steady_clock::now();

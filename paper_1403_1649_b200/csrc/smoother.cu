@@ -1,6 +1,8 @@
 // smoother.cu — inverse diagonal, Arnoldi spectral-radius estimate, sweeps.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "chunked.cuh"
@@ -25,25 +27,6 @@ __global__ void k_inv_diag(const idx* rp, const idx* col, const double* val, int
     return;
   }
   inv[i] = __ddiv_rn(1.0, d);
-}
-
-// Sequential symmetric Gauss-Seidel (smoother.cpp:105-119): strictly ordered by
-// definition, so one thread walks the rows.
-__global__ void k_sgs(const idx* rp, const idx* col, const double* val, int64_t n,
-                      const double* inv, const double* b, double* x) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  for (int64_t i = 0; i < n; ++i) {
-    double s = b[i];
-    for (idx k = rp[i]; k < rp[i + 1]; ++k)
-      if (col[k] != i) s = __dsub_rn(s, __dmul_rn(val[k], x[col[k]]));
-    x[i] = __dmul_rn(s, inv[i]);
-  }
-  for (int64_t i = n - 1; i >= 0; --i) {
-    double s = b[i];
-    for (idx k = rp[i]; k < rp[i + 1]; ++k)
-      if (col[k] != i) s = __dsub_rn(s, __dmul_rn(val[k], x[col[k]]));
-    x[i] = __dmul_rn(s, inv[i]);
-  }
 }
 
 // One fused MGS step of the Arnoldi column on the device, in the reference's chunked dot
@@ -183,6 +166,7 @@ void setup_smoother(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, Smo
     s.rho_est = estimate_rho(A, s.inv_diag.get(), arnoldi_m, seed, ops);
     s.omega = (4.0 / 3.0) / s.rho_est;
   }
+  if (kind == 2) build_sgs_schedule(A, s);
   const double w = (kind == 0) ? 1.0 : s.omega;  // smoother.cpp:120
   s.wdiag.resize(n);
   if (n > 0)
@@ -198,11 +182,6 @@ void smooth_sweep(const SmootherDev& s, const DevCsr& A, const double* b, const 
   a.d = s.wdiag.get();
   a.pred = pred;
   spmv_run(A, Epi::kJacobi, a, prof);
-}
-
-void smooth_sgs(const SmootherDev& s, const DevCsr& A, const double* b, double* x) {
-  AGG_LAUNCH(k_sgs, 1, 32, 0, A.rowptr.get(), A.col.get(), A.val.get(), A.n_rows,
-             s.inv_diag.get(), b, x);
 }
 
 }  // namespace aggmg_b200

@@ -7,6 +7,26 @@
 
 namespace aggmg_b200 {
 
+// Level schedule of one symmetric Gauss-Seidel direction (sgs.cu; built on the host at
+// setup).  Row i's level is 1 + the highest level of the rows it reads new values from (j < i
+// going forward, j > i going backward); rows of one level are independent.  Slot t = the
+// t-th row in level order; A is stored per slot with the diagonal dropped, the first `ell`
+// entries in an ELL block whose codes say where each x value comes from (sgs.cu).
+struct SgsDirection {
+  int ell = 4, cta = 512;           // ELL width and single-CTA run size
+  DevBuf<int> rows;                 // slot t -> row id
+  DevBuf<int4> rec;                 // slot t: {row, off-diagonal count, 1/A_ii}
+  DevBuf<int> offsets;              // level l = slots [offsets[l], offsets[l+1])
+  std::vector<int64_t> h_offsets;   // host copy
+  DevBuf<uint32_t> code;            // ELL block: codes in uint4 chunks, values in double2
+  DevBuf<double> val;               //   chunks; entries past `ell` continue in
+                                    //   ocol[optr[t], optr[t+1])
+  DevBuf<idx> optr, ocol;
+  DevBuf<double> oval;
+  struct Run { int64_t l0, l1; bool narrow; };
+  std::vector<Run> runs;            // consecutive narrow levels share one single-CTA launch
+};
+
 struct SmootherDev {
   int kind = 1;  // AGGMG_SMOOTHER_*
   DevBuf<double> inv_diag;
@@ -14,6 +34,8 @@ struct SmootherDev {
   double omega = 1.0;
   double rho_est = 1.0;
   int arnoldi_m = 5;
+  SgsDirection sgs_fw, sgs_bw;           // kind == sgs only
+  DevBuf<double> sgs_tmp, sgs_bp, sgs_xp;  // forward output; b and x in slot order (n each)
 };
 
 // Hooks that run the Arnoldi estimate on a row-partitioned operator: the Krylov vectors
@@ -36,6 +58,10 @@ void setup_smoother(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, Smo
 // into x_out (x_out may not alias x); sgs in place on x.
 void smooth_sweep(const SmootherDev& s, const DevCsr& A, const double* b, const double* x,
                   double* x_out, const int* pred = nullptr, int prof = 0);
-void smooth_sgs(const SmootherDev& s, const DevCsr& A, const double* b, double* x);
+// Symmetric Gauss-Seidel in place on x; the level schedule comes from setup_smoother (or
+// build_sgs_schedule for a caller-supplied state).  pred = device flag gating the sweep.
+void smooth_sgs(const SmootherDev& s, const DevCsr& A, const double* b, double* x,
+                const int* pred = nullptr);
+void build_sgs_schedule(const DevCsr& A, SmootherDev& s);
 
 }  // namespace aggmg_b200

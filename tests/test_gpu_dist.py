@@ -159,6 +159,14 @@ def test_dist_errors_propagate(gpu):
         run_dist(A, 2, cfg, agglomerate=5)
 
 
+def test_dist_rejects_sgs(gpu):
+    # sgs is one global sequential sweep: a row partition cannot reproduce it
+    A = gpu.generate_poisson(2, 16, 16)
+    cfg = M.SetupConfig(alpha=0.25, reuse_caches=True, coarse_size_max=10, smoother=M.SGS)
+    with pytest.raises(M.Error, match="sgs"):
+        run_dist(A, 2, cfg, agglomerate=50)
+
+
 def test_dist_aniso_fgmres_three_ranks_uneven(gpu):
     A = gpu.generate_poisson(3, 22, 18, 16, 1e-3)
     cfg = M.SetupConfig(alpha=0.5, reuse_caches=True, coarse_size_max=50)

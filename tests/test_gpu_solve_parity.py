@@ -59,6 +59,54 @@ def test_smoothers_bit_exact(gpu, ref):
         np.testing.assert_array_equal(bits(gpu.smooth(st, A, b, x)), bits(ref.smooth(st, A, b, x)))
 
 
+def _with_diag(A, seed):
+    """random nonsymmetric pattern plus a dominant diagonal (sgs needs 1/A_ii)"""
+    from helpers import from_triplets
+    rng = np.random.default_rng(seed)
+    r = np.repeat(np.arange(A.n_rows), np.diff(A.row_offsets))
+    rows = np.concatenate([r, np.arange(A.n_rows)])
+    cols = np.concatenate([A.col_indices, np.arange(A.n_rows)])
+    vals = np.concatenate([A.values, rng.uniform(4, 5, A.n_rows)])
+    return from_triplets(A.n_rows, A.n_cols, rows, cols, vals)
+
+
+def test_sgs_level_schedule_bit_exact(gpu, ref):
+    # the level-scheduled sweep against the reference's sequential one: narrow levels (2-D,
+    # 1-D chain), wide levels (3-D 40^3: planes of up to ~2,400 rows), long rows (27-point),
+    # nonsymmetric patterns (rows read columns whose rows do not read them back)
+    rng = np.random.default_rng(11)
+    mats = [ref.generate_poisson(2, 20, 20), ref.generate_poisson(3, 40, 40, 40),
+            ref.generate_poisson(3, 30, 20, 10, 1e-3), laplacian_1d(3000), random_spd(300, 0.1, 2),
+            _with_diag(random_sparse(500, 500, 0.01, 4), 5), gpu.generate_jump27(14, 13, 12, 1e6, 3)]
+    for A in mats:
+        s = ref.setup_smoother(A, M.JACOBI, 5, 0)
+        st = M.SmootherState(M.SGS, s.inv_diag, 1.0, 1.0)
+        b, x = rng.uniform(-1, 1, A.n_rows), rng.uniform(-1, 1, A.n_rows)
+        np.testing.assert_array_equal(bits(gpu.smooth(st, A, b, x)), bits(ref.smooth(st, A, b, x)))
+
+
+@pytest.mark.parametrize("ci", [0, 1, 2])
+def test_sgs_hierarchy_preconditioner(gpu, ref, ci):
+    A = ref.generate_poisson(2, 60, 60)
+    cfg = M.SetupConfig(coarse_size_max=40, reuse_caches=True, smoother=M.SGS)
+    hg, hr = gpu.setup_hierarchy(A, None, cfg), ref.setup_hierarchy(A, None, cfg)
+    r = np.random.default_rng(5).uniform(-1, 1, A.n_rows)
+    zg, zr = gpu.apply_preconditioner(hg, CFGS[ci], r), ref.apply_preconditioner(hr, CFGS[ci], r)
+    assert rel_norm(zg, zr) <= 1e-12
+
+
+def test_sgs_fgmres(gpu, ref):
+    A = ref.generate_poisson(3, 24, 24, 24)
+    cfg = M.SetupConfig(alpha=0.5, reuse_caches=True, smoother=M.SGS)
+    hg, hr = gpu.setup_hierarchy(A, None, cfg), ref.setup_hierarchy(A, None, cfg)
+    sc = M.SolverConfig(method=M.FGMRES, tol=1e-8, max_iters=200, restart=30)
+    b = np.ones(A.n_rows)
+    rg, rr = gpu.fgmres(A, b, None, hg, None, sc), ref.fgmres(A, b, None, hr, None, sc)
+    assert rg.report.iterations == rr.report.iterations
+    assert hist_close(rg.report.residual_history, rr.report.residual_history)
+    assert rel_norm(rg.x, rr.x) <= 1e-10
+
+
 CFGS = [M.CycleConfig(), M.CycleConfig(kind=M.CYCLE_V), M.CycleConfig(kind=M.CYCLE_K),
         M.CycleConfig(inner=M.INNER_CG), M.CycleConfig(t=1e9), M.CycleConfig(t=0.0)]
 

@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1403_1649_b200 import aggmg as M  # noqa: E402
 
 KINDS = {0: "spmv", 1: "residual", 2: "jacobi_zero+residual", 3: "jacobi", 4: "spmv+dot",
-         5: "spmv*invdiag", 6: "jacobi+dot2"}
+         5: "spmv*invdiag", 6: "jacobi+dot2", 7: "sgs"}
 
 
 def main():
@@ -23,8 +23,9 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--kinds", default="0,1,2,3,4")
     ap.add_argument("--only", default="", help="e.g. L1.A:0 — run just this matrix:kind")
-    ap.add_argument("--problem", default="c2", choices=["c2", "c4"],
-                    help="c2: 7-point Poisson n^3; c4: 27-point jump 1e6 (32^3 blocks) n^3")
+    ap.add_argument("--problem", default="c2", choices=["c1", "c2", "c4"],
+                    help="c1: 5-point Poisson n^2; c2: 7-point Poisson n^3; "
+                         "c4: 27-point jump 1e6 (32^3 blocks) n^3")
     args = ap.parse_args()
     lib = M.b200().lib
     assert lib.fn("init")(0) == 0, lib.fn("last_error")()
@@ -33,9 +34,11 @@ def main():
     dm = C.c_void_p()
     if args.problem == "c4":
         assert lib.fn("dmatrix_jump27")(args.n, args.n, args.n, 1e6, 32, C.byref(dm)) == 0
+    elif args.problem == "c1":
+        assert lib.fn("dmatrix_poisson")(2, args.n, args.n, 1, 1.0, -1, C.byref(dm)) == 0
     else:
         assert lib.fn("dmatrix_poisson")(3, args.n, args.n, args.n, 1.0, -1, C.byref(dm)) == 0
-    cfg = M.SetupConfig(alpha=0.5, reuse_caches=True)._c()
+    cfg = M.SetupConfig(alpha=0.25 if args.problem == "c1" else 0.5, reuse_caches=True)._c()
     h = C.c_void_p()
     assert lib.fn("setup_hierarchy_device")(dm, C.byref(cfg), C.byref(h)) == 0
     mats = {"L0.A": dm}
