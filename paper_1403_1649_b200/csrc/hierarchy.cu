@@ -52,16 +52,7 @@ void factor_coarsest(DevHierarchy& h) {
   const int64_t nL = L.A->n_rows;
   require(nL <= std::max<int64_t>(h.cfg.coarse_size_max, kDenseSolveCap),
           "setup: coarsest level has " + std::to_string(nL) + " unknowns, too large for a dense solve");
-  std::vector<int64_t> rp(nL + 1), col(L.A->nnz);
-  std::vector<double> val(L.A->nnz);
-  download_csr(*L.A, rp.data(), col.data(), val.data());
-  std::vector<double> dense(static_cast<size_t>(nL) * nL, 0.0);  // dense.cpp:16-22
-  for (int64_t i = 0; i < nL; ++i)
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) dense[i * nL + col[k]] = val[k];
-  h.coarse_lu.factor(std::move(dense), nL);
-  const std::vector<double> inv = h.coarse_lu.inverse();
-  h.coarse_inv.resize(static_cast<int64_t>(inv.size()));
-  h.coarse_inv.upload(inv.data(), static_cast<int64_t>(inv.size()));
+  invert_coarsest(*L.A, h.coarse_inv);  // coarse.cu (dense.cpp:16-79 on the device)
   sync();
 }
 

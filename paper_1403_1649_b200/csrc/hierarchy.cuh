@@ -65,7 +65,6 @@ struct DevHierarchy {
   int graph_uses = 0;
   SetupCfg cfg;
   std::vector<std::string> warnings;
-  HostLu coarse_lu;
   DevBuf<double> coarse_inv;  // explicit inverse of the coarsest operator (row-major)
   double setup_ms = 0.0;
   bool workspace_ready = false;
@@ -87,5 +86,7 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
                                               const SetupCfg& cfg);
 void refresh_values(DevHierarchy& h, const double* new_values_dev);
 void factor_coarsest(DevHierarchy& h);
+// Explicit inverse of the coarsest operator (row-major) by device Gauss-Jordan (coarse.cu).
+void invert_coarsest(const DevCsr& A, DevBuf<double>& inv);
 
 }  // namespace aggmg_b200

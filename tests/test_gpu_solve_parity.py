@@ -224,3 +224,36 @@ def test_exact_reduction_mode(gpu, ref):
         check_solve(gpu, ref, ref.generate_poisson(2, 100, 100), 0.25, M.PCG)
     finally:
         lib.fn("set_exact_reductions")(0)
+
+
+def test_coarsest_zero_pivot(gpu, ref):
+    # singular coarsest operator (Neumann 1-D Laplacian, one level): the device Gauss-Jordan
+    # reports the reference LU's zero pivot (dense.cpp:42)
+    n = 40
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        d = 1.0 if i in (0, n - 1) else 2.0
+        rows.append(i); cols.append(i); vals.append(d)
+        if i > 0:
+            rows.append(i); cols.append(i - 1); vals.append(-1.0)
+        if i + 1 < n:
+            rows.append(i); cols.append(i + 1); vals.append(-1.0)
+    from helpers import from_triplets
+    A = from_triplets(n, n, rows, cols, vals)
+    cfg = M.SetupConfig(coarse_size_max=100, reuse_caches=True)
+    for impl in (gpu, ref):
+        with pytest.raises(M.Error, match=f"zero pivot at index {n - 1}"):
+            impl.setup_hierarchy(A, None, cfg)
+
+
+def test_coarsest_inverse_sizes(gpu, ref):
+    # one-level hierarchies: the preconditioner is the coarsest direct solve alone
+    rng = np.random.default_rng(9)
+    for n in (1, 7, 300, 1200):
+        A = random_spd(n, min(1.0, 8.0 / n), n)
+        cfg = M.SetupConfig(coarse_size_max=2000, reuse_caches=True)
+        hg, hr = gpu.setup_hierarchy(A, None, cfg), ref.setup_hierarchy(A, None, cfg)
+        r = rng.uniform(-1, 1, n)
+        cc = M.CycleConfig(kind=M.CYCLE_V)
+        zg, zr = gpu.apply_preconditioner(hg, cc, r), ref.apply_preconditioner(hr, cc, r)
+        assert rel_norm(zg, zr) <= 1e-12
