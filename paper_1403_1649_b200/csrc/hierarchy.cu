@@ -67,6 +67,7 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
   AGG_CUDA(cudaEventRecord(e0, stream()));
 
   auto h = std::make_unique<DevHierarchy>();
+  SmootherBatch smoothers;  // after h: joins the side stream before h's buffers die
   h->cfg = cfg;
   h->levels.emplace_back();
   h->levels[0].A = A0;
@@ -118,8 +119,9 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
       Ac = galerkin_direct(A, agg, fine.tr.pval.get());
     }
     st.mark(lv + "galerkin");
-    setup_smoother(A, cfg.smoother, cfg.arnoldi_m, level_seed(cfg.seed, k + cfg.level_offset, kSmootherTag),
-                   fine.smoother);
+    smoothers.add(A, cfg.smoother, cfg.arnoldi_m,
+                  level_seed(cfg.seed, k + cfg.level_offset, kSmootherTag), fine.smoother,
+                  static_cast<int>(k));
     st.mark(lv + "smoother");
     fine.has_smoother = true;
     fine.agg = std::move(agg);
@@ -131,6 +133,9 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
   }
   factor_coarsest(*h);
   st.mark("coarsest LU");
+  // the Arnoldi estimates ran on the side stream under the coarsening
+  smoothers.finish([&](int k) -> SmootherDev& { return h->levels[k].smoother; });
+  st.mark("smoother join");
   AGG_CUDA(cudaEventRecord(e1, stream()));
   AGG_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
@@ -149,14 +154,17 @@ void refresh_values(DevHierarchy& h, const double* new_values_dev) {
   h.graphs.clear();
   DevLevel& L0 = h.levels[0];
   copy_double(L0.A->val.get(), new_values_dev, L0.A->nnz);
+  SmootherBatch smoothers;
   for (int64_t k = 0; k + 1 < h.n_levels(); ++k) {
     DevLevel& fine = h.levels[k];
     DevCsrPtr Ac = apply_galerkin_cache(fine.gal, *fine.A, fine.tr.pval.get());
     copy_double(h.levels[k + 1].A->val.get(), Ac->val.get(), Ac->nnz);
-    setup_smoother(*fine.A, h.cfg.smoother, h.cfg.arnoldi_m,
-                   level_seed(h.cfg.seed, k + h.cfg.level_offset, kSmootherTag), fine.smoother);
+    smoothers.add(*fine.A, h.cfg.smoother, h.cfg.arnoldi_m,
+                  level_seed(h.cfg.seed, k + h.cfg.level_offset, kSmootherTag), fine.smoother,
+                  static_cast<int>(k));
   }
   factor_coarsest(h);
+  smoothers.finish([&](int k) -> SmootherDev& { return h.levels[k].smoother; });
 }
 
 DevHierarchy::~DevHierarchy() {

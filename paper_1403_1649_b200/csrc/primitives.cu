@@ -112,12 +112,13 @@ struct RedScratch {
   }
 };
 RedScratch& red() {
-  static thread_local RedScratch r;
+  static thread_local RedScratch rs[2];  // [1]: kernels on a redirected (side) stream
+  RedScratch& r = rs[stream_redirected() ? 1 : 0];
   if (!r.partials) {
     r.cap = 1 << 20;
     AGG_CUDA(cudaMalloc(&r.partials, sizeof(double) * 3 * r.cap));
     AGG_CUDA(cudaMalloc(&r.ticket, sizeof(unsigned) * 64));
-    AGG_CUDA(cudaMemset(r.ticket, 0, sizeof(unsigned) * 64));
+    AGG_CUDA(cudaMemsetAsync(r.ticket, 0, sizeof(unsigned) * 64, stream()));
   }
   return r;
 }

@@ -100,9 +100,16 @@ void ensure_init() {
   if (!ctx().ready) init_device(0);
 }
 
+namespace {
+thread_local cudaStream_t g_redirect = nullptr;
+}
+StreamRedirect::StreamRedirect(cudaStream_t s) : prev_(g_redirect) { g_redirect = s; }
+StreamRedirect::~StreamRedirect() { g_redirect = prev_; }
+bool stream_redirected() { return g_redirect != nullptr; }
+
 cudaStream_t stream() {
   ensure_init();
-  return ctx().stream;
+  return g_redirect ? g_redirect : ctx().stream;
 }
 int sm_count() {
   ensure_init();
@@ -158,7 +165,7 @@ void* dev_alloc(size_t bytes) {
   BlockCache& c = bcache();
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(stream(), &cap);  // a captured allocation must stay a graph node
-  if (c.enabled && bytes >= kCacheMin && cap == cudaStreamCaptureStatusNone) {
+  if (c.enabled && bytes >= kCacheMin && cap == cudaStreamCaptureStatusNone && !g_redirect) {
     const size_t sc = size_class(bytes);
     auto it = c.free_by_size.find(sc);
     if (it != c.free_by_size.end() && !it->second.empty()) {
@@ -181,6 +188,11 @@ void dev_free(void* p) {
   if (!p) return;
   BlockCache& c = bcache();
   auto it = c.live.find(p);
+  if (g_redirect) {  // stream-ordered release on the redirected stream, never re-cached
+    if (it != c.live.end()) c.live.erase(it);
+    cudaFreeAsync(p, g_redirect);
+    return;
+  }
   if (it == c.live.end()) {  // small block, or one handed out by another thread
     cudaFreeAsync(p, ctx().stream);
     return;

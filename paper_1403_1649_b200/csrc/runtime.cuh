@@ -25,6 +25,21 @@ void host_to_device_narrow(int32_t* dst, const int64_t* src, size_t n, int64_t l
 void init_device(int device);  // creates the calling thread's context on `device`
 int current_device();
 cudaStream_t side_stream();  // a second stream of the calling thread (overlapped exchanges)
+// While alive, the calling thread's kernels and stream-ordered allocations go to `s` instead
+// of its main stream (work that overlaps the main stream, e.g. the smoother's Arnoldi chains
+// during setup).  Allocations made inside bypass the per-thread block cache, whose reuse rule
+// assumes a single stream; the reduction scratch switches to a second set.
+class StreamRedirect {
+ public:
+  explicit StreamRedirect(cudaStream_t s);
+  ~StreamRedirect();
+  StreamRedirect(const StreamRedirect&) = delete;
+  StreamRedirect& operator=(const StreamRedirect&) = delete;
+
+ private:
+  cudaStream_t prev_;
+};
+bool stream_redirected();
 void* dev_alloc(size_t bytes);
 void dev_free(void* p);
 

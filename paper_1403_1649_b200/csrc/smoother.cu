@@ -40,7 +40,8 @@ struct ArnoldiStepOp {
   double* w;
   const double* vn;  // next basis vector (nullptr: last step, out = w . w)
   double mh;
-  __device__ bool active() const { return true; }
+  const int* go;  // device flag (batched setup): 0 after an Arnoldi breakdown
+  __device__ bool active() const { return !go || *go; }
   __device__ void inactive() const {}
   __device__ void init() { mh = hsrc ? -*hsrc : 0.0; }
   __device__ void operator()(int64_t t, double* p) const {
@@ -61,7 +62,9 @@ struct ArnoldiStepOp {
   __device__ void finalize(double*) const {}
 };
 
-__global__ void k_hdiv(const double* s, double* h) { *h = s[0] / s[1]; }
+__global__ void k_hdiv(const double* s, double* h, const int* go = nullptr) {
+  if (!go || *go) *h = s[0] / s[1];
+}
 
 double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t seed,
                     const ArnoldiOps* ops) {
@@ -96,6 +99,7 @@ double estimate_rho(const DevCsr& A, const double* inv_diag, int m, uint64_t see
     spmv_run(A, Epi::kScaleDiag, a);
     for (int i = -1; i <= j; ++i) {  // i = -1: the first dots, no axpy
       ArnoldiStepOp op;
+      op.go = nullptr;
       op.hsrc = i >= 0 ? Hc.get() + i : nullptr;
       op.vi = i >= 0 ? V[i].get() : nullptr;
       op.w = w.get();
@@ -182,6 +186,175 @@ void smooth_sweep(const SmootherDev& s, const DevCsr& A, const double* b, const 
   a.d = s.wdiag.get();
   a.pred = pred;
   spmv_run(A, Epi::kJacobi, a, prof);
+}
+
+// ---- batched (overlapped) smoother setup ---------------------------------------------------
+
+namespace {
+
+// qn = ||V0|| from the exact dot; V0 *= 1/qn (smoother.cpp:51-54)
+__global__ void k_arn_start(const double* d2, double* inv_qn, int* go, int* status) {
+  const double qn = sqrt(d2[0]);
+  if (!(qn > 0.0)) {
+    *status = 1;
+    *go = 0;
+  } else {
+    *inv_qn = 1.0 / qn;
+  }
+}
+__global__ void k_scale_by(int64_t n, const double* f, const double* x, double* y, const int* go) {
+  if (!*go) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __dmul_rn(x[i], *f);
+}
+// end of column j (smoother.cpp:62-81): record h(0..j, j), breakdown test, h(j+1, j), 1/h
+__global__ void k_arn_col(int j, int m, const double* Hc, const double* slots, double* H,
+                          double* inv_h, int* meff, int* go) {
+  if (!*go) return;
+  double h_scale = 0.0;
+  for (int i = 0; i <= j; ++i) {
+    H[i * m + j] = Hc[i];
+    h_scale = fmax(h_scale, fabs(Hc[i]));
+  }
+  const double hj = sqrt(slots[0]);
+  if (hj <= 1e-12 * fmax(h_scale, 1.0)) {
+    *meff = j + 1;
+    *go = 0;
+    return;
+  }
+  H[(j + 1) * m + j] = hj;
+  *inv_h = 1.0 / hj;
+}
+
+}  // namespace
+
+struct SmootherBatch::Job {
+  int key = 0;
+  int m = 0;
+  std::vector<DevBuf<double>> V;
+  DevBuf<double> w, Hc, slots, H, scal;  // scal: [0] |V0|^2, [1] 1/|V0|, [2] 1/h
+  DevBuf<int> flags;                     // [0] go, [1] m_eff, [2] status
+  cudaEvent_t done = nullptr;
+  ~Job() {
+    if (done) cudaEventDestroy(done);
+  }
+};
+
+SmootherBatch::SmootherBatch() = default;
+
+SmootherBatch::~SmootherBatch() {
+  if (!jobs_.empty()) cudaStreamSynchronize(side_stream());  // buffers die after the chains
+}
+
+void SmootherBatch::add(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, SmootherDev& s,
+                        int key) {
+  const int64_t n = A.n_rows;
+  if (kind != 1 || n == 0) {  // nothing to overlap
+    setup_smoother(A, kind, arnoldi_m, seed, s);
+    return;
+  }
+  require(A.n_rows == A.n_cols, "smoother: matrix must be square");
+  require(arnoldi_m >= 1 && arnoldi_m <= 5, "smoother: arnoldi_m must be in [1, 5]");
+  s.kind = kind;
+  s.arnoldi_m = arnoldi_m;
+  s.inv_diag.resize(n);
+  DevBuf<int> bad(1);
+  fill_int(bad.get(), 1, INT32_MAX);
+  AGG_LAUNCH(k_inv_diag, grid_for(n, 256), 256, 0, A.rowptr.get(), A.col.get(), A.val.get(), n,
+             s.inv_diag.get(), bad.get());
+  const int b = read_scalar(bad.get());
+  if (b != INT32_MAX) throw Error("smoother: zero diagonal at row " + std::to_string(b));
+
+  auto job = std::make_unique<Job>();
+  const int m = static_cast<int>(std::min<int64_t>(arnoldi_m, n));
+  job->key = key;
+  job->m = m;
+  // every buffer the side stream touches is allocated here, on the main stream, and lives
+  // until finish() has joined
+  for (int j = 0; j < m; ++j) job->V.emplace_back(n);
+  job->w.resize(n);
+  job->Hc.resize(m + 1);
+  job->slots.resize(2);
+  job->H.resize(static_cast<int64_t>(m + 1) * m);
+  job->H.zero();
+  job->scal.resize(3);
+  job->flags.resize(3);
+  const int f0[3] = {1, m, 0};
+  job->flags.upload(f0, 3);
+  cudaEvent_t ready;
+  AGG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  AGG_CUDA(cudaEventRecord(ready, stream()));  // A, inv_diag and the buffers are ready
+  cudaStream_t side = side_stream();
+  AGG_CUDA(cudaStreamWaitEvent(side, ready, 0));
+  cudaEventDestroy(ready);
+  {
+    StreamRedirect on_side(side);
+    const int* go = job->flags.get();
+    int* gom = job->flags.get();
+    double* V0 = job->V[0].get();
+    vec_uniform_sym(n, seed, V0);
+    DotOp<1> d0;
+    d0.a[0] = V0;
+    d0.b[0] = V0;
+    d0.pred = nullptr;
+    launch_dot_exact<1>(d0, n, job->scal.get());
+    AGG_LAUNCH(k_arn_start, 1, 1, 0, job->scal.get(), job->scal.get() + 1, gom,
+               job->flags.get() + 2);
+    AGG_LAUNCH(k_scale_by, grid_for(n, 256), 256, 0, n, job->scal.get() + 1, V0, V0, go);
+    for (int j = 0; j < m; ++j) {
+      SpmvArgs a;
+      a.x = job->V[j].get();
+      a.y = job->w.get();
+      a.d = s.inv_diag.get();
+      a.pred = go;
+      spmv_run(A, Epi::kScaleDiag, a);
+      for (int i = -1; i <= j; ++i) {
+        ArnoldiStepOp op;
+        op.go = go;
+        op.hsrc = i >= 0 ? job->Hc.get() + i : nullptr;
+        op.vi = i >= 0 ? job->V[i].get() : nullptr;
+        op.w = job->w.get();
+        op.vn = i < j ? job->V[i + 1].get() : nullptr;
+        launch_chunked<2>(op, n, job->slots.get());
+        if (i < j) AGG_LAUNCH(k_hdiv, 1, 1, 0, job->slots.get(), job->Hc.get() + i + 1, go);
+      }
+      AGG_LAUNCH(k_arn_col, 1, 1, 0, j, m, job->Hc.get(), job->slots.get(), job->H.get(),
+                 job->scal.get() + 2, job->flags.get() + 1, gom);
+      if (j + 1 < m)
+        AGG_LAUNCH(k_scale_by, grid_for(n, 256), 256, 0, n, job->scal.get() + 2, job->w.get(),
+                   job->V[j + 1].get(), go);
+    }
+    AGG_CUDA(cudaEventCreateWithFlags(&job->done, cudaEventDisableTiming));
+    AGG_CUDA(cudaEventRecord(job->done, side));
+  }
+  jobs_.push_back(std::move(job));
+}
+
+void SmootherBatch::finish(const std::function<SmootherDev&(int)>& level) {
+  if (jobs_.empty()) return;
+  AGG_CUDA(cudaStreamSynchronize(side_stream()));
+  auto jobs = std::move(jobs_);
+  for (auto& j : jobs) {
+    const int m = j->m;
+    std::vector<double> H(static_cast<size_t>(m + 1) * m);
+    int flags[3];
+    AGG_CUDA(cudaMemcpy(H.data(), j->H.get(), sizeof(double) * H.size(), cudaMemcpyDeviceToHost));
+    AGG_CUDA(cudaMemcpy(flags, j->flags.get(), sizeof(flags), cudaMemcpyDeviceToHost));
+    require(flags[2] == 0, "smoother: degenerate start vector");
+    const int m_eff = flags[1];
+    std::vector<double> Hm(static_cast<size_t>(m_eff) * m_eff);
+    for (int r = 0; r < m_eff; ++r)
+      for (int c = 0; c < m_eff; ++c) Hm[static_cast<size_t>(r) * m_eff + c] = H[static_cast<size_t>(r) * m + c];
+    double rho = 0.0;
+    for (const auto& ev : hessenberg_eigenvalues(Hm, m_eff)) rho = std::max(rho, std::abs(ev));
+    require(rho > 0.0, "smoother: spectral radius estimate collapsed to zero");
+    SmootherDev& s = level(j->key);
+    s.rho_est = rho;
+    s.omega = (4.0 / 3.0) / rho;
+    const int64_t n = s.inv_diag.size();
+    s.wdiag.resize(n);
+    AGG_LAUNCH(k_scale_diag, grid_for(n, 256), 256, 0, s.inv_diag.get(), s.omega, n, s.wdiag.get());
+  }
 }
 
 }  // namespace aggmg_b200

@@ -2,6 +2,8 @@
 #pragma once
 
 #include <functional>
+#include <memory>
+#include <vector>
 
 #include "sparse.cuh"
 
@@ -53,6 +55,27 @@ struct ArnoldiOps {
 // damped Jacobi with start vector uniform_sym(seed, i)).
 void setup_smoother(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, SmootherDev& s,
                     const ArnoldiOps* ops = nullptr);
+
+// Smoother setup for every level of a one-GPU hierarchy with the damped-Jacobi Arnoldi
+// estimates overlapped with the rest of setup.  add() computes the inverse diagonal at once
+// (zero diagonals fail there, in level order) and issues the level's Arnoldi process
+// (smoother.cpp:43-84) entirely on the device on the side stream — breakdown handled by a
+// device flag, no host reads — so the latency-bound dot chains run under the next levels'
+// coarsening.  finish() joins, reads each Hessenberg matrix once, and sets rho/omega exactly
+// as setup_smoother does (same kernels, same operation order: omega is bit-identical).
+class SmootherBatch {
+ public:
+  SmootherBatch();
+  ~SmootherBatch();  // joins the side stream if finish() was not reached (error paths)
+  // `s` must stay at a stable address only during add(); finish() resolves each job's state
+  // again through level(key) (hierarchy levels live in a growing vector)
+  void add(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, SmootherDev& s, int key);
+  void finish(const std::function<SmootherDev&(int)>& level);
+
+ private:
+  struct Job;
+  std::vector<std::unique_ptr<Job>> jobs_;
+};
 
 // One sweep on device vectors (smoother.cpp:101-124): jacobi/damped Jacobi out of place
 // into x_out (x_out may not alias x); sgs in place on x.
