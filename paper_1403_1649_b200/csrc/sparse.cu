@@ -177,6 +177,47 @@ struct EpiTraits {
 // loads and stages val * x[col] in shared memory; phase 2 sums each row sequentially in
 // storage order and applies the epilogue.  Fused dot products accumulate per thread
 // across row blocks and are reduced once per CTA (fixed grid => deterministic).
+// Per-row epilogue of the SpMV family: y / residual / Jacobi / scaled output and the fused
+// dot contributions, from the row's sequential sum.
+template <Epi E>
+__device__ __forceinline__ void row_epilogue(const SpmvArgs& a, const double* __restrict__ x,
+                                             int64_t rg, double sum, double* v) {
+  constexpr int NP = EpiTraits<E>::np;
+  double yv = sum;
+  if constexpr (E == Epi::kJacobiDot2) {
+    yv = __dadd_rn(x[rg], __dmul_rn(a.d[rg], __dsub_rn(a.b[rg], sum)));
+    a.y[rg] = yv;
+  } else if constexpr (E == Epi::kSpmv || NP > 0) {
+    a.y[rg] = sum;
+  } else if constexpr (E == Epi::kResidual) {
+    a.y[rg] = __dsub_rn(a.b[rg], sum);
+  } else if constexpr (E == Epi::kResidualZero) {
+    const double br = a.b[rg];
+    a.y[rg] = __dsub_rn(br, sum);                                // r = b - A x1
+    a.x_out[rg] = __dadd_rn(0.0, __dmul_rn(a.d[rg], br));         // x1 = 0 + wd b
+  } else if constexpr (E == Epi::kJacobi) {
+    a.y[rg] = __dadd_rn(x[rg], __dmul_rn(a.d[rg], __dsub_rn(a.b[rg], sum)));
+  } else if constexpr (E == Epi::kScaleDiag) {
+    a.y[rg] = __dmul_rn(sum, a.d[rg]);
+  }
+  if constexpr (E == Epi::kJacobiDot2) {
+    v[0] = __dadd_rn(v[0], __dmul_rn(a.b[rg], yv));  // r . z
+    v[1] = __dadd_rn(v[1], __dmul_rn(a.c[rg], yv));  // r_old . z
+  } else if constexpr (NP > 0) {
+    const double lhs = a.dot_with_x ? x[rg] : sum;
+    if constexpr (NP == 1) {
+      v[0] = __dadd_rn(v[0], __dmul_rn(a.u[rg], sum));
+    } else if constexpr (NP == 2) {
+      v[0] = __dadd_rn(v[0], __dmul_rn(lhs, sum));     // rho  = v.v (gmres) | c.v (cg)
+      v[1] = __dadd_rn(v[1], __dmul_rn(lhs, a.c[rg]));  // alpha = v.rc       | c.rc
+    } else {
+      v[0] = __dadd_rn(v[0], __dmul_rn(lhs, a.u[rg]));  // gamma = w.v | d.v
+      v[1] = __dadd_rn(v[1], __dmul_rn(lhs, sum));     // beta  = w.w | d.w
+      v[2] = __dadd_rn(v[2], __dmul_rn(lhs, a.c[rg]));  // alpha2 = w.rt | d.rt
+    }
+  }
+}
+
 template <Epi E>
 __global__ void __launch_bounds__(kStreamThreads)
     k_csr_stream(const idx* __restrict__ rowptr, const idx* __restrict__ col,
@@ -244,39 +285,7 @@ __global__ void __launch_bounds__(kStreamThreads)
       const int64_t rg = r + a.row_base;  // row index of the epilogue vectors
       double sum = 0.0;
       for (idx k = s; k < t; ++k) sum = __dadd_rn(sum, prod[k]);
-      double yv = sum;
-      if constexpr (E == Epi::kJacobiDot2) {
-        yv = __dadd_rn(x[rg], __dmul_rn(a.d[rg], __dsub_rn(a.b[rg], sum)));
-        a.y[rg] = yv;
-      } else if constexpr (E == Epi::kSpmv || NP > 0) {
-        a.y[rg] = sum;
-      } else if constexpr (E == Epi::kResidual) {
-        a.y[rg] = __dsub_rn(a.b[rg], sum);
-      } else if constexpr (E == Epi::kResidualZero) {
-        const double br = a.b[rg];
-        a.y[rg] = __dsub_rn(br, sum);                                // r = b - A x1
-        a.x_out[rg] = __dadd_rn(0.0, __dmul_rn(a.d[rg], br));         // x1 = 0 + wd b
-      } else if constexpr (E == Epi::kJacobi) {
-        a.y[rg] = __dadd_rn(x[rg], __dmul_rn(a.d[rg], __dsub_rn(a.b[rg], sum)));
-      } else if constexpr (E == Epi::kScaleDiag) {
-        a.y[rg] = __dmul_rn(sum, a.d[rg]);
-      }
-      if constexpr (E == Epi::kJacobiDot2) {
-        v[0] = __dadd_rn(v[0], __dmul_rn(a.b[rg], yv));  // r . z
-        v[1] = __dadd_rn(v[1], __dmul_rn(a.c[rg], yv));  // r_old . z
-      } else if constexpr (NP > 0) {
-        const double lhs = a.dot_with_x ? x[rg] : sum;
-        if constexpr (NP == 1) {
-          v[0] = __dadd_rn(v[0], __dmul_rn(a.u[rg], sum));
-        } else if constexpr (NP == 2) {
-          v[0] = __dadd_rn(v[0], __dmul_rn(lhs, sum));     // rho  = v.v (gmres) | c.v (cg)
-          v[1] = __dadd_rn(v[1], __dmul_rn(lhs, a.c[rg]));  // alpha = v.rc       | c.rc
-        } else {
-          v[0] = __dadd_rn(v[0], __dmul_rn(lhs, a.u[rg]));  // gamma = w.v | d.v
-          v[1] = __dadd_rn(v[1], __dmul_rn(lhs, sum));     // beta  = w.w | d.w
-          v[2] = __dadd_rn(v[2], __dmul_rn(lhs, a.c[rg]));  // alpha2 = w.rt | d.rt
-        }
-      }
+      row_epilogue<E>(a, x, rg, sum, v);
     }
     __syncthreads();  // prod is reused by the next row block
   }
@@ -298,7 +307,7 @@ void launch_stream(const DevCsr& A, const SpmvArgs& a) {
   static thread_local bool raised = false;
   if (smem > 48 * 1024 && !raised) {
     AGG_CUDA(cudaFuncSetAttribute(k_csr_stream<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
+                                  226 * 1024));  // + the static reduction scratch <= 227 KB
     raised = true;
   }
   // persistent grid: as many CTAs as can be co-resident
