@@ -1019,6 +1019,7 @@ std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, c
           "setup: the sgs smoother is a global sequential sweep; a row-partitioned hierarchy "
           "supports jacobi and damped_jacobi");
   const int me = comm.rank();
+  pool_reserve(16 * static_cast<size_t>(A0->A.nnz * 12 + A0->A.n_rows * 8) + (size_t{256} << 20));
   comm.barrier();
   const auto t0 = std::chrono::steady_clock::now();
   PhaseTimer timer;

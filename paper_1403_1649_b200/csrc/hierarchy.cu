@@ -61,6 +61,9 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
   require(A0->n_rows == A0->n_cols, "setup: matrix must be square");
   require(cfg.coarse_size_max >= 1, "setup: coarse_size_max must be at least 1");
   require(cfg.max_levels >= 1, "setup: max_levels must be at least 1");
+  // working set of setup + a Krylov solve: ~16x the operator (strength graphs, Galerkin
+  // scratch and caches, coarse levels, FGMRES(30) basis)
+  pool_reserve(16 * static_cast<size_t>(A0->nnz * 12 + A0->n_rows * 8) + (size_t{256} << 20));
   cudaEvent_t e0, e1;
   AGG_CUDA(cudaEventCreate(&e0));
   AGG_CUDA(cudaEventCreate(&e1));

@@ -4,6 +4,7 @@
 #include <condition_variable>
 #include <functional>
 #include <cstring>
+#include <list>
 #include <mutex>
 #include <thread>
 #include <unordered_map>
@@ -71,6 +72,31 @@ ProfState& prof() {
 
 }  // namespace
 
+// Stream-ordered pool growth maps physical memory on demand, and a hierarchy's setup + solve
+// allocates tens of GB in hundreds of blocks of many sizes: measured on B200, on-demand
+// growth cost up to 0.8 s per c4 step and 0.5 s per c3 step.  pool_reserve(bytes) maps one
+// block of that size into the pool (which keeps freed memory: release threshold = max) the
+// first time a caller needs more than the pool has ever reserved, so the pool sub-allocates
+// instead of growing block by block.  AGGMG_POOL_RESERVE_GB reserves up front at init.
+void pool_reserve(size_t bytes) {
+  ensure_init();
+  static std::mutex m;
+  static size_t reserved = 0;
+  std::lock_guard<std::mutex> lk(m);
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return;
+  bytes = std::min(bytes, static_cast<size_t>(0.6 * static_cast<double>(fr + reserved)));
+  if (bytes <= reserved) return;
+  void* p = nullptr;
+  cudaStream_t st = ctx().stream;
+  if (cudaMallocAsync(&p, bytes, st) == cudaSuccess) {
+    cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
+    reserved = bytes;
+  }
+  cudaGetLastError();
+}
+
 void init_device(int device) {
   Context& c = ctx();
   std::lock_guard<std::mutex> lk(ctx_mutex());
@@ -91,6 +117,15 @@ void init_device(int device) {
   AGG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t threshold = UINT64_MAX;  // keep freed blocks cached: setup reallocates per level
   AGG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  if (const char* r = std::getenv("AGGMG_POOL_RESERVE_GB")) {
+    void* p = nullptr;
+    const size_t bytes = static_cast<size_t>(std::atof(r) * double(size_t{1} << 30));
+    if (bytes && cudaMallocAsync(&p, bytes, c.stream) == cudaSuccess) {
+      cudaFreeAsync(p, c.stream);
+      cudaStreamSynchronize(c.stream);
+    }
+    cudaGetLastError();
+  }
   AGG_CUDA(cudaMallocHost(&c.pinned, 4096 * sizeof(double)));
   c.pinned_n = 4096;
   c.ready = true;
@@ -135,7 +170,13 @@ int current_device() {
 namespace {
 constexpr size_t kCacheMin = size_t{1} << 20;  // smaller buffers: the CUDA pool is fast enough
 struct BlockCache {
+  // free blocks by size class, plus their age order: when caching a block would pass the
+  // limit the oldest cached blocks are released first, so the cache follows the current
+  // working set (setup's many sizes, then a Krylov solve's many equal vectors) instead of
+  // pinning whatever filled it first
   std::unordered_map<size_t, std::vector<void*>> free_by_size;
+  std::list<std::pair<void*, size_t>> lru;  // oldest first
+  std::unordered_map<void*, std::list<std::pair<void*, size_t>>::iterator> where;
   std::unordered_map<void*, size_t> live;  // blocks handed out by this context
   size_t cached = 0;
   size_t limit = 0;
@@ -145,10 +186,42 @@ struct BlockCache {
     enabled = !(e && e[0] == '0');
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) limit = tot / 4;
+    if (const char* l = std::getenv("AGGMG_CACHE_LIMIT_MB")) limit = size_t(std::atoll(l)) << 20;
+    if (const char* m = std::getenv("AGGMG_CACHE_MAX_BLOCK_MB")) max_block = size_t(std::atoll(m)) << 20;
   }
+  size_t max_block = ~size_t{0};
   ~BlockCache() {  // a rank thread exits: hand the cached blocks back
     for (auto& kv : free_by_size)
       for (void* p : kv.second) cudaFree(p);
+  }
+  void* take(size_t sc) {
+    auto it = free_by_size.find(sc);
+    if (it == free_by_size.end() || it->second.empty()) return nullptr;
+    void* p = it->second.back();
+    it->second.pop_back();
+    auto w = where.find(p);
+    lru.erase(w->second);
+    where.erase(w);
+    cached -= sc;
+    return p;
+  }
+  void put(void* p, size_t sc) {
+    free_by_size[sc].push_back(p);
+    lru.emplace_back(p, sc);
+    where[p] = std::prev(lru.end());
+    cached += sc;
+  }
+  void evict_oldest(cudaStream_t st) {
+    const auto [p, sc] = lru.front();
+    lru.pop_front();
+    where.erase(p);
+    auto& v = free_by_size[sc];
+    v.erase(std::find(v.begin(), v.end(), p));
+    cached -= sc;
+    cudaFreeAsync(p, st);
+  }
+  void release_all(cudaStream_t st) {
+    while (!lru.empty()) evict_oldest(st);
   }
 };
 BlockCache& bcache() {
@@ -160,29 +233,36 @@ size_t size_class(size_t b) {  // 1 MB granularity keeps near-equal requests in 
 }
 }  // namespace
 
+namespace {
+// stream-ordered allocation; on failure the cached blocks are handed back and it is retried
+void* pool_alloc(size_t bytes, BlockCache& c) {
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, bytes, stream());
+  if (e == cudaErrorMemoryAllocation && c.cached > 0) {
+    cudaGetLastError();
+    c.release_all(ctx().stream);
+    AGG_CUDA(cudaStreamSynchronize(ctx().stream));
+    e = cudaMallocAsync(&p, bytes, stream());
+  }
+  if (e != cudaSuccess) AGG_CUDA(e);
+  return p;
+}
+}  // namespace
+
 void* dev_alloc(size_t bytes) {
   ensure_init();
   BlockCache& c = bcache();
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(stream(), &cap);  // a captured allocation must stay a graph node
-  if (c.enabled && bytes >= kCacheMin && cap == cudaStreamCaptureStatusNone && !g_redirect) {
+  if (c.enabled && bytes >= kCacheMin && bytes <= c.max_block && cap == cudaStreamCaptureStatusNone &&
+      !g_redirect) {
     const size_t sc = size_class(bytes);
-    auto it = c.free_by_size.find(sc);
-    if (it != c.free_by_size.end() && !it->second.empty()) {
-      void* p = it->second.back();
-      it->second.pop_back();
-      c.cached -= sc;
-      c.live[p] = sc;
-      return p;
-    }
-    void* p = nullptr;
-    AGG_CUDA(cudaMallocAsync(&p, sc, stream()));
+    void* p = c.take(sc);
+    if (!p) p = pool_alloc(sc, c);
     c.live[p] = sc;
     return p;
   }
-  void* p = nullptr;
-  AGG_CUDA(cudaMallocAsync(&p, bytes, stream()));
-  return p;
+  return pool_alloc(bytes, c);
 }
 void dev_free(void* p) {
   if (!p) return;
@@ -199,12 +279,12 @@ void dev_free(void* p) {
   }
   const size_t sc = it->second;
   c.live.erase(it);
-  if (c.cached + sc > c.limit) {  // bounded: release instead of caching
+  if (sc > c.limit) {  // larger than the whole cache: release
     cudaFreeAsync(p, ctx().stream);
     return;
   }
-  c.free_by_size[sc].push_back(p);
-  c.cached += sc;
+  while (c.cached + sc > c.limit) c.evict_oldest(ctx().stream);
+  c.put(p, sc);
 }
 
 void sync() { AGG_CUDA(cudaStreamSynchronize(stream())); }

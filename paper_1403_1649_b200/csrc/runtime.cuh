@@ -41,6 +41,9 @@ class StreamRedirect {
 };
 bool stream_redirected();
 void* dev_alloc(size_t bytes);
+// Make sure the stream-ordered pool holds at least `bytes` of mapped memory (capped at 60% of
+// what the device has left); setup calls it with its working-set estimate.
+void pool_reserve(size_t bytes);
 void dev_free(void* p);
 
 // Move-only device array allocated from the stream-ordered pool.
