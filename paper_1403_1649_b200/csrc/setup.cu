@@ -89,6 +89,91 @@ __global__ void k_merge_rows(const idx* crp, const idx* ccol, const idx* trp, co
   if (!mode) out[i] = cnt;
 }
 
+// S = C u C^T and the influence counts without materialising C^T (strength.cpp:74-111).
+// Strength graphs are structurally symmetric almost everywhere, so each entry (r, c) is
+// probed for its mirror (c, r) by binary search in the sorted row c: a mirrored entry adds
+// nothing to S, an unmirrored one adds r to row c of S.  influence(c) = |{r : c in C_r}| =
+// (entries of row c whose mirror exists) + (unmirrored entries pointing at c).
+__device__ __forceinline__ bool row_has(const idx* ccol, idx lo, idx hi, idx v) {
+  while (lo < hi) {
+    const idx mid = (lo + hi) >> 1;
+    const idx x = __ldg(ccol + mid);
+    if (x == v) return true;
+    if (x < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return false;
+}
+// pass 1: mirrored count per row, unmirrored entries counted per receiving row
+__global__ void k_sym_probe(const idx* __restrict__ crp, const idx* __restrict__ ccol, int64_t n,
+                            idx* mirrored, idx* extra_cnt, int8_t* has_extra,
+                            unsigned long long* total) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned u = 0;
+  if (r < n) {
+    idx f = 0;
+    const idx k1 = crp[r + 1];
+    for (idx k = crp[r]; k < k1; ++k) {
+      const idx c = ccol[k];
+      if (row_has(ccol, __ldg(crp + c), __ldg(crp + c + 1), static_cast<idx>(r))) {
+        ++f;
+      } else {
+        atomicAdd(&extra_cnt[c], 1);
+        ++u;
+      }
+    }
+    mirrored[r] = f;
+    has_extra[r] = u ? 1 : 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) u += __shfl_down_sync(0xffffffffu, u, o);
+  if ((threadIdx.x & 31) == 0 && u) atomicAdd(total, static_cast<unsigned long long>(u));
+}
+// pass 2 (rows with unmirrored entries only): r goes into row c's extra bucket
+__global__ void k_sym_extras(const idx* __restrict__ crp, const idx* __restrict__ ccol, int64_t n,
+                             const int8_t* has_extra, const idx* eoff, idx* cursor, idx* ecol) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n || !has_extra[r]) return;
+  for (idx k = crp[r]; k < crp[r + 1]; ++k) {
+    const idx c = ccol[k];
+    if (!row_has(ccol, __ldg(crp + c), __ldg(crp + c + 1), static_cast<idx>(r)))
+      ecol[eoff[c] + atomicAdd(&cursor[c], 1)] = static_cast<idx>(r);
+  }
+}
+__global__ void k_sym_counts(const idx* crp, const idx* mirrored, const idx* extra_cnt, int64_t n,
+                             idx* influence, idx* scnt) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  influence[r] = mirrored[r] + extra_cnt[r];
+  scnt[r] = crp[r + 1] - crp[r] + extra_cnt[r];
+}
+// S row = C row merged with its (sorted) extra bucket; buckets are rare and short
+__global__ void k_sym_fill(const idx* __restrict__ crp, const idx* __restrict__ ccol,
+                           const idx* srp, const idx* eoff, const idx* extra_cnt, idx* ecol,
+                           int64_t n, idx* scol) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  idx a = crp[r];
+  const idx ae = crp[r + 1];
+  idx* o = scol + srp[r];
+  const idx ne = extra_cnt[r];
+  if (ne == 0) {
+    for (; a < ae; ++a) *o++ = ccol[a];
+    return;
+  }
+  idx* e = ecol + eoff[r];
+  for (idx x = 1; x < ne; ++x) {  // insertion sort of the bucket
+    const idx v = e[x];
+    idx y = x;
+    for (; y > 0 && e[y - 1] > v; --y) e[y] = e[y - 1];
+    e[y] = v;
+  }
+  idx b = 0;
+  while (a < ae || b < ne) {
+    if (b >= ne || (a < ae && ccol[a] < e[b])) *o++ = ccol[a++];
+    else *o++ = e[b++];
+  }
+}
+
 // ---- a6 MIS(2) ---------------------------------------------------------------------------
 struct __align__(16) Tuple {
   double v;
@@ -952,27 +1037,40 @@ void influence_and_symmetrize(const DevCsr& C, DevBuf<idx>& influence, DevCsrPtr
   require(C.n_rows == C.n_cols, "symmetrize: matrix must be square");
   const int64_t n = C.n_rows;
   influence.resize(n);
-  influence.zero();
-  if (C.nnz > 0) AGG_LAUNCH(k_col_count, grid_for(C.nnz, 256), 256, 0, C.col.get(), C.nnz, influence.get());
-  DevBuf<idx> trp(n + 1), cursor(n), tmp(C.nnz), tcol(C.nnz);
-  scan_to_offsets_async(influence.get(), trp.get(), n);
-  cursor.zero();
-  if (n > 0)
-    AGG_LAUNCH(k_scatter_pattern_t, grid_for(n, 256), 256, 0, C.rowptr.get(), C.col.get(), n,
-               trp.get(), cursor.get(), tmp.get());
-  segmented_sort(trp.get(), n, tmp.get(), tcol.get());
   S = std::make_shared<DevCsr>();
   S->n_rows = S->n_cols = n;
   S->rowptr.resize(n + 1);
-  DevBuf<idx> scnt(n);
-  if (n > 0)
-    AGG_LAUNCH(k_merge_rows, grid_for(n, 256), 256, 0, C.rowptr.get(), C.col.get(), trp.get(),
-               tcol.get(), n, 0, nullptr, scnt.get());
+  if (n == 0) {
+    S->nnz = 0;
+    fill_int(S->rowptr.get(), 1, 0);
+    return;
+  }
+  DevBuf<idx> mirrored(n), ecnt(n), eoff(n + 1), scnt(n);
+  DevBuf<int8_t> has_extra(n);
+  DevBuf<unsigned long long> total(1);
+  ecnt.zero();
+  total.zero();
+  const unsigned g = grid_for(n, 256);
+  AGG_LAUNCH(k_sym_probe, g, 256, 0, C.rowptr.get(), C.col.get(), n, mirrored.get(), ecnt.get(),
+             has_extra.get(), total.get());
+  const unsigned long long ne = read_scalar(total.get());
+  DevBuf<idx> ecol(static_cast<int64_t>(ne));
+  if (ne > 0) {
+    scan_to_offsets_async(ecnt.get(), eoff.get(), n);
+    DevBuf<idx> cursor(n);
+    cursor.zero();
+    AGG_LAUNCH(k_sym_extras, g, 256, 0, C.rowptr.get(), C.col.get(), n, has_extra.get(), eoff.get(),
+               cursor.get(), ecol.get());
+  } else {
+    eoff.zero();
+  }
+  AGG_LAUNCH(k_sym_counts, g, 256, 0, C.rowptr.get(), mirrored.get(), ecnt.get(), n,
+             influence.get(), scnt.get());
   S->nnz = scan_to_offsets(scnt.get(), S->rowptr.get(), n);
   S->col.resize(S->nnz);
-  if (n > 0 && S->nnz > 0)
-    AGG_LAUNCH(k_merge_rows, grid_for(n, 256), 256, 0, C.rowptr.get(), C.col.get(), trp.get(),
-               tcol.get(), n, 1, S->rowptr.get(), S->col.get());
+  if (S->nnz > 0)
+    AGG_LAUNCH(k_sym_fill, g, 256, 0, C.rowptr.get(), C.col.get(), S->rowptr.get(), eoff.get(),
+               ecnt.get(), ecol.get(), n, S->col.get());
 }
 
 Mis2Dev mis2(const DevCsr& S, const idx* influence, uint64_t seed) {
