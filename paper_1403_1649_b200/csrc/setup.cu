@@ -52,6 +52,66 @@ __global__ void k_strength(const idx* __restrict__ rowptr, const idx* __restrict
   }
 }
 
+// The same row rule over CSR-stream row blocks (sparse.cuh): the block's columns and values
+// are staged into shared memory with coalesced vector loads, then one thread per row applies
+// k_strength's three passes from shared memory (same operations, same order).
+constexpr int kStrThreads = 256;
+__global__ void __launch_bounds__(kStrThreads)
+    k_strength_stream(const idx* __restrict__ rowptr, const idx* __restrict__ col,
+                      const double* __restrict__ val, int64_t n, int rpb, int64_t nblocks,
+                      int stage, double alpha, int fail_zero, int mode, const idx* out_rowptr,
+                      idx* out, int* bad_row) {
+  extern __shared__ __align__(16) double sstage[];
+  double* sv = sstage;
+  idx* sc = reinterpret_cast<idx*>(sstage + stage);
+  for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+    const int64_t r0 = rb * rpb, r1 = min(r0 + static_cast<int64_t>(rpb), n);
+    const idx e0 = rowptr[r0], e1 = rowptr[r1];
+    const idx ea = e0 & ~1;
+    for (idx e = ea + 2 * static_cast<idx>(threadIdx.x); e < e1; e += 2 * kStrThreads) {
+      const double2 v2 = __ldcs(reinterpret_cast<const double2*>(val + e));
+      const int2 c2 = __ldcs(reinterpret_cast<const int2*>(col + e));
+      *reinterpret_cast<double2*>(sv + (e - ea)) = v2;
+      *reinterpret_cast<int2*>(sc + (e - ea)) = c2;
+    }
+    __syncthreads();
+    const int64_t i = r0 + threadIdx.x;
+    if (threadIdx.x < rpb && i < r1) {
+      const idx lo = rowptr[i] - ea, hi = rowptr[i + 1] - ea;
+      const idx ii = static_cast<idx>(i);
+      double d = 0.0;
+      for (idx k = lo; k < hi; ++k)
+        if (sc[k] == ii) d = sv[k];
+      double sg;
+      if (d == 0.0) {  // strength.cpp:18-21
+        if (fail_zero) atomicMin(bad_row, static_cast<int>(i));
+        sg = 1.0;
+      } else {
+        sg = d > 0.0 ? 1.0 : -1.0;
+      }
+      const double ns = -sg;
+      double m = 0.0;
+      for (idx k = lo; k < hi; ++k) {
+        if (sc[k] == ii) continue;
+        m = dmax_ref(m, __dmul_rn(ns, sv[k]));
+      }
+      const double thr = __dmul_rn(alpha, m);
+      if (mode == 0) {
+        idx c = 0;
+        if (m > 0.0)
+          for (idx k = lo; k < hi; ++k)
+            if (sc[k] != ii && __dmul_rn(ns, sv[k]) > thr) ++c;
+        out[i] = c;
+      } else if (m > 0.0) {
+        idx p = out_rowptr[i];
+        for (idx k = lo; k < hi; ++k)
+          if (sc[k] != ii && __dmul_rn(ns, sv[k]) > thr) out[p++] = sc[k];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---- a4/a5 influence + symmetrize -------------------------------------------------------
 __global__ void k_col_count(const idx* col, int64_t nnz, idx* cnt) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1007,6 +1067,38 @@ DevCsrPtr classic_strength(const DevCsr& A, double alpha, int zero_diag_policy) 
 
 // Rows of a (possibly row-partitioned) operator whose owned columns are 0..n_rows-1 in
 // local ids: the diagonal of row i is column i, halo columns never are.
+namespace {
+// one strength pass: CSR-stream staged when A has a row-block plan that fits, else thread-per-row
+void strength_pass(const DevCsr& A, double alpha, int fail_zero, int mode, const idx* out_rowptr,
+                   idx* out, int* bad) {
+  const int64_t n = A.n_rows;
+  if (n == 0) return;
+  const int stage = ((A.smem_entries + 3) / 2) * 2 + 2;
+  const size_t smem = static_cast<size_t>(stage) * (sizeof(double) + sizeof(idx));
+  // staging pays for long rows only (measured: 27-point 8.5 -> 4.3 ms; 7- and 14-entry rows
+  // are faster thread-per-row)
+  const bool long_rows = A.nnz >= 20 * n;
+  if (long_rows && A.rows_per_block > 0 && A.rows_per_block <= kStrThreads && smem <= 48 * 1024) {
+    const int64_t nblocks = (n + A.rows_per_block - 1) / A.rows_per_block;
+    static thread_local size_t cached_smem = 0;
+    static thread_local int per_sm = 1;
+    if (cached_smem != smem) {
+      AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_strength_stream,
+                                                             kStrThreads, smem));
+      per_sm = std::max(1, per_sm);
+      cached_smem = smem;
+    }
+    const int64_t grid = std::min<int64_t>(nblocks, static_cast<int64_t>(per_sm) * sm_count());
+    AGG_LAUNCH(k_strength_stream, static_cast<unsigned>(grid), kStrThreads, smem, A.rowptr.get(),
+               A.col.get(), A.val.get(), n, A.rows_per_block, nblocks, stage, alpha, fail_zero, mode,
+               out_rowptr, out, bad);
+    return;
+  }
+  AGG_LAUNCH(k_strength, grid_for(n, 256), 256, 0, A.rowptr.get(), A.col.get(), A.val.get(), n,
+             alpha, fail_zero, mode, out_rowptr, out, bad);
+}
+}  // namespace
+
 DevCsrPtr strength_rows(const DevCsr& A, double alpha, int zero_diag_policy) {
   require(alpha > 0.0 && alpha < 1.0, "strength: alpha must be in (0, 1)");
   const int64_t n = A.n_rows;
@@ -1017,9 +1109,7 @@ DevCsrPtr strength_rows(const DevCsr& A, double alpha, int zero_diag_policy) {
   DevBuf<idx> cnt(n);
   DevBuf<int> bad(1);
   fill_int(bad.get(), 1, INT32_MAX);
-  if (n > 0)
-    AGG_LAUNCH(k_strength, grid_for(n, 256), 256, 0, A.rowptr.get(), A.col.get(), A.val.get(), n,
-               alpha, zero_diag_policy, 0, nullptr, cnt.get(), bad.get());
+  strength_pass(A, alpha, zero_diag_policy, 0, nullptr, cnt.get(), bad.get());
   C->nnz = scan_to_offsets(cnt.get(), C->rowptr.get(), n);
   if (zero_diag_policy) {
     const int b = read_scalar(bad.get());
@@ -1027,9 +1117,7 @@ DevCsrPtr strength_rows(const DevCsr& A, double alpha, int zero_diag_policy) {
       throw Error("strength: zero or missing diagonal at row " + std::to_string(b));
   }
   C->col.resize(C->nnz);
-  if (n > 0 && C->nnz > 0)
-    AGG_LAUNCH(k_strength, grid_for(n, 256), 256, 0, A.rowptr.get(), A.col.get(), A.val.get(), n,
-               alpha, 0, 1, C->rowptr.get(), C->col.get(), bad.get());
+  if (C->nnz > 0) strength_pass(A, alpha, 0, 1, C->rowptr.get(), C->col.get(), bad.get());
   return C;
 }
 
