@@ -26,6 +26,7 @@ transport/overhead diagnostic, not a scaling number).
 """
 import argparse
 import ctypes as C
+import datetime
 import json
 import os
 import statistics
@@ -74,25 +75,34 @@ def load_traffic():
 class ClockSampler:
     """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device):
         self.device = device
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
+        if os.environ.get("AGGMG_BENCH_NO_CLOCKS") == "1":  # diagnosis only
+            self.t0 = time.time()
+            return self
+        # started ahead of the timed region (nvidia-smi's own start-up takes driver time that
+        # would otherwise land in the first timed step); samples outside [t0, t1] are dropped
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(1.0)
         except OSError:
             self.proc = None
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
+        self.t1 = time.time()
         self.lines = []
         if self.proc:
             self.proc.terminate()
@@ -101,7 +111,16 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            for ln in out.splitlines():
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                if self.t0 - 0.25 <= ts <= self.t1 + 0.25:
+                    self.lines.append(",".join(parts[1:]))
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
@@ -557,7 +576,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-prof", action="store_true", help="skip per-launch CUDA-event timing")

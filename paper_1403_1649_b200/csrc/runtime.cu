@@ -81,8 +81,10 @@ ProfState& prof() {
 void pool_reserve(size_t bytes) {
   ensure_init();
   static std::mutex m;
-  static size_t reserved = 0;
+  static size_t reserved = 0, requested = 0;
   std::lock_guard<std::mutex> lk(m);
+  if (bytes <= requested) return;  // (cudaMemGetInfo stalls now and then: ask only when growing)
+  requested = bytes;
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return;
   bytes = std::min(bytes, static_cast<size_t>(0.6 * static_cast<double>(fr + reserved)));

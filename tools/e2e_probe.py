@@ -20,7 +20,7 @@ def main(n=256):
     setup = M.SetupConfig(alpha=0.5, reuse_caches=True)
     solver = M.SolverConfig(method=M.PCG, tol=1e-8, max_iters=500)
     gpu.setup_and_solve(A, b, setup, M.CycleConfig(), solver)
-    for _ in range(2):
+    for _ in range(5):
         ca = A._c()
         t0 = time.perf_counter()
         dm = C.c_void_p()

@@ -27,7 +27,7 @@ c = M.CycleConfig()._c()
 v = M.SolverConfig(method=M.FGMRES if kind == "aniso" else M.PCG, tol=1e-8, max_iters=500,
                    restart=30)._c()
 hist = np.zeros(600)
-for step in range(4):
+for step in range(int(os.environ.get("STEPS", "4"))):
     t0 = time.perf_counter()
     h = C.c_void_p()
     assert lib.fn("setup_hierarchy_device")(dm, C.byref(s), C.byref(h)) == 0
