@@ -117,38 +117,6 @@ __global__ void k_col_count(const idx* col, int64_t nnz, idx* cnt) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k < nnz) atomicAdd(&cnt[col[k]], 1);
 }
-__global__ void k_scatter_pattern_t(const idx* rowptr, const idx* col, int64_t n, const idx* trow,
-                                    idx* cursor, idx* tcol) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  for (idx k = rowptr[i]; k < rowptr[i + 1]; ++k) {
-    const idx j = col[k];
-    tcol[trow[j] + atomicAdd(&cursor[j], 1)] = static_cast<idx>(i);
-  }
-}
-// Sorted merge of C row i and C^T row i (strength.cpp:86-103).  mode 0 counts.
-__global__ void k_merge_rows(const idx* crp, const idx* ccol, const idx* trp, const idx* tcol,
-                             int64_t n, int mode, const idx* srp, idx* out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  idx a = crp[i], ae = crp[i + 1], b = trp[i], be = trp[i + 1];
-  idx cnt = 0;
-  idx* o = mode ? out + srp[i] : nullptr;
-  while (a < ae || b < be) {
-    idx j;
-    if (b >= be || (a < ae && ccol[a] <= tcol[b])) {
-      j = ccol[a];
-      if (b < be && tcol[b] == j) ++b;
-      ++a;
-    } else {
-      j = tcol[b++];
-    }
-    if (o) o[cnt] = j;
-    ++cnt;
-  }
-  if (!mode) out[i] = cnt;
-}
-
 // S = C u C^T and the influence counts without materialising C^T (strength.cpp:74-111).
 // Strength graphs are structurally symmetric almost everywhere, so each entry (r, c) is
 // probed for its mirror (c, r) by binary search in the sorted row c: a mirrored entry adds
