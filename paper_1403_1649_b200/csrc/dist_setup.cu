@@ -1113,6 +1113,7 @@ void dist_refresh_values(DistHierarchy& h, const double* new_values_local) {
   h.drop_graphs();  // the smoother arrays are rebuilt below; captured pointers would dangle
   DistCsr& A0 = h.kd() ? *h.levels[0].A : *h.tail_A;
   copy_double(A0.A.val.get(), new_values_local, A0.A.nnz);
+  A0.A.refresh_sell();
   for (int64_t k = 0; k < h.kd(); ++k) {
     DistLevel& L = h.levels[k];
     DistGalerkin& g = *L.galc;
@@ -1136,6 +1137,7 @@ void dist_refresh_values(DistHierarchy& h, const double* new_values_local) {
     DistCsr& next = (k + 1 < h.kd()) ? *h.levels[k + 1].A : *h.tail_A;
     require(Ac->nnz == next.A.nnz, "refresh_values: coarse pattern changed");
     copy_double(next.A.val.get(), Ac->val.get(), Ac->nnz);
+    next.A.refresh_sell();
     dist_smoother(comm, L, h.cfg, k);
   }
   // the agglomerated tail: gather level kd's new values (row order = rank order) to rank 0

@@ -157,11 +157,13 @@ void refresh_values(DevHierarchy& h, const double* new_values_dev) {
   h.graphs.clear();
   DevLevel& L0 = h.levels[0];
   copy_double(L0.A->val.get(), new_values_dev, L0.A->nnz);
+  L0.A->refresh_sell();
   SmootherBatch smoothers;
   for (int64_t k = 0; k + 1 < h.n_levels(); ++k) {
     DevLevel& fine = h.levels[k];
     DevCsrPtr Ac = apply_galerkin_cache(fine.gal, *fine.A, fine.tr.pval.get());
     copy_double(h.levels[k + 1].A->val.get(), Ac->val.get(), Ac->nnz);
+    h.levels[k + 1].A->refresh_sell();
     smoothers.add(*fine.A, h.cfg.smoother, h.cfg.arnoldi_m,
                   level_seed(h.cfg.seed, k + h.cfg.level_offset, kSmootherTag), fine.smoother,
                   static_cast<int>(k));

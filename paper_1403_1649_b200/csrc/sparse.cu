@@ -60,6 +60,26 @@ __global__ void k_max_block_span(const idx* rowptr, int64_t n, int rpb, int* out
 
 }  // namespace
 
+// ---- SELL-32 copy -------------------------------------------------------------------------
+__global__ void k_slice_width(const idx* rowptr, int64_t n, int64_t nslices, idx* w) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= nslices) return;
+  idx m = 0;
+  const int64_t r1 = min(n, 32 * (s + 1));
+  for (int64_t r = 32 * s; r < r1; ++r) m = max(m, rowptr[r + 1] - rowptr[r]);
+  w[s] = 32 * m;
+}
+__global__ void k_sell_fill(const idx* rowptr, const idx* col, const double* val, int64_t n,
+                            const idx* sptr, idx* scol, double* sval, int with_cols) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const idx base = sptr[r >> 5] + static_cast<idx>(r & 31), k0 = rowptr[r], len = rowptr[r + 1] - k0;
+  for (idx k = 0; k < len; ++k) {
+    if (with_cols) scol[base + 32 * k] = col[k0 + k];
+    sval[base + 32 * k] = val[k0 + k];
+  }
+}
+
 constexpr int kStreamThreads = 256;
 constexpr int kStreamTarget = 2048;  // staged products per row block (16 KB)
 
@@ -98,6 +118,37 @@ void DevCsr::plan() {
   require(static_cast<int64_t>(smem_entries) * 8 <= 227 * 1024,
           "spmv: a row has " + std::to_string(max_row) +
               " entries, beyond the CSR-stream staging capacity");
+  // SELL-32 for large square operators with longer, moderately regular rows (AGGMG_SELL=0
+  // disables).  Measured (tools/kernel_bench.py): 27-point level 0 0.72 -> 0.99 of peak, c2
+  // level 1 (13.6 per row) 0.59 -> 0.69; the restriction R (gathers dominate) and the
+  // L2-resident coarse levels are slower as SELL, so they keep the CSR-stream kernel.
+  static const bool sell_on = [] {
+    const char* e = std::getenv("AGGMG_SELL");
+    return !(e && e[0] == '0');
+  }();
+  sell = false;
+  if (sell_on && n_rows == n_cols && mean >= 10.0 && n_rows >= (int64_t{1} << 19) && max_row <= 64) {
+    const int64_t ns = (n_rows + 31) / 32;
+    DevBuf<idx> w(ns);
+    AGG_LAUNCH(k_slice_width, grid_for(ns, 256), 256, 0, rowptr.get(), n_rows, ns, w.get());
+    sell_ptr.resize(ns + 1);
+    const int64_t slots = scan_to_offsets(w.get(), sell_ptr.get(), ns);
+    if (slots <= static_cast<int64_t>(1.5 * static_cast<double>(nnz)) + 32 * 64) {
+      sell_col.resize(slots);
+      sell_val.resize(slots);
+      AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(),
+                 n_rows, sell_ptr.get(), sell_col.get(), sell_val.get(), 1);
+      sell = true;
+    } else {
+      sell_ptr.reset();
+    }
+  }
+}
+
+void DevCsr::refresh_sell() {
+  if (!sell || n_rows == 0) return;
+  AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
+             sell_ptr.get(), sell_col.get(), sell_val.get(), 0);
 }
 
 DevCsrPtr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, const int64_t* col,
@@ -301,10 +352,74 @@ __global__ void __launch_bounds__(kStreamThreads)
   }
 }
 
+// SELL-32 SpMV family: a thread per row, a warp per slice; slot k of the 32 rows of a warp is
+// one coalesced 256-byte load of values and 128 bytes of columns, no staging and no block
+// barriers.  Each row sums its own entries in CSR order (the slot order), and the same
+// epilogues apply: bit-identical to k_csr_stream.
+template <Epi E>
+__global__ void __launch_bounds__(256)
+    k_sell(const idx* __restrict__ rowptr, const idx* __restrict__ sptr, const idx* __restrict__ scol,
+           const double* __restrict__ sval, int64_t n, SpmvArgs a, double* partials, unsigned* ticket) {
+  constexpr int NP = EpiTraits<E>::np;
+  constexpr int NPX = NP > 0 ? NP : 1;
+  __shared__ __align__(16) double red_smem[32 * 3 + 2];
+  if (a.pred && !*a.pred) return;
+  const double* __restrict__ x = a.x;
+  double v[NPX];
+#pragma unroll
+  for (int k = 0; k < NPX; ++k) v[k] = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const idx len = rowptr[r + 1] - rowptr[r];
+    const idx* c = scol + sptr[r >> 5] + (r & 31);
+    const double* vv = sval + sptr[r >> 5] + (r & 31);
+    double sum = 0.0;
+    idx k = 0;
+    for (; k + 4 <= len; k += 4) {
+      const idx c0 = __ldcs(c + 32 * k), c1 = __ldcs(c + 32 * (k + 1)), c2 = __ldcs(c + 32 * (k + 2)),
+                c3 = __ldcs(c + 32 * (k + 3));
+      const double v0 = __ldcs(vv + 32 * k), v1 = __ldcs(vv + 32 * (k + 1)),
+                   v2 = __ldcs(vv + 32 * (k + 2)), v3 = __ldcs(vv + 32 * (k + 3));
+      const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
+      sum = __dadd_rn(sum, __dmul_rn(v0, x0));
+      sum = __dadd_rn(sum, __dmul_rn(v1, x1));
+      sum = __dadd_rn(sum, __dmul_rn(v2, x2));
+      sum = __dadd_rn(sum, __dmul_rn(v3, x3));
+    }
+    for (; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldcs(vv + 32 * k), __ldg(x + __ldcs(c + 32 * k))));
+    row_epilogue<E>(a, x, r, sum, v);
+  }
+  if constexpr (NP > 0) {
+    block_reduce<NPX>(v, red_smem);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int k = 0; k < NP; ++k) partials[blockIdx.x * NP + k] = v[k];
+    finish_reduction<NPX>(partials, ticket, a.dots_out, red_smem);
+  }
+}
+
+template <Epi E>
+void launch_sell(const DevCsr& A, const SpmvArgs& a) {
+  static thread_local int per_sm = 0;
+  if (!per_sm) {
+    AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sell<E>, 256, 0));
+    per_sm = std::max(1, per_sm);
+  }
+  const int64_t grid = std::min<int64_t>(grid_for(A.n_rows, 256), static_cast<int64_t>(per_sm) * sm_count());
+  AGG_LAUNCH(k_sell<E>, static_cast<unsigned>(grid), 256, 0, A.rowptr.get(), A.sell_ptr.get(),
+             A.sell_col.get(), A.sell_val.get(), A.n_rows, a, reduce_partials(), reduce_ticket());
+}
+
 template <Epi E>
 void launch_stream(const DevCsr& A, const SpmvArgs& a) {
   const int64_t nrows = a.row_count >= 0 ? a.row_count : A.n_rows - a.row_base;
   if (nrows <= 0) return;
+  if constexpr (E != Epi::kResidualZero) {
+    if (A.sell && a.row_base == 0 && a.row_count < 0) {
+      launch_sell<E>(A, a);
+      return;
+    }
+  }
   const int64_t nblocks = (nrows + A.rows_per_block - 1) / A.rows_per_block;
   const size_t smem = sizeof(double) * A.smem_entries;
   static thread_local bool raised = false;

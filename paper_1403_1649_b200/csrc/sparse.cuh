@@ -24,8 +24,14 @@ struct DevCsr {
   int max_row = 0;         // longest row
   int rows_per_block = 0;  // CSR-stream plan
   int smem_entries = 0;
+  // SELL-32 copy for operators with longer rows (sparse.cu): slice s = rows [32s, 32s+32),
+  // slot k of its row r at sell_ptr[s] + 32k + (r & 31) — the row's k-th CSR entry
+  bool sell = false;
+  DevBuf<idx> sell_ptr, sell_col;
+  DevBuf<double> sell_val;
 
-  void plan();  // computes max_row / rows_per_block (synchronises)
+  void plan();          // computes max_row / rows_per_block, builds the SELL copy (synchronises)
+  void refresh_sell();  // after val changed in place: recopy the SELL values
 };
 using DevCsrPtr = std::shared_ptr<DevCsr>;
 
