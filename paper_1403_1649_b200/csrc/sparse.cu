@@ -118,16 +118,22 @@ void DevCsr::plan() {
   require(static_cast<int64_t>(smem_entries) * 8 <= 227 * 1024,
           "spmv: a row has " + std::to_string(max_row) +
               " entries, beyond the CSR-stream staging capacity");
-  // SELL-32 for large square operators with longer, moderately regular rows (AGGMG_SELL=0
-  // disables).  Measured (tools/kernel_bench.py): 27-point level 0 0.72 -> 0.99 of peak, c2
-  // level 1 (13.6 per row) 0.59 -> 0.69; the restriction R (gathers dominate) and the
-  // L2-resident coarse levels are slower as SELL, so they keep the CSR-stream kernel.
+  // SELL-32 for large square operators with rows of 4-64 entries (AGGMG_SELL=0 disables).
+  // Measured (tools/kernel_bench.py): 27-point level 0 0.72 -> 0.99 of peak, 7-point level 0
+  // 0.88 -> 0.97, c2 level 1 (13.6 per row) 0.59 -> 0.69; the restriction R (gathers
+  // dominate) and the L2-resident coarse levels are slower as SELL and keep CSR-stream.
   static const bool sell_on = [] {
     const char* e = std::getenv("AGGMG_SELL");
     return !(e && e[0] == '0');
   }();
   sell = false;
-  if (sell_on && n_rows == n_cols && mean >= 10.0 && n_rows >= (int64_t{1} << 19) && max_row <= 64) {
+  static const double sell_min_mean = [] {
+    const char* e = std::getenv("AGGMG_SELL_MIN_MEAN");
+    return e ? std::atof(e) : 4.0;
+  }();
+  sell_short = mean < 10.0;
+  if (sell_on && n_rows == n_cols && mean >= sell_min_mean && n_rows >= (int64_t{1} << 19) &&
+      max_row <= 64) {
     const int64_t ns = (n_rows + 31) / 32;
     DevBuf<idx> w(ns);
     AGG_LAUNCH(k_slice_width, grid_for(ns, 256), 256, 0, rowptr.get(), n_rows, ns, w.get());
@@ -415,7 +421,10 @@ void launch_stream(const DevCsr& A, const SpmvArgs& a) {
   const int64_t nrows = a.row_count >= 0 ? a.row_count : A.n_rows - a.row_base;
   if (nrows <= 0) return;
   if constexpr (E != Epi::kResidualZero) {
-    if (A.sell && a.row_base == 0 && a.row_count < 0) {
+    // short rows (7-point level 0): the Jacobi + PCG-dots sweep measured faster as CSR-stream
+    // (0.845 vs 0.824 of peak), every other epilogue faster as SELL (0.95-0.97 vs 0.86-0.89)
+    const bool skip = E == Epi::kJacobiDot2 && A.sell_short;
+    if (A.sell && !skip && a.row_base == 0 && a.row_count < 0) {
       launch_sell<E>(A, a);
       return;
     }

@@ -27,6 +27,7 @@ struct DevCsr {
   // SELL-32 copy for operators with longer rows (sparse.cu): slice s = rows [32s, 32s+32),
   // slot k of its row r at sell_ptr[s] + 32k + (r & 31) — the row's k-th CSR entry
   bool sell = false;
+  bool sell_short = false;  // mean row length < 10
   DevBuf<idx> sell_ptr, sell_col;
   DevBuf<double> sell_val;
 
