@@ -132,8 +132,10 @@ void DevCsr::plan() {
     return e ? std::atof(e) : 4.0;
   }();
   sell_short = mean < 10.0;
-  if (sell_on && n_rows == n_cols && mean >= sell_min_mean && n_rows >= (int64_t{1} << 19) &&
-      max_row <= 64) {
+  // near-square: the operators, including a partitioned level's local rows (columns = owned +
+  // halo); not the restriction (n_c x n)
+  if (sell_on && n_cols >= n_rows && n_cols <= n_rows + n_rows / 2 && mean >= sell_min_mean &&
+      n_rows >= (int64_t{1} << 19) && max_row <= 64) {
     const int64_t ns = (n_rows + 31) / 32;
     DevBuf<idx> w(ns);
     AGG_LAUNCH(k_slice_width, grid_for(ns, 256), 256, 0, rowptr.get(), n_rows, ns, w.get());
@@ -365,7 +367,8 @@ __global__ void __launch_bounds__(kStreamThreads)
 template <Epi E>
 __global__ void __launch_bounds__(256)
     k_sell(const idx* __restrict__ rowptr, const idx* __restrict__ sptr, const idx* __restrict__ scol,
-           const double* __restrict__ sval, int64_t n, SpmvArgs a, double* partials, unsigned* ticket) {
+           const double* __restrict__ sval, int64_t row0, int64_t n, SpmvArgs a, double* partials,
+           unsigned* ticket) {
   constexpr int NP = EpiTraits<E>::np;
   constexpr int NPX = NP > 0 ? NP : 1;
   __shared__ __align__(16) double red_smem[32 * 3 + 2];
@@ -375,7 +378,9 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int k = 0; k < NPX; ++k) v[k] = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
+  // rows [row0, row0 + n) (a sub-range for the partitioned path's interior / boundary split)
+  for (int64_t r = row0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < row0 + n;
+       r += stride) {
     const idx len = rowptr[r + 1] - rowptr[r];
     const idx* c = scol + sptr[r >> 5] + (r & 31);
     const double* vv = sval + sptr[r >> 5] + (r & 31);
@@ -411,9 +416,11 @@ void launch_sell(const DevCsr& A, const SpmvArgs& a) {
     AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sell<E>, 256, 0));
     per_sm = std::max(1, per_sm);
   }
-  const int64_t grid = std::min<int64_t>(grid_for(A.n_rows, 256), static_cast<int64_t>(per_sm) * sm_count());
+  const int64_t nrows = a.row_count >= 0 ? a.row_count : A.n_rows - a.row_base;
+  const int64_t grid = std::min<int64_t>(grid_for(nrows, 256), static_cast<int64_t>(per_sm) * sm_count());
   AGG_LAUNCH(k_sell<E>, static_cast<unsigned>(grid), 256, 0, A.rowptr.get(), A.sell_ptr.get(),
-             A.sell_col.get(), A.sell_val.get(), A.n_rows, a, reduce_partials(), reduce_ticket());
+             A.sell_col.get(), A.sell_val.get(), a.row_base, nrows, a, reduce_partials(),
+             reduce_ticket());
 }
 
 template <Epi E>
@@ -424,7 +431,7 @@ void launch_stream(const DevCsr& A, const SpmvArgs& a) {
     // short rows (7-point level 0): the Jacobi + PCG-dots sweep measured faster as CSR-stream
     // (0.845 vs 0.824 of peak), every other epilogue faster as SELL (0.95-0.97 vs 0.86-0.89)
     const bool skip = E == Epi::kJacobiDot2 && A.sell_short;
-    if (A.sell && !skip && a.row_base == 0 && a.row_count < 0) {
+    if (A.sell && !skip) {
       launch_sell<E>(A, a);
       return;
     }
