@@ -1,4 +1,5 @@
 #!/bin/bash
+# usage: tools/build_variant.sh <name> -DFOO=1 ...; then VARIANTS="<name>" bash tools/variant_compare.sh on the GPU box
 # kernel_bench every built variant in build/variants/ (c2 and c4 problems)
 for v in ${VARIANTS:-$(ls build/variants)}; do
   for P in ${PROBLEMS:-c2 c4}; do
