@@ -82,8 +82,24 @@ __global__ void __launch_bounds__(kB) k_mgs_step(int64_t n, const double* hcol, 
   __shared__ double smem[32];
   const double mh = -hcol[i];
   double acc[1] = {0.0};
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+  // 16-byte accesses: three streams of a 450 MB basis vector per step need the bytes in flight
+  const int64_t np = n >> 1;
+  const double2* Vi2 = reinterpret_cast<const double2*>(Vi);
+  const double2* Vn2 = reinterpret_cast<const double2*>(Vnext);
+  double2* w2 = reinterpret_cast<double2*>(w);
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < np;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double2 v = w2[t];
+    const double2 a = Vi2[t];
+    v.x = __dadd_rn(v.x, __dmul_rn(mh, a.x));
+    v.y = __dadd_rn(v.y, __dmul_rn(mh, a.y));
+    w2[t] = v;
+    const double2 o = Vnext ? Vn2[t] : v;
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(o.x, v.x));
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(o.y, v.y));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t t = n - 1;
     const double v = __dadd_rn(w[t], __dmul_rn(mh, Vi[t]));
     w[t] = v;
     const double o = Vnext ? Vnext[t] : v;
@@ -92,6 +108,10 @@ __global__ void __launch_bounds__(kB) k_mgs_step(int64_t n, const double* hcol, 
   block_reduce<1>(acc, smem);
   if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
   finish_reduction<1>(partials, ticket, out, smem);
+}
+unsigned mgs_grid(int64_t n) {
+  const int64_t want = (n / 2 + kB - 1) / kB;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 8 * int64_t{sm_count()})));
 }
 
 // ---- reference-order (exact) variants of the fused vector kernels ---------------------
@@ -386,7 +406,7 @@ SolveOut fgmres(const DevCsr& A, const double* b, double* x, const Precond& M,
           op.w = w.get();
           launch_chunked<1>(op, n, hcol.get() + i + 1);
         } else {
-          AGG_LAUNCH(k_mgs_step, reduce_grid(n), kB, 0, n, hcol.get(), i, V[i].get(), vnext,
+          AGG_LAUNCH(k_mgs_step, mgs_grid(n), kB, 0, n, hcol.get(), i, V[i].get(), vnext,
                      w.get(), hcol.get() + i + 1, reduce_partials(), reduce_ticket());
           reduce(dist, hcol.get() + i + 1, 1);
         }
