@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kRedBlock) k_dot(DotArgs args, int64_t n, doub
 
 unsigned reduce_grid(int64_t n) {
   const int64_t want = (n + kRedBlock * 8 - 1) / (kRedBlock * 8);
-  const int64_t cap = 4 * static_cast<int64_t>(sm_count());
+  const int64_t cap = 8 * static_cast<int64_t>(sm_count());
   return static_cast<unsigned>(std::max<int64_t>(1, std::min(want, cap)));
 }
 double* reduce_partials() { return red().partials; }
