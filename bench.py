@@ -269,6 +269,9 @@ def run_b200(args, world, rank, local):
         check(lib.fn("dmatrix_poisson")(dims, nx, ny, nz, eps, -1, C.byref(dm)))
     n_, nnz_ = C.c_int64(), C.c_int64()
     check(lib.fn("dmatrix_size")(dm, C.byref(n_), C.byref(nnz_)))
+    sell_ = C.c_int32()
+    check(lib.fn("dmatrix_format")(dm, C.byref(sell_)))
+    l0_sell = bool(sell_.value)
     n, nnz = n_.value, nnz_.value
     hist = np.zeros(solver.max_iters + 2)
 
@@ -350,11 +353,17 @@ def run_b200(args, world, rank, local):
     roof = None
     if jc > 0:
         achieved = (jb / jc) / ((jt / jc) / 1e3) / 1e9
-        traffic = load_traffic().get(args.config, {}).get("jacobidot2_l0_dram_bytes_per_launch")
+        if l0_sell:
+            tkey = "jacobi_sell_l0_dram_bytes_per_launch"
+            kname = ("k_sell<Epi::kJacobi> on level 0: the damped-Jacobi post-smoothing sweep "
+                     "over the SELL-32 copy of the operator")
+        else:
+            tkey = "jacobidot2_l0_dram_bytes_per_launch"
+            kname = ("k_csr_stream<Epi::kJacobiDot2> on level 0: the fused damped-Jacobi "
+                     "post-smoothing sweep that also produces PCG's (r.z, r_old.z)")
+        traffic = load_traffic().get(args.config, {}).get(tkey)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "kernel": ("k_csr_stream<Epi::kJacobiDot2> on level 0: the fused damped-Jacobi "
-                           "post-smoothing sweep that also produces PCG's (r.z, r_old.z)"),
+                "frac": achieved / peak, "traffic": traffic, "kernel": kname,
                 "bytes_per_launch": jb / jc, "avg_launch_ms": jt / jc, "launches": jc,
                 "peak_source": peak_src,
                 "share_of_step": jt / elapsed_ms if world == 1 else None}

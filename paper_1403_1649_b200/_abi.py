@@ -143,6 +143,7 @@ SIGNATURES = {
     "dmatrix_poisson": (I, [I, L, L, L, C.c_double, I, C.POINTER(vp)]),
     "dmatrix_jump27": (I, [L, L, L, C.c_double, L, C.POINTER(vp)]),
     "dmatrix_size": (I, [vp, i64p, i64p]),
+    "dmatrix_format": (I, [vp, i32p]),
     "dmatrix_to_host": (I, [vp, csrp]),
     "dmatrix_free": (None, [vp]),
     "setup_hierarchy_device": (I, [vp, C.POINTER(SetupConfigC), C.POINTER(vp)]),

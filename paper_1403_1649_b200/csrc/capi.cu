@@ -904,6 +904,10 @@ int aggmg_dmatrix_jump27(int64_t nx, int64_t ny, int64_t nz, double jump, int64_
     *out = m.release();
   });
 }
+int aggmg_dmatrix_format(const aggmg_dmatrix* A, int* sell) {
+  return guarded([&] { *sell = A->A->sell ? 1 : 0; });
+}
+
 int aggmg_dmatrix_size(const aggmg_dmatrix* A, int64_t* n, int64_t* nnz) {
   return guarded([&] {
     if (n) *n = A->A->n_rows;

@@ -225,7 +225,10 @@ void postsmooth(DevHierarchy& h, DevLevel& L, const double* b, double* x, const 
     smooth_sgs(L.smoother, *L.A, b, x, pred);
     return;
   }
-  if (top && !pred && h.top_dot_out) {  // PCG's (r.z, r_old.z) ride on the last sweep
+  // PCG's (r.z, r_old.z) ride on the last sweep — on CSR-stream operators.  With a SELL-32
+  // copy the plain sweep (0.97 of peak) plus PCG's separate two-product dot measured faster
+  // than the fused sweep (0.82-0.85): c2 solve -0.5 ms.
+  if (top && !pred && h.top_dot_out && !L.A->sell) {
     SpmvArgs a;
     a.x = L.t.get();
     a.y = x;
