@@ -195,7 +195,9 @@ void dist_cycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, const
   ja.b = b;
   ja.d = L.smoother.wdiag.get();
   ja.pred = pred;
-  if (k == 0 && !pred && h.top_dot_out) {  // PCG's (r.z, r_old.z) ride on the last sweep
+  // PCG's (r.z, r_old.z) ride on the last sweep on CSR-stream operators (SELL-32: plain sweep
+  // + PCG's separate dot, as on one GPU)
+  if (k == 0 && !pred && h.top_dot_out && !L.A->A.sell) {
     ja.c = h.top_dot_c;
     ja.dots_out = h.top_dot_out;
     dist_spmv(comm, *L.A, Epi::kJacobiDot2, ja, prof);

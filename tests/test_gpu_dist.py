@@ -254,3 +254,25 @@ def test_dist_refresh_values_matches_one_gpu(gpu, P):
     D.run_threads(P, fn)
     compare_hierarchy(hg, out, f"refresh P={P}")
     del Anew
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_dist_sell_operators_match_one_gpu(gpu, P):
+    # local slabs past the SELL-32 threshold (>= 2^19 rows per rank): the partitioned sweeps run
+    # SELL over the interior / boundary row sub-ranges; same iterations, histories within 1e-10,
+    # one rank bit-identical
+    A = gpu.generate_poisson(3, 104, 104, 104)
+    assert A.n_rows // P >= 1 << 19
+    cfg = M.SetupConfig(alpha=0.5, reuse_caches=True)
+    sc = M.SolverConfig(method=M.PCG, tol=1e-8, max_iters=200)
+    cyc = M.CycleConfig()
+    hg = gpu.setup_hierarchy(A, None, cfg)
+    rg = gpu.pcg(A, np.ones(A.n_rows), None, hg, cyc, sc)
+    res = run_dist(A, P, cfg, agglomerate=100_000, solver=sc, cycle=cyc)
+    assert res[0]["info"][1] >= 1  # at least level 0 partitioned
+    s0 = res[0]["solve"]
+    assert s0.report.iterations == rg.report.iterations
+    hd, hs = np.array(s0.report.residual_history), np.array(rg.report.residual_history)
+    if P == 1:
+        assert np.array_equal(bits(hd), bits(hs))
+    assert np.max(np.abs(hd - hs)) <= 1e-10 * hs[0]
