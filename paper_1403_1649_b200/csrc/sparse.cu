@@ -134,8 +134,10 @@ void DevCsr::plan() {
   sell_short = mean < 10.0;
   // near-square: the operators, including a partitioned level's local rows (columns = owned +
   // halo); not the restriction (n_c x n)
-  if (sell_on && n_cols >= n_rows && n_cols <= n_rows + n_rows / 2 && mean >= sell_min_mean &&
-      n_rows >= (int64_t{1} << 19) && max_row <= 64) {
+  // (slot offsets are int32: every slice padded to the longest row must stay below 2^31)
+  const bool fits = ((n_rows + 31) / 32) * 32 * static_cast<int64_t>(max_row) < INT32_MAX;
+  if (sell_on && fits && n_cols >= n_rows && n_cols <= n_rows + n_rows / 2 &&
+      mean >= sell_min_mean && n_rows >= (int64_t{1} << 19) && max_row <= 64) {
     const int64_t ns = (n_rows + 31) / 32;
     DevBuf<idx> w(ns);
     AGG_LAUNCH(k_slice_width, grid_for(ns, 256), 256, 0, rowptr.get(), n_rows, ns, w.get());
