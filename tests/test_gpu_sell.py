@@ -56,3 +56,13 @@ def test_sell_refresh_values(gpu):
     assert r1.report.iterations == r2.report.iterations
     np.testing.assert_array_equal(bits(np.array(r1.report.residual_history)),
                                   bits(np.array(r2.report.residual_history)))
+
+
+def test_sell_arnoldi_omega_bit_exact(gpu, ref):
+    # the damped-Jacobi Arnoldi estimate runs its SpMVs through the SELL-32 kernel on operators
+    # this large; omega and rho stay bit-identical to the reference
+    A = gpu.generate_poisson(3, 104, 104, 104)
+    sg = gpu.setup_smoother(A, M.DAMPED_JACOBI, 5, 11)
+    sr = ref.setup_smoother(A, M.DAMPED_JACOBI, 5, 11)
+    assert sg.omega == sr.omega and sg.rho_est == sr.rho_est
+    np.testing.assert_array_equal(bits(sg.inv_diag), bits(sr.inv_diag))
