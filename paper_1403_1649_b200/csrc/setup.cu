@@ -1031,6 +1031,89 @@ __global__ void k_gal_numeric(int64_t nnz_c, const idx* seg_off, const idx* entr
   out[s] = acc;
 }
 
+__global__ void k_max_rowlen(const idx* rp, int64_t n, int* out) {
+  int m = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = max(m, rp[i + 1] - rp[i]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// Row-walk numeric reduce (same sums as k_gal_numeric, different data path): a warp per coarse
+// row walks its members ascending and each member's CSR row in order — contiguous reads of
+// A and slot_of_csr instead of gathers through entry / entry_row — and adds every product into
+// its slot in walk order (equal-slot lanes of one round add one after another, lowest lane
+// first), which is the segment's stored order.  Coarse rows of <= 64 entries.
+constexpr int kWalkWarps = 8, kWalkSlots = 64;
+__global__ void __launch_bounds__(kWalkWarps * 32)
+    k_gal_numeric_walk(int64_t nc, const idx* goff, const idx* grows, const idx* arp,
+                       const idx* acol, const double* aval, const idx* slot_of_csr,
+                       const double* pv, const idx* crp, double* out) {
+  __shared__ double s_acc[kWalkWarps][kWalkSlots];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t I = static_cast<int64_t>(blockIdx.x) * kWalkWarps + w;
+  if (I >= nc) return;
+  double* acc = s_acc[w];
+  const idx s0 = crp[I], ns = crp[I + 1] - s0;
+  for (int t = lane; t < kWalkSlots; t += 32) acc[t] = 0.0;
+  __syncwarp();
+  for (idx mb = goff[I]; mb < goff[I + 1]; mb += 32) {
+    const idx m = mb + lane;
+    const int nm = static_cast<int>(min(static_cast<idx>(32), goff[I + 1] - mb));
+    idx i = 0, lo = 0, len = 0;
+    double pvi = 0.0;
+    if (lane < nm) {
+      i = grows[m];
+      lo = arp[i];
+      len = arp[i + 1] - lo;
+      pvi = pv[i];
+    }
+    idx incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const idx t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const idx excl = incl - len;
+    const idx T = __shfl_sync(0xffffffffu, incl, 31);
+    for (idx pb = 0; pb < T; pb += 32) {
+      const idx p = pb + lane;
+      int a = 0, b = nm;  // last member with excl <= p
+#pragma unroll
+      for (int step = 0; step < 6; ++step) {
+        const int mid = (a + b) >> 1;
+        const idx em = __shfl_sync(0xffffffffu, excl, mid & 31);
+        if (b - a > 1) {
+          if (em <= p) a = mid;
+          else b = mid;
+        }
+      }
+      const idx mlo = __shfl_sync(0xffffffffu, lo, a);
+      const idx mex = __shfl_sync(0xffffffffu, excl, a);
+      const double mpv = __shfl_sync(0xffffffffu, pvi, a);
+      int sl = -1 - lane;
+      double c = 0.0;
+      if (p < T) {
+        const idx k = mlo + (p - mex);
+        c = __dmul_rn(__dmul_rn(mpv, aval[k]), pv[acol[k]]);
+        sl = slot_of_csr[k] - s0;
+      }
+      const unsigned grp = __match_any_sync(0xffffffffu, sl);
+      const int rk = __popc(grp & ((1u << lane) - 1u));
+      int mx = rk;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int step = 0; step <= mx; ++step) {
+        if (p < T && rk == step) acc[sl] = __dadd_rn(acc[sl], c);
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+  for (idx t = lane; t < ns; t += 32) out[s0 + t] = acc[t];
+}
+
 __global__ void k_fingerprint(const idx* rowptr, int64_t n, const idx* col, int64_t nnz,
                               const idx* assignment, unsigned long long* out) {
   unsigned long long h = 0;
@@ -1356,6 +1439,21 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
   AGG_CUDA(cudaMemcpyAsync(g.segment_offsets.get() + g.nnz_coarse, &nnz32, sizeof(idx),
                            cudaMemcpyHostToDevice, stream()));
   sync();  // nnz32 lives on the host stack
+  if (!partial) {
+    g.group_offsets.resize(nc + 1);
+    AGG_CUDA(cudaMemcpyAsync(g.group_offsets.get(), agg.agg_row_offsets.get(), sizeof(idx) * (nc + 1),
+                             cudaMemcpyDeviceToDevice, stream()));
+    g.group_rows.resize(A.n_rows);
+    if (A.n_rows > 0)
+      AGG_CUDA(cudaMemcpyAsync(g.group_rows.get(), agg.rows_by_coarse.get(), sizeof(idx) * A.n_rows,
+                               cudaMemcpyDeviceToDevice, stream()));
+    DevBuf<int> mr(1);
+    mr.zero();
+    if (nc > 0)
+      AGG_LAUNCH(k_max_rowlen, grid_for(nc, 256, 4 * sm_count()), 256, 0, g.coarse_rowptr.get(), nc,
+                 mr.get());
+    g.max_coarse_row = read_scalar(mr.get());
+  }
   if (!partial && fingerprint) g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
   return g;
 }
@@ -1372,9 +1470,15 @@ DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const doub
   if (g.nnz_coarse > 0) {
     AGG_CUDA(cudaMemcpyAsync(Ac->col.get(), g.coarse_col.get(), sizeof(idx) * g.nnz_coarse,
                              cudaMemcpyDeviceToDevice, stream()));
-    AGG_LAUNCH(k_gal_numeric, grid_for(g.nnz_coarse, 256), 256, 0, g.nnz_coarse,
-               g.segment_offsets.get(), g.entry.get(), g.entry_row.get(), A.col.get(), A.val.get(),
-               pval, Ac->val.get());
+    if (g.group_offsets.size() == g.n_coarse + 1 && g.max_coarse_row <= kWalkSlots)
+      AGG_LAUNCH(k_gal_numeric_walk, static_cast<unsigned>((g.n_coarse + kWalkWarps - 1) / kWalkWarps),
+                 kWalkWarps * 32, 0, g.n_coarse, g.group_offsets.get(), g.group_rows.get(),
+                 A.rowptr.get(), A.col.get(), A.val.get(), g.slot_of_csr.get(), pval,
+                 g.coarse_rowptr.get(), Ac->val.get());
+    else
+      AGG_LAUNCH(k_gal_numeric, grid_for(g.nnz_coarse, 256), 256, 0, g.nnz_coarse,
+                 g.segment_offsets.get(), g.entry.get(), g.entry_row.get(), A.col.get(),
+                 A.val.get(), pval, Ac->val.get());
   }
   Ac->plan();
   return Ac;

@@ -55,6 +55,9 @@ struct GalerkinDev {
   int64_t n_fine = 0, n_coarse = 0, nnz_fine = 0, nnz_coarse = 0;
   DevBuf<idx> coarse_rowptr, coarse_col;
   DevBuf<idx> entry, entry_row, segment_offsets, slot_of_csr;
+  DevBuf<idx> group_offsets, group_rows;  // copy of the aggregate grouping (not for partial
+                                          // caches): the row-walk numeric reduce
+  int max_coarse_row = 0;
   uint64_t pattern_hash = 0;
 };
 // partial: the groups cover only some rows of A (rows of other groups, and halo rows, are
