@@ -190,6 +190,26 @@ __global__ void k_gemv(int64_t n, const double* __restrict__ M, const double* __
   if (lane == 0) x[row] = s;
 }
 
+// LuFactors::solve (dense.cpp:63-79) in the reference's operation order: forward
+// substitution with the row permutation, back substitution with the division by U_ii.  One
+// thread — the sums are sequential by definition; only the exact-reduction mode uses it.
+__global__ void k_lu_solve(int64_t n, const double* __restrict__ lu, const int* __restrict__ perm,
+                           const double* __restrict__ b, double* __restrict__ x, const int* pred) {
+  if (!on(pred) || threadIdx.x != 0) return;
+  for (int64_t i = 0; i < n; ++i) {
+    double s = b[perm[i]];
+    const double* ri = lu + i * n;
+    for (int64_t j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(ri[j], x[j]));
+    x[i] = s;
+  }
+  for (int64_t i = n - 1; i >= 0; --i) {
+    double s = x[i];
+    const double* ri = lu + i * n;
+    for (int64_t j = i + 1; j < n; ++j) s = __dsub_rn(s, __dmul_rn(ri[j], x[j]));
+    x[i] = __ddiv_rn(s, ri[i]);
+  }
+}
+
 // the global finest level (profiling families time level 0 only)
 bool finest(const DevHierarchy& h, int64_t k) { return k + h.cfg.level_offset == 0; }
 
@@ -322,8 +342,8 @@ void subcycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b, 
     return;
   }
   char keybuf[256];
-  std::snprintf(keybuf, sizeof(keybuf), "%d/%d/%d/%.17g/%d/%lld/%p/%p/%p", vee ? 1 : 0, cfg.kind,
-                cfg.k_levels, cfg.t, cfg.inner, static_cast<long long>(k),
+  std::snprintf(keybuf, sizeof(keybuf), "%d/%d/%d/%d/%.17g/%d/%lld/%p/%p/%p", exact_reductions() ? 1 : 0,
+                vee ? 1 : 0, cfg.kind, cfg.k_levels, cfg.t, cfg.inner, static_cast<long long>(k),
                 static_cast<const void*>(b), static_cast<void*>(x_out),
                 static_cast<const void*>(pred));
   const std::string key(keybuf);
@@ -543,6 +563,10 @@ bool cycle_accelerated(const CycleCfg& cfg, int64_t k) { return accelerated(cfg,
 void coarse_solve(DevHierarchy& h, const double* b, double* x, const int* pred) {
   const int64_t n = h.levels.back().A->n_rows;
   if (n == 0) return;
+  if (exact_reductions() && h.coarse_lu_ready) {  // bit-identical substitution (slow: n^2 chain)
+    AGG_LAUNCH(k_lu_solve, 1, 32, 0, n, h.coarse_lu.get(), h.coarse_perm.get(), b, x, pred);
+    return;
+  }
   AGG_LAUNCH(k_gemv, grid_for(n * 32, 256), 256, 0, n, h.coarse_inv.get(), b, x, pred);
 }
 

@@ -7,6 +7,7 @@
 #include <sstream>
 
 #include "hierarchy.cuh"
+#include "chunked.cuh"
 #include "vecops.cuh"
 
 namespace aggmg_b200 {
@@ -53,6 +54,24 @@ void factor_coarsest(DevHierarchy& h) {
   require(nL <= std::max<int64_t>(h.cfg.coarse_size_max, kDenseSolveCap),
           "setup: coarsest level has " + std::to_string(nL) + " unknowns, too large for a dense solve");
   invert_coarsest(*L.A, h.coarse_inv);  // coarse.cu (dense.cpp:16-79 on the device)
+  h.coarse_lu_ready = false;
+  if (exact_reductions() && nL > 0) {
+    // the reference's own factorisation order, for the bit-identical substitution kernel
+    std::vector<int64_t> rp(nL + 1), col(L.A->nnz);
+    std::vector<double> val(L.A->nnz);
+    download_csr(*L.A, rp.data(), col.data(), val.data());
+    std::vector<double> dense(static_cast<size_t>(nL) * nL, 0.0);  // dense.cpp:16-22
+    for (int64_t i = 0; i < nL; ++i)
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) dense[i * nL + col[k]] = val[k];
+    HostLu lu;
+    lu.factor(std::move(dense), nL);
+    h.coarse_lu.resize(nL * nL);
+    h.coarse_lu.upload(lu.lu.data(), nL * nL);
+    std::vector<int> perm(lu.perm.begin(), lu.perm.end());
+    h.coarse_perm.resize(nL);
+    h.coarse_perm.upload(perm.data(), nL);
+    h.coarse_lu_ready = true;
+  }
   sync();
 }
 

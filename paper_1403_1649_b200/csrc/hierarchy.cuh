@@ -66,6 +66,11 @@ struct DevHierarchy {
   SetupCfg cfg;
   std::vector<std::string> warnings;
   DevBuf<double> coarse_inv;  // explicit inverse of the coarsest operator (row-major)
+  // exact-reduction mode (aggmg_set_exact_reductions(1) before setup): the reference's LU
+  // factors (dense.cpp:16-79, host restatement) for a bit-identical substitution
+  DevBuf<double> coarse_lu;
+  DevBuf<int> coarse_perm;
+  bool coarse_lu_ready = false;
   double setup_ms = 0.0;
   bool workspace_ready = false;
   // PCG hook: the finest level's last damped-Jacobi sweep of a preconditioner application

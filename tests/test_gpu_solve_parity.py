@@ -215,13 +215,37 @@ def test_refresh_values(gpu, ref):
         gpu.refresh_values(h0, v)
 
 
-def test_exact_reduction_mode(gpu, ref):
-    """Reference-order solve reductions: same iterations, closer histories."""
+EXACT_CASES = [
+    ("3d-aniso-fgmres", (3, 24, 24, 24, 1e-3), 0.5, M.DAMPED_JACOBI, M.CycleConfig(), M.FGMRES),
+    ("2d-pcg", (2, 100, 100, 1, 1.0), 0.25, M.DAMPED_JACOBI, M.CycleConfig(), M.PCG),
+    ("2d-aniso-undamped-k", (2, 149, 152, 1, 1e-3), 0.25, M.JACOBI,
+     M.CycleConfig(kind=M.CYCLE_K, inner=M.INNER_GMRES, t=0.25), M.PCG),
+    ("3d-vcycle-cg-inner", (3, 20, 18, 16, 1.0), 0.5, M.DAMPED_JACOBI,
+     M.CycleConfig(kind=M.CYCLE_V, inner=M.INNER_CG), M.FGMRES),
+    ("2d-sgs", (2, 80, 80, 1, 1.0), 0.25, M.SGS, M.CycleConfig(), M.FGMRES),
+]
+
+
+@pytest.mark.parametrize("case", EXACT_CASES, ids=[c[0] for c in EXACT_CASES])
+def test_exact_reduction_mode_bit_identical(gpu, ref, case):
+    """aggmg_set_exact_reductions(1) before setup: the reference's 8192-chunk reduction order
+    everywhere and the reference's LU substitution on the coarsest level.  The whole solve is
+    then bit-identical to the reference: every residual-history entry and the solution."""
+    name, (dims, nx, ny, nz, eps), alpha, smoother, cyc, method = case
     lib = gpu.lib
     lib.fn("set_exact_reductions")(1)
     try:
-        check_solve(gpu, ref, ref.generate_poisson(3, 24, 24, 24, 1e-3), 0.5, M.FGMRES)
-        check_solve(gpu, ref, ref.generate_poisson(2, 100, 100), 0.25, M.PCG)
+        A = ref.generate_poisson(dims, nx, ny, nz, eps)
+        cfg = M.SetupConfig(alpha=alpha, reuse_caches=True, smoother=smoother)
+        hg, hr = gpu.setup_hierarchy(A, None, cfg), ref.setup_hierarchy(A, None, cfg)
+        sc = M.SolverConfig(method=method, tol=1e-8, max_iters=300, restart=30)
+        b = np.ones(A.n_rows)
+        f, g = (gpu.pcg, ref.pcg) if method == M.PCG else (gpu.fgmres, ref.fgmres)
+        rg, rr = f(A, b, None, hg, cyc, sc), g(A, b, None, hr, cyc, sc)
+        assert rg.report.iterations == rr.report.iterations
+        np.testing.assert_array_equal(bits(np.array(rg.report.residual_history)),
+                                      bits(np.array(rr.report.residual_history)))
+        np.testing.assert_array_equal(bits(rg.x), bits(rr.x))
     finally:
         lib.fn("set_exact_reductions")(0)
 
