@@ -57,6 +57,8 @@ inline void check(int rc) {
 }  // namespace detail
 
 inline void set_num_threads(int n) { aggmg_set_num_threads(n); }
+// B200 extension: bit-identical solves (see aggmg_set_exact_reductions in aggmg_b200.h)
+inline void set_exact_reductions(bool on) { aggmg_set_exact_reductions(on ? 1 : 0); }
 inline int num_threads() { return aggmg_num_threads(); }
 
 // ---- sparse.hpp ------------------------------------------------------------------------

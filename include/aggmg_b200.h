@@ -111,7 +111,10 @@ int aggmg_num_threads(void);                     /* parallel.hpp:29 — reports 
 int64_t aggmg_kernel_launches(void);             /* number of kernels this library has launched */
 /* Solve-phase dot products in the reference's 8192-chunk sequential order (1) or as
  * deterministic tree reductions (0, default).  Setup (Arnoldi omega) and aggmg_dot /
- * aggmg_norm2 always use the reference order (vector_ops.hpp:16-40). */
+ * aggmg_norm2 always use the reference order (vector_ops.hpp:16-40).  Set to 1 BEFORE setup
+ * and the hierarchy also keeps the reference's coarsest LU factors (dense.cpp:16-79) for a
+ * substitution in the reference's order: solves are then bit-identical to the reference
+ * (slower: sequential reductions and an n^2 coarse substitution chain). */
 void aggmg_set_exact_reductions(int on);
 int aggmg_exact_reductions(void);
 void aggmg_setup_config_default(aggmg_setup_config* c);
