@@ -3,7 +3,9 @@
 (cache path), preconditioner applications within 1e-12, PCG / FGMRES iteration counts equal
 with histories within 1e-10 * ||r0||.  Problems: 2-D / 3-D Poisson with random sizes and
 anisotropy, 27-point jump operators, random SPD matrices; random smoother / cycle / solver
-settings.  Usage: parity_sweep.py [seconds] [seed]"""
+settings.  Usage: parity_sweep.py [seconds] [seed] [exact]
+exact: aggmg_set_exact_reductions(1) for the whole sweep, and the bar becomes bit-identical
+residual histories and solutions."""
 import os
 import sys
 import time
@@ -39,6 +41,9 @@ def main():
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
     gpu, ref = M.b200(), M.ref()
     assert gpu.lib.fn("init")(0) == 0
+    exact = len(sys.argv) > 3 and sys.argv[3] == "exact"
+    if exact:
+        gpu.lib.fn("set_exact_reductions")(1)
     t0, count, fails = time.time(), 0, 0
     while time.time() - t0 < budget:
         name, A, alpha = problem(gpu, rng)
@@ -69,6 +74,11 @@ def main():
             assert rg.report.iterations == rr.report.iterations, \
                 f"iterations {rg.report.iterations} vs {rr.report.iterations}"
             hg_, hr_ = np.array(rg.report.residual_history), np.array(rr.report.residual_history)
+            if exact:
+                assert hg_.shape == hr_.shape and np.array_equal(bits(hg_), bits(hr_)), "exact history"
+                assert np.array_equal(bits(rg.x), bits(rr.x)), "exact x"
+                count += 1
+                continue
             dev = np.max(np.abs(hg_ - hr_)) / hr_[0]
             if dev > 1e-10:
                 # rounding-order sensitivity or a real difference?  rerun with the reference's
