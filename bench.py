@@ -337,6 +337,23 @@ def run_b200(args, world, rank, local):
                "iterations": res.report.iterations}
         del Ah
 
+    # ---- side number: the same step in bit-identical mode (aggmg_set_exact_reductions) ----
+    exact = None
+    if not args.no_exact:
+        lib.fn("set_exact_reductions")(1)
+        step(None)
+        erec = []
+        dist.barrier()
+        check(lib.fn("synchronize")())
+        check(lib.fn("timer_start")())
+        for _ in range(2):
+            step(erec)
+        check(lib.fn("timer_stop")(C.byref(ms)))
+        lib.fn("set_exact_reductions")(0)
+        exact = {"ms_per_step": dist.max(ms.value) / 2, "iterations": erec[0]["iterations"],
+                 "note": "aggmg_set_exact_reductions(1): residual history and x bit-identical "
+                         "to the reference (DESIGN.md section 5); not the headline"}
+
     # ---- CPU baseline (reference, all host cores, bounded sample) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and os.path.exists(_abi.REF_LIB):
@@ -384,7 +401,8 @@ def run_b200(args, world, rank, local):
                    "level0_spmv_residual_gbs": spmv_gbs,
                    "galerkin": "cached sort/segmented reduce (reference reuse_caches=true order)",
                    "l2": f"inputs larger than L2 (A alone is {(12 * nnz + 4 * n) / 1e9:.2f} GB)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "exact_mode": exact},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -588,6 +606,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-exact", action="store_true", help="skip the bit-identical-mode side number")
     ap.add_argument("--no-prof", action="store_true", help="skip per-launch CUDA-event timing")
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--mode", default="auto", choices=["auto", "single", "dist", "replicas"],

@@ -191,22 +191,90 @@ __global__ void k_gemv(int64_t n, const double* __restrict__ M, const double* __
 }
 
 // LuFactors::solve (dense.cpp:63-79) in the reference's operation order: forward
-// substitution with the row permutation, back substitution with the division by U_ii.  One
-// thread — the sums are sequential by definition; only the exact-reduction mode uses it.
-__global__ void k_lu_solve(int64_t n, const double* __restrict__ lu, const int* __restrict__ perm,
-                           const double* __restrict__ b, double* __restrict__ x, const int* pred) {
+// substitution with the row permutation, back substitution with the division by U_ii.  Only
+// the exact-reduction mode uses it.  One CTA of kLuThreads.
+//  forward, column order: after columns 0..j-1 have been subtracted, s_j is final (x_j);
+//    every row i > j then subtracts L_ij x_j.  Each row still subtracts in ascending j, so
+//    the result is the reference's; the critical path is n barriers, not n^2/2 subtractions.
+//    L is read from the column-major copy lt (coalesced), one column ahead.
+//  backward, row order: row i's chain s -= U_ij x_j (ascending j > i) starts with x_{i+1},
+//    so it is serial by definition.  Lane 0 runs the chain of row i from products that
+//    warps 1.. computed during the previous row (U_ij x_j, j >= i+2, double-buffered in
+//    shared memory), while they compute row i-1's products for j >= i+1.
+// Operators above kLuRows * kLuThreads rows (coarse_size_max raised past the dense cap) take
+// the one-thread k_lu_serial.
+constexpr int kLuThreads = 1024;
+constexpr int kLuRows = 5;  // rows per thread: kDenseSolveCap (5000) / kLuThreads, rounded up
+
+__global__ void __launch_bounds__(kLuThreads) k_lu_solve(int n, const double* __restrict__ lu,
+                                                        const double* __restrict__ lt,
+                                                        const int* __restrict__ perm,
+                                                        const double* __restrict__ b,
+                                                        double* __restrict__ x, const int* pred) {
+  if (!on(pred)) return;
+  extern __shared__ double sh[];
+  double* xs = sh;          // n: x
+  double* pb = sh + n;      // 2n: product buffers
+  const int t = threadIdx.x;
+  double s[kLuRows], lcur[kLuRows];
+#pragma unroll
+  for (int r = 0; r < kLuRows; ++r) {
+    const int i = t + r * kLuThreads;
+    s[r] = i < n ? b[perm[i]] : 0.0;
+    lcur[r] = (i < n && i > 0) ? lt[i] : 0.0;  // column 0
+  }
+  if (t == 0 && n > 0) xs[0] = s[0];
+  __syncthreads();
+  for (int j = 0; j + 1 < n; ++j) {
+    const double xj = xs[j];
+    double lnext[kLuRows];
+#pragma unroll
+    for (int r = 0; r < kLuRows; ++r) {
+      const int i = t + r * kLuThreads;
+      lnext[r] = (i < n && i > j + 1) ? lt[static_cast<int64_t>(j + 1) * n + i] : 0.0;
+      if (i < n && i > j) s[r] = __dsub_rn(s[r], __dmul_rn(lcur[r], xj));
+      if (i == j + 1) xs[i] = s[r];
+      lcur[r] = lnext[r];
+    }
+    __syncthreads();
+  }
+  // backward (xs holds y)
+  const int lane = t & 31, w = t >> 5;
+  for (int i = n - 1; i >= 0; --i) {
+    if (w == 0) {
+      if (lane == 0) {
+        const double* ui = lu + static_cast<int64_t>(i) * n;
+        double acc = xs[i];
+        if (i + 1 < n) acc = __dsub_rn(acc, __dmul_rn(ui[i + 1], xs[i + 1]));
+        const double* p = pb + (i & 1) * n;
+#pragma unroll 8
+        for (int j = i + 2; j < n; ++j) acc = __dsub_rn(acc, p[j]);
+        xs[i] = __ddiv_rn(acc, ui[i]);
+      }
+    } else if (i > 0) {
+      const double* ur = lu + static_cast<int64_t>(i - 1) * n;
+      double* p = pb + ((i - 1) & 1) * n;
+      for (int j = i + 1 + (t - 32); j < n; j += kLuThreads - 32) p[j] = __dmul_rn(ur[j], xs[j]);
+    }
+    __syncthreads();
+  }
+  for (int i = t; i < n; i += kLuThreads) x[i] = xs[i];
+}
+
+__global__ void k_lu_serial(int64_t n, const double* __restrict__ lu, const int* __restrict__ perm,
+                            const double* __restrict__ b, double* __restrict__ x, const int* pred) {
   if (!on(pred) || threadIdx.x != 0) return;
   for (int64_t i = 0; i < n; ++i) {
-    double s = b[perm[i]];
+    double acc = b[perm[i]];
     const double* ri = lu + i * n;
-    for (int64_t j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(ri[j], x[j]));
-    x[i] = s;
+    for (int64_t j = 0; j < i; ++j) acc = __dsub_rn(acc, __dmul_rn(ri[j], x[j]));
+    x[i] = acc;
   }
   for (int64_t i = n - 1; i >= 0; --i) {
-    double s = x[i];
+    double acc = x[i];
     const double* ri = lu + i * n;
-    for (int64_t j = i + 1; j < n; ++j) s = __dsub_rn(s, __dmul_rn(ri[j], x[j]));
-    x[i] = __ddiv_rn(s, ri[i]);
+    for (int64_t j = i + 1; j < n; ++j) acc = __dsub_rn(acc, __dmul_rn(ri[j], x[j]));
+    x[i] = __ddiv_rn(acc, ri[i]);
   }
 }
 
@@ -564,7 +632,19 @@ void coarse_solve(DevHierarchy& h, const double* b, double* x, const int* pred) 
   const int64_t n = h.levels.back().A->n_rows;
   if (n == 0) return;
   if (exact_reductions() && h.coarse_lu_ready) {  // bit-identical substitution (slow: n^2 chain)
-    AGG_LAUNCH(k_lu_solve, 1, 32, 0, n, h.coarse_lu.get(), h.coarse_perm.get(), b, x, pred);
+    const size_t smem = 3 * n * sizeof(double);
+    if (n <= int64_t{kLuRows} * kLuThreads && smem <= 200 * 1024) {
+      static thread_local bool attr = false;  // per rank thread (one device each)
+      if (!attr) {
+        AGG_CUDA(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+        attr = true;
+      }
+      AGG_LAUNCH(k_lu_solve, 1, kLuThreads, smem, static_cast<int>(n), h.coarse_lu.get(),
+                 h.coarse_lu_t.get(), h.coarse_perm.get(), b, x, pred);
+    } else {
+      AGG_LAUNCH(k_lu_serial, 1, 32, 0, n, h.coarse_lu.get(), h.coarse_perm.get(), b, x, pred);
+    }
     return;
   }
   AGG_LAUNCH(k_gemv, grid_for(n * 32, 256), 256, 0, n, h.coarse_inv.get(), b, x, pred);

@@ -67,6 +67,11 @@ void factor_coarsest(DevHierarchy& h) {
     lu.factor(std::move(dense), nL);
     h.coarse_lu.resize(nL * nL);
     h.coarse_lu.upload(lu.lu.data(), nL * nL);
+    std::vector<double> lt(static_cast<size_t>(nL) * nL);
+    for (int64_t i = 0; i < nL; ++i)
+      for (int64_t j = 0; j < nL; ++j) lt[j * nL + i] = lu.lu[i * nL + j];
+    h.coarse_lu_t.resize(nL * nL);
+    h.coarse_lu_t.upload(lt.data(), nL * nL);
     std::vector<int> perm(lu.perm.begin(), lu.perm.end());
     h.coarse_perm.resize(nL);
     h.coarse_perm.upload(perm.data(), nL);

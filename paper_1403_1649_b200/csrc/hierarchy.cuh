@@ -69,6 +69,7 @@ struct DevHierarchy {
   // exact-reduction mode (aggmg_set_exact_reductions(1) before setup): the reference's LU
   // factors (dense.cpp:16-79, host restatement) for a bit-identical substitution
   DevBuf<double> coarse_lu;
+  DevBuf<double> coarse_lu_t;  // the same, column-major (the forward substitution's order)
   DevBuf<int> coarse_perm;
   bool coarse_lu_ready = false;
   double setup_ms = 0.0;

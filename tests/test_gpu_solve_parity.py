@@ -223,6 +223,11 @@ EXACT_CASES = [
     ("3d-vcycle-cg-inner", (3, 20, 18, 16, 1.0), 0.5, M.DAMPED_JACOBI,
      M.CycleConfig(kind=M.CYCLE_V, inner=M.INNER_CG), M.FGMRES),
     ("2d-sgs", (2, 80, 80, 1, 1.0), 0.25, M.SGS, M.CycleConfig(), M.FGMRES),
+    # large coarsest operators: the substitution kernel's multi-row-per-thread paths
+    ("2d-two-level-big-coarsest", (2, 150, 150, 1, 1.0), 0.25, M.DAMPED_JACOBI,
+     M.CycleConfig(), M.PCG, {"max_levels": 2}),
+    ("2d-one-level-4900", (2, 70, 70, 1, 1e-2), 0.25, M.DAMPED_JACOBI, M.CycleConfig(), M.FGMRES,
+     {"max_levels": 1}),
 ]
 
 
@@ -231,12 +236,13 @@ def test_exact_reduction_mode_bit_identical(gpu, ref, case):
     """aggmg_set_exact_reductions(1) before setup: the reference's 8192-chunk reduction order
     everywhere and the reference's LU substitution on the coarsest level.  The whole solve is
     then bit-identical to the reference: every residual-history entry and the solution."""
-    name, (dims, nx, ny, nz, eps), alpha, smoother, cyc, method = case
+    name, (dims, nx, ny, nz, eps), alpha, smoother, cyc, method = case[:6]
+    extra = case[6] if len(case) > 6 else {}
     lib = gpu.lib
     lib.fn("set_exact_reductions")(1)
     try:
         A = ref.generate_poisson(dims, nx, ny, nz, eps)
-        cfg = M.SetupConfig(alpha=alpha, reuse_caches=True, smoother=smoother)
+        cfg = M.SetupConfig(alpha=alpha, reuse_caches=True, smoother=smoother, **extra)
         hg, hr = gpu.setup_hierarchy(A, None, cfg), ref.setup_hierarchy(A, None, cfg)
         sc = M.SolverConfig(method=method, tol=1e-8, max_iters=300, restart=30)
         b = np.ones(A.n_rows)

@@ -27,7 +27,18 @@ c = M.CycleConfig()._c()
 v = M.SolverConfig(method=M.FGMRES if kind == "aniso" else M.PCG, tol=1e-8, max_iters=500,
                    restart=30)._c()
 hist = np.zeros(600)
-for step in range(int(os.environ.get("STEPS", "4"))):
+if os.environ.get("EXACT"):  # aggmg_set_exact_reductions(1): the bit-identical mode
+    lib.fn("set_exact_reductions")(1)
+prof = None
+if os.environ.get("KERNELS"):  # CUPTI kernel table of the last step (torch.profiler)
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.init()
+steps = int(os.environ.get("STEPS", "4"))
+for step in range(steps):
+    if os.environ.get("KERNELS") and step == steps - 1:
+        prof = profile(activities=[ProfilerActivity.CUDA])
+        prof.__enter__()
     t0 = time.perf_counter()
     h = C.c_void_p()
     assert lib.fn("setup_hierarchy_device")(dm, C.byref(s), C.byref(h)) == 0
@@ -44,3 +55,6 @@ for step in range(int(os.environ.get("STEPS", "4"))):
     t3 = time.perf_counter()
     print(f"step {step}: setup {1e3*(t1-t0):.1f} ms, solve {1e3*(t2-t1):.1f} ms ({rep.iterations} its), "
           f"free {1e3*(t3-t2):.1f} ms; report: solve {1e3*rep.solve_seconds:.1f} ms", flush=True)
+if prof is not None:
+    prof.__exit__(None, None, None)
+    print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=60))
