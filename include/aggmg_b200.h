@@ -252,7 +252,8 @@ int aggmg_dmatrix_jump27(int64_t nx, int64_t ny, int64_t nz, double jump, int64_
                          aggmg_dmatrix** out);
 int aggmg_dmatrix_size(const aggmg_dmatrix* A, int64_t* n_rows, int64_t* nnz);
 /* 1 in *sell when the operator carries a SELL-32 copy (large operators, 4-64 entries per row:
- * its SpMV-family kernels run sliced-ELL), else 0 (CSR-stream) */
+ * its SpMV-family kernels run sliced-ELL), 2 when that copy also stores its values as one-byte
+ * codes into a table of the <= 256 distinct values (stencil operators), else 0 (CSR-stream) */
 int aggmg_dmatrix_format(const aggmg_dmatrix* A, int* sell);
 int aggmg_dmatrix_to_host(const aggmg_dmatrix* A, aggmg_csr* out);
 void aggmg_dmatrix_free(aggmg_dmatrix* A);

@@ -905,7 +905,7 @@ int aggmg_dmatrix_jump27(int64_t nx, int64_t ny, int64_t nz, double jump, int64_
   });
 }
 int aggmg_dmatrix_format(const aggmg_dmatrix* A, int* sell) {
-  return guarded([&] { *sell = A->A->sell ? 1 : 0; });
+  return guarded([&] { *sell = A->A->sell ? (A->A->sell_vi ? 2 : 1) : 0; });
 }
 
 int aggmg_dmatrix_size(const aggmg_dmatrix* A, int64_t* n, int64_t* nnz) {

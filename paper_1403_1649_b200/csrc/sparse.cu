@@ -2,6 +2,7 @@
 // the device-side problem generators.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "sparse.cuh"
@@ -61,12 +62,13 @@ __global__ void k_max_block_span(const idx* rowptr, int64_t n, int rpb, int* out
 }  // namespace
 
 // ---- SELL-32 copy -------------------------------------------------------------------------
-__global__ void k_slice_width(const idx* rowptr, int64_t n, int64_t nslices, idx* w) {
+__global__ void k_slice_width(const idx* rowptr, int64_t n, int64_t nslices, int pad4, idx* w) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= nslices) return;
   idx m = 0;
   const int64_t r1 = min(n, 32 * (s + 1));
   for (int64_t r = 32 * s; r < r1; ++r) m = max(m, rowptr[r + 1] - rowptr[r]);
+  if (pad4) m = (m + 3) & ~3;  // packed dictionary codes: whole 4-slot groups per slice
   w[s] = 32 * m;
 }
 __global__ void k_sell_fill(const idx* rowptr, const idx* col, const double* val, int64_t n,
@@ -77,6 +79,75 @@ __global__ void k_sell_fill(const idx* rowptr, const idx* col, const double* val
   for (idx k = 0; k < len; ++k) {
     if (with_cols) scol[base + 32 * k] = col[k0 + k];
     sval[base + 32 * k] = val[k0 + k];
+  }
+}
+
+// ---- value dictionary (CSR-VI style) ----------------------------------------------------
+// Hash set of the distinct value bit patterns: open addressing over kDictSlots, one CAS per
+// new pattern.  A warp first groups equal patterns (__match_any_sync), so a stencil matrix
+// costs a few probes per 32 values.  More than kDictMax patterns, or a value whose pattern is
+// the empty marker, leaves the operator without a dictionary.
+constexpr int kDictSlots = 1024;
+constexpr int kDictMax = 256;
+constexpr unsigned long long kDictEmpty = ~0ull;
+
+__device__ __forceinline__ unsigned dict_hash(unsigned long long u) {
+  u ^= u >> 33;
+  u *= 0xff51afd7ed558ccdull;
+  u ^= u >> 33;
+  return static_cast<unsigned>(u) & (kDictSlots - 1);
+}
+
+__global__ void k_dict_insert(const double* __restrict__ val, int64_t nnz,
+                              unsigned long long* slots, int* state /* [count, bad] */) {
+  volatile int* bad = state + 1;
+  auto give_up = [&] {
+    if (!*bad) atomicExch(state + 1, 1);
+  };
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t start = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // warp-uniform trip count, so every lane reaches the flag check and __match_any_sync
+  for (int64_t base = start - (threadIdx.x & 31); base < nnz; base += stride) {
+    if (__shfl_sync(0xffffffffu, *bad, 0)) return;  // too many distinct values: stop reading
+    const int64_t i = base + (threadIdx.x & 31);
+    const unsigned long long u = i < nnz ? __double_as_longlong(val[i]) : kDictEmpty - 1;
+    const unsigned peers = __match_any_sync(0xffffffffu, u);
+    if (i >= nnz || (threadIdx.x & 31) != __ffs(peers) - 1) continue;  // one lane per pattern
+    if (u == kDictEmpty) {
+      give_up();
+      continue;
+    }
+    unsigned h = dict_hash(u);
+    for (int probe = 0;; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+      if (probe == kDictSlots) {
+        give_up();
+        break;
+      }
+      const unsigned long long cur = slots[h];
+      if (cur == u) break;
+      if (cur != kDictEmpty) continue;
+      const unsigned long long old = atomicCAS(slots + h, kDictEmpty, u);
+      if (old == kDictEmpty) {
+        if (atomicAdd(state, 1) >= kDictMax) give_up();
+        break;
+      }
+      if (old == u) break;
+    }
+  }
+}
+
+__global__ void k_sell_codes(const idx* rowptr, const double* val, int64_t n, const idx* sptr,
+                             const unsigned long long* __restrict__ slots,
+                             const unsigned char* __restrict__ code_of_slot, unsigned char* scode) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const idx k0 = rowptr[r], len = rowptr[r + 1] - k0;
+  for (idx k = 0; k < len; ++k) {
+    const unsigned long long u = __double_as_longlong(val[k0 + k]);
+    unsigned h = dict_hash(u);
+    while (slots[h] != u) h = (h + 1) & (kDictSlots - 1);  // present by construction
+    // packed: the codes of slots 4g..4g+3 of a row are one 32-bit word (byte k & 3)
+    scode[sptr[r >> 5] + 32 * (k & ~3) + 4 * (r & 31) + (k & 3)] = code_of_slot[h];
   }
 }
 
@@ -140,25 +211,78 @@ void DevCsr::plan() {
       mean >= sell_min_mean && n_rows >= (int64_t{1} << 19) && max_row <= 64) {
     const int64_t ns = (n_rows + 31) / 32;
     DevBuf<idx> w(ns);
-    AGG_LAUNCH(k_slice_width, grid_for(ns, 256), 256, 0, rowptr.get(), n_rows, ns, w.get());
+    DevBuf<unsigned long long> dslots;
+    sell_pad4 = dict_scan(dslots) && (((n_rows + 31) / 32) * 32 * int64_t{max_row + 3} < INT32_MAX);
+    AGG_LAUNCH(k_slice_width, grid_for(ns, 256), 256, 0, rowptr.get(), n_rows, ns, sell_pad4 ? 1 : 0,
+               w.get());
     sell_ptr.resize(ns + 1);
     const int64_t slots = scan_to_offsets(w.get(), sell_ptr.get(), ns);
-    if (slots <= static_cast<int64_t>(1.5 * static_cast<double>(nnz)) + 32 * 64) {
+    if (slots <= static_cast<int64_t>((sell_pad4 ? 1.75 : 1.5) * static_cast<double>(nnz)) + 32 * 64) {
       sell_col.resize(slots);
       sell_val.resize(slots);
       AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(),
                  n_rows, sell_ptr.get(), sell_col.get(), sell_val.get(), 1);
       sell = true;
+      build_dict();
     } else {
       sell_ptr.reset();
     }
   }
 }
 
+// the distinct value patterns of val into slots (a kDictSlots hash set); false when there are
+// more than kDictMax of them (or AGGMG_SELL_VI=0)
+bool DevCsr::dict_scan(DevBuf<unsigned long long>& slots) const {
+  static const bool vi_on = [] {
+    const char* e = std::getenv("AGGMG_SELL_VI");
+    return !(e && e[0] == '0');
+  }();
+  if (!vi_on || nnz == 0) return false;
+  slots.resize(kDictSlots);
+  AGG_CUDA(cudaMemsetAsync(slots.get(), 0xff, kDictSlots * sizeof(unsigned long long), stream()));
+  DevBuf<int> state(2);
+  state.zero();
+  AGG_LAUNCH(k_dict_insert, grid_for(nnz, 256, 8 * sm_count()), 256, 0, val.get(), nnz, slots.get(),
+             state.get());
+  const std::vector<int> st = state.to_host();
+  return st[1] == 0 && st[0] <= kDictMax;
+}
+
+void DevCsr::build_dict() {
+  sell_vi = false;
+  DevBuf<unsigned long long> slots;
+  if (!sell || !sell_pad4 || !dict_scan(slots)) {  // layout without whole 4-slot groups: plain
+    sell_code.reset();
+    sell_tab.reset();
+    return;
+  }
+  const std::vector<unsigned long long> hs = slots.to_host();
+  std::vector<double> tab;
+  std::vector<unsigned char> code(kDictSlots, 0);
+  for (int h = 0; h < kDictSlots; ++h) {
+    if (hs[h] == kDictEmpty) continue;
+    code[h] = static_cast<unsigned char>(tab.size());
+    double v;
+    std::memcpy(&v, &hs[h], sizeof v);
+    tab.push_back(v);
+  }
+  tab.resize(kDictMax, 0.0);
+  sell_tab.resize(kDictMax);
+  sell_tab.upload(tab.data(), kDictMax);
+  DevBuf<unsigned char> cos(kDictSlots);
+  cos.upload(code.data(), kDictSlots);
+  sell_code.resize(static_cast<int64_t>(sell_col.size()));
+  AGG_LAUNCH(k_sell_codes, grid_for(n_rows, 256), 256, 0, rowptr.get(), val.get(), n_rows,
+             sell_ptr.get(), slots.get(), cos.get(), sell_code.get());
+  sync();  // the temporaries above are freed on return
+  sell_vi = true;
+}
+
 void DevCsr::refresh_sell() {
   if (!sell || n_rows == 0) return;
   AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
              sell_ptr.get(), sell_col.get(), sell_val.get(), 0);
+  build_dict();
 }
 
 DevCsrPtr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, const int64_t* col,
@@ -366,15 +490,23 @@ __global__ void __launch_bounds__(kStreamThreads)
 // one coalesced 256-byte load of values and 128 bytes of columns, no staging and no block
 // barriers.  Each row sums its own entries in CSR order (the slot order), and the same
 // epilogues apply: bit-identical to k_csr_stream.
-template <Epi E>
+// With the value dictionary (VI) a slot's value is one byte, its code into the operator's
+// table of distinct values (shared memory); the value, and so every sum, is the same double.
+template <Epi E, bool VI>
 __global__ void __launch_bounds__(256)
     k_sell(const idx* __restrict__ rowptr, const idx* __restrict__ sptr, const idx* __restrict__ scol,
-           const double* __restrict__ sval, int64_t row0, int64_t n, SpmvArgs a, double* partials,
+           const double* __restrict__ sval, const unsigned char* __restrict__ scode,
+           const double* __restrict__ stab, int64_t row0, int64_t n, SpmvArgs a, double* partials,
            unsigned* ticket) {
   constexpr int NP = EpiTraits<E>::np;
   constexpr int NPX = NP > 0 ? NP : 1;
   __shared__ __align__(16) double red_smem[32 * 3 + 2];
+  __shared__ double s_tab[VI ? 256 : 1];
   if (a.pred && !*a.pred) return;
+  if constexpr (VI) {
+    s_tab[threadIdx.x] = stab[threadIdx.x];  // blockDim.x == 256 == the table size
+    __syncthreads();
+  }
   const double* __restrict__ x = a.x;
   double v[NPX];
 #pragma unroll
@@ -384,22 +516,43 @@ __global__ void __launch_bounds__(256)
   for (int64_t r = row0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < row0 + n;
        r += stride) {
     const idx len = rowptr[r + 1] - rowptr[r];
-    const idx* c = scol + sptr[r >> 5] + (r & 31);
-    const double* vv = sval + sptr[r >> 5] + (r & 31);
+    const idx sbase = sptr[r >> 5];
+    const idx* c = scol + sbase + (r & 31);
     double sum = 0.0;
-    idx k = 0;
-    for (; k + 4 <= len; k += 4) {
-      const idx c0 = __ldcs(c + 32 * k), c1 = __ldcs(c + 32 * (k + 1)), c2 = __ldcs(c + 32 * (k + 2)),
-                c3 = __ldcs(c + 32 * (k + 3));
-      const double v0 = __ldcs(vv + 32 * k), v1 = __ldcs(vv + 32 * (k + 1)),
-                   v2 = __ldcs(vv + 32 * (k + 2)), v3 = __ldcs(vv + 32 * (k + 3));
-      const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
-      sum = __dadd_rn(sum, __dmul_rn(v0, x0));
-      sum = __dadd_rn(sum, __dmul_rn(v1, x1));
-      sum = __dadd_rn(sum, __dmul_rn(v2, x2));
-      sum = __dadd_rn(sum, __dmul_rn(v3, x3));
+    if constexpr (VI) {
+      // codes of slots k..k+3: one 32-bit word per row (the packed layout, sell_code)
+      const unsigned* cw = reinterpret_cast<const unsigned*>(scode + sbase) + (r & 31);
+      for (idx k = 0; k < len; k += 4) {
+        const unsigned w = __ldcs(cw + 8 * k);  // + 32 (k / 4) words
+        if (k + 4 <= len) {
+          const idx c0 = __ldcs(c + 32 * k), c1 = __ldcs(c + 32 * (k + 1)),
+                    c2 = __ldcs(c + 32 * (k + 2)), c3 = __ldcs(c + 32 * (k + 3));
+          const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
+          sum = __dadd_rn(sum, __dmul_rn(s_tab[w & 255u], x0));
+          sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> 8) & 255u], x1));
+          sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> 16) & 255u], x2));
+          sum = __dadd_rn(sum, __dmul_rn(s_tab[w >> 24], x3));
+        } else {
+          for (idx j = 0; j < len - k; ++j)
+            sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> (8 * j)) & 255u], __ldg(x + __ldcs(c + 32 * (k + j)))));
+        }
+      }
+    } else {
+      const double* vv = sval + sbase + (r & 31);
+      idx k = 0;
+      for (; k + 4 <= len; k += 4) {
+        const idx c0 = __ldcs(c + 32 * k), c1 = __ldcs(c + 32 * (k + 1)), c2 = __ldcs(c + 32 * (k + 2)),
+                  c3 = __ldcs(c + 32 * (k + 3));
+        const double v0 = __ldcs(vv + 32 * k), v1 = __ldcs(vv + 32 * (k + 1)),
+                     v2 = __ldcs(vv + 32 * (k + 2)), v3 = __ldcs(vv + 32 * (k + 3));
+        const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
+        sum = __dadd_rn(sum, __dmul_rn(v0, x0));
+        sum = __dadd_rn(sum, __dmul_rn(v1, x1));
+        sum = __dadd_rn(sum, __dmul_rn(v2, x2));
+        sum = __dadd_rn(sum, __dmul_rn(v3, x3));
+      }
+      for (; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldcs(vv + 32 * k), __ldg(x + __ldcs(c + 32 * k))));
     }
-    for (; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldcs(vv + 32 * k), __ldg(x + __ldcs(c + 32 * k))));
     row_epilogue<E>(a, x, r, sum, v);
   }
   if constexpr (NP > 0) {
@@ -411,18 +564,27 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <Epi E>
-void launch_sell(const DevCsr& A, const SpmvArgs& a) {
+template <Epi E, bool VI>
+void launch_sell_t(const DevCsr& A, const SpmvArgs& a) {
   static thread_local int per_sm = 0;
   if (!per_sm) {
-    AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sell<E>, 256, 0));
+    AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sell<E, VI>, 256, 0));
     per_sm = std::max(1, per_sm);
   }
   const int64_t nrows = a.row_count >= 0 ? a.row_count : A.n_rows - a.row_base;
   const int64_t grid = std::min<int64_t>(grid_for(nrows, 256), static_cast<int64_t>(per_sm) * sm_count());
-  AGG_LAUNCH(k_sell<E>, static_cast<unsigned>(grid), 256, 0, A.rowptr.get(), A.sell_ptr.get(),
-             A.sell_col.get(), A.sell_val.get(), a.row_base, nrows, a, reduce_partials(),
-             reduce_ticket());
+  const auto kern = k_sell<E, VI>;
+  AGG_LAUNCH(kern, static_cast<unsigned>(grid), 256, 0, A.rowptr.get(), A.sell_ptr.get(),
+             A.sell_col.get(), A.sell_val.get(), A.sell_code.get(), A.sell_tab.get(), a.row_base,
+             nrows, a, reduce_partials(), reduce_ticket());
+}
+
+template <Epi E>
+void launch_sell(const DevCsr& A, const SpmvArgs& a) {
+  if (A.sell_vi)
+    launch_sell_t<E, true>(A, a);
+  else
+    launch_sell_t<E, false>(A, a);
 }
 
 template <Epi E>
@@ -466,7 +628,10 @@ void launch_stream(const DevCsr& A, const SpmvArgs& a) {
 
 double spmv_bytes(const DevCsr& A, Epi epi) {
   const double n = static_cast<double>(A.n_rows), nnz = static_cast<double>(A.nnz);
-  double b = 12.0 * nnz + 4.0 * (n + 1) + 8.0 * static_cast<double>(A.n_cols) + 8.0 * n;
+  // the launch_stream dispatch: SELL with a value dictionary reads 4 + 1 bytes per entry
+  const bool vi = A.sell && A.sell_vi && epi != Epi::kResidualZero &&
+                  !(epi == Epi::kJacobiDot2 && A.sell_short);
+  double b = (vi ? 5.0 : 12.0) * nnz + 4.0 * (n + 1) + 8.0 * static_cast<double>(A.n_cols) + 8.0 * n;
   switch (epi) {
     case Epi::kResidual: b += 8.0 * n; break;
     case Epi::kResidualZero: b += 8.0 * n + 16.0 * n; break;  // wd gathered, x1 written

@@ -30,9 +30,17 @@ struct DevCsr {
   bool sell_short = false;  // mean row length < 10
   DevBuf<idx> sell_ptr, sell_col;
   DevBuf<double> sell_val;
+  // value dictionary (operators with <= 256 distinct values, e.g. stencil matrices): slot k's
+  // value is sell_tab[sell_code[slot]] — the same double, one byte per entry instead of eight
+  bool sell_vi = false;
+  bool sell_pad4 = false;  // slice widths are whole 4-slot groups (the packed code layout)
+  DevBuf<unsigned char> sell_code;  // byte of slot k of row r: slice base + 32(k & ~3) + 4(r & 31) + (k & 3)
+  DevBuf<double> sell_tab;
 
   void plan();          // computes max_row / rows_per_block, builds the SELL copy (synchronises)
-  void refresh_sell();  // after val changed in place: recopy the SELL values
+  void refresh_sell();  // after val changed in place: recopy the SELL values (and dictionary)
+  void build_dict();    // (re)builds or drops the value dictionary from val
+  bool dict_scan(DevBuf<unsigned long long>& slots) const;
 };
 using DevCsrPtr = std::shared_ptr<DevCsr>;
 

@@ -66,3 +66,55 @@ def test_sell_arnoldi_omega_bit_exact(gpu, ref):
     sr = ref.setup_smoother(A, M.DAMPED_JACOBI, 5, 11)
     assert sg.omega == sr.omega and sg.rho_est == sr.rho_est
     np.testing.assert_array_equal(bits(sg.inv_diag), bits(sr.inv_diag))
+
+
+def _dmatrix_format(gpu, A):
+    """aggmg_dmatrix_format of A uploaded as a device matrix: 0 CSR, 1 SELL, 2 SELL + dictionary."""
+    import ctypes as C
+    lib = gpu.lib
+    dm = C.c_void_p()
+    csr = A._c()
+    assert lib.fn("dmatrix_from_host")(C.byref(csr), C.byref(dm)) == 0, lib.fn("last_error")().decode()
+    f = C.c_int32()
+    assert lib.fn("dmatrix_format")(dm, C.byref(f)) == 0
+    lib.fn("dmatrix_free")(dm)
+    return f.value
+
+
+@pytest.mark.parametrize("distinct", [1, 2, 256, 257])
+def test_sell_value_dictionary_bit_exact(gpu, ref, distinct):
+    # <= 256 distinct values: SELL stores one-byte codes into a value table; 257: plain SELL.
+    # Either way the SpMV is bit-identical to the reference.
+    A = gpu.generate_poisson(3, 82, 82, 82)
+    rng = np.random.default_rng(distinct)
+    table = rng.uniform(-2, 2, distinct)
+    table[0] = -0.0  # signed zero is its own pattern
+    codes = rng.integers(0, distinct, A.values.shape[0])
+    codes[:distinct] = np.arange(distinct)  # every value occurs
+    B = M.SparseMatrix(A.n_rows, A.n_cols, A.row_offsets, A.col_indices, table[codes])
+    x = rng.uniform(-1, 1, A.n_cols)
+    np.testing.assert_array_equal(bits(gpu.spmv(B, x)), bits(ref.spmv(B, x)))
+    assert _dmatrix_format(gpu, B) == (2 if distinct <= 256 else 1)
+
+
+def test_sell_value_dictionary_refresh(gpu):
+    # refresh_values that leaves the dictionary range (random values) and comes back
+    A = gpu.generate_poisson(3, 82, 82, 82)
+    rng = np.random.default_rng(5)
+    v = A.values.copy()  # random diagonal shifts: SPD, thousands of distinct values
+    rows = np.repeat(np.arange(A.n_rows), np.diff(A.row_offsets))
+    diag = A.col_indices == rows
+    v[diag] += rng.uniform(0.0, 1.0, int(diag.sum()))
+    A_rand = M.SparseMatrix(A.n_rows, A.n_cols, A.row_offsets, A.col_indices, v)
+    assert _dmatrix_format(gpu, A_rand) == 1 and _dmatrix_format(gpu, A) == 2
+    cfg = M.SetupConfig(alpha=0.5, reuse_caches=True)
+    sc = M.SolverConfig(method=M.PCG, tol=1e-8, max_iters=200)
+    b = np.ones(A.n_rows)
+    h = gpu.setup_hierarchy(A, None, cfg)
+    for B in (A_rand, A):
+        gpu.refresh_values(h, B.values)
+        r1 = gpu.pcg(B, b, None, h, M.CycleConfig(), sc)
+        r2 = gpu.pcg(B, b, None, gpu.setup_hierarchy(B, None, cfg), M.CycleConfig(), sc)
+        assert r1.report.iterations == r2.report.iterations
+        np.testing.assert_array_equal(bits(np.array(r1.report.residual_history)),
+                                      bits(np.array(r2.report.residual_history)))

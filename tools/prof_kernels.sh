@@ -7,7 +7,7 @@ for spec in "$@"; do
   IFS=: read -r mat kind epi <<< "$spec"
   tag="${mat/./_}_${kind}"
   timeout 300 ncu --set full --clock-control none --import-source on \
-    --kernel-name-base demangled -k "regex:Epi\\)${epi}>" -c 2 \
+    --kernel-name-base demangled -k "regex:Epi\\)${epi}[,>]" -c 2 \
     -o "gpurun_out/prof_${tag}" python tools/kernel_bench.py --only "${mat}:${kind}" --reps 2 \
     > "gpurun_out/ncu_${tag}.log" 2>&1
 done
