@@ -272,6 +272,7 @@ def run_b200(args, world, rank, local):
     sell_ = C.c_int32()
     check(lib.fn("dmatrix_format")(dm, C.byref(sell_)))
     l0_sell = bool(sell_.value)
+    l0_vi = sell_.value == 2  # SELL-32 with the one-byte value dictionary
     n, nnz = n_.value, nnz_.value
     hist = np.zeros(solver.max_iters + 2)
 
@@ -370,7 +371,11 @@ def run_b200(args, world, rank, local):
     roof = None
     if jc > 0:
         achieved = (jb / jc) / ((jt / jc) / 1e3) / 1e9
-        if l0_sell:
+        if l0_vi:
+            tkey = "jacobi_sell_vi_l0_dram_bytes_per_launch"
+            kname = ("k_sell<Epi::kJacobi, VI> on level 0: the damped-Jacobi post-smoothing sweep "
+                     "over the SELL-32 copy of the operator, values as one-byte dictionary codes")
+        elif l0_sell:
             tkey = "jacobi_sell_l0_dram_bytes_per_launch"
             kname = ("k_sell<Epi::kJacobi> on level 0: the damped-Jacobi post-smoothing sweep "
                      "over the SELL-32 copy of the operator")
