@@ -136,9 +136,10 @@ __global__ void k_dict_insert(const double* __restrict__ val, int64_t nnz,
   }
 }
 
-__global__ void k_sell_codes(const idx* rowptr, const double* val, int64_t n, const idx* sptr,
-                             const unsigned long long* __restrict__ slots,
-                             const unsigned char* __restrict__ code_of_slot, unsigned char* scode) {
+__global__ void k_sell_codes(const idx* rowptr, const idx* col, const double* val, int64_t n,
+                             const idx* sptr, const unsigned long long* __restrict__ slots,
+                             const unsigned char* __restrict__ code_of_slot, unsigned char* scode,
+                             idx* pcol) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const idx k0 = rowptr[r], len = rowptr[r + 1] - k0;
@@ -147,7 +148,9 @@ __global__ void k_sell_codes(const idx* rowptr, const double* val, int64_t n, co
     unsigned h = dict_hash(u);
     while (slots[h] != u) h = (h + 1) & (kDictSlots - 1);  // present by construction
     // packed: the codes of slots 4g..4g+3 of a row are one 32-bit word (byte k & 3)
-    scode[sptr[r >> 5] + 32 * (k & ~3) + 4 * (r & 31) + (k & 3)] = code_of_slot[h];
+    const idx at = sptr[r >> 5] + 32 * (k & ~3) + 4 * (r & 31) + (k & 3);
+    scode[at] = code_of_slot[h];
+    pcol[at] = col[k0 + k];  // the same packing: 4 consecutive slots of a row are one int4
   }
 }
 
@@ -254,6 +257,7 @@ void DevCsr::build_dict() {
   if (!sell || !sell_pad4 || !dict_scan(slots)) {  // layout without whole 4-slot groups: plain
     sell_code.reset();
     sell_tab.reset();
+    sell_pcol.reset();
     return;
   }
   const std::vector<unsigned long long> hs = slots.to_host();
@@ -272,8 +276,9 @@ void DevCsr::build_dict() {
   DevBuf<unsigned char> cos(kDictSlots);
   cos.upload(code.data(), kDictSlots);
   sell_code.resize(static_cast<int64_t>(sell_col.size()));
-  AGG_LAUNCH(k_sell_codes, grid_for(n_rows, 256), 256, 0, rowptr.get(), val.get(), n_rows,
-             sell_ptr.get(), slots.get(), cos.get(), sell_code.get());
+  sell_pcol.resize(static_cast<int64_t>(sell_col.size()));
+  AGG_LAUNCH(k_sell_codes, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
+             sell_ptr.get(), slots.get(), cos.get(), sell_code.get(), sell_pcol.get());
   sync();  // the temporaries above are freed on return
   sell_vi = true;
 }
@@ -496,7 +501,7 @@ template <Epi E, bool VI>
 __global__ void __launch_bounds__(256)
     k_sell(const idx* __restrict__ rowptr, const idx* __restrict__ sptr, const idx* __restrict__ scol,
            const double* __restrict__ sval, const unsigned char* __restrict__ scode,
-           const double* __restrict__ stab, int64_t row0, int64_t n, SpmvArgs a, double* partials,
+           const idx* __restrict__ pcol, const double* __restrict__ stab, int64_t row0, int64_t n, SpmvArgs a, double* partials,
            unsigned* ticket) {
   constexpr int NP = EpiTraits<E>::np;
   constexpr int NPX = NP > 0 ? NP : 1;
@@ -522,19 +527,22 @@ __global__ void __launch_bounds__(256)
     if constexpr (VI) {
       // codes of slots k..k+3: one 32-bit word per row (the packed layout, sell_code)
       const unsigned* cw = reinterpret_cast<const unsigned*>(scode + sbase) + (r & 31);
+      // columns in the same packing (sell_pcol): slots k..k+3 of a row are one int4
+      const int4* pc = reinterpret_cast<const int4*>(pcol + sbase) + (r & 31);
       for (idx k = 0; k < len; k += 4) {
         const unsigned w = __ldcs(cw + 8 * k);  // + 32 (k / 4) words
+        const int4 q = __ldcs(pc + 8 * k);
         if (k + 4 <= len) {
-          const idx c0 = __ldcs(c + 32 * k), c1 = __ldcs(c + 32 * (k + 1)),
-                    c2 = __ldcs(c + 32 * (k + 2)), c3 = __ldcs(c + 32 * (k + 3));
-          const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
+          const double x0 = __ldg(x + q.x), x1 = __ldg(x + q.y), x2 = __ldg(x + q.z), x3 = __ldg(x + q.w);
           sum = __dadd_rn(sum, __dmul_rn(s_tab[w & 255u], x0));
           sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> 8) & 255u], x1));
           sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> 16) & 255u], x2));
           sum = __dadd_rn(sum, __dmul_rn(s_tab[w >> 24], x3));
         } else {
-          for (idx j = 0; j < len - k; ++j)
-            sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> (8 * j)) & 255u], __ldg(x + __ldcs(c + 32 * (k + j)))));
+          const idx cq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (j < len - k) sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> (8 * j)) & 255u], __ldg(x + cq[j])));
         }
       }
     } else {
@@ -575,7 +583,7 @@ void launch_sell_t(const DevCsr& A, const SpmvArgs& a) {
   const int64_t grid = std::min<int64_t>(grid_for(nrows, 256), static_cast<int64_t>(per_sm) * sm_count());
   const auto kern = k_sell<E, VI>;
   AGG_LAUNCH(kern, static_cast<unsigned>(grid), 256, 0, A.rowptr.get(), A.sell_ptr.get(),
-             A.sell_col.get(), A.sell_val.get(), A.sell_code.get(), A.sell_tab.get(), a.row_base,
+             A.sell_col.get(), A.sell_val.get(), A.sell_code.get(), A.sell_pcol.get(), A.sell_tab.get(), a.row_base,
              nrows, a, reduce_partials(), reduce_ticket());
 }
 

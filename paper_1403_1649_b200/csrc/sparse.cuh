@@ -36,6 +36,7 @@ struct DevCsr {
   bool sell_pad4 = false;  // slice widths are whole 4-slot groups (the packed code layout)
   DevBuf<unsigned char> sell_code;  // byte of slot k of row r: slice base + 32(k & ~3) + 4(r & 31) + (k & 3)
   DevBuf<double> sell_tab;
+  DevBuf<idx> sell_pcol;  // the columns in sell_code's packing (int4 per 4 slots of a row)
 
   void plan();          // computes max_row / rows_per_block, builds the SELL copy (synchronises)
   void refresh_sell();  // after val changed in place: recopy the SELL values (and dictionary)
