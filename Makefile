@@ -5,7 +5,7 @@ NVCC      ?= /usr/local/cuda/bin/nvcc
 HOSTCXX   ?= /usr/bin/g++
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -ccbin $(HOSTCXX) \
-             -Xcompiler -fPIC,-O2,-Wall -Xptxas -v,-warn-spills
+             -Xcompiler -fPIC,-O2,-Wall,-ffp-contract=off -Xptxas -v,-warn-spills
 SRC_DIR   := paper_1403_1649_b200/csrc
 OBJ_DIR   := build/obj
 LIB       := paper_1403_1649_b200/lib/libaggmg_b200.so
@@ -31,7 +31,7 @@ $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 
 $(OBJ_DIR)/%.cpp.o: $(SRC_DIR)/%.cpp $(HDRS)
 	@mkdir -p $(OBJ_DIR)
-	$(HOSTCXX) -std=c++17 -O2 -fPIC -Wall -I/usr/local/cuda/include -c $< -o $@
+	$(HOSTCXX) -std=c++17 -O2 -fPIC -Wall -ffp-contract=off -I/usr/local/cuda/include -c $< -o $@
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)

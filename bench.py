@@ -197,10 +197,12 @@ def configs_c(M, alpha, method, tol=1e-8, max_iters=500):
 def cpu_reference_run(M, cfg_name, sample_n, threads):
     """One setup+solve of the reference (oracle/_ref) on a bounded sample grid."""
     label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[cfg_name]
-    r = M.ref()
+    from oracle import checkers
+
+    r = checkers.ref()
     r.lib.fn("set_num_threads")(threads)
     if dims == 27:
-        A = M.oracle().generate_jump27(sample_n, sample_n, sample_n, eps, JUMP_BLOCK)
+        A = checkers.oracle().generate_jump27(sample_n, sample_n, sample_n, eps, JUMP_BLOCK)
     elif dims == 3:
         A = r.generate_poisson(3, sample_n, sample_n, sample_n, eps)
     else:
@@ -357,7 +359,7 @@ def run_b200(args, world, rank, local):
 
     # ---- CPU baseline (reference, all host cores, bounded sample) ----
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and os.path.exists(_abi.REF_LIB):
+    if rank == 0 and world == 1 and not args.no_cpu and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libaggmg_ref.so")):
         threads = os.cpu_count() or 1
         sample_n = 512 if dims == 2 else (96 if dims == 27 else 128)
         ns, dt, cres = cpu_reference_run(M, args.config, sample_n, threads)

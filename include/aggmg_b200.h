@@ -117,6 +117,11 @@ int64_t aggmg_kernel_launches(void);             /* number of kernels this libra
  * (slower: 1.3-1.7x per step on the bench configs). */
 void aggmg_set_exact_reductions(int on);
 int aggmg_exact_reductions(void);
+/* The SELL-32 copy of a large operator stores its values as one-byte codes into a table of
+ * its distinct values when there are <= 256 of them (stencil matrices; same doubles, same
+ * results).  on = 0 keeps plain fp64 values: operators planned or refreshed afterwards use the
+ * 12-byte-per-entry layout (the variable-coefficient case; bench.py's no-dictionary line). */
+void aggmg_set_value_dictionary(int on);
 void aggmg_setup_config_default(aggmg_setup_config* c);
 void aggmg_cycle_config_default(aggmg_cycle_config* c);
 void aggmg_solver_config_default(aggmg_solver_config* c);

@@ -5,6 +5,6 @@ this package is the Python binding of that boundary (see aggmg.py)."""
 from .aggmg import (  # noqa: F401
     CYCLE_HYBRID, CYCLE_K, CYCLE_V, DAMPED_JACOBI, FGMRES, INNER_CG, INNER_GMRES, JACOBI, PCG,
     SGS, Aggregation, CycleConfig, Error, CudaError, Hierarchy, Mis2Result, SetupConfig,
-    SolverConfig, SparseMatrix, b200, ones_vector, oracle, ref)
+    SolverConfig, SparseMatrix, b200, ones_vector)
 
 __version__ = "0.1.0"

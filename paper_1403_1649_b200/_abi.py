@@ -157,6 +157,7 @@ SIGNATURES = {
     "hierarchy_level_dmatrix": (I, [vp, L, I, C.POINTER(vp)]),
     "set_exact_reductions": (None, [I]),
     "exact_reductions": (I, []),
+    "set_value_dictionary": (None, [I]),
     "timer_start": (I, []),
     "timer_stop": (I, [f64p]),
     "setup_config_default": (None, [C.POINTER(SetupConfigC)]),
@@ -203,8 +204,6 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # AGGMG_LIB: an alternative build of the product library (kernel-variant experiments)
 PRODUCT_LIB = os.environ.get("AGGMG_LIB") or os.path.join(REPO, "paper_1403_1649_b200", "lib",
                                                           "libaggmg_b200.so")
-ORACLE_LIB = os.path.join(REPO, "oracle", "liboracle.so")
-REF_LIB = os.path.join(REPO, "oracle", "_ref", "libaggmg_ref.so")
 
 
 class LibraryMissing(RuntimeError):

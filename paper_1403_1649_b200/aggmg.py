@@ -2,11 +2,12 @@
 
 Names, argument meaning, defaults and error behaviour follow the reference so parity
 tests read like its own doctest suites.  Every call crosses the C-ABI
-(include/aggmg_b200.h) into one implementation:
+(include/aggmg_b200.h) into the product library:
 
-    b200()    the product: hand-written sm_100a kernels (fails loudly without a GPU build)
-    oracle()  the C restatement in oracle/ (test infrastructure)
-    ref()     the unmodified reference compiled from /root/reference (test infrastructure)
+    b200()    hand-written sm_100a kernels (fails loudly without a GPU build)
+
+The CPU checkers the tests compare against (the C restatement and the unmodified
+reference) live outside this package, in oracle/checkers.py (test infrastructure).
 """
 from __future__ import annotations
 
@@ -617,37 +618,15 @@ class Backend:
         return self._csr_out("generate_jump27", nx, ny, nz, jump, block)
 
 
-_backends = {}
-
-
-def _get(name: str) -> Backend:
-    b = _backends.get(name)
-    if b is None:
-        if name == "b200":
-            lib = _abi.Lib(_abi.PRODUCT_LIB, "aggmg_")
-        elif name == "oracle":
-            lib = _abi.Lib(_abi.ORACLE_LIB, "aggmg_oracle_")
-        elif name == "ref":
-            lib = _abi.Lib(_abi.REF_LIB, "aggmg_ref_")
-        else:
-            raise ValueError(name)
-        b = _backends[name] = Backend(lib, name)
-    return b
+_product = None
 
 
 def b200() -> Backend:
     """The product: the sm_100a kernels behind include/aggmg_b200.h."""
-    return _get("b200")
-
-
-def oracle() -> Backend:
-    """TEST INFRASTRUCTURE: the C restatement in oracle/."""
-    return _get("oracle")
-
-
-def ref() -> Backend:
-    """TEST INFRASTRUCTURE: the unmodified reference compiled into oracle/_ref/."""
-    return _get("ref")
+    global _product
+    if _product is None:
+        _product = Backend(_abi.Lib(_abi.PRODUCT_LIB, "aggmg_"), "b200")
+    return _product
 
 
 def ones_vector(n: int) -> np.ndarray:  # poisson.hpp:28

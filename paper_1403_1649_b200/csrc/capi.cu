@@ -275,6 +275,7 @@ int aggmg_synchronize(void) { return guarded([&] { sync(); }); }
 void aggmg_set_num_threads(int) {}
 void aggmg_set_exact_reductions(int on) { set_exact_reductions(on != 0); }
 int aggmg_exact_reductions(void) { return exact_reductions() ? 1 : 0; }
+void aggmg_set_value_dictionary(int on) { value_dictionary_switch().store(on ? 1 : 0); }
 int aggmg_num_threads(void) {
   int n = 0;
   guarded([&] { n = sm_count(); });

@@ -634,11 +634,11 @@ void coarse_solve(DevHierarchy& h, const double* b, double* x, const int* pred) 
   if (exact_reductions() && h.coarse_lu_ready) {  // bit-identical substitution (slow: n^2 chain)
     const size_t smem = 3 * n * sizeof(double);
     if (n <= int64_t{kLuRows} * kLuThreads && smem <= 200 * 1024) {
-      static thread_local bool attr = false;  // per rank thread (one device each)
-      if (!attr) {
+      static std::atomic<unsigned long long> attr{0};  // the attribute is per device
+      if (device_pending(attr)) {
         AGG_CUDA(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       200 * 1024));
-        attr = true;
+        mark_device(attr);
       }
       AGG_LAUNCH(k_lu_solve, 1, kLuThreads, smem, static_cast<int>(n), h.coarse_lu.get(),
                  h.coarse_lu_t.get(), h.coarse_perm.get(), b, x, pred);

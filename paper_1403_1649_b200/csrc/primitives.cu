@@ -1,4 +1,5 @@
 // primitives.cu — scans, deterministic reductions, segmented rank sort.
+#include <atomic>
 #include "primitives.cuh"
 
 #include "chunked.cuh"
@@ -162,7 +163,7 @@ double* reduce_partials() { return red().partials; }
 unsigned* reduce_ticket() { return red().ticket; }
 
 namespace {
-bool g_exact = false;
+std::atomic<bool> g_exact{false};  // read by rank threads, written by the host API
 template <int NP>
 void dot_exact(const DotArgs& args, int64_t n, double* out, const int* pred) {
   DotOp<NP> op;
@@ -175,11 +176,11 @@ void dot_exact(const DotArgs& args, int64_t n, double* out, const int* pred) {
 }
 }  // namespace
 
-bool exact_reductions() { return g_exact; }
-void set_exact_reductions(bool on) { g_exact = on; }
+bool exact_reductions() { return g_exact.load(); }
+void set_exact_reductions(bool on) { g_exact.store(on); }
 
 void dot_device(const DotArgs& args, int64_t n, double* out, const int* pred, int exact) {
-  if (exact == 1 || (exact < 0 && g_exact)) {
+  if (exact == 1 || (exact < 0 && g_exact.load())) {
     switch (args.np) {
       case 1: dot_exact<1>(args, n, out, pred); return;
       case 2: dot_exact<2>(args, n, out, pred); return;

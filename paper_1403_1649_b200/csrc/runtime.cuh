@@ -2,6 +2,7 @@
 // RAII device buffers, pinned scalar readback, kernel-family profiling.
 #pragma once
 
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <utility>
@@ -24,6 +25,14 @@ void host_to_device_narrow(int32_t* dst, const int64_t* src, size_t n, int64_t l
                            int64_t* first_bad);
 void init_device(int device);  // creates the calling thread's context on `device`
 int current_device();
+// One-time per-device initialisation (kernel attributes are per device): true until
+// mark_device(seen) ran on the calling thread's current device.
+inline bool device_pending(const std::atomic<unsigned long long>& seen) {
+  return !(seen.load() & (1ull << (current_device() & 63)));
+}
+inline void mark_device(std::atomic<unsigned long long>& seen) {
+  seen.fetch_or(1ull << (current_device() & 63));
+}
 cudaStream_t side_stream();  // a second stream of the calling thread (overlapped exchanges)
 // While alive, the calling thread's kernels and stream-ordered allocations go to `s` instead
 // of its main stream (work that overlaps the main stream, e.g. the smoother's Arnoldi chains

@@ -1401,11 +1401,11 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
     // scratch (measured on the 27-point operator: 4096 -> 2048 took the phase 29 -> 25 ms)
     const int cap = std::min(kGalCapSmem, read_scalar(maxlen.get()));
     const size_t smem = static_cast<size_t>(cap) * 5 * sizeof(idx);
-    static thread_local bool raised = false;  // one value for every thread: the attribute is global
-    if (!raised) {
+    static std::atomic<unsigned long long> raised{0};  // the attribute is per device
+    if (device_pending(raised)) {
       AGG_CUDA(cudaFuncSetAttribute(k_gal_symbolic_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kGalCapBig * 5 * static_cast<int>(sizeof(idx))));
-      raised = true;
+      mark_device(raised);
     }
     // global scratch only for the rows longer than the shared-memory capacity
     DevBuf<int64_t> blen(nbig), boff(nbig + 1);

@@ -1,5 +1,6 @@
 // sparse.cu — device CSR, upload/validation, CSR-stream SpMV family, transpose and
 // the device-side problem generators.
+#include <atomic>
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -215,32 +216,45 @@ void DevCsr::plan() {
     const int64_t ns = (n_rows + 31) / 32;
     DevBuf<idx> w(ns);
     DevBuf<unsigned long long> dslots;
-    sell_pad4 = dict_scan(dslots) && (((n_rows + 31) / 32) * 32 * int64_t{max_row + 3} < INT32_MAX);
-    AGG_LAUNCH(k_slice_width, grid_for(ns, 256), 256, 0, rowptr.get(), n_rows, ns, sell_pad4 ? 1 : 0,
-               w.get());
-    sell_ptr.resize(ns + 1);
-    const int64_t slots = scan_to_offsets(w.get(), sell_ptr.get(), ns);
-    if (slots <= static_cast<int64_t>((sell_pad4 ? 1.75 : 1.5) * static_cast<double>(nnz)) + 32 * 64) {
-      sell_col.resize(slots);
-      sell_val.resize(slots);
-      AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(),
-                 n_rows, sell_ptr.get(), sell_col.get(), sell_val.get(), 1);
-      sell = true;
-      build_dict();
-    } else {
+    const bool dict = dict_scan(dslots);  // one scan, reused by build_codes below
+    // the dictionary's packed layout pads slices to whole 4-slot groups; when that busts the
+    // slot budget (rows of 4-5 entries pad to 8), the plain unpadded layout is tried next
+    const bool fits4 = ns * 32 * int64_t{max_row + 3} < INT32_MAX;
+    for (const bool pad4 : {dict && fits4, false}) {
+      AGG_LAUNCH(k_slice_width, grid_for(ns, 256), 256, 0, rowptr.get(), n_rows, ns, pad4 ? 1 : 0,
+                 w.get());
+      sell_ptr.resize(ns + 1);
+      sell_slots = scan_to_offsets(w.get(), sell_ptr.get(), ns);
+      if (sell_slots <= static_cast<int64_t>((pad4 ? 1.75 : 1.5) * static_cast<double>(nnz)) + 32 * 64) {
+        sell = true;
+        sell_pad4 = pad4;
+        break;
+      }
+      if (!pad4) break;
+    }
+    if (!sell) {
       sell_ptr.reset();
+    } else if (sell_pad4) {
+      build_codes(dslots);
+    } else {
+      fill_plain();
     }
   }
 }
 
 // the distinct value patterns of val into slots (a kDictSlots hash set); false when there are
-// more than kDictMax of them (or AGGMG_SELL_VI=0)
-bool DevCsr::dict_scan(DevBuf<unsigned long long>& slots) const {
-  static const bool vi_on = [] {
+// more than kDictMax of them (or the dictionary is switched off: AGGMG_SELL_VI=0 /
+// aggmg_set_value_dictionary(0))
+std::atomic<int>& value_dictionary_switch() {
+  static std::atomic<int> on{[] {
     const char* e = std::getenv("AGGMG_SELL_VI");
-    return !(e && e[0] == '0');
-  }();
-  if (!vi_on || nnz == 0) return false;
+    return (e && e[0] == '0') ? 0 : 1;
+  }()};
+  return on;
+}
+
+bool DevCsr::dict_scan(DevBuf<unsigned long long>& slots) const {
+  if (!value_dictionary_switch().load() || nnz == 0) return false;
   slots.resize(kDictSlots);
   AGG_CUDA(cudaMemsetAsync(slots.get(), 0xff, kDictSlots * sizeof(unsigned long long), stream()));
   DevBuf<int> state(2);
@@ -251,15 +265,22 @@ bool DevCsr::dict_scan(DevBuf<unsigned long long>& slots) const {
   return st[1] == 0 && st[0] <= kDictMax;
 }
 
-void DevCsr::build_dict() {
+// the plain SELL copy (4-byte column + 8-byte value per slot); drops the dictionary
+void DevCsr::fill_plain() {
   sell_vi = false;
-  DevBuf<unsigned long long> slots;
-  if (!sell || !sell_pad4 || !dict_scan(slots)) {  // layout without whole 4-slot groups: plain
-    sell_code.reset();
-    sell_tab.reset();
-    sell_pcol.reset();
-    return;
-  }
+  sell_code.reset();
+  sell_tab.reset();
+  sell_pcol.reset();
+  // (padding slots are never read: every row stops at its own length)
+  if (sell_col.size() != sell_slots) sell_col.resize(sell_slots);
+  if (sell_val.size() != sell_slots) sell_val.resize(sell_slots);
+  AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
+             sell_ptr.get(), sell_col.get(), sell_val.get(), 1);
+}
+
+// the dictionary copy (packed columns + one-byte codes) from the slots of a successful
+// dict_scan; the plain copy is then not kept (the VI kernels never read it)
+void DevCsr::build_codes(const DevBuf<unsigned long long>& slots) {
   const std::vector<unsigned long long> hs = slots.to_host();
   std::vector<double> tab;
   std::vector<unsigned char> code(kDictSlots, 0);
@@ -275,19 +296,25 @@ void DevCsr::build_dict() {
   sell_tab.upload(tab.data(), kDictMax);
   DevBuf<unsigned char> cos(kDictSlots);
   cos.upload(code.data(), kDictSlots);
-  sell_code.resize(static_cast<int64_t>(sell_col.size()));
-  sell_pcol.resize(static_cast<int64_t>(sell_col.size()));
+  if (sell_code.size() != sell_slots) {
+    sell_code.resize(sell_slots);
+    sell_pcol.resize(sell_slots);
+  }
   AGG_LAUNCH(k_sell_codes, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
              sell_ptr.get(), slots.get(), cos.get(), sell_code.get(), sell_pcol.get());
   sync();  // the temporaries above are freed on return
   sell_vi = true;
+  sell_col.reset();
+  sell_val.reset();
 }
 
 void DevCsr::refresh_sell() {
   if (!sell || n_rows == 0) return;
-  AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
-             sell_ptr.get(), sell_col.get(), sell_val.get(), 0);
-  build_dict();
+  DevBuf<unsigned long long> dslots;
+  if (sell_pad4 && dict_scan(dslots))
+    build_codes(dslots);
+  else
+    fill_plain();  // the new values lost the dictionary (or the layout never had one)
 }
 
 DevCsrPtr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, const int64_t* col,
@@ -610,11 +637,11 @@ void launch_stream(const DevCsr& A, const SpmvArgs& a) {
   }
   const int64_t nblocks = (nrows + A.rows_per_block - 1) / A.rows_per_block;
   const size_t smem = sizeof(double) * A.smem_entries;
-  static thread_local bool raised = false;
-  if (smem > 48 * 1024 && !raised) {
+  static std::atomic<unsigned long long> raised{0};
+  if (smem > 48 * 1024 && device_pending(raised)) {
     AGG_CUDA(cudaFuncSetAttribute(k_csr_stream<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   226 * 1024));  // + the static reduction scratch <= 227 KB
-    raised = true;
+    mark_device(raised);
   }
   // persistent grid: as many CTAs as can be co-resident
   static thread_local size_t cached_smem = 0;

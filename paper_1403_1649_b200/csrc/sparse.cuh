@@ -11,6 +11,7 @@
 // bit-identical to the CPU oracle (built without FMA).
 #pragma once
 
+#include <atomic>
 #include <memory>
 
 #include "primitives.cuh"
@@ -39,9 +40,11 @@ struct DevCsr {
   DevBuf<idx> sell_pcol;  // the columns in sell_code's packing (int4 per 4 slots of a row)
 
   void plan();          // computes max_row / rows_per_block, builds the SELL copy (synchronises)
-  void refresh_sell();  // after val changed in place: recopy the SELL values (and dictionary)
-  void build_dict();    // (re)builds or drops the value dictionary from val
+  int64_t sell_slots = 0;  // padded slot count of the SELL layout
+  void refresh_sell();  // after val changed in place: rebuild the SELL copy (dictionary or plain)
   bool dict_scan(DevBuf<unsigned long long>& slots) const;
+  void fill_plain();
+  void build_codes(const DevBuf<unsigned long long>& slots);
 };
 using DevCsrPtr = std::shared_ptr<DevCsr>;
 
@@ -106,5 +109,9 @@ DevCsrPtr generate_jump27_rows(int64_t nx, int64_t ny, int64_t nz, double jump, 
                                int64_t row0, int64_t nrows);
 
 double spmv_bytes(const DevCsr& A, Epi epi);
+
+// process-wide switch of the SELL value dictionary (default on; AGGMG_SELL_VI=0 starts it off);
+// takes effect for operators planned (or refreshed) afterwards
+std::atomic<int>& value_dictionary_switch();
 
 }  // namespace aggmg_b200

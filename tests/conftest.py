@@ -28,11 +28,15 @@ def gpu():
 def ref():
     from paper_1403_1649_b200 import aggmg
 
-    return aggmg.ref()
+    from oracle import checkers
+
+    return checkers.ref()
 
 
 @pytest.fixture(scope="session")
 def orc():
     from paper_1403_1649_b200 import aggmg
 
-    return aggmg.oracle()
+    from oracle import checkers
+
+    return checkers.oracle()

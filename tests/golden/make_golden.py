@@ -36,7 +36,9 @@ def worked_example():
 
 
 def main():
-    r = M.ref()
+    from oracle.checkers import ref
+
+    r = ref()
     out = {}
     # 1. Eq. 8 worked example: cache order and exact grouped sums
     A = worked_example()

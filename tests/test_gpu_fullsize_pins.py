@@ -1,0 +1,116 @@
+"""Full-size parity against the UNMODIFIED reference at the BASELINE configurations.
+
+tests/golden/fullsize_pins.json holds, per config, the reference's own cache-path hierarchy
+digested level by level (SHA-256 of A, P, R, B, inv_diag; omega and rho as exact hex floats)
+and its PCG / FGMRES(30) solve (iteration count, every residual-history entry, a digest of x),
+generated on the GPU box's host by tests/golden/make_fullsize_pins.py from oracle/_ref.
+
+Here the B200 path runs the same configuration exactly as bench.py does (device-generated
+matrix, setup_hierarchy_device, solve_device), so these are the kernels the headline times:
+level 0 in SELL-32 with the one-byte value dictionary, level 1 in SELL-32, the rest CSR-stream.
+  - setup: every level bit-identical to the reference (digests equal);
+  - default solve: iteration count equal, |h_k - h_k^ref| <= 1e-10 * h_0^ref, x within 1e-10;
+  - exact-reduction mode: every history entry and every bit of x identical.
+"""
+import ctypes as C
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1403_1649_b200 import _abi
+from paper_1403_1649_b200 import aggmg as M
+
+from golden.fullsize import CONFIGS, JUMP_BLOCK, MAX_ITERS, RESTART, TOL, level_digest, vec_digest
+
+pytestmark = pytest.mark.gpu
+
+PINS_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "fullsize_pins.json")
+PINS = json.load(open(PINS_PATH)) if os.path.exists(PINS_PATH) else {}
+
+
+def _check(rc, lib):
+    assert rc == 0, lib.fn("last_error")().decode()
+
+
+def _device_matrix(lib, name):
+    gen, dims, nx, ny, nz, eps, alpha, method = CONFIGS[name]
+    dm = C.c_void_p()
+    if gen == "jump27":
+        _check(lib.fn("dmatrix_jump27")(nx, ny, nz, eps, JUMP_BLOCK, C.byref(dm)), lib)
+    else:
+        _check(lib.fn("dmatrix_poisson")(dims, nx, ny, nz, eps, -1, C.byref(dm)), lib)
+    return dm
+
+
+def _solve(gpu, h, name, n):
+    gen, dims, nx, ny, nz, eps, alpha, method = CONFIGS[name]
+    lib = gpu.lib
+    sc = M.SolverConfig(method=M.PCG if method == "pcg" else M.FGMRES, tol=TOL,
+                        max_iters=MAX_ITERS, restart=RESTART)._c()
+    cc = M.CycleConfig()._c()
+    rep = _abi.SolveReportC()
+    hist = np.zeros(MAX_ITERS + 2)
+    rep.history = hist.ctypes.data_as(_abi.f64p)
+    rep.history_capacity = hist.shape[0]
+    x = np.zeros(n)
+    _check(lib.fn("solve_device")(h._h, C.byref(cc), C.byref(sc), x.ctypes.data_as(_abi.f64p),
+                                  C.byref(rep)), lib)
+    return rep, hist[: rep.history_length].copy(), x
+
+
+def _setup(gpu, dm, name):
+    alpha = CONFIGS[name][6]
+    cfg = M.SetupConfig(alpha=alpha, reuse_caches=True)
+    h = C.c_void_p()
+    _check(gpu.lib.fn("setup_hierarchy_device")(dm, C.byref(cfg._c()), C.byref(h)), gpu.lib)
+    return M.Hierarchy(gpu, h, cfg)
+
+
+def _level_format(gpu, h, k):
+    dk = C.c_void_p()
+    _check(gpu.lib.fn("hierarchy_level_dmatrix")(h._h, k, 0, C.byref(dk)), gpu.lib)
+    fmt = C.c_int32()
+    _check(gpu.lib.fn("dmatrix_format")(dk, C.byref(fmt)), gpu.lib)
+    gpu.lib.fn("dmatrix_free")(dk)
+    return fmt.value
+
+
+@pytest.mark.parametrize("name", sorted(PINS))
+def test_fullsize_bit_identical_to_reference(gpu, name):
+    pin = PINS[name]
+    lib = gpu.lib
+    dm = _device_matrix(lib, name)
+    try:
+        # ---- setup: level by level, bit for bit ----
+        h = _setup(gpu, dm, name)
+        assert h.n_levels() == len(pin["levels"])
+        if pin["n"] >= (1 << 19):
+            # the headline kernels: SELL-32 at level 0, with the value dictionary on stencils
+            assert _level_format(gpu, h, 0) >= 1
+        for k, want in enumerate(pin["levels"]):
+            got = level_digest(h, k)
+            assert got == want, (name, k, {key: (got.get(key), want.get(key)) for key in want
+                                           if got.get(key) != want.get(key)})
+        # ---- default solve: iterations equal, history within 1e-10 of h_0 ----
+        ref_hist = np.array([float.fromhex(v) for v in pin["history"]])
+        rep, hist, x = _solve(gpu, h, name, pin["n"])
+        assert rep.converged and rep.iterations == pin["iterations"]
+        assert hist.shape == ref_hist.shape
+        assert np.max(np.abs(hist - ref_hist)) <= 1e-10 * ref_hist[0]
+        assert abs(np.linalg.norm(x) - pin["x_norm"]) <= 1e-10 * pin["x_norm"]
+        del h
+        # ---- exact-reduction mode: the whole solve bit-identical ----
+        lib.fn("set_exact_reductions")(1)
+        try:
+            h = _setup(gpu, dm, name)
+            rep, hist, x = _solve(gpu, h, name, pin["n"])
+            del h
+        finally:
+            lib.fn("set_exact_reductions")(0)
+        assert rep.iterations == pin["iterations"]
+        assert [float(v).hex() for v in hist] == pin["history"]
+        assert vec_digest(x) == pin["x"]
+    finally:
+        lib.fn("dmatrix_free")(dm)

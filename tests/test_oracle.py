@@ -14,7 +14,9 @@ import golden_util as G
 from helpers import (assert_csr_bits, assert_pattern, bits, laplacian_1d, random_graph,
                      random_sparse, random_spd)
 
-HAVE_REF = os.path.exists(_abi.REF_LIB)
+from oracle.checkers import REF_LIB  # noqa: E402
+
+HAVE_REF = os.path.exists(REF_LIB)
 needs_ref = pytest.mark.skipif(not HAVE_REF, reason="reference shim not built")
 
 

@@ -15,6 +15,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 from paper_1403_1649_b200 import aggmg as M  # noqa: E402
+from oracle import checkers  # noqa: E402
 from helpers import bits, random_spd  # noqa: E402
 
 
@@ -39,7 +40,7 @@ def problem(gpu, rng):
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
-    gpu, ref = M.b200(), M.ref()
+    gpu, ref = M.b200(), checkers.ref()
     assert gpu.lib.fn("init")(0) == 0
     exact = len(sys.argv) > 3 and sys.argv[3] == "exact"
     if exact:

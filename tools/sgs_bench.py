@@ -10,6 +10,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1403_1649_b200 import aggmg as M  # noqa: E402
+from oracle import checkers  # noqa: E402
 
 
 def run(impl, A, alpha, reps):
@@ -31,7 +32,7 @@ def run(impl, A, alpha, reps):
 def main():
     n2 = int(sys.argv[1]) if len(sys.argv) > 1 else 512
     n3 = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-    gpu, ref = M.b200(), M.ref()
+    gpu, ref = M.b200(), checkers.ref()
     assert gpu.lib.fn("init")(0) == 0
     for name, A, alpha in ((f"2d {n2}^2", gpu.generate_poisson(2, n2, n2), 0.25),
                            (f"3d {n3}^3", gpu.generate_poisson(3, n3, n3, n3), 0.5)):

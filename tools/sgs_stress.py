@@ -5,9 +5,10 @@ import sys, numpy as np
 sys.path.insert(0, '.')
 sys.path.insert(0, 'tests')
 from paper_1403_1649_b200 import aggmg as M
+from oracle import checkers  # noqa: E402
 from helpers import bits
 gpu = M.b200(); assert gpu.lib.fn("init")(0) == 0
-ref = M.ref()
+ref = checkers.ref()
 rng = np.random.default_rng(0)
 for dim, nn, alpha in ((2, 512, 0.25), (3, 64, 0.5)):
     A0 = ref.generate_poisson(dim, nn, nn, nn if dim == 3 else 1)
