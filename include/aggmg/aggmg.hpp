@@ -16,18 +16,22 @@
 //   cycles.hpp           CycleKind, InnerKind, CycleConfig, vcycle, kcycle, apply_preconditioner
 //   krylov.hpp           SolverConfig, SolveReport, SolveResult, Preconditioner, fgmres, pcg
 //   poisson.hpp          PoissonSpec, generate_poisson, ones_vector
-// Differences, by design: the hierarchy lives in HBM (Hierarchy::device); host copies of
-// the levels are materialised when SetupConfig::keep_host_levels is true (default), and
-// pcg/fgmres accept the AMG preconditioner returned by amg_preconditioner() or an empty
-// (identity) preconditioner — arbitrary host callbacks would defeat the device solve.
+// Differences, by design: the hierarchy lives in HBM (Hierarchy::device); the host copies of
+// its levels (Hierarchy::levels) are materialised on first access.  pcg/fgmres take any
+// Preconditioner: the AMG preconditioner returned by amg_preconditioner() runs inside the
+// device Krylov loop; any other callable (a lambda around apply_preconditioner, a Jacobi
+// scaling, ...) is called on the host once per application, with r and z copied across.
 #ifndef AGGMG_B200_AGGMG_HPP
 #define AGGMG_B200_AGGMG_HPP
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <functional>
 #include <iomanip>
+#include <exception>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <sstream>
 #include <stdexcept>
@@ -291,7 +295,8 @@ struct SetupConfig {
   int arnoldi_m = 5;
   std::uint64_t seed = 42;
   bool reuse_caches = false;
-  bool keep_host_levels = true;  // B200 addition: materialise Level host copies
+  bool keep_host_levels = true;  // B200 addition (kept for source compatibility): levels are
+                                 // always materialised lazily, on first access
   aggmg_setup_config c() const {
     return aggmg_setup_config{alpha, coarse_size_max, max_levels, static_cast<int32_t>(smoother),
                               arnoldi_m, reuse_caches ? 1 : 0, seed};
@@ -304,8 +309,72 @@ struct Level {
   SmootherState smoother;
 };
 
+// Host view of the device levels (hierarchy.hpp:46 `std::vector<Level> levels`): the reads a
+// reference caller makes (size, [k], at, front, back, iteration) materialise every level's
+// A / P / R / B / smoother from HBM on first use, once, shared by copies of the Hierarchy.
+class LevelList {
+ public:
+  LevelList() = default;
+  LevelList(std::shared_ptr<aggmg_hierarchy> dev, SmootherKind kind)
+      : state_(std::make_shared<State>()) {
+    state_->dev = std::move(dev);
+    state_->kind = kind;
+  }
+  size_t size() const {
+    const auto dev = state_ ? state_->dev.lock() : nullptr;
+    return dev ? static_cast<size_t>(aggmg_hierarchy_n_levels(dev.get())) : 0;
+  }
+  bool empty() const { return size() == 0; }
+  const Level& operator[](size_t k) const { return all()[k]; }
+  const Level& at(size_t k) const { return all().at(k); }
+  const Level& front() const { return all().front(); }
+  const Level& back() const { return all().back(); }
+  std::vector<Level>::const_iterator begin() const { return all().begin(); }
+  std::vector<Level>::const_iterator end() const { return all().end(); }
+
+ private:
+  struct State {
+    std::weak_ptr<aggmg_hierarchy> dev;  // not an owner: Hierarchy::device's use count stays
+                                         // the number of Hierarchy values holding it
+    SmootherKind kind = SmootherKind::damped_jacobi;
+    std::once_flag once;
+    std::vector<Level> levels;
+  };
+  static void check(int rc) {
+    if (rc != AGGMG_OK) throw Error(aggmg_last_error());
+  }
+  const std::vector<Level>& all() const {
+    static const std::vector<Level> none;
+    if (!state_) return none;
+    std::call_once(state_->once, [s = state_.get()] {
+      const auto dev = s->dev.lock();
+      require(dev != nullptr, "hierarchy: levels read after the hierarchy was destroyed");
+      const int64_t L = aggmg_hierarchy_n_levels(dev.get());
+      for (int64_t k = 0; k < L; ++k) {
+        Level lvl;
+        aggmg_csr m{};
+        check(aggmg_hierarchy_level_A(dev.get(), k, &m));
+        lvl.A = SparseMatrix::adopt(m);
+        check(aggmg_hierarchy_level_P(dev.get(), k, &m));
+        lvl.P = SparseMatrix::adopt(m);
+        check(aggmg_hierarchy_level_R(dev.get(), k, &m));
+        lvl.R = SparseMatrix::adopt(m);
+        lvl.B.resize(lvl.A.n_rows);
+        check(aggmg_hierarchy_level_B(dev.get(), k, lvl.B.data()));
+        lvl.smoother.kind = s->kind;
+        lvl.smoother.inv_diag.resize(lvl.A.n_rows);
+        check(aggmg_hierarchy_level_smoother(dev.get(), k, &lvl.smoother.omega,
+                                             &lvl.smoother.rho_est, lvl.smoother.inv_diag.data()));
+        s->levels.push_back(std::move(lvl));
+      }
+    });
+    return state_->levels;
+  }
+  std::shared_ptr<State> state_;
+};
+
 struct Hierarchy {
-  std::vector<Level> levels;  // host mirror (SetupConfig::keep_host_levels)
+  LevelList levels;  // host view, materialised on first access
   SetupConfig config;
   std::vector<std::string> warnings;
   std::shared_ptr<aggmg_hierarchy> device;
@@ -318,26 +387,7 @@ inline void mirror(Hierarchy& h) {
   h.warnings.clear();
   for (int64_t i = 0; i < aggmg_hierarchy_n_warnings(h.device.get()); ++i)
     h.warnings.emplace_back(aggmg_hierarchy_warning(h.device.get(), i));
-  h.levels.clear();
-  if (!h.config.keep_host_levels) return;
-  const int64_t L = aggmg_hierarchy_n_levels(h.device.get());
-  for (int64_t k = 0; k < L; ++k) {
-    Level lvl;
-    aggmg_csr m{};
-    check(aggmg_hierarchy_level_A(h.device.get(), k, &m));
-    lvl.A = SparseMatrix::adopt(m);
-    check(aggmg_hierarchy_level_P(h.device.get(), k, &m));
-    lvl.P = SparseMatrix::adopt(m);
-    check(aggmg_hierarchy_level_R(h.device.get(), k, &m));
-    lvl.R = SparseMatrix::adopt(m);
-    lvl.B.resize(lvl.A.n_rows);
-    check(aggmg_hierarchy_level_B(h.device.get(), k, lvl.B.data()));
-    lvl.smoother.kind = h.config.smoother;
-    lvl.smoother.inv_diag.resize(lvl.A.n_rows);
-    check(aggmg_hierarchy_level_smoother(h.device.get(), k, &lvl.smoother.omega,
-                                         &lvl.smoother.rho_est, lvl.smoother.inv_diag.data()));
-    h.levels.push_back(std::move(lvl));
-  }
+  h.levels = LevelList(h.device, h.config.smoother);
 }
 }  // namespace detail
 
@@ -355,7 +405,15 @@ inline Hierarchy setup_hierarchy(SparseMatrix A0, Vector B0, const SetupConfig& 
   return h;
 }
 
+// hierarchy.cpp:90-104.  Value semantics as in the reference: when the caller still holds the
+// hierarchy (auto h2 = refresh_values(h, v)), the refresh runs on a device copy and h keeps
+// solving the old system; refresh_values(std::move(h), v) refreshes in place.
 inline Hierarchy refresh_values(Hierarchy h, const std::vector<double>& new_values) {
+  if (h.device.use_count() > 1) {
+    aggmg_hierarchy* copy = nullptr;
+    detail::check(aggmg_hierarchy_clone(h.device.get(), &copy));
+    h.device.reset(copy, aggmg_hierarchy_free);
+  }
   detail::check(aggmg_refresh_values(h.device.get(), new_values.data(),
                                      static_cast<int64_t>(new_values.size())));
   detail::mirror(h);
@@ -483,15 +541,32 @@ inline Preconditioner amg_preconditioner(const Hierarchy& h, const CycleConfig& 
 }
 
 namespace detail {
+// C trampoline for an arbitrary host Preconditioner (aggmg_precond_fn); exceptions thrown by
+// the callable are carried across the C boundary and rethrown by krylov()
+struct HostPrecond {
+  const Preconditioner* M = nullptr;
+  std::exception_ptr error;
+  static int call(const double* r, double* z, int64_t n, void* user) {
+    auto* self = static_cast<HostPrecond*>(user);
+    try {
+      const Vector zv = (*self->M)(Vector(r, r + n));
+      require(static_cast<int64_t>(zv.size()) == n, "krylov: preconditioner output length mismatch");
+      std::copy(zv.begin(), zv.end(), z);
+      return 0;
+    } catch (...) {
+      self->error = std::current_exception();
+      return 1;
+    }
+  }
+};
+
 inline SolveResult krylov(bool use_pcg, const SparseMatrix& A, const Vector& b, const Vector& x0,
                           const Preconditioner& M, const SolverConfig& cfg) {
   const aggmg_hierarchy* h = nullptr;
   aggmg_cycle_config cc;
   aggmg_cycle_config_default(&cc);
-  if (M) {
-    const AmgPreconditioner* amg = M.target<AmgPreconditioner>();
-    require(amg != nullptr,
-            "krylov: the device solver takes the AMG preconditioner (amg_preconditioner) or none");
+  const AmgPreconditioner* amg = M ? M.target<AmgPreconditioner>() : nullptr;
+  if (amg) {  // the device cycle, inside the device Krylov loop
     h = amg->device.get();
     cc = amg->cfg.c();
   }
@@ -503,8 +578,19 @@ inline SolveResult krylov(bool use_pcg, const SparseMatrix& A, const Vector& b, 
   rep.history_capacity = static_cast<int64_t>(out.report.residual_history.size());
   const aggmg_csr ca = A.c();
   const aggmg_solver_config sc = cfg.c();
-  check(use_pcg ? aggmg_pcg(&ca, b.data(), x0.data(), h, &cc, &sc, out.x.data(), &rep)
-                : aggmg_fgmres(&ca, b.data(), x0.data(), h, &cc, &sc, out.x.data(), &rep));
+  if (M && !amg) {  // any other callable: a host callback per application
+    HostPrecond hp;
+    hp.M = &M;
+    const int rc = use_pcg ? aggmg_pcg_cb(&ca, b.data(), x0.data(), &HostPrecond::call, &hp, &sc,
+                                          out.x.data(), &rep)
+                           : aggmg_fgmres_cb(&ca, b.data(), x0.data(), &HostPrecond::call, &hp,
+                                             &sc, out.x.data(), &rep);
+    if (hp.error) std::rethrow_exception(hp.error);
+    check(rc);
+  } else {
+    check(use_pcg ? aggmg_pcg(&ca, b.data(), x0.data(), h, &cc, &sc, out.x.data(), &rep)
+                  : aggmg_fgmres(&ca, b.data(), x0.data(), h, &cc, &sc, out.x.data(), &rep));
+  }
   out.report.converged = rep.converged != 0;
   out.report.iterations = rep.iterations;
   out.report.residual_history.resize(static_cast<size_t>(rep.history_length));

@@ -186,8 +186,13 @@ int aggmg_hessenberg_eigenvalues(int64_t n, const double* H_row_major, double* r
 /* hierarchy.hpp:57 / hierarchy.cpp:34-88 */
 int aggmg_setup_hierarchy(const aggmg_csr* A0, const double* B0, const aggmg_setup_config* cfg,
                           aggmg_hierarchy** out);
-/* hierarchy.hpp:64 / hierarchy.cpp:90-104 (in place) */
+/* hierarchy.hpp:64 / hierarchy.cpp:90-104, in place on h.  The reference takes the
+ * Hierarchy by value; a caller that keeps the old hierarchy clones it first (the C++ drop-in
+ * does so whenever its handle is shared).  A level-0 operator shared with a device matrix
+ * (aggmg_setup_hierarchy_device) is copied, never rewritten. */
 int aggmg_refresh_values(aggmg_hierarchy* h, const double* new_values, int64_t count);
+/* deep copy of a hierarchy (every level in HBM; Hierarchy's copy semantics) */
+int aggmg_hierarchy_clone(const aggmg_hierarchy* h, aggmg_hierarchy** out);
 void aggmg_hierarchy_free(aggmg_hierarchy* h);
 int64_t aggmg_hierarchy_n_levels(const aggmg_hierarchy* h);                 /* hierarchy.hpp:46 */
 int aggmg_hierarchy_level_size(const aggmg_hierarchy* h, int64_t k, int64_t* n, int64_t* nnz);
@@ -228,6 +233,19 @@ int aggmg_pcg(const aggmg_csr* A, const double* b, const double* x0, const aggmg
 int aggmg_fgmres(const aggmg_csr* A, const double* b, const double* x0, const aggmg_hierarchy* M,
                  const aggmg_cycle_config* cycle, const aggmg_solver_config* cfg, double* x,
                  aggmg_solve_report* report);
+
+/* krylov.hpp:38-50 with an arbitrary host preconditioner (the reference's
+ * std::function<Vector(const Vector&)>, e.g. the CLI's lambda aggmg_main.cpp:194-196 or the
+ * Jacobi preconditioner of test_krylov.cpp:129-156).  The Krylov loop stays on the device;
+ * each application copies r (n doubles) to the host, calls M(r, z, n, user) and copies z back.
+ * M returns 0 on success; nonzero aborts the solve with AGGMG_ERR ("preconditioner callback
+ * failed").  M == NULL is the identity. */
+typedef int (*aggmg_precond_fn)(const double* r, double* z, int64_t n, void* user);
+int aggmg_pcg_cb(const aggmg_csr* A, const double* b, const double* x0, aggmg_precond_fn M,
+                 void* user, const aggmg_solver_config* cfg, double* x, aggmg_solve_report* report);
+int aggmg_fgmres_cb(const aggmg_csr* A, const double* b, const double* x0, aggmg_precond_fn M,
+                    void* user, const aggmg_solver_config* cfg, double* x,
+                    aggmg_solve_report* report);
 
 /* One call = reference CLI `solve` pipeline (aggmg_main.cpp:163-210): setup_hierarchy(A, B0)
  * then pcg/fgmres(A, b, x0) preconditioned by the hierarchy.  B0/x0 may be NULL (ones / zeros).

@@ -465,6 +465,37 @@ int aggmg_ref_fgmres(const aggmg_csr* A, const double* b, const double* x0, cons
   return run(A, b, x0, h, c, s, x, r, false);
 }
 
+// the reference's Krylov solvers with a host callback preconditioner (any std::function)
+static int run_cb(const aggmg_csr* A, const double* b, const double* x0, aggmg_precond_fn fn,
+                  void* user, const aggmg_solver_config* cfg, double* x, aggmg_solve_report* rep,
+                  bool use_pcg) {
+  return guarded([&] {
+    const aggmg::SparseMatrix M = to_ref(A);
+    const int64_t n = A->n_rows;
+    aggmg::Preconditioner P;
+    if (fn)
+      P = [fn, user](const aggmg::Vector& r) {
+        aggmg::Vector z(r.size());
+        if (fn(r.data(), z.data(), static_cast<int64_t>(r.size()), user) != 0)
+          throw aggmg::Error("krylov: the preconditioner callback failed");
+        return z;
+      };
+    const aggmg::SolverConfig sc = to_ref(cfg);
+    auto res = use_pcg ? aggmg::pcg(M, vec(b, n), vec(x0, n), P, sc)
+                       : aggmg::fgmres(M, vec(b, n), vec(x0, n), P, sc);
+    std::memcpy(x, res.x.data(), sizeof(double) * n);
+    fill_report(res.report, rep);
+  });
+}
+int aggmg_ref_pcg_cb(const aggmg_csr* A, const double* b, const double* x0, aggmg_precond_fn fn,
+                     void* user, const aggmg_solver_config* s, double* x, aggmg_solve_report* r) {
+  return run_cb(A, b, x0, fn, user, s, x, r, true);
+}
+int aggmg_ref_fgmres_cb(const aggmg_csr* A, const double* b, const double* x0, aggmg_precond_fn fn,
+                        void* user, const aggmg_solver_config* s, double* x, aggmg_solve_report* r) {
+  return run_cb(A, b, x0, fn, user, s, x, r, false);
+}
+
 // Reference CLI pipeline (aggmg_main.cpp:163-210): setup then solve, timed separately.
 int aggmg_ref_setup_and_solve(const aggmg_csr* A, const double* b, const double* B0,
                               const double* x0, const aggmg_setup_config* setup,

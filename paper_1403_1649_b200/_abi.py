@@ -77,6 +77,9 @@ class SolveReportC(C.Structure):
 csrp = C.POINTER(CSR)
 # int (*)(aggmg_comm*, int rank, void* user)
 RANK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p)
+# aggmg_precond_fn: z = M(r) over host arrays of n doubles
+PRECOND_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64,
+                         C.c_void_p)
 I = C.c_int
 L = C.c_int64
 
@@ -107,6 +110,7 @@ SIGNATURES = {
     "hessenberg_eigenvalues": (I, [L, f64p, f64p, f64p]),
     "setup_hierarchy": (I, [csrp, f64p, C.POINTER(SetupConfigC), C.POINTER(vp)]),
     "refresh_values": (I, [vp, f64p, L]),
+    "hierarchy_clone": (I, [vp, C.POINTER(vp)]),
     "hierarchy_free": (None, [vp]),
     "hierarchy_n_levels": (L, [vp]),
     "hierarchy_level_size": (I, [vp, L, i64p, i64p]),
@@ -127,6 +131,10 @@ SIGNATURES = {
                 C.POINTER(SolveReportC)]),
     "fgmres": (I, [csrp, f64p, f64p, vp, C.POINTER(CycleConfigC), C.POINTER(SolverConfigC), f64p,
                    C.POINTER(SolveReportC)]),
+    "pcg_cb": (I, [csrp, f64p, f64p, PRECOND_FN, vp, C.POINTER(SolverConfigC), f64p,
+                   C.POINTER(SolveReportC)]),
+    "fgmres_cb": (I, [csrp, f64p, f64p, PRECOND_FN, vp, C.POINTER(SolverConfigC), f64p,
+                      C.POINTER(SolveReportC)]),
     "setup_and_solve": (I, [csrp, f64p, f64p, f64p, C.POINTER(SetupConfigC),
                             C.POINTER(CycleConfigC), C.POINTER(SolverConfigC), f64p,
                             C.POINTER(SolveReportC)]),

@@ -324,7 +324,9 @@ class Backend:
 
     # -- plumbing --
     def _call(self, name, *args):
-        rc = self.lib.fn(name)(*args)
+        self._check(self.lib.fn(name)(*args))
+
+    def _check(self, rc):
         if rc != 0:
             msg = self.lib.fn("last_error")().decode()
             raise (CudaError if rc == 2 else Error)(msg)
@@ -552,9 +554,29 @@ class Backend:
         rep.history = _p(hist, _abi.f64p)
         rep.history_capacity = hist.shape[0]
         cc, sc, ca = cycle._c(), cfg._c(), A._c()
-        self._call(name, C.byref(ca), _p(b, _abi.f64p), _p(x0, _abi.f64p),
-                   M._h if M is not None else None, C.byref(cc), C.byref(sc), _p(x, _abi.f64p),
-                   C.byref(rep))
+        if M is not None and not isinstance(M, Hierarchy):
+            # any host callable r -> z (the reference's std::function Preconditioner)
+            failure = []
+
+            def thunk(r_ptr, z_ptr, nn, _user):
+                try:
+                    r = np.ctypeslib.as_array(r_ptr, shape=(nn,)).copy()
+                    np.ctypeslib.as_array(z_ptr, shape=(nn,))[:] = _f64(M(r), nn)
+                    return 0
+                except Exception as e:  # noqa: BLE001 - re-raised after the C call
+                    failure.append(e)
+                    return 1
+
+            cb = _abi.PRECOND_FN(thunk)
+            rc = self.lib.fn(name + "_cb")(C.byref(ca), _p(b, _abi.f64p), _p(x0, _abi.f64p), cb,
+                                           None, C.byref(sc), _p(x, _abi.f64p), C.byref(rep))
+            if failure:
+                raise failure[0]
+            self._check(rc)
+        else:
+            self._call(name, C.byref(ca), _p(b, _abi.f64p), _p(x0, _abi.f64p),
+                       M._h if M is not None else None, C.byref(cc), C.byref(sc),
+                       _p(x, _abi.f64p), C.byref(rep))
         return SolveResult(x, SolveReport(bool(rep.converged), rep.iterations,
                                           hist[: rep.history_length].tolist(), 0.0,
                                           rep.solve_seconds, rep.note.decode()))

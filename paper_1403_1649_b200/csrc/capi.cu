@@ -624,6 +624,15 @@ int aggmg_refresh_values(aggmg_hierarchy* h, const double* values, int64_t count
   });
 }
 
+int aggmg_hierarchy_clone(const aggmg_hierarchy* h, aggmg_hierarchy** out) {
+  return guarded([&] {
+    require(h && h->h, "hierarchy: null handle");
+    auto c = std::make_unique<aggmg_hierarchy>();
+    c->h = clone_hierarchy(*h->h);
+    *out = c.release();
+  });
+}
+
 void aggmg_hierarchy_free(aggmg_hierarchy* h) { delete h; }
 
 int64_t aggmg_hierarchy_n_levels(const aggmg_hierarchy* h) { return h && h->h ? h->h->n_levels() : 0; }
@@ -775,6 +784,38 @@ static int run_krylov(const aggmg_csr* A, const double* b, const double* x0,
     sync();
     fill_report(o, rep);
   });
+}
+
+static int run_krylov_cb(const aggmg_csr* A, const double* b, const double* x0,
+                         aggmg_precond_fn fn, void* user, const aggmg_solver_config* cfg,
+                         double* x, aggmg_solve_report* rep, int method) {
+  return guarded([&] {
+    const int64_t n = A->n_rows;
+    const char* who = method == AGGMG_SOLVER_PCG ? "pcg" : "fgmres";
+    require(A->n_rows == A->n_cols, std::string(who) + ": matrix must be square");
+    auto dA = up(A);
+    auto db = up_vec(b, n), dx = up_vec(x0, n);
+    Precond M;
+    M.host_fn = fn;
+    M.host_user = user;
+    SolverCfg s = to_cfg(cfg);
+    s.method = method;
+    SolveOut o = method == AGGMG_SOLVER_PCG ? pcg(*dA, db.get(), dx.get(), M, s)
+                                           : fgmres(*dA, db.get(), dx.get(), M, s);
+    dx.download(x, n);
+    sync();
+    fill_report(o, rep);
+  });
+}
+
+int aggmg_pcg_cb(const aggmg_csr* A, const double* b, const double* x0, aggmg_precond_fn M,
+                 void* user, const aggmg_solver_config* cfg, double* x, aggmg_solve_report* report) {
+  return run_krylov_cb(A, b, x0, M, user, cfg, x, report, AGGMG_SOLVER_PCG);
+}
+int aggmg_fgmres_cb(const aggmg_csr* A, const double* b, const double* x0, aggmg_precond_fn M,
+                    void* user, const aggmg_solver_config* cfg, double* x,
+                    aggmg_solve_report* report) {
+  return run_krylov_cb(A, b, x0, M, user, cfg, x, report, AGGMG_SOLVER_FGMRES);
 }
 
 int aggmg_pcg(const aggmg_csr* A, const double* b, const double* x0, const aggmg_hierarchy* M,

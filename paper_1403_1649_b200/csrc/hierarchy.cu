@@ -180,6 +180,9 @@ void refresh_values(DevHierarchy& h, const double* new_values_dev) {
     if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
   h.graphs.clear();
   DevLevel& L0 = h.levels[0];
+  // level 0 may share its storage with the caller's device matrix (setup_hierarchy_device):
+  // the refresh must not rewrite the caller's values
+  if (L0.A.use_count() > 1) L0.A = clone_csr(*L0.A);
   copy_double(L0.A->val.get(), new_values_dev, L0.A->nnz);
   L0.A->refresh_sell();
   SmootherBatch smoothers;
@@ -194,6 +197,107 @@ void refresh_values(DevHierarchy& h, const double* new_values_dev) {
   }
   factor_coarsest(h);
   smoothers.finish([&](int k) -> SmootherDev& { return h.levels[k].smoother; });
+}
+
+DevCsrPtr clone_csr(const DevCsr& A) {
+  auto C = std::make_shared<DevCsr>();
+  C->n_rows = A.n_rows;
+  C->n_cols = A.n_cols;
+  C->nnz = A.nnz;
+  C->rowptr.copy_from(A.rowptr);
+  C->col.copy_from(A.col);
+  C->val.copy_from(A.val);
+  C->max_row = A.max_row;
+  C->rows_per_block = A.rows_per_block;
+  C->smem_entries = A.smem_entries;
+  C->sell = A.sell;
+  C->sell_short = A.sell_short;
+  C->sell_ptr.copy_from(A.sell_ptr);
+  C->sell_col.copy_from(A.sell_col);
+  C->sell_val.copy_from(A.sell_val);
+  C->sell_vi = A.sell_vi;
+  C->sell_pad4 = A.sell_pad4;
+  C->sell_code.copy_from(A.sell_code);
+  C->sell_tab.copy_from(A.sell_tab);
+  C->sell_pcol.copy_from(A.sell_pcol);
+  C->sell_slots = A.sell_slots;
+  return C;
+}
+
+namespace {
+void clone_sgs(SgsDirection& d, const SgsDirection& s) {
+  d.ell = s.ell;
+  d.cta = s.cta;
+  d.rows.copy_from(s.rows);
+  d.rec.copy_from(s.rec);
+  d.offsets.copy_from(s.offsets);
+  d.h_offsets = s.h_offsets;
+  d.code.copy_from(s.code);
+  d.val.copy_from(s.val);
+  d.optr.copy_from(s.optr);
+  d.ocol.copy_from(s.ocol);
+  d.oval.copy_from(s.oval);
+  d.runs = s.runs;
+}
+}  // namespace
+
+std::unique_ptr<DevHierarchy> clone_hierarchy(const DevHierarchy& h) {
+  auto c = std::make_unique<DevHierarchy>();
+  c->cfg = h.cfg;
+  c->warnings = h.warnings;
+  c->setup_ms = h.setup_ms;
+  c->coarse_inv.copy_from(h.coarse_inv);
+  c->coarse_lu.copy_from(h.coarse_lu);
+  c->coarse_lu_t.copy_from(h.coarse_lu_t);
+  c->coarse_perm.copy_from(h.coarse_perm);
+  c->coarse_lu_ready = h.coarse_lu_ready;
+  c->levels.resize(h.levels.size());
+  for (size_t k = 0; k < h.levels.size(); ++k) {
+    const DevLevel& s = h.levels[k];
+    DevLevel& d = c->levels[k];
+    d.A = clone_csr(*s.A);
+    d.B.copy_from(s.B);
+    d.has_smoother = s.has_smoother;
+    d.smoother.kind = s.smoother.kind;
+    d.smoother.inv_diag.copy_from(s.smoother.inv_diag);
+    d.smoother.wdiag.copy_from(s.smoother.wdiag);
+    d.smoother.omega = s.smoother.omega;
+    d.smoother.rho_est = s.smoother.rho_est;
+    d.smoother.arnoldi_m = s.smoother.arnoldi_m;
+    clone_sgs(d.smoother.sgs_fw, s.smoother.sgs_fw);
+    clone_sgs(d.smoother.sgs_bw, s.smoother.sgs_bw);
+    d.smoother.sgs_tmp.copy_from(s.smoother.sgs_tmp);
+    d.smoother.sgs_bp.copy_from(s.smoother.sgs_bp);
+    d.smoother.sgs_xp.copy_from(s.smoother.sgs_xp);
+    d.has_next = s.has_next;
+    d.mis_sweeps = s.mis_sweeps;
+    d.agg.n_fine = s.agg.n_fine;
+    d.agg.n_agg = s.agg.n_agg;
+    d.agg.assignment.copy_from(s.agg.assignment);
+    d.agg.representatives.copy_from(s.agg.representatives);
+    d.agg.agg_row_offsets.copy_from(s.agg.agg_row_offsets);
+    d.agg.rows_by_coarse.copy_from(s.agg.rows_by_coarse);
+    d.tr.pval.copy_from(s.tr.pval);
+    d.tr.coarse_b.copy_from(s.tr.coarse_b);
+    d.tr.R = s.tr.R;  // never written after setup (refresh keeps P and R)
+    d.tr.p_nnz = s.tr.p_nnz;
+    d.gal.n_fine = s.gal.n_fine;
+    d.gal.n_coarse = s.gal.n_coarse;
+    d.gal.nnz_fine = s.gal.nnz_fine;
+    d.gal.nnz_coarse = s.gal.nnz_coarse;
+    d.gal.coarse_rowptr.copy_from(s.gal.coarse_rowptr);
+    d.gal.coarse_col.copy_from(s.gal.coarse_col);
+    d.gal.entry.copy_from(s.gal.entry);
+    d.gal.entry_row.copy_from(s.gal.entry_row);
+    d.gal.segment_offsets.copy_from(s.gal.segment_offsets);
+    d.gal.slot_of_csr.copy_from(s.gal.slot_of_csr);
+    d.gal.group_offsets.copy_from(s.gal.group_offsets);
+    d.gal.group_rows.copy_from(s.gal.group_rows);
+    d.gal.max_coarse_row = s.gal.max_coarse_row;
+    d.gal.pattern_hash = s.gal.pattern_hash;
+  }
+  sync();
+  return c;
 }
 
 DevHierarchy::~DevHierarchy() {

@@ -91,6 +91,11 @@ struct DevHierarchy {
 std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev,
                                               const SetupCfg& cfg);
 void refresh_values(DevHierarchy& h, const double* new_values_dev);
+// Deep copy (every level's operator, transfer, cache and smoother; no captured graphs): the
+// reference's refresh_values takes the hierarchy BY VALUE (hierarchy.cpp:90), so a refresh of
+// a hierarchy someone else still holds works on a copy.
+std::unique_ptr<DevHierarchy> clone_hierarchy(const DevHierarchy& h);
+DevCsrPtr clone_csr(const DevCsr& A);
 void factor_coarsest(DevHierarchy& h);
 // Explicit inverse of the coarsest operator (row-major) by device Gauss-Jordan (coarse.cu).
 void invert_coarsest(const DevCsr& A, DevBuf<double>& inv);

@@ -174,9 +174,17 @@ __global__ void k_multi_axpy(int64_t n, AxpyList L, double* __restrict__ x) {
 unsigned egrid(int64_t n) { return grid_for(n, kB, 8 * static_cast<int64_t>(sm_count())); }
 
 void apply_M(const Precond& M, const double* r, double* z, int64_t n, const KrylovDist* dist) {
-  if (dist && dist->precond)
+  if (dist && dist->precond) {
     dist->precond(r, z);
-  else if (M.h)
+  } else if (M.host_fn) {  // one device->host->device round trip per application
+    M.host_r.resize(n);
+    M.host_z.resize(n);
+    device_to_host(M.host_r.data(), r, sizeof(double) * n);
+    sync();
+    require(M.host_fn(M.host_r.data(), M.host_z.data(), n, M.host_user) == 0,
+            "krylov: the preconditioner callback failed");
+    host_to_device(z, M.host_z.data(), sizeof(double) * n);
+  } else if (M.h)
     apply_preconditioner(*M.h, M.cfg, r, z);
   else
     copy_double(z, r, n);

@@ -25,10 +25,18 @@ struct SolveOut {
   std::string note;
 };
 
-// Preconditioner: nullptr hierarchy = identity (krylov.cpp:23-25).
+// Host preconditioner z = M(r) over host arrays of n entries (the reference's std::function
+// Preconditioner, krylov.hpp:38); nonzero return = failure.
+using HostPrecondFn = int (*)(const double* r, double* z, int64_t n, void* user);
+
+// Preconditioner: the device AMG cycle of h, or a host callback, or (neither) the identity
+// (krylov.cpp:23-25).
 struct Precond {
   DevHierarchy* h = nullptr;
   CycleCfg cfg;
+  HostPrecondFn host_fn = nullptr;
+  void* host_user = nullptr;
+  mutable std::vector<double> host_r, host_z;  // staging of the callback's arguments
 };
 
 // Hooks for a row-partitioned operator (dist_solve.cu): A is this rank's rows with local

@@ -92,6 +92,11 @@ class DevBuf {
   void download(T* h, int64_t n) const {
     if (n > 0) device_to_host(h, p_, sizeof(T) * static_cast<size_t>(n));
   }
+  // device-to-device deep copy of o (stream-ordered)
+  void copy_from(const DevBuf& o) {
+    resize(o.n_);
+    if (n_ > 0) AGG_CUDA(cudaMemcpyAsync(p_, o.p_, sizeof(T) * n_, cudaMemcpyDeviceToDevice, stream()));
+  }
   std::vector<T> to_host() const {
     std::vector<T> v(n_);
     download(v.data(), n_);
