@@ -343,6 +343,8 @@ int aggmg_dist_matrix_jump27(aggmg_comm* c, int64_t nx, int64_t ny, int64_t nz, 
                              int64_t block, aggmg_dist_matrix** out);
 int aggmg_dist_matrix_info(const aggmg_dist_matrix* A, int64_t* n_global, int64_t* row0,
                            int64_t* n_local, int64_t* nnz_local);
+/* this rank's rows: 1 = SELL-32 copy, 2 = SELL-32 with the value dictionary, 0 = CSR-stream */
+int aggmg_dist_matrix_format(const aggmg_dist_matrix* A, int* sell);
 void aggmg_dist_matrix_free(aggmg_dist_matrix* A);
 
 /* setup_hierarchy (hierarchy.hpp:57) over the ranks; B0_local (host, this rank's rows) may be

@@ -189,6 +189,7 @@ SIGNATURES = {
     "dist_matrix_poisson": (I, [vp, I, L, L, L, C.c_double, I, C.POINTER(vp)]),
     "dist_matrix_jump27": (I, [vp, L, L, L, C.c_double, L, C.POINTER(vp)]),
     "dist_matrix_info": (I, [vp, i64p, i64p, i64p, i64p]),
+    "dist_matrix_format": (I, [vp, C.POINTER(C.c_int32)]),
     "dist_matrix_free": (None, [vp]),
     "dist_setup": (I, [vp, vp, f64p, C.POINTER(SetupConfigC), L, C.POINTER(vp)]),
     "dist_solve": (I, [vp, C.POINTER(CycleConfigC), C.POINTER(SolverConfigC), f64p, f64p,

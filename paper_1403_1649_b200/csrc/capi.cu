@@ -1209,6 +1209,14 @@ int aggmg_dist_matrix_info(const aggmg_dist_matrix* A, int64_t* n_global, int64_
   });
 }
 
+int aggmg_dist_matrix_format(const aggmg_dist_matrix* A, int* sell) {
+  return guarded([&] {
+    require(A && A->A, "null dist matrix");
+    const DevCsr& M = A->A->A;
+    *sell = M.sell ? (M.sell_vi ? 2 : 1) : 0;
+  });
+}
+
 void aggmg_dist_matrix_free(aggmg_dist_matrix* A) { delete A; }
 
 int aggmg_dist_setup(aggmg_comm* c, const aggmg_dist_matrix* A0, const double* B0_local,
