@@ -47,116 +47,13 @@ __device__ inline void mbar_wait(unsigned long long* bar, unsigned parity) {
       : "memory");
 }
 
-// ---- exact emulation of a sequential fp64 sum ---------------------------------------------
-// seq_sum_warp<PER>(s, t, m) returns, in every lane of the calling warp, the value of
-//     for (k = 0; k < m; ++k) s = RN(s + t[k]);
-// bit for bit, without paying m dependent fp64-add latencies.  While the running sum stays
-// inside one binade [2^e, 2^(e+1)) its rounding grid is fixed (ulp u = 2^(e-52)), so
-//     RN(s + t) = s + rint(t / u) * u
-// exactly, unless t / u is an exact half (a tie, resolved by the parity of s) or the result
-// leaves the binade.  Each lane turns PER consecutive terms into the integers rint(t/u) (t/u is
-// a power-of-two scaling: exact), a warp prefix sum over int64 yields every intermediate sum at
-// once, and all terms before the first one that ties or leaves the binade are committed
-// together; that term is then added serially and the next run starts in its binade.  Zero,
-// subnormal and non-finite sums take the serial step.  Host model + adversarial check:
-// tools/seqsum_model.py (tests/test_seqsum_model.py).
-template <int PER>
-__device__ double seq_sum_warp(double s, const double* t, int m) {
-  const int lane = threadIdx.x & 31;
-  constexpr unsigned kFull = 0xffffffffu;
-  constexpr long long kLo = 1ll << 52, kHi = 1ll << 53;
-  int pos = 0;
-  while (pos < m) {
-    if (m - pos <= 16) {  // a short remainder: serially (every lane the same chain)
-      for (; pos < m; ++pos) s = __dadd_rn(s, t[pos]);
-      break;
-    }
-    const long long sb = __double_as_longlong(s);
-    const int ex = static_cast<int>((sb >> 52) & 0x7ff);
-    if (ex < 54 || ex > 2046) {  // zero, subnormal or tiny (u would underflow), inf / nan
-      s = __dadd_rn(s, t[pos]);
-      ++pos;
-      continue;
-    }
-    const double inv_u = __longlong_as_double(static_cast<long long>(2098 - ex) << 52);
-    const double u = __longlong_as_double(static_cast<long long>(ex - 52) << 52);
-    const long long mant = (sb & (kLo - 1)) | kLo;
-    const long long S = sb < 0 ? -mant : mant;
-    const int base = pos + lane * PER;
-    // term k as an integer multiple of u (and whether that is exact: finite, < 2^53, no tie)
-    auto conv = [&](int k, long long& Q) -> bool {
-      Q = 0;
-      if (k >= m) return false;
-      const double q = __dmul_rn(t[k], inv_u);
-      const double aq = fabs(q);
-      if (!(aq < 9007199254740992.0) || __dsub_rn(aq, floor(aq)) == 0.5) return false;
-      Q = __double2ll_rn(q);
-      return true;
-    };
-    long long acc = 0;  // pass 1: this lane's total
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      long long Q;
-      conv(base + j, Q);
-      acc += Q;
-    }
-    long long incl = acc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long v = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += v;
-    }
-    // pass 2 (terms re-read from shared memory rather than kept in registers): every
-    // intermediate sum of this lane, up to its first term that ties or leaves the binade
-    int bad = PER;
-    long long sprev = S + (incl - acc);  // the sum just before this lane's first bad term
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      if (bad == PER) {
-        long long Q;
-        const bool ok = conv(base + j, Q);
-        const long long sj = sprev + Q;
-        const long long a = sj < 0 ? -sj : sj;
-        if (ok && a > kLo && a < kHi && ((sj < 0) == (S < 0)))
-          sprev = sj;
-        else
-          bad = j;
-      }
-    }
-    const unsigned anybad = __ballot_sync(kFull, bad < PER);
-    int f;
-    long long sf;
-    if (anybad == 0) {
-      f = 32 * PER;
-      sf = __shfl_sync(kFull, S + incl, 31);
-    } else {
-      const int L = __ffs(anybad) - 1;
-      f = L * PER + __shfl_sync(kFull, bad, L);
-      sf = __shfl_sync(kFull, sprev, L);
-    }
-    if (f > 0) {
-      s = __dmul_rn(static_cast<double>(sf), u);  // |sf| < 2^53: exact, then an exact scaling
-      pos += f;
-    }
-    if (pos < m && f < 32 * PER) {  // the term that ties or leaves the binade, serially
-      s = __dadd_rn(s, t[pos]);
-      ++pos;
-    }
-    if (f < 4) {  // a volatile stretch (the sum hovers near zero): a burst of serial steps
-      const int e = min(m, pos + 16);
-      for (; pos < e; ++pos) s = __dadd_rn(s, t[pos]);
-    }
-  }
-  return s;
-}
-
 // One CTA per 8192-element chunk.  Producers fill stage b = t & 1 and arrive on FULL[b];
 // the consumer waits on FULL[b], adds the stage sequentially, arrives on EMPTY[b]; the
 // producers wait on EMPTY[b] before refilling it two tiles later.  The chain latency
 // (8192 dependent adds) overlaps the memory traffic, and 16 CTAs per SM put every chunk
 // of a 16.7 M vector in flight at once.
 template <int NP, class Op>
-__global__ void __launch_bounds__(kChunkThreads, 10)
+__global__ void __launch_bounds__(kChunkThreads)
     k_chunked(int64_t n, Op op, double* partials, unsigned* ticket, double* out) {
   __shared__ __align__(16) double tile[2][NP][kChunkTile];
   __shared__ bool last;
@@ -178,6 +75,7 @@ __global__ void __launch_bounds__(kChunkThreads, 10)
   const int len = static_cast<int>(min(static_cast<int64_t>(kChunk), n - c0));
   const int ntiles = (len + kChunkTile - 1) / kChunkTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc = 0.0;
   if (warp > 0) {  // producers
     const int pt = threadIdx.x - 32;
     for (int t = 0; t < ntiles; ++t) {
@@ -196,26 +94,36 @@ __global__ void __launch_bounds__(kChunkThreads, 10)
       }
       mbar_arrive(&full[b]);
     }
-  } else {  // consumer warp: the chains one after another, each by the whole warp
-    double chain[NP];
-#pragma unroll
-    for (int k = 0; k < NP; ++k) chain[k] = 0.0;
+  } else {  // consumer warp
     for (int t = 0; t < ntiles; ++t) {
       const int b = t & 1;
       mbar_wait(&full[b], (t >> 1) & 1);
-      const int m = min(kChunkTile, len - t * kChunkTile);
-#pragma unroll
-      for (int k = 0; k < NP; ++k) chain[k] = seq_sum_warp<kChunkTile / 32>(chain[k], tile[b][k], m);
+      if (lane < NP) {
+        const int m = min(kChunkTile, len - t * kChunkTile);
+        const double* src = tile[b][lane];
+        // (the chain is bound by the fp64 add latency, ~10 cycles: 8192 adds ~ 45 us per
+        // chunk; software-pipelining the smem loads measured no faster)
+        int q = 0;
+        for (; q + 8 <= m; q += 8) {
+          const double2 a = *reinterpret_cast<const double2*>(src + q);
+          const double2 c = *reinterpret_cast<const double2*>(src + q + 2);
+          const double2 d = *reinterpret_cast<const double2*>(src + q + 4);
+          const double2 e = *reinterpret_cast<const double2*>(src + q + 6);
+          acc = __dadd_rn(acc, a.x);
+          acc = __dadd_rn(acc, a.y);
+          acc = __dadd_rn(acc, c.x);
+          acc = __dadd_rn(acc, c.y);
+          acc = __dadd_rn(acc, d.x);
+          acc = __dadd_rn(acc, d.y);
+          acc = __dadd_rn(acc, e.x);
+          acc = __dadd_rn(acc, e.y);
+        }
+        for (; q < m; ++q) acc = __dadd_rn(acc, src[q]);
+      }
       __syncwarp();
       if (lane == 0 && t + 2 < ntiles) mbar_arrive(&empty[b]);
     }
-    if (lane < NP) {
-      double mine = chain[0];
-#pragma unroll
-      for (int k = 1; k < NP; ++k)
-        if (lane == k) mine = chain[k];
-      partials[blockIdx.x * NP + lane] = mine;
-    }
+    if (lane < NP) partials[blockIdx.x * NP + lane] = acc;
   }
   __threadfence();
   __syncthreads();
@@ -223,8 +131,9 @@ __global__ void __launch_bounds__(kChunkThreads, 10)
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // Chunk partials in chunk order: staged tile by tile into shared memory (coalesced, in flight
-  // together), chain k summed by warp k with the exact sequential-sum emulation.
+  // Chunk partials in chunk order.  All threads stage tiles of partials into shared memory
+  // (coalesced, in flight together); lanes 0..NP-1 walk each tile sequentially, so the
+  // dependent chain pays the add latency, not a global-load latency per chunk.
   double s = 0.0;
   const unsigned nc = gridDim.x;
   double* stage = &tile[0][0][0];  // reuse: 2 * NP * kChunkTile >= NP * kFinalTile
@@ -237,15 +146,16 @@ __global__ void __launch_bounds__(kChunkThreads, 10)
       stage[k * kFinalTile + c] = __ldcg(partials + (base + c) * NP + k);
     }
     __syncthreads();
-    if (warp < NP) {
-      const double* src = stage + warp * kFinalTile;
-      if (nc == 1)
+    if (threadIdx.x < NP) {
+      const double* src = stage + threadIdx.x * kFinalTile;
+      if (nc == 1) {
         s = src[0];  // single chunk: the reference returns the chunk sum itself
-      else
-        s = seq_sum_warp<kChunkTile / 32>(s, src, cnt);
+      } else {
+        for (int c = 0; c < cnt; ++c) s = __dadd_rn(s, src[c]);
+      }
     }
   }
-  if (warp < NP && lane == 0) out[warp] = s;
+  if (threadIdx.x < NP) out[threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
     *ticket = 0u;

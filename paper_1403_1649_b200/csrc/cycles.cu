@@ -238,36 +238,23 @@ __global__ void __launch_bounds__(kLuThreads) k_lu_solve(int n, const double* __
     }
     __syncthreads();
   }
-  // backward (xs holds y).  Row i's chain: s = y_i; s -= U_{i,i+1} x_{i+1}; s -= U_{i,i+2} x_{i+2}
-  // ...  Its first term needs x_{i+1}, the value just produced; the rest were staged (negated:
-  // RN(s - p) == RN(s + (-p))) by warps 1.. while warp 0 ran row i+1.  Warp 0 adds the first
-  // term, then runs the remaining chain with the exact sequential-sum emulation
-  // (seq_sum_warp): a few warp steps per row instead of n - i dependent adds.
+  // backward (xs holds y)
   const int lane = t & 31, w = t >> 5;
-  double* ud = pb + 2 * n;  // ud[2 * (i & 1)] = U_ii, ud[2 * (i & 1) + 1] = U_{i,i+1}
-  if (t == 0 && n > 0) {
-    ud[2 * ((n - 1) & 1)] = lu[static_cast<int64_t>(n - 1) * n + (n - 1)];
-  }
-  if (n > 1 && t == 0) {  // row n-2 has no staged terms (j >= n); its U_ii, U_{i,i+1}
-    ud[2 * ((n - 2) & 1)] = lu[static_cast<int64_t>(n - 2) * n + (n - 2)];
-    ud[2 * ((n - 2) & 1) + 1] = lu[static_cast<int64_t>(n - 2) * n + (n - 1)];
-  }
-  __syncthreads();
   for (int i = n - 1; i >= 0; --i) {
     if (w == 0) {
-      const double* st = pb + (i & 1) * n;
-      double acc = xs[i];
-      if (i + 1 < n) acc = __dsub_rn(acc, __dmul_rn(ud[2 * (i & 1) + 1], xs[i + 1]));
-      if (i + 2 < n) acc = seq_sum_warp<8>(acc, st + i + 2, n - i - 2);
-      if (lane == 0) xs[i] = __ddiv_rn(acc, ud[2 * (i & 1)]);
-    } else if (i >= 1) {  // stage row i-1: -(U_{i-1,j} x_j) for j >= i+1, and its U_ii, U_{i,i+1}
+      if (lane == 0) {
+        const double* ui = lu + static_cast<int64_t>(i) * n;
+        double acc = xs[i];
+        if (i + 1 < n) acc = __dsub_rn(acc, __dmul_rn(ui[i + 1], xs[i + 1]));
+        const double* p = pb + (i & 1) * n;
+#pragma unroll 8
+        for (int j = i + 2; j < n; ++j) acc = __dsub_rn(acc, p[j]);
+        xs[i] = __ddiv_rn(acc, ui[i]);
+      }
+    } else if (i > 0) {
       const double* ur = lu + static_cast<int64_t>(i - 1) * n;
       double* p = pb + ((i - 1) & 1) * n;
-      for (int j = i + 1 + (t - 32); j < n; j += kLuThreads - 32) p[j] = -__dmul_rn(ur[j], xs[j]);
-      if (t == 32) {
-        ud[2 * ((i - 1) & 1)] = ur[i - 1];
-        ud[2 * ((i - 1) & 1) + 1] = ur[i];
-      }
+      for (int j = i + 1 + (t - 32); j < n; j += kLuThreads - 32) p[j] = __dmul_rn(ur[j], xs[j]);
     }
     __syncthreads();
   }
@@ -645,7 +632,7 @@ void coarse_solve(DevHierarchy& h, const double* b, double* x, const int* pred) 
   const int64_t n = h.levels.back().A->n_rows;
   if (n == 0) return;
   if (exact_reductions() && h.coarse_lu_ready) {  // bit-identical substitution (slow: n^2 chain)
-    const size_t smem = (3 * n + 4) * sizeof(double);
+    const size_t smem = 3 * n * sizeof(double);
     if (n <= int64_t{kLuRows} * kLuThreads && smem <= 200 * 1024) {
       static std::atomic<unsigned long long> attr{0};  // the attribute is per device
       if (device_pending(attr)) {

@@ -9,7 +9,8 @@ Here the B200 path runs the same configuration exactly as bench.py does (device-
 matrix, setup_hierarchy_device, solve_device), so these are the kernels the headline times:
 level 0 in SELL-32 with the one-byte value dictionary, level 1 in SELL-32, the rest CSR-stream.
   - setup: every level bit-identical to the reference (digests equal);
-  - default solve: iteration count equal, |h_k - h_k^ref| <= 1e-10 * h_0^ref, x within 1e-10;
+  - default solve: iteration count equal, |h_k - h_k^ref| <= 1e-10 * max_j h_j^ref (PCG
+    residual norms are not monotone: c1's h_1 is 57 h_0), ||x|| within 1e-10;
   - exact-reduction mode: every history entry and every bit of x identical.
 """
 import ctypes as C
@@ -98,7 +99,7 @@ def test_fullsize_bit_identical_to_reference(gpu, name):
         rep, hist, x = _solve(gpu, h, name, pin["n"])
         assert rep.converged and rep.iterations == pin["iterations"]
         assert hist.shape == ref_hist.shape
-        assert np.max(np.abs(hist - ref_hist)) <= 1e-10 * ref_hist[0]
+        assert np.max(np.abs(hist - ref_hist)) <= 1e-10 * np.max(ref_hist)
         assert abs(np.linalg.norm(x) - pin["x_norm"]) <= 1e-10 * pin["x_norm"]
         del h
         # ---- exact-reduction mode: the whole solve bit-identical ----
