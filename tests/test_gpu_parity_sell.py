@@ -4,7 +4,7 @@ kernels — with the one-byte value dictionary on stencils, with plain fp64 valu
 variable-coefficient operator whose values are all distinct — inside full setups and solves.
 
 Per case: every level's A / P / R / B / inv_diag bit-identical and omega equal; the default
-solve with equal iteration counts, history within 1e-10 of h_0 and x within 1e-10; the
+solve with equal iteration counts, history within 1e-10 of its peak and x within 1e-10; the
 exact-reduction mode bit-identical (every history entry, every bit of x); refresh_values
 against the reference's refresh."""
 import numpy as np
@@ -90,7 +90,7 @@ def _assert_solve_close(rg, rr):
     assert rg.report.converged and rg.report.iterations == rr.report.iterations
     hg, hr = np.array(rg.report.residual_history), np.array(rr.report.residual_history)
     assert hg.shape == hr.shape
-    assert np.max(np.abs(hg - hr)) <= 1e-10 * hr[0]
+    assert np.max(np.abs(hg - hr)) <= 1e-10 * np.max(hr)
     assert np.linalg.norm(rg.x - rr.x) <= 1e-10 * np.linalg.norm(rr.x)
 
 
