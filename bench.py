@@ -16,13 +16,19 @@ quoted on (configs[1]: 3-D 7-point Poisson 256^3, PCG + hybrid K-cycle, fp64).
           bytes per launch / CUDA-event launch time vs MEASURED_PEAKS.json hbm_gbs.
   cpu_baseline  the unmodified reference (oracle/_ref) on all host cores, bounded sample.
 
-Multi-GPU (torchrun, --gpus N > 1): the ROW-PARTITIONED solver: the grid of
-the config is stacked N times along its slowest axis (weak scaling, the config's problem per
-GPU), each rank generates and owns one slab, setup and solve exchange halos and scalars over
-NCCL, coarse levels are agglomerated on rank 0.  --mode replicas instead runs N independent
-copies; --emulate-ranks R runs the partitioned path as R rank threads on one GPU (a
-transport/overhead diagnostic, not a scaling number).
---impl reference times the reference CPU implementation on the host cores instead.
+Multi-GPU (--gpus N > 1; launched by torchrun, or by bench.py itself when WORLD_SIZE is
+unset): the ROW-PARTITIONED solver.  Weak scaling (default) keeps the config's
+problem per GPU and doubles the grid along x, then y, then z (256^3 on 1 GPU,
+512x256x256 on 2, 512x512x256 on 4, 512^3 on 8); --scaling strong keeps the config's grid
+(e.g. --config c5: 512^3 on every N).  Each rank generates and owns one z-slab, setup and solve
+exchange halos and scalars over NCCL, coarse levels are agglomerated on rank 0.  --mode
+replicas instead runs N independent copies; --emulate-ranks R runs the partitioned path as R
+rank threads on one GPU (a transport/overhead diagnostic, not a scaling number).
+
+--impl reference times the reference CPU implementation (oracle/_ref: the unmodified reference
+sources compiled by oracle/Makefile) on all host cores, on the SAME configuration: every timed
+step is one full setup + solve of the config's grid (the warm-up steps use a 64^3 grid of the
+same class, to keep the arm within the driver's budget).  Both arms print the same `config`.
 """
 import argparse
 import ctypes as C
@@ -186,6 +192,48 @@ class Dist:
             self.dist.destroy_process_group()
 
 
+def world_grid(cfg_name, world, scaling):
+    """The global grid at `world` GPUs: weak scaling doubles x, then y, then z,
+    a remaining odd factor stacks along z; strong scaling keeps the config's grid."""
+    label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[cfg_name]
+    if scaling == "strong" or world == 1:
+        return nx, ny, nz
+    g = [nx, ny, nz]
+    axes = [0, 1] if dims == 2 else [0, 1, 2]
+    w, i = world, 0
+    while w % 2 == 0:
+        g[axes[i % len(axes)]] *= 2
+        w //= 2
+        i += 1
+    g[axes[-1]] *= w
+    return tuple(g)
+
+
+def grid_nnz(dims, nx, ny, nz):
+    """Stored entries of the generated operators (Dirichlet rows eliminated)."""
+    n = nx * ny * nz
+    if dims == 27:
+        return (3 * nx - 2) * (3 * ny - 2) * (3 * nz - 2)
+    if dims == 2:
+        return n + 2 * ((nx - 1) * ny + nx * (ny - 1))
+    return n + 2 * ((nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1))
+
+
+def workload_config(cfg_name, world, scaling):
+    """The `config` object of the JSON line: identical in the B200 and the reference arms."""
+    label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[cfg_name]
+    gx, gy, gz = world_grid(cfg_name, world, scaling)
+    return {
+        "workload": label, "grid": [gx, gy, gz], "n": gx * gy * gz,
+        "nnz": grid_nnz(dims, gx, gy, gz),
+        "solver": "pcg" if method == "pcg" else "fgmres(30)", "tol": 1e-8,
+        "preconditioner": f"hybrid K-cycle AMG (k_levels 2, t 0.25, inner GMRES), alpha {alpha}, "
+                          "coarse_size_max 600, damped Jacobi, seed 42",
+        "rhs": "b = B0 = ones, x0 = 0",
+        "scaling": scaling if world > 1 else "weak",
+    }
+
+
 def configs_c(M, alpha, method, tol=1e-8, max_iters=500):
     setup = M.SetupConfig(alpha=alpha, reuse_caches=True)
     cycle = M.CycleConfig()
@@ -194,53 +242,70 @@ def configs_c(M, alpha, method, tol=1e-8, max_iters=500):
     return setup, cycle, solver
 
 
-def cpu_reference_run(M, cfg_name, sample_n, threads):
-    """One setup+solve of the reference (oracle/_ref) on a bounded sample grid."""
-    label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[cfg_name]
+def reference_matrix(cfg_name, grid):
+    """The config's matrix on the host, generated by the reference itself (poisson.cpp) or, for
+    the 27-point jump problem that has no reference generator, by the C restatement."""
     from oracle import checkers
 
+    label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[cfg_name]
+    gx, gy, gz = grid
+    if dims == 27:
+        return checkers.oracle().generate_jump27(gx, gy, gz, eps, JUMP_BLOCK)
+    return checkers.ref().generate_poisson(2 if dims == 2 else 3, gx, gy, gz, eps)
+
+
+def cpu_reference_run(M, cfg_name, A, threads, reuse_caches=False):
+    """One setup + solve by the reference (oracle/_ref) on all host threads."""
+    from oracle import checkers
+
+    label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[cfg_name]
     r = checkers.ref()
     r.lib.fn("set_num_threads")(threads)
-    if dims == 27:
-        A = checkers.oracle().generate_jump27(sample_n, sample_n, sample_n, eps, JUMP_BLOCK)
-    elif dims == 3:
-        A = r.generate_poisson(3, sample_n, sample_n, sample_n, eps)
-    else:
-        A = r.generate_poisson(2, sample_n, sample_n, 1, eps)
     setup, cycle, solver = configs_c(M, alpha, method)
-    setup.reuse_caches = False  # the reference's default (faster) Galerkin path
+    setup.reuse_caches = reuse_caches
     t0 = time.perf_counter()
     res = r.setup_and_solve(A, np.ones(A.n_rows), setup, cycle, solver)
-    dt = time.perf_counter() - t0
-    return A.n_rows, dt, res
+    return time.perf_counter() - t0, res
 
 
 def run_reference_arm(args, world, rank):
+    """The reference's own CPU implementation on the same configuration (rank 0 only)."""
     from paper_1403_1649_b200 import aggmg as M
 
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
     dims = CONFIGS[args.config][1]
-    sample_n = args.ref_sample or (512 if dims == 2 else (64 if dims == 27 else 96))
-    times, n = [], 0
-    for i in range(args.warmup + args.steps):
-        n, dt, res = cpu_reference_run(M, args.config, sample_n, threads)
-        if i >= args.warmup:
-            times.append(dt)
+    grid = world_grid(args.config, args.gpus, args.scaling)
+    small = (64, 64, 1) if dims == 2 else (64, 64, 64)
+    Aw = reference_matrix(args.config, small)
+    for _ in range(args.warmup):
+        cpu_reference_run(M, args.config, Aw, threads)
+    del Aw
+    A = reference_matrix(args.config, grid)
+    times = []
+    for _ in range(args.steps):
+        dt, res = cpu_reference_run(M, args.config, A, threads)
+        times.append(dt)
     total = sum(times)
-    value = n * len(times) / total
-    sample = (f"{sample_n}^{2 if dims == 2 else 3} grid of the same problem class, full setup+solve per step "
-              f"(reference default Galerkin path), {res.report.iterations} iterations")
+    value = A.n_rows * len(times) / total
+    sample = (f"the full configuration ({grid[0]}x{grid[1]}x{grid[2]}, {A.n_rows} unknowns) every timed step: "
+              f"setup_hierarchy + {'pcg' if CONFIGS[args.config][7] == 'pcg' else 'fgmres'} to 1e-8 "
+              f"({res.report.iterations} iterations), the reference's default Galerkin path "
+              f"(reuse_caches = false, its faster one); warm-up steps on a 64^{2 if dims == 2 else 3} grid")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": args.scaling if args.gpus > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config][0], "sample": sample},
+        "config": workload_config(args.config, args.gpus, args.scaling),
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": {"step_seconds": times, "iterations": res.report.iterations,
+                   "setup_seconds": res.report.setup_seconds,
+                   "solve_seconds": res.report.solve_seconds},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -340,6 +405,57 @@ def run_b200(args, world, rank, local):
                "iterations": res.report.iterations}
         del Ah
 
+    # ---- e2e through the reference's own call sequence (setup_hierarchy(A, B0)
+    # then pcg / fgmres(A, b, x0, M)): the matrix crosses the boundary twice, as in the reference
+    e2e_ref_api = None
+    if not args.no_e2e and world == 1:
+        Ah = (gpu.generate_jump27(nx, ny, nz, eps, JUMP_BLOCK) if dims == 27
+              else gpu.generate_poisson(dims, nx, ny, nz, eps))
+        b = np.ones(n)
+        krylov = gpu.pcg if method == "pcg" else gpu.fgmres
+
+        def api_step():
+            hh = gpu.setup_hierarchy(Ah, None, setup)
+            return krylov(Ah, b, None, hh, cycle, solver)
+
+        api_step()  # warm-up
+        t0 = time.perf_counter()
+        for _ in range(2):
+            res = api_step()
+        dt = (time.perf_counter() - t0) / 2
+        e2e_ref_api = {"value": n / dt, "unit": "DOF/s", "ms_per_step": 1e3 * dt,
+                       "h2d_bytes_per_step": int(2 * (Ah.row_offsets.nbytes + Ah.col_indices.nbytes
+                                                      + Ah.values.nbytes) + b.nbytes),
+                       "d2h_bytes_per_step": int(n * 8), "iterations": res.report.iterations,
+                       "calls": "aggmg_setup_hierarchy + aggmg_pcg/aggmg_fgmres (C-ABI, host arrays)"}
+        del Ah
+
+    # ---- side number: the step with plain fp64 SELL values (no value dictionary): the cost
+    # on operators with more than 256 distinct values (variable coefficients)
+    no_dict = None
+    if not args.no_exact and world == 1 and l0_vi:
+        lib.fn("set_value_dictionary")(0)
+        dm2 = C.c_void_p()
+        if dims == 27:
+            check(lib.fn("dmatrix_jump27")(nx, ny, nz, eps, JUMP_BLOCK, C.byref(dm2)))
+        else:
+            check(lib.fn("dmatrix_poisson")(dims, nx, ny, nz, eps, -1, C.byref(dm2)))
+        dm_saved, dm = dm, dm2
+        step(None)
+        nrec = []
+        check(lib.fn("synchronize")())
+        check(lib.fn("timer_start")())
+        for _ in range(2):
+            step(nrec)
+        check(lib.fn("timer_stop")(C.byref(ms)))
+        lib.fn("set_value_dictionary")(1)
+        dm = dm_saved
+        lib.fn("dmatrix_free")(dm2)
+        no_dict = {"ms_per_step": ms.value / 2, "setup_ms": nrec[0]["setup_ms"],
+                   "solve_ms": 1e3 * nrec[0]["solve_s"], "iterations": nrec[0]["iterations"],
+                   "note": "aggmg_set_value_dictionary(0): SELL-32 with 8-byte values, as on a "
+                           "variable-coefficient operator; not the headline"}
+
     # ---- side number: the same step in bit-identical mode (aggmg_set_exact_reductions) ----
     exact = None
     if not args.no_exact:
@@ -360,12 +476,22 @@ def run_b200(args, world, rank, local):
     # ---- CPU baseline (reference, all host cores, bounded sample) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libaggmg_ref.so")):
+        # the reference on the SAME configuration, once per Galerkin path: the default direct
+        # R(AP) products (its faster path) and the cached sort/segmented reduce this library
+        # reproduces bit for bit (reuse_caches = true)
         threads = os.cpu_count() or 1
-        sample_n = 512 if dims == 2 else (96 if dims == 27 else 128)
-        ns, dt, cres = cpu_reference_run(M, args.config, sample_n, threads)
-        cpu = {"value": ns / dt, "unit": "DOF/s", "cores": threads, "kind": "reference",
-               "sample": f"one setup+solve of the {sample_n}^{2 if dims == 2 else 3} grid (reference default "
-                         f"Galerkin path, {cres.report.iterations} its, {dt:.1f} s)"}
+        A = reference_matrix(args.config, (nx, ny, nz))
+        dt, cres = cpu_reference_run(M, args.config, A, threads, reuse_caches=False)
+        dt2, cres2 = cpu_reference_run(M, args.config, A, threads, reuse_caches=True)
+        cpu = {"value": n / dt, "unit": "DOF/s", "cores": threads, "kind": "reference",
+               "sample": f"one full setup+solve of the configuration ({nx}x{ny}x{nz}) by the reference, "
+                         f"default Galerkin path: {dt:.1f} s ({cres.report.setup_seconds:.1f} s setup, "
+                         f"{cres.report.iterations} its)",
+               "cache_path": {"value": n / dt2, "seconds": dt2,
+                              "setup_seconds": cres2.report.setup_seconds,
+                              "iterations": cres2.report.iterations,
+                              "note": "reuse_caches = true: the summation order the B200 path reproduces"}}
+        del A
 
     peak, peak_src = load_peak()
     jt, jc, jb = fam["jacobi_l0"]
@@ -400,7 +526,8 @@ def run_b200(args, world, rank, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": ("synthetic: device-generated " + ("27-point jumping-coefficient matrix (DESIGN.md §7)"
                  if dims == 27 else "Poisson matrix (poisson.cpp semantics)") + ", b = B0 = ones, x0 = 0"),
-        "config": {"workload": label, "n": n, "nnz": nnz, "levels": r0.get("levels"),
+        "config": workload_config(args.config, 1, "weak"),
+        "detail": {"levels": r0.get("levels"),
                    "iterations": r0.get("iterations"), "converged": r0.get("converged"),
                    "setup_ms": statistics.median(r["setup_ms"] for r in records),
                    "solve_ms": 1e3 * statistics.median(r["solve_s"] for r in records),
@@ -409,7 +536,8 @@ def run_b200(args, world, rank, local):
                    "galerkin": "cached sort/segmented reduce (reference reuse_caches=true order)",
                    "l2": f"inputs larger than L2 (A alone is {(12 * nnz + 4 * n) / 1e9:.2f} GB)",
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                   "exact_mode": exact},
+                   "exact_mode": exact, "no_value_dictionary": no_dict,
+                   "e2e_reference_call_sequence": e2e_ref_api},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -423,13 +551,6 @@ def run_b200(args, world, rank, local):
     return 0
 
 
-def dist_grid(dims, nx, ny, nz, world):
-    """Weak scaling: the config's grid per rank, stacked along the slowest axis."""
-    if dims == 2:
-        return nx, ny * world, 1
-    return nx, ny, nz * world
-
-
 def rank_bench(comm, rank, local, args, sync_max, sync_sum):
     """One rank of the partitioned benchmark (NCCL process or emulated rank thread).
     sync_max / sync_sum reduce a float over the ranks (host)."""
@@ -439,13 +560,15 @@ def rank_bench(comm, rank, local, args, sync_max, sync_sum):
     lib = M.b200().lib
     world = comm.size
     label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[args.config]
-    gx, gy, gz = dist_grid(dims, nx, ny, nz, world)
+    gx, gy, gz = world_grid(args.config, world, args.scaling)
     setup, cycle, solver = configs_c(M, alpha, method)
     if dims == 27:
         dA = D.DistMatrix.jump27(comm, gx, gy, gz, eps, JUMP_BLOCK)
     else:
         dA = D.DistMatrix.poisson(comm, dims, gx, gy, gz, eps)
     n_glob, row0, nloc, nnz_loc = dA.info()
+    fmt = C.c_int32()
+    lib.fn("dist_matrix_format")(dA._h, C.byref(fmt))
     nnz_glob = sync_sum(float(nnz_loc))
 
     def step(record):
@@ -512,22 +635,24 @@ def rank_bench(comm, rank, local, args, sync_max, sync_sum):
     jt, jc, jb = fam.get("jacobi_l0", (0, 0, 0))
     if jc > 0:
         achieved = (jb / jc) / ((jt / jc) / 1e3) / 1e9
+        kname = {2: "k_sell<Epi::kJacobi, VI> (SELL-32, one-byte value codes)",
+                 1: "k_sell<Epi::kJacobi> (SELL-32)",
+                 0: "k_csr_stream<Epi::kJacobi>"}[fmt.value]
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None,
-                "kernel": "k_csr_stream<Epi::kJacobi> on level 0 (rank 0's slab)",
+                "kernel": kname + " on level 0: the damped-Jacobi sweep over rank 0's slab",
                 "bytes_per_launch": jb / jc, "avg_launch_ms": jt / jc, "launches": jc,
                 "peak_source": peak_src, "share_of_step": jt / elapsed_ms}
     r0 = records[0] if records else {}
     return {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": ("synthetic: device-generated " + ("27-point jumping-coefficient matrix"
                  if dims == 27 else "Poisson matrix (poisson.cpp semantics)")
                  + ", one row slab per rank, b = B0 = ones, x0 = 0"),
-        "config": {"workload": label + f" per GPU, stacked x{world} along the slowest axis",
-                   "grid": [gx, gy, gz], "n": n_glob, "nnz": int(nnz_glob),
-                   "levels": r0.get("levels"), "distributed_levels": r0.get("distributed_levels"),
+        "config": workload_config(args.config, world, args.scaling),
+        "detail": {"levels": r0.get("levels"), "distributed_levels": r0.get("distributed_levels"),
                    "agglomerate_rows": args.agglomerate,
                    "iterations": r0.get("iterations"), "converged": r0.get("converged"),
                    "setup_ms": statistics.median(r["setup_ms"] for r in records),
@@ -603,6 +728,42 @@ def run_emulated(args):
     return 0
 
 
+def spawn_ranks(n):
+    """`python bench.py --gpus N` without a launcher: start N ranks through torch.distributed.run
+    on this node (127.0.0.1, a free port); rank 0 prints the JSON line to our stdout."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, world, rank):
+    """Launcher / rendezvous check on CPU: every rank joins a gloo group, the ranks agree on the
+    global grid, and rank 0 prints a config-only line."""
+    import torch
+    import torch.distributed as tdist
+
+    if world > 1:
+        tdist.init_process_group("gloo")
+    grid = world_grid(args.config, world, args.scaling)
+    rows = grid[0] * grid[1] * grid[2]
+    t = torch.tensor([float(rows // world + (1 if rank < rows % world else 0))], dtype=torch.float64)
+    if world > 1:
+        tdist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "n_gpus": world, "dry_run": True,
+                          "rows_covered": int(t.item()), "scaling": args.scaling,
+                          "config": workload_config(args.config, world, args.scaling)}), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -621,7 +782,16 @@ def main():
     ap.add_argument("--agglomerate", type=int, default=0,
                     help="rows at or below which a level is gathered on rank 0 (0 = default)")
     ap.add_argument("--emulate-ranks", type=int, default=0)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak keeps the config's problem per GPU, strong keeps its grid")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: ranks rendezvous over gloo, agree on the "
+                         "workload and print the config line (tests/test_bench_launcher.py)")
     args = ap.parse_args()
+    world, rank, local = dist_env()
+    if (args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200"
+            and args.emulate_ranks == 0 and args.mode != "replicas"):
+        return spawn_ranks(args.gpus)  # one process per GPU, like the driver's torchrun
     # Native libraries (NCCL's version banner, driver messages) write to fd 1; point fd 1 at
     # stderr and keep the real stdout for the JSON line alone.
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
@@ -629,7 +799,8 @@ def main():
     real_stdout = os.dup(1)
     os.dup2(2, 1)
     sys.stdout = os.fdopen(real_stdout, "w", buffering=1)
-    world, rank, local = dist_env()
+    if args.dry_run:
+        return run_dry(args, world, rank)
     if args.impl == "reference":
         return run_reference_arm(args, world, rank)
     if args.emulate_ranks > 0:
