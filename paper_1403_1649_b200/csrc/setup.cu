@@ -241,7 +241,8 @@ __global__ void k_mis_init(const idx* infl, int64_t n, uint64_t seed, Tuple* cur
   state[i] = 0;
 }
 
-// mid_i = max over {i} u N(i) of cur (aggregation.cpp:31-41)
+// mid_i = max over {i} u N(i) of cur (aggregation.cpp:31-41).  Grid-stride over the rows (a
+// persistent grid): pass 2 then reduces its decided count per CTA, one atomic per CTA.
 __global__ void k_mis_pass1(const idx* __restrict__ rp, const idx* __restrict__ col, int64_t n,
                             const Tuple* cur, Tuple* mid, MisCtl* ctl) {
   const int undecided = *reinterpret_cast<volatile int*>(&ctl->undecided);
@@ -250,25 +251,29 @@ __global__ void k_mis_pass1(const idx* __restrict__ rp, const idx* __restrict__ 
     if (undecided > 0) ctl->sweeps += 1;
   }
   if (undecided == 0) return;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  Tuple best = load_tuple(cur + i);
-  const idx k0 = rp[i], k1 = rp[i + 1];
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    Tuple best = load_tuple(cur + i);
+    const idx k0 = rp[i], k1 = rp[i + 1];
 #pragma unroll 8
-  for (idx k = k0; k < k1; ++k) {  // unrolled: the gathers of a row issue together
-    const Tuple t = load_tuple(cur + col[k]);
-    if (tuple_less(best, t)) best = t;
+    for (idx k = k0; k < k1; ++k) {  // unrolled: the gathers of a row issue together
+      const Tuple t = load_tuple(cur + col[k]);
+      if (tuple_less(best, t)) best = t;
+    }
+    mid[i] = best;
   }
-  mid[i] = best;
 }
 
 // far_i = max over {i} u N(i) of mid; decide; broadcast the state (aggregation.cpp:64-79)
-__global__ void k_mis_pass2(const idx* __restrict__ rp, const idx* __restrict__ col, int64_t n,
-                            const Tuple* mid, Tuple* cur, int8_t* state, MisCtl* ctl) {
+__global__ void __launch_bounds__(256) k_mis_pass2(const idx* __restrict__ rp, const idx* __restrict__ col,
+                                                   int64_t n, const Tuple* mid, Tuple* cur,
+                                                   int8_t* state, MisCtl* ctl) {
+  __shared__ int s_dec[8];
   if (!ctl->active) return;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int decided = 0;
-  if (i < n && state[i] == 0) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    if (state[i] != 0) continue;
     Tuple far = load_tuple(mid + i);
     const idx k0 = rp[i], k1 = rp[i + 1];
 #pragma unroll 8
@@ -284,11 +289,19 @@ __global__ void k_mis_pass2(const idx* __restrict__ rp, const idx* __restrict__ 
     if (st != 0) {
       state[i] = st;
       cur[i].s = st;
-      decided = 1;
+      ++decided;
     }
   }
-  const unsigned ballot = __ballot_sync(0xffffffffu, decided);
-  if ((threadIdx.x & 31) == 0 && ballot) atomicSub(&ctl->undecided, __popc(ballot));
+  // one atomic per CTA (a same-address atomic per warp serialised 0.5 M of them per sweep)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) decided += __shfl_down_sync(0xffffffffu, decided, o);
+  if ((threadIdx.x & 31) == 0) s_dec[threadIdx.x >> 5] = decided;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += s_dec[w];
+    if (tot) atomicSub(&ctl->undecided, tot);
+  }
 }
 
 // ---- MIS(2) late sweeps on the undecided set -----------------------------------------------
@@ -487,78 +500,164 @@ constexpr int kGalHash = 512;    // tier 2: distinct coarse columns per row (has
 // Member-parallel gather of coarse row I's fine entries into (key, k, row) slots:
 // lanes own member rows, a warp scan of the row lengths gives each member its slot
 // range, so slot order = (member row ascending, storage order) = global storage order.
-__device__ inline void gal_gather_warp(idx m0, idx m1, const idx* rows, const idx* arp,
-                                       const idx* acol, const idx* assignment,
-                                       unsigned long long* skey, idx* skk, idx* sri, int lane) {
-  idx base = 0;
-  for (idx mb = m0; mb < m1; mb += 32) {
-    const idx m = mb + lane;
-    idx i = 0, lo = 0, len = 0;
-    if (m < m1) {
-      i = rows[m];
-      lo = arp[i];
-      len = arp[i + 1] - lo;
-    }
-    idx incl = len;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const idx t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const idx off = base + incl - len;
-    for (idx t = 0; t < len; ++t) {
-      const idx k = lo + t, p = off + t;
-      skey[p] = (static_cast<unsigned long long>(assignment[acol[k]]) << 32) |
-                static_cast<unsigned long long>(p);
-      skk[p] = k;
-      sri[p] = i;
-    }
-    base += __shfl_sync(0xffffffffu, incl, 31);
-  }
-}
-
 // Tier 1 — warp per coarse row I: gather the fine entries of I's member rows, sort them
 // by coarse column J with the gather position as the tie-break (= the reference's stable
 // sort by key I*nc+J, galerkin.cpp:52-62) and emit entry / entry_row / sorted J; count
 // the distinct J (coarse row length).  Rows longer than kGalCap go to tier 2.
+// O(L) per row, no comparison sort:
+//  1. gather, entry-parallel: member starts by a warp scan of the member lengths, every lane
+//     resolves its entries' member by a binary search, so the acol / assignment loads of the
+//     whole row are in flight together;
+//  2. distinct J in a per-warp shared hash table with their counts; the (few) distinct J
+//     ranked against each other; start offsets by a warp scan in J order;
+//  3. stable scatter in gather order, 32 entries at a time: __match_any_sync groups equal J,
+//     an entry's slot is the J's cursor plus its rank among the equal lanes before it.
+constexpr int kGalHash1 = 128;     // tier 1 hash slots per warp (distinct J per coarse row <= L)
+constexpr int kGalMembers1 = 64;   // tier 1 members per coarse row (aggregates are ~10-30 rows)
 __global__ void __launch_bounds__(kGalWarps * 32)
     k_gal_symbolic(const idx* goff, const idx* rows, const idx* arp, const idx* acol,
                    const idx* assignment, int64_t nc, const idx* eoff, idx* entry, idx* entry_row,
                    idx* sorted_j, idx* cnnz, idx* big_list, int* big_count) {
-  __shared__ unsigned long long s_key[kGalWarps][kGalCap];
-  __shared__ idx s_kk[kGalWarps][kGalCap], s_ri[kGalWarps][kGalCap], s_j[kGalWarps][kGalCap];
+  __shared__ idx s_j[kGalWarps][kGalCap], s_kk[kGalWarps][kGalCap], s_ri[kGalWarps][kGalCap];
+  __shared__ idx s_moff[kGalWarps][kGalMembers1], s_mlo[kGalWarps][kGalMembers1],
+      s_mrow[kGalWarps][kGalMembers1];
+  __shared__ idx s_hj[kGalWarps][kGalHash1], s_hc[kGalWarps][kGalHash1];
+  __shared__ idx s_dj[kGalWarps][kGalHash1], s_ds[kGalWarps][kGalHash1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned kFull = 0xffffffffu;
   const int64_t I = static_cast<int64_t>(blockIdx.x) * kGalWarps + w;
   if (I >= nc) return;
-  unsigned long long* skey = s_key[w];
-  idx* skk = s_kk[w];
-  idx* sri = s_ri[w];
-  idx* sj = s_j[w];
   const idx base_e = eoff[I];
   const idx L = eoff[I + 1] - base_e;
-  if (L > kGalCap) {
+  const idx m0 = goff[I], nm = goff[I + 1] - m0;
+  if (L > kGalCap || nm > kGalMembers1) {
     if (lane == 0) big_list[atomicAdd(big_count, 1)] = static_cast<idx>(I);
     return;
   }
-  gal_gather_warp(goff[I], goff[I + 1], rows, arp, acol, assignment, skey, skk, sri, lane);
-  __syncwarp();
-  for (idx q = lane; q < L; q += 32) {
-    const unsigned long long key = skey[q];
-    idx rank = 0;
-    for (idx z = 0; z < L; ++z) rank += (skey[z] < key) ? 1 : 0;
-    entry[base_e + rank] = skk[q];
-    entry_row[base_e + rank] = sri[q];
-    sj[rank] = static_cast<idx>(key >> 32);
+  idx* sj = s_j[w];
+  idx* skk = s_kk[w];
+  idx* sri = s_ri[w];
+  idx* moff = s_moff[w];
+  idx* mlo = s_mlo[w];
+  idx* mrow = s_mrow[w];
+  idx* hj = s_hj[w];
+  idx* hc = s_hc[w];
+  for (int q = lane; q < kGalHash1; q += 32) {
+    hj[q] = -1;
+    hc[q] = 0;
+  }
+  // ---- 1. gather ----
+  idx run = 0;
+  for (idx mb = 0; mb < nm; mb += 32) {
+    const idx m = mb + lane;
+    idx len = 0;
+    if (m < nm) {
+      const idx i = rows[m0 + m];
+      const idx lo = arp[i];
+      len = arp[i + 1] - lo;
+      mlo[m] = lo;
+      mrow[m] = i;
+    }
+    idx incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const idx t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (m < nm) moff[m] = run + incl - len;
+    run += __shfl_sync(kFull, incl, 31);
   }
   __syncwarp();
-  idx cnt = 0;
-  for (idx b = 0; b < L; b += 32) {
-    const idx r = b + lane;
-    const bool st = r < L && (r == 0 || sj[r] != sj[r - 1]);
-    cnt += __popc(__ballot_sync(0xffffffffu, st));
-    if (r < L) sorted_j[base_e + r] = sj[r];
+  for (idx p = lane; p < L; p += 32) {
+    idx lo = 0, hi = nm;  // the last member whose start is <= p
+    while (hi - lo > 1) {
+      const idx mid = (lo + hi) >> 1;
+      if (moff[mid] <= p)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    const idx k = mlo[lo] + (p - moff[lo]);
+    sj[p] = assignment[acol[k]];
+    skk[p] = k;
+    sri[p] = mrow[lo];
   }
-  if (lane == 0) cnnz[I] = cnt;
+  __syncwarp();
+  // ---- 2. distinct J, counts, starts ----
+  bool over = false;
+  for (idx p = lane; p < L; p += 32) {
+    const idx J = sj[p];
+    unsigned h = (static_cast<unsigned>(J) * 2654435761u) & (kGalHash1 - 1);
+    int probes = 0;
+    while (true) {
+      const idx old = atomicCAS(&hj[h], -1, J);
+      if (old == -1 || old == J) break;
+      h = (h + 1) & (kGalHash1 - 1);
+      if (++probes == kGalHash1) break;  // more distinct J than slots
+    }
+    if (probes == kGalHash1)
+      over = true;
+    else
+      atomicAdd(&hc[h], 1);
+  }
+  if (__any_sync(kFull, over)) {  // a coarse row of > kGalHash1 columns: tier 2
+    if (lane == 0) big_list[atomicAdd(big_count, 1)] = static_cast<idx>(I);
+    return;
+  }
+  __syncwarp();
+  // compact the occupied slots (slot order), then rank each distinct J among them
+  idx* dj = s_dj[w];   // distinct J in slot order
+  idx* ds = s_ds[w];   // their hash slots
+  idx nd = 0;
+  for (int q0 = 0; q0 < kGalHash1; q0 += 32) {
+    const int q = q0 + lane;
+    const bool occ = hj[q] != -1;
+    const unsigned bal = __ballot_sync(kFull, occ);
+    if (occ) {
+      const idx at = nd + __popc(bal & ((1u << lane) - 1));
+      dj[at] = hj[q];
+      ds[at] = q;
+    }
+    nd += __popc(bal);
+  }
+  __syncwarp();
+  // start of each distinct J = sum of the counts of the smaller J (nd is small: a coarse row)
+  idx start[kGalHash1 / 32];
+#pragma unroll
+  for (int r = 0; r < kGalHash1 / 32; ++r) {
+    const idx d = lane + 32 * r;
+    start[r] = 0;
+    if (d < nd) {
+      const idx J = dj[d];
+      for (idx e = 0; e < nd; ++e) start[r] += dj[e] < J ? hc[ds[e]] : 0;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < kGalHash1 / 32; ++r)  // counts -> cursors
+    if (lane + 32 * r < nd) hc[ds[lane + 32 * r]] = start[r];
+  __syncwarp();
+  // ---- 3. stable scatter in gather order ----
+  for (idx pb = 0; pb < L; pb += 32) {
+    const idx p = pb + lane;
+    const bool act = p < L;
+    const idx J = act ? sj[p] : -1 - lane;  // inactive lanes never match a real J
+    unsigned h = (static_cast<unsigned>(J) * 2654435761u) & (kGalHash1 - 1);
+    if (act)
+      while (hj[h] != J) h = (h + 1) & (kGalHash1 - 1);
+    const unsigned peers = __match_any_sync(kFull, J);
+    const idx cur = act ? hc[h] : 0;
+    const idx slot = cur + __popc(peers & ((1u << lane) - 1));
+    if (act) {
+      entry[base_e + slot] = skk[p];
+      entry_row[base_e + slot] = sri[p];
+      sorted_j[base_e + slot] = J;
+    }
+    __syncwarp();
+    if (act && lane == __ffs(peers) - 1) hc[h] = cur + __popc(peers);
+    __syncwarp();
+  }
+  if (lane == 0) cnnz[I] = nd;
 }
 
 // Tier 2 — one CTA (256 threads) per long coarse row (L > kGalCap gathered entries).
@@ -1250,13 +1349,14 @@ Mis2Dev mis2(const DevCsr& S, const idx* influence, uint64_t seed) {
   ctl.upload(&h0, 1);
   AGG_LAUNCH(k_mis_init, grid_for(n, 256), 256, 0, influence, n, seed, cur.get(), res.state.get());
   const unsigned g = grid_for(n, 256);
+  const unsigned gp = grid_for(n, 256, 8 * int64_t{sm_count()});  // the sweeps' persistent grid
   // Sweeps are issued in batches; once every node is decided the kernels exit at entry,
   // so the device-side sweep counter matches the reference's loop count exactly.
   int batch = 8;
   while (true) {
     for (int b = 0; b < batch; ++b) {
-      AGG_LAUNCH(k_mis_pass1, g, 256, 0, S.rowptr.get(), S.col.get(), n, cur.get(), mid.get(), ctl.get());
-      AGG_LAUNCH(k_mis_pass2, g, 256, 0, S.rowptr.get(), S.col.get(), n, mid.get(), cur.get(),
+      AGG_LAUNCH(k_mis_pass1, gp, 256, 0, S.rowptr.get(), S.col.get(), n, cur.get(), mid.get(), ctl.get());
+      AGG_LAUNCH(k_mis_pass2, gp, 256, 0, S.rowptr.get(), S.col.get(), n, mid.get(), cur.get(),
                  res.state.get(), ctl.get());
     }
     const MisCtl h = read_scalar(ctl.get());
