@@ -16,8 +16,15 @@ OBJS      := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(CU_SRCS)) \
 HDRS      := $(wildcard $(SRC_DIR)/*.cuh) $(wildcard $(SRC_DIR)/*.hpp) include/aggmg_b200.h
 
 DEMO      := build/cpp_dropin_demo
+CLI       := build/aggmg
 
-all: $(LIB) oracle $(DEMO)
+all: $(LIB) oracle $(DEMO) $(CLI)
+
+# the reference command line (aggmg_main.cpp: generate / solve / bench) over the drop-in header
+$(CLI): tools/aggmg_cli.cpp include/aggmg/aggmg.hpp include/aggmg_b200.h $(LIB)
+	@mkdir -p build
+	$(HOSTCXX) -std=c++20 -O2 -Wall -Iinclude $< -Lpaper_1403_1649_b200/lib -laggmg_b200 \
+	  -Wl,-rpath,'$$ORIGIN/../paper_1403_1649_b200/lib' -o $@
 
 # reference-style C++ caller built against the drop-in header include/aggmg/aggmg.hpp
 $(DEMO): tools/cpp_dropin_demo.cpp include/aggmg/aggmg.hpp include/aggmg_b200.h $(LIB)

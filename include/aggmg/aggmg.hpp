@@ -15,7 +15,8 @@
 //                        hierarchy_report, format_table, format_records
 //   cycles.hpp           CycleKind, InnerKind, CycleConfig, vcycle, kcycle, apply_preconditioner
 //   krylov.hpp           SolverConfig, SolveReport, SolveResult, Preconditioner, fgmres, pcg
-//   poisson.hpp          PoissonSpec, generate_poisson, ones_vector
+//   poisson.hpp          PoissonSpec, generate_poisson, ones_vector, random_vector
+//   matrix_market.hpp    MmOptions, read/write_matrix_market_file, read/write_vector_market_file
 // Differences, by design: the hierarchy lives in HBM (Hierarchy::device); the host copies of
 // its levels (Hierarchy::levels) are materialised on first access.  pcg/fgmres take any
 // Preconditioner: the AMG preconditioner returned by amg_preconditioner() runs inside the
@@ -623,6 +624,36 @@ inline SparseMatrix generate_poisson(const PoissonSpec& s) {
   return SparseMatrix::adopt(out);
 }
 inline Vector ones_vector(index_t n) { return Vector(static_cast<size_t>(n), 1.0); }
+inline Vector random_vector(index_t n, std::uint64_t seed) {  // poisson.hpp:30
+  Vector x(static_cast<size_t>(n));
+  detail::check(aggmg_random_vector(n, seed, x.data()));
+  return x;
+}
+
+// ---- matrix_market.hpp ---------------------------------------------------------------------
+
+struct MmOptions {
+  bool allow_pattern = false;
+};
+inline SparseMatrix read_matrix_market_file(const std::string& path, const MmOptions& opts = {}) {
+  aggmg_csr out{};
+  detail::check(aggmg_read_matrix_market_file(path.c_str(), opts.allow_pattern ? 1 : 0, &out));
+  return SparseMatrix::adopt(out);
+}
+inline void write_matrix_market_file(const std::string& path, const SparseMatrix& A) {
+  const aggmg_csr c = A.c();
+  detail::check(aggmg_write_matrix_market_file(path.c_str(), &c));
+}
+inline Vector read_vector_market_file(const std::string& path) {
+  int64_t n = 0;
+  detail::check(aggmg_read_vector_market_file(path.c_str(), nullptr, 0, &n));
+  Vector x(static_cast<size_t>(n));
+  detail::check(aggmg_read_vector_market_file(path.c_str(), x.data(), n, &n));
+  return x;
+}
+inline void write_vector_market_file(const std::string& path, const Vector& x) {
+  detail::check(aggmg_write_vector_market_file(path.c_str(), x.data(), static_cast<int64_t>(x.size())));
+}
 
 }  // namespace aggmg
 

@@ -260,6 +260,8 @@ int aggmg_setup_and_solve(const aggmg_csr* A, const double* b, const double* B0,
 /* poisson.hpp:17-26 / poisson.cpp:15-77, host generator */
 int aggmg_generate_poisson(int dims, int64_t nx, int64_t ny, int64_t nz, double epsilon,
                            int weak_axis, aggmg_csr* A);
+/* poisson.hpp:30 / poisson.cpp:81-87: x_i = uniform_sym(seed, i) in (-1, 1) */
+int aggmg_random_vector(int64_t n, uint64_t seed, double* x);
 /* 27-point variable-coefficient diffusion with coefficient jumps (BASELINE config 4;
  * no reference generator exists, definition in DESIGN.md) */
 int aggmg_generate_jump27(int64_t nx, int64_t ny, int64_t nz, double jump, int64_t block,

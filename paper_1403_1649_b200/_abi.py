@@ -139,6 +139,7 @@ SIGNATURES = {
                             C.POINTER(CycleConfigC), C.POINTER(SolverConfigC), f64p,
                             C.POINTER(SolveReportC)]),
     "generate_poisson": (I, [I, L, L, L, C.c_double, I, csrp]),
+    "random_vector": (I, [L, C.c_uint64, f64p]),
     "generate_jump27": (I, [L, L, L, C.c_double, L, csrp]),
     "set_num_threads": (None, [I]),
     "num_threads": (I, []),

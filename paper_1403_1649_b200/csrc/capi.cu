@@ -912,6 +912,25 @@ int aggmg_generate_jump27_rows(int64_t nx, int64_t ny, int64_t nz, double jump, 
   return guarded([&] { host_to_out(generate_jump27_host(nx, ny, nz, jump, block, row0, nrows), A); });
 }
 
+namespace {
+// x_i = uniform_sym(seed, i) (poisson.cpp:81-87, rng.hpp:32-34)
+__global__ void k_random_vector(int64_t n, uint64_t seed, double* x) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = uniform_sym(seed, static_cast<uint64_t>(i));
+}
+}  // namespace
+
+int aggmg_random_vector(int64_t n, uint64_t seed, double* x) {
+  return guarded([&] {
+    require(n >= 0, "random_vector: negative length");
+    if (n == 0) return;
+    DevBuf<double> d(n);
+    AGG_LAUNCH(k_random_vector, grid_for(n, 256), 256, 0, n, seed, d.get());
+    d.download(x, n);
+    sync();
+  });
+}
+
 int aggmg_generate_poisson(int dims, int64_t nx, int64_t ny, int64_t nz, double eps, int weak_axis,
                            aggmg_csr* A) {
   return guarded([&] { host_to_out(generate_poisson_host(dims, nx, ny, nz, eps, weak_axis), A); });
