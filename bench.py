@@ -192,10 +192,10 @@ class Dist:
             self.dist.destroy_process_group()
 
 
-def world_grid(cfg_name, world, scaling):
-    """The global grid at `world` GPUs: weak scaling doubles x, then y, then z,
-    a remaining odd factor stacks along z; strong scaling keeps the config's grid."""
-    label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[cfg_name]
+def world_grid_dims(dims, nx, ny, nz, world, scaling="weak"):
+    """The global grid at `world` GPUs from a per-GPU grid: weak scaling doubles x, then y, then
+    z, a remaining odd factor stacks along the slowest axis; strong scaling keeps
+    the grid."""
     if scaling == "strong" or world == 1:
         return nx, ny, nz
     g = [nx, ny, nz]
@@ -207,6 +207,13 @@ def world_grid(cfg_name, world, scaling):
         i += 1
     g[axes[-1]] *= w
     return tuple(g)
+
+
+def world_grid(cfg_name, world, scaling):
+    """The config's global grid at `world` GPUs (weak: 256^3 -> 512x256x256 -> 512x512x256 ->
+    512^3 for c2)."""
+    label, dims, nx, ny, nz, eps, alpha, method = CONFIGS[cfg_name]
+    return world_grid_dims(dims, nx, ny, nz, world, scaling)
 
 
 def grid_nnz(dims, nx, ny, nz):

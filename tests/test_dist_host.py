@@ -67,7 +67,7 @@ def _rank_main(rank, world, port, q):
     obj = [bytes(range(128)) if rank == 0 else None]
     tdist.broadcast_object_list(obj, src=0)
     dims, nx, ny, nz = 3, 6, 5, 4
-    gx, gy, gz = bench.dist_grid(dims, nx, ny, nz, world)
+    gx, gy, gz = bench.world_grid_dims(dims, nx, ny, nz, world)
     n = gx * gy * gz
     r0, r1 = n * rank // world, n * (rank + 1) // world
     slab = D.host_rows("poisson", r0, r1 - r0, gx, gy, gz, dims=3)
@@ -92,8 +92,8 @@ def test_two_gloo_ranks_bootstrap_and_slabs():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert (gx, gy, gz) == (6, 5, 8)  # weak scaling: the grid per rank stacked along z
-    assert gathered[0][0] == 0 and gathered[0][1] == gathered[1][0] and gathered[1][1] == 6 * 5 * 8
+    assert (gx, gy, gz) == (12, 5, 4)  # weak scaling: x doubled first
+    assert gathered[0][0] == 0 and gathered[0][1] == gathered[1][0] and gathered[1][1] == 12 * 5 * 4
     assert gathered[1][5] == bytes(range(128))  # the id rank 0 broadcast
     full = M.b200().generate_poisson(3, gx, gy, gz)
     parts = [M.SparseMatrix(g[1] - g[0], full.n_cols, g[2], g[3], g[4]) for g in gathered]
