@@ -7,8 +7,6 @@
 #include <tuple>
 #include <vector>
 
-#include <cooperative_groups.h>
-
 #include "chunked.cuh"
 
 #include "cycles.cuh"
@@ -280,175 +278,6 @@ __global__ void k_lu_serial(int64_t n, const double* __restrict__ lu, const int*
   }
 }
 
-// ---- fused V-cycle tail ------------------------------------------------------------------
-// The coarse levels of a V-cycle (L2-resident operators, a few thousand to ~10^5 rows) are
-// latency-bound: a visit is ~16 small kernels, each paying its launch and drain.  k_vtail runs
-// the whole V-cycle from level k0 to the coarsest as ONE cooperative kernel — the same
-// phases, separated by grid barriers instead of kernel boundaries:
-//   x_k0 = 0 + wd b                                  (zero-guess damped-Jacobi sweep)
-//   per level down: r = b - A x;  rc = R r  and  x_{k+1} = 0 + wd_{k+1} rc
-//   coarsest: x = A^-1 b                             (explicit inverse, k_gemv's arithmetic)
-//   per level up:   t = x + P xc;  x = t + wd (b - A t)
-// Every row sums its entries sequentially in storage order, like the CSR-stream / SELL kernels
-// (sparse.cpp:57-62), so the results are bit-identical to the unfused sequence.
-namespace cg = cooperative_groups;
-constexpr int kTailThreads = 512;
-constexpr int kTailMaxLevels = 12;
-constexpr int64_t kTailMaxNnz = int64_t{4} << 20;  // operators up to ~48 MB: L2-resident
-
-struct TailLevel {
-  int64_t n;
-  const idx *rp, *col;
-  const double *val, *wd;
-  const idx *Rrp, *Rcol;  // restriction to the next level
-  const double* Rval;
-  const idx* agg;
-  const double* pval;
-  const double* b;  // this level's right-hand side
-  double *x, *r, *t;
-  double *rc, *xc;  // the next level's right-hand side and iterate
-};
-struct TailArgs {
-  int nlev;  // levels above the coarsest
-  TailLevel lv[kTailMaxLevels];
-  int64_t nc;  // coarsest: x = inv b
-  const double* inv;
-  const int* pred;
-};
-
-__device__ __forceinline__ double tail_row(const idx* __restrict__ rp, const idx* __restrict__ col,
-                                           const double* __restrict__ val,
-                                           const double* __restrict__ x, int64_t i) {
-  double sum = 0.0;
-  const idx k1 = rp[i + 1];
-#pragma unroll 4
-  for (idx k = rp[i]; k < k1; ++k) sum = __dadd_rn(sum, __dmul_rn(val[k], x[col[k]]));
-  return sum;
-}
-
-__global__ void __launch_bounds__(kTailThreads) k_vtail(const TailArgs a) {
-  if (a.pred && !*a.pred) return;  // uniform over the grid
-  cg::grid_group grid = cg::this_grid();
-  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  {
-    const TailLevel& L = a.lv[0];
-    for (int64_t i = tid; i < L.n; i += nth) L.x[i] = __dadd_rn(0.0, __dmul_rn(L.wd[i], L.b[i]));
-  }
-  grid.sync();
-  for (int l = 0; l < a.nlev; ++l) {
-    const TailLevel& L = a.lv[l];
-    for (int64_t i = tid; i < L.n; i += nth)
-      L.r[i] = __dsub_rn(L.b[i], tail_row(L.rp, L.col, L.val, L.x, i));
-    grid.sync();
-    const bool next_smooth = l + 1 < a.nlev;
-    const int64_t nn = next_smooth ? a.lv[l + 1].n : a.nc;
-    const double* wdn = next_smooth ? a.lv[l + 1].wd : nullptr;
-    for (int64_t J = tid; J < nn; J += nth) {
-      const double s = tail_row(L.Rrp, L.Rcol, L.Rval, L.r, J);
-      L.rc[J] = s;
-      if (next_smooth) L.xc[J] = __dadd_rn(0.0, __dmul_rn(wdn[J], s));
-    }
-    grid.sync();
-  }
-  {  // coarsest: warp per row, the lane-strided fma + shuffle tree of k_gemv
-    const TailLevel& P = a.lv[a.nlev - 1];
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = tid >> 5, nwarps = nth >> 5;
-    for (int64_t row = warp; row < a.nc; row += nwarps) {
-      const double* m = a.inv + row * a.nc;
-      double s = 0.0;
-      for (int64_t j = lane; j < a.nc; j += 32) s = fma(m[j], P.rc[j], s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-      if (lane == 0) P.xc[row] = s;
-    }
-  }
-  grid.sync();
-  for (int l = a.nlev - 1; l >= 0; --l) {
-    const TailLevel& L = a.lv[l];
-    for (int64_t i = tid; i < L.n; i += nth)
-      L.t[i] = __dadd_rn(L.x[i], __dadd_rn(0.0, __dmul_rn(L.pval[i], L.xc[L.agg[i]])));
-    grid.sync();
-    for (int64_t i = tid; i < L.n; i += nth)
-      L.x[i] = __dadd_rn(L.t[i], __dmul_rn(L.wd[i], __dsub_rn(L.b[i], tail_row(L.rp, L.col, L.val, L.t, i))));
-    if (l > 0) grid.sync();
-  }
-}
-
-// The fused tail applies to a zero-guess V-cycle from level k when every level from k down is
-// damped / plain Jacobi with an L2-sized operator, the coarsest solve is the explicit inverse
-// (not the exact-reduction mode's substitution), and the depth fits TailArgs.
-bool vtail_applies(const DevHierarchy& h, int64_t k) {
-  static const bool on = [] {
-    const char* e = std::getenv("AGGMG_VTAIL");
-    return !(e && e[0] == '0');
-  }();
-  if (!on || exact_reductions() || k >= h.coarsest() || h.coarsest() - k > kTailMaxLevels) return false;
-  for (int64_t q = k; q < h.coarsest(); ++q) {
-    const DevLevel& L = h.levels[q];
-    if (L.smoother.kind == 2 || !L.has_next || L.A->nnz > kTailMaxNnz) return false;
-  }
-  return h.coarse_inv.size() > 0;
-}
-
-void vtail_run(DevHierarchy& h, int64_t k, const double* b, double* x_out, const int* pred) {
-  TailArgs a{};
-  a.nlev = static_cast<int>(h.coarsest() - k);
-  for (int q = 0; q < a.nlev; ++q) {
-    DevLevel& L = h.levels[k + q];
-    TailLevel& T = a.lv[q];
-    T.n = L.A->n_rows;
-    T.rp = L.A->rowptr.get();
-    T.col = L.A->col.get();
-    T.val = L.A->val.get();
-    T.wd = L.smoother.wdiag.get();
-    T.Rrp = L.tr.R->rowptr.get();
-    T.Rcol = L.tr.R->col.get();
-    T.Rval = L.tr.R->val.get();
-    T.agg = L.agg.assignment.get();
-    T.pval = L.tr.pval.get();
-    T.b = q == 0 ? b : h.levels[k + q - 1].rc.get();
-    T.x = q == 0 ? x_out : h.levels[k + q - 1].xc.get();
-    T.r = L.r.get();
-    T.t = L.t.get();
-    T.rc = L.rc.get();
-    T.xc = L.xc.get();
-  }
-  a.nc = h.levels.back().A->n_rows;
-  a.inv = h.coarse_inv.get();
-  a.pred = pred;
-  struct Occ {
-    std::atomic<unsigned long long> seen{0};
-    int per_sm[64] = {0};
-  };
-  static Occ occ;
-  const int dev = current_device() & 63;
-  if (device_pending(occ.seen)) {
-    int per = 0;
-    AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vtail, kTailThreads, 0));
-    occ.per_sm[dev] = std::max(1, std::min(per, 2));
-    mark_device(occ.seen);
-  }
-  int64_t rows = 0;
-  for (int q = 0; q < a.nlev; ++q) rows = std::max(rows, a.lv[q].n);
-  const int64_t want = (rows + kTailThreads - 1) / kTailThreads;
-  const unsigned grid = static_cast<unsigned>(
-      std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(occ.per_sm[dev]) * sm_count())));
-  cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(grid);
-  lc.blockDim = dim3(kTailThreads);
-  lc.dynamicSmemBytes = 0;
-  lc.stream = stream();
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  AGG_CUDA(cudaLaunchKernelEx(&lc, k_vtail, a));
-  note_launch();
-}
-
 // the global finest level (profiling families time level 0 only)
 bool finest(const DevHierarchy& h, int64_t k) { return k + h.cfg.level_offset == 0; }
 
@@ -668,10 +497,6 @@ void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in,
   LevelScope ls(static_cast<int>(k + h.cfg.level_offset));
   if (k == h.coarsest()) {
     coarse_solve(h, b, x_out, pred);
-    return;
-  }
-  if (!x_in && vtail_applies(h, k)) {  // the whole V-cycle below k as one kernel
-    vtail_run(h, k, b, x_out, pred);
     return;
   }
   DevLevel& L = h.levels[k];
