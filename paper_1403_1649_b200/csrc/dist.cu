@@ -484,8 +484,11 @@ __global__ void k_row_len(const idx* rp, int64_t n, idx* len) {
 }
 }  // namespace
 
-DevCsrPtr gather_to_root(Comm& comm, const DistCsr& M, int root) {
+namespace {
+// root >= 0: the matrix assembled on that rank only; root < 0: on every rank
+DevCsrPtr gather_csr(Comm& comm, const DistCsr& M, int root) {
   const int me = comm.rank(), P = comm.size();
+  const bool all = root < 0;
   const std::vector<int64_t> nnz_all = comm.allgather_host({M.A.nnz});
   DevBuf<idx> gcol = global_cols(M);
   DevBuf<idx> len(M.A.n_rows);
@@ -493,11 +496,14 @@ DevCsrPtr gather_to_root(Comm& comm, const DistCsr& M, int root) {
     AGG_LAUNCH(k_row_len, grid_for(M.A.n_rows, 256), 256, 0, M.A.rowptr.get(), M.A.n_rows, len.get());
   DevCsrPtr G;
   std::vector<CommMsg> s, r;
-  s.push_back({root, len.get(), sizeof(idx) * M.A.n_rows});
-  s.push_back({root, gcol.get(), sizeof(idx) * M.A.nnz});
-  s.push_back({root, M.A.val.get(), sizeof(double) * M.A.nnz});
+  for (int q = 0; q < P; ++q) {
+    if (!all && q != root) continue;
+    s.push_back({q, len.get(), sizeof(idx) * M.A.n_rows});
+    s.push_back({q, gcol.get(), sizeof(idx) * M.A.nnz});
+    s.push_back({q, M.A.val.get(), sizeof(double) * M.A.nnz});
+  }
   DevBuf<idx> all_len;
-  if (me == root) {
+  if (all || me == root) {
     const int64_t n = M.rows.n();
     int64_t nnz = 0;
     for (int64_t c : nnz_all) nnz += c;
@@ -518,11 +524,25 @@ DevCsrPtr gather_to_root(Comm& comm, const DistCsr& M, int root) {
     }
   }
   comm.exchange(s, r);
-  if (me == root) {
+  if (all || me == root) {
     scan_to_offsets(all_len.get(), G->rowptr.get(), G->n_rows);
     G->plan();
   }
   return G;
+}
+}  // namespace
+
+DevCsrPtr gather_to_root(Comm& comm, const DistCsr& M, int root) { return gather_csr(comm, M, root); }
+DevCsrPtr gather_to_all(Comm& comm, const DistCsr& M) { return gather_csr(comm, M, -1); }
+
+void allgather_vector(Comm& comm, const Partition& part, const double* x_loc, double* x_all) {
+  const int P = comm.size();
+  std::vector<CommMsg> s, r;
+  for (int q = 0; q < P; ++q) {
+    s.push_back({q, const_cast<double*>(x_loc), sizeof(double) * part.count(comm.rank())});
+    r.push_back({q, x_all + part.begin(q), sizeof(double) * part.count(q)});
+  }
+  comm.exchange(s, r);
 }
 
 void gather_vector(Comm& comm, const Partition& part, const double* x_loc, double* x_root, int root) {

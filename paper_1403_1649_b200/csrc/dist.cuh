@@ -93,6 +93,9 @@ DevBuf<idx> global_cols(const DistCsr& M);
 
 // Gathers a row-partitioned matrix (global cols) / vector onto rank `root` as one DevCsr.
 DevCsrPtr gather_to_root(Comm& comm, const DistCsr& M, int root);
+DevCsrPtr gather_to_all(Comm& comm, const DistCsr& M);  // the same matrix on every rank
+// x_all[part.begin(q) + i] = rank q's x_loc[i] on every rank
+void allgather_vector(Comm& comm, const Partition& part, const double* x_loc, double* x_all);
 void gather_vector(Comm& comm, const Partition& part, const double* x_loc, double* x_root, int root);
 void scatter_vector(Comm& comm, const Partition& part, const double* x_root, double* x_loc, int root);
 

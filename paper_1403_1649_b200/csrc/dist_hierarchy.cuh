@@ -56,13 +56,13 @@ struct DistHierarchy {
   Partition tail_rows;                 // row partition of level kd before the gather
   DistCsrPtr tail_A;                   // level kd's rows on this rank (refresh_values)
   int64_t tail_halo_cap = 0;           // halo slots the level-kd vectors need (P of level kd-1)
-  std::unique_ptr<DevHierarchy> tail;  // rank 0 only: global levels kd..
+  std::unique_ptr<DevHierarchy> tail;  // global levels kd.., replicated on every rank
   int64_t n_levels_total = 0;          // global level count (same on every rank)
   std::vector<int64_t> level_rows, level_nnz;  // global sizes per level
   std::vector<std::string> warnings;
   double setup_ms = 0.0;
   bool workspace_ready = false;
-  // tail-side buffers on rank 0 (gathered rc, xc) and the per-rank tail pieces
+  // tail-side buffers (the allgathered rc, the replicated correction) and tail workspace
   DevBuf<double> tail_b, tail_x;
   DevBuf<double> tail_work_c, tail_work_v, tail_work_rt, tail_work_d, tail_work_w;
   DevBuf<KScalars> tail_ks;

@@ -1060,14 +1060,16 @@ std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, c
     ++k;
   }
   phase("levels");
-  // agglomerate level kd onto rank 0 and continue with the one-GPU setup there
+  // agglomerate level kd onto EVERY rank and continue with the one-GPU setup there: the ranks
+  // build (and later run) identical copies of the tail — deterministic kernels on identical
+  // inputs — so no rank idles while another works and the solve needs no scatter back
   h->tail_rows = A->rows;
   h->tail_A = A;
-  DevCsrPtr Ag = gather_to_root(comm, *A, 0);
-  DevBuf<double> Bg(me == 0 ? A->rows.n() : 0);
-  gather_vector(comm, A->rows, B.get(), Bg.get(), 0);
+  DevCsrPtr Ag = gather_to_all(comm, *A);
+  DevBuf<double> Bg(A->rows.n());
+  allgather_vector(comm, A->rows, B.get(), Bg.get());
   std::vector<int64_t> meta(3, 0);  // tail level count, warnings flag
-  if (me == 0) {
+  {
     SetupCfg tc = cfg;
     tc.level_offset = k;
     tc.max_levels = cfg.max_levels - static_cast<int>(k);
@@ -1076,14 +1078,14 @@ std::unique_ptr<DistHierarchy> dist_setup_hierarchy(Comm& comm, DistCsrPtr A0, c
   }
   const std::vector<int64_t> m_all = comm.allgather_host(meta);
   h->n_levels_total = k + m_all[0];
-  if (me == 0) h->warnings = h->tail->warnings;
+  h->warnings = h->tail->warnings;
   // global sizes per level (same on every rank)
   for (auto& L : h->levels) {
     h->level_rows.push_back(L.A->rows.n());
     h->level_nnz.push_back(comm.allreduce_host_sum(L.A->A.nnz));
   }
   std::vector<int64_t> tail_sizes;
-  if (me == 0)
+  if (me == 0)  // (every rank holds the same tail; rank 0's sizes are published)
     for (auto& L : h->tail->levels) {
       tail_sizes.push_back(L.A->n_rows);
       tail_sizes.push_back(L.A->nnz);
@@ -1140,23 +1142,22 @@ void dist_refresh_values(DistHierarchy& h, const double* new_values_local) {
     next.A.refresh_sell();
     dist_smoother(comm, L, h.cfg, k);
   }
-  // the agglomerated tail: gather level kd's new values (row order = rank order) to rank 0
+  // the agglomerated tail: level kd's new values (row order = rank order) to every rank, each
+  // refreshing its copy of the tail
   const std::vector<int64_t> cnt = comm.allgather_host({h.tail_A->A.nnz});
   DevBuf<double> all;
   std::vector<CommMsg> s, r;
-  s.push_back({0, h.tail_A->A.val.get(), sizeof(double) * h.tail_A->A.nnz});
-  if (comm.rank() == 0) {
-    int64_t tot = 0;
-    for (int64_t c : cnt) tot += c;
-    all.resize(tot);
-    int64_t off = 0;
-    for (int q = 0; q < comm.size(); ++q) {
-      r.push_back({q, all.get() + off, sizeof(double) * cnt[q]});
-      off += cnt[q];
-    }
+  int64_t tot = 0;
+  for (int64_t c : cnt) tot += c;
+  all.resize(tot);
+  int64_t off = 0;
+  for (int q = 0; q < comm.size(); ++q) {
+    s.push_back({q, h.tail_A->A.val.get(), sizeof(double) * h.tail_A->A.nnz});
+    r.push_back({q, all.get() + off, sizeof(double) * cnt[q]});
+    off += cnt[q];
   }
   comm.exchange(s, r);
-  if (comm.rank() == 0) refresh_values(*h.tail, all.get());
+  refresh_values(*h.tail, all.get());
   comm.barrier();
 }
 

@@ -118,14 +118,14 @@ void dist_subcycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, co
 void dist_coarse(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kparent, const int* pred) {
   Comm& comm = *h.comm;
   DistLevel& L = h.levels[k];
-  if (k + 1 == h.kd()) {  // the agglomerated tail on rank 0
-    gather_vector(comm, h.tail_rows, L.rc.get(), h.tail_b.get(), 0);
-    if (comm.rank() == 0) {
-      CoarseWork W{h.tail_work_c.get(), h.tail_work_v.get(), h.tail_work_rt.get(),
-                   h.tail_work_d.get(), h.tail_work_w.get(), h.tail_ks.get()};
-      coarse_correction(*h.tail, cfg, kparent, 0, h.tail_b.get(), h.tail_x.get(), W, pred);
-    }
-    scatter_vector(comm, h.tail_rows, h.tail_x.get(), L.xc.get(), 0);
+  if (k + 1 == h.kd()) {  // the agglomerated tail, replicated on every rank
+    allgather_vector(comm, h.tail_rows, L.rc.get(), h.tail_b.get());
+    CoarseWork W{h.tail_work_c.get(), h.tail_work_v.get(), h.tail_work_rt.get(),
+                 h.tail_work_d.get(), h.tail_work_w.get(), h.tail_ks.get()};
+    coarse_correction(*h.tail, cfg, kparent, 0, h.tail_b.get(), h.tail_x.get(), W, pred);
+    // every rank computed the same correction: keep this rank's rows, no scatter
+    const int me = comm.rank();
+    copy_double(L.xc.get(), h.tail_x.get() + h.tail_rows.begin(me), h.tail_rows.count(me));
     return;
   }
   DistLevel& C = h.levels[k + 1];
@@ -212,11 +212,11 @@ void dist_cycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, const
 
 void dist_apply_preconditioner(DistHierarchy& h, const CycleCfg& cfg, const double* r, double* z) {
   h.ensure_workspace();
-  if (h.kd() == 0) {  // everything agglomerated: the one-GPU cycle on rank 0
+  if (h.kd() == 0) {  // everything agglomerated: the one-GPU cycle, replicated on every rank
     Comm& comm = *h.comm;
-    gather_vector(comm, h.tail_rows, r, h.tail_b.get(), 0);
-    if (comm.rank() == 0) apply_preconditioner(*h.tail, cfg, h.tail_b.get(), h.tail_x.get());
-    scatter_vector(comm, h.tail_rows, h.tail_x.get(), z, 0);
+    allgather_vector(comm, h.tail_rows, r, h.tail_b.get());
+    apply_preconditioner(*h.tail, cfg, h.tail_b.get(), h.tail_x.get());
+    copy_double(z, h.tail_x.get() + h.tail_rows.begin(comm.rank()), h.tail_rows.count(comm.rank()));
     return;
   }
   dist_cycle(h, cfg, 0, cycle_accelerated(cfg, 0), r, z, nullptr);
