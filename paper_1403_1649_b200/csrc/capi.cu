@@ -10,6 +10,7 @@
 #include <vector>
 
 #include <thread>
+#include <type_traits>
 
 #include "../../include/aggmg_b200.h"
 #include "chunked.cuh"
@@ -108,7 +109,11 @@ void down(const DevCsr& A, aggmg_csr* out, bool unit_values = false) {
 template <class T>
 DevBuf<T> up_vec(const T* h, int64_t n) {
   DevBuf<T> d(n);
-  d.upload(h, n);
+  if constexpr (std::is_same_v<T, double>) {
+    if (n > 0) host_to_device_values(d.get(), h, static_cast<size_t>(n));
+  } else {
+    d.upload(h, n);
+  }
   return d;
 }
 

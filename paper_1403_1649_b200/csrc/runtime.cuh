@@ -18,6 +18,9 @@ void ensure_init();
 // chunk (pageable cudaMemcpy alone reaches ~11 GB/s on the B200 box).  Small ones are plain
 // stream-ordered cudaMemcpyAsync.
 void host_to_device(void* dst, const void* src, size_t bytes);
+// fp64 arrays: large ones cross PCIe as one-byte codes per 64 K-value piece when the piece has
+// <= 256 distinct values (decoded on the device, bit-identical); other pieces travel raw
+void host_to_device_values(double* dst, const double* src, size_t n);
 void device_to_host(void* dst, const void* src, size_t bytes);
 // int64 host indices -> int32 device indices, narrowed on the host while staging (halves the
 // index bytes on the wire); *first_bad = first position whose value is outside [lo, hi), or -1.

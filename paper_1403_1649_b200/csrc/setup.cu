@@ -404,11 +404,17 @@ __global__ void k_agg_pass2(const idx* srp, const idx* scol, const idx* arp, con
   if (r == -1) {
     idx best = -1;
     double best_w = -1.0;
+    // A(i, j) by a merge walk of the sorted rows S_i and A_i (no search per neighbour);
+    // A(j, i) by a lower_bound in row j (sparse.cpp:15-20)
+    idx a = arp[i];
+    const idx a1 = arp[i + 1];
     for (idx k = srp[i]; k < srp[i + 1]; ++k) {
       const idx j = scol[k];
+      while (a < a1 && acol[a] < j) ++a;
       const idx ja = rep[j];
       if (ja == -1) continue;
-      const double w = dmax_ref(fabs(csr_at(arp, acol, aval, i, j)), fabs(csr_at(arp, acol, aval, j, i)));
+      const double aij = (a < a1 && acol[a] == j) ? aval[a] : 0.0;
+      const double w = dmax_ref(fabs(aij), fabs(csr_at(arp, acol, aval, j, i)));
       if (w > best_w || (w == best_w && ja < best)) {
         best_w = w;
         best = ja;

@@ -342,7 +342,7 @@ DevCsrPtr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, cons
   host_to_device_narrow(A->rowptr.get(), rowptr, static_cast<size_t>(n_rows + 1), 0, nnz + 1, &bad_rp);
   host_to_device_narrow(A->col.get(), col, static_cast<size_t>(nnz), 0, validate ? n_cols : INT32_MAX,
                         &bad_col);
-  A->val.upload(val, nnz);
+  if (nnz > 0) host_to_device_values(A->val.get(), val, static_cast<size_t>(nnz));
   if (n_rows > 0)
     AGG_LAUNCH(k_check_rows, grid_for(n_rows, 256), 256, 0, A->rowptr.get(), A->col.get(), n_rows,
                nnz, bad.get(), validate ? 1 : 0);
