@@ -282,7 +282,8 @@ int aggmg_dmatrix_size(const aggmg_dmatrix* A, int64_t* n_rows, int64_t* nnz);
 int aggmg_dmatrix_format(const aggmg_dmatrix* A, int* sell);
 int aggmg_dmatrix_to_host(const aggmg_dmatrix* A, aggmg_csr* out);
 void aggmg_dmatrix_free(aggmg_dmatrix* A);
-/* setup_hierarchy on a device matrix (B0 = ones); the hierarchy shares A's storage */
+/* setup_hierarchy on a device matrix (B0 = ones); the hierarchy shares A's storage.  Level 0's
+ * kernel layout (its SELL-32 copy and value dictionary) is rebuilt as part of the setup. */
 int aggmg_setup_hierarchy_device(const aggmg_dmatrix* A0, const aggmg_setup_config* cfg,
                                  aggmg_hierarchy** out);
 /* device view of level k's operator (which = 0) or restriction R (which = 1); shares storage */

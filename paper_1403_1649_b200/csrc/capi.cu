@@ -989,6 +989,9 @@ int aggmg_setup_hierarchy_device(const aggmg_dmatrix* A0, const aggmg_setup_conf
                                  aggmg_hierarchy** out) {
   return guarded([&] {
     auto h = std::make_unique<aggmg_hierarchy>();
+    // level 0's kernel layout (SELL-32 copy, value dictionary) is part of setup: rebuilt here,
+    // not inherited from the matrix's creation, so a timed setup pays for it
+    A0->A->plan();
     h->h = setup_hierarchy(A0->A, nullptr, to_cfg(cfg));
     *out = h.release();
   });
