@@ -140,8 +140,8 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     st.mark(lv + "transfer");
     DevCsrPtr Ac;
     if (cfg.reuse_caches) {  // hierarchy.cpp:69-71: cached sort / segmented reduce
-      fine.gal = build_galerkin_cache(A, agg, false, false, fine.tr.pval.get(), &Ac);
-      if (!Ac) Ac = apply_galerkin_cache(fine.gal, A, fine.tr.pval.get());
+      fine.gal = build_galerkin_cache(A, agg, false, false);
+      Ac = apply_galerkin_cache(fine.gal, A, fine.tr.pval.get());
     } else {  // hierarchy.cpp:73: galerkin_direct, the reference default
       Ac = galerkin_direct(A, agg, fine.tr.pval.get());
     }

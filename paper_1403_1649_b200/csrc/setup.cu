@@ -523,8 +523,7 @@ constexpr int kGalMembers1 = 64;   // tier 1 members per coarse row (aggregates 
 __global__ void __launch_bounds__(kGalWarps * 32)
     k_gal_symbolic(const idx* goff, const idx* rows, const idx* arp, const idx* acol,
                    const idx* assignment, int64_t nc, const idx* eoff, idx* entry, idx* entry_row,
-                   idx* sorted_j, idx* cnnz, idx* big_list, int* big_count, const double* aval,
-                   const double* pv, double* seg_val) {
+                   idx* sorted_j, idx* cnnz, idx* big_list, int* big_count) {
   __shared__ idx s_j[kGalWarps][kGalCap], s_kk[kGalWarps][kGalCap], s_ri[kGalWarps][kGalCap];
   __shared__ idx s_moff[kGalWarps][kGalMembers1], s_mlo[kGalWarps][kGalMembers1],
       s_mrow[kGalWarps][kGalMembers1];
@@ -665,24 +664,6 @@ __global__ void __launch_bounds__(kGalWarps * 32)
     __syncwarp();
   }
   if (lane == 0) cnnz[I] = nd;
-  // ---- 4. (first setup) the coarse values: each distinct J's segment summed in stored order,
-  // (pv[row] * a_e) * pv[col_e] from +0 (galerkin.cpp:128-135, as k_gal_numeric), one lane per
-  // segment; the sum lands at the segment's first fine-entry position for k_gal_fill ----
-  if (seg_val) {
-#pragma unroll
-    for (int r = 0; r < kGalHash1 / 32; ++r) {
-      const idx d = lane + 32 * r;
-      if (d < nd) {
-        const idx s0 = start[r], s1 = hc[ds[d]];
-        double acc = 0.0;
-        for (idx q = s0; q < s1; ++q) {
-          const idx e = entry[base_e + q];
-          acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(pv[entry_row[base_e + q]], aval[e]), pv[acol[e]]));
-        }
-        seg_val[base_e + s0] = acc;
-      }
-    }
-  }
 }
 
 // Tier 2 — one CTA (256 threads) per long coarse row (L > kGalCap gathered entries).
@@ -1113,8 +1094,7 @@ __global__ void __launch_bounds__(256)
 
 // Warp per coarse row: segment boundaries -> coarse columns, segment offsets, slot_of_csr.
 __global__ void k_gal_fill(int64_t nc, const idx* eoff, const idx* sorted_j, const idx* entry,
-                           const idx* crp, idx* ccol, idx* seg_off, idx* slot_of_csr,
-                           const double* seg_val, double* ac_val) {
+                           const idx* crp, idx* ccol, idx* seg_off, idx* slot_of_csr) {
   const int64_t I = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (I >= nc) return;
@@ -1134,7 +1114,6 @@ __global__ void k_gal_fill(int64_t nc, const idx* eoff, const idx* sorted_j, con
       if (st) {
         ccol[seg] = jc;
         seg_off[seg] = base_e + r;
-        if (seg_val) ac_val[seg] = seg_val[base_e + r];
       }
       slot_of_csr[entry[base_e + r]] = seg;
     }
@@ -1494,8 +1473,7 @@ TransferDev build_transfer(const AggDev& agg, const double* fine_b) {
   return t;
 }
 
-GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial, bool fingerprint,
-                                 const double* pval, DevCsrPtr* Ac_out) {
+GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial, bool fingerprint) {
   require(partial || A.n_rows == A.n_cols, "galerkin: matrix must be square");
   require(agg.n_fine == A.n_rows, "galerkin: aggregation size mismatch");
   const int64_t nc = agg.n_agg;
@@ -1509,9 +1487,6 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
   DevBuf<idx> ecnt(nc), eoff(nc + 1), sorted_j(A.nnz), cnnz(nc), big_list(nc > 0 ? nc : 1);
   DevBuf<int> big_count(1);
   big_count.zero();
-  // with pval (a first setup), tier 1 also sums the coarse values: no numeric pass over A
-  const bool fused = pval && Ac_out && !partial;
-  DevBuf<double> seg_val(fused ? A.nnz : 0);
   if (nc > 0)
     AGG_LAUNCH(k_group_entry_counts, grid_for(nc, 256), 256, 0, agg.agg_row_offsets.get(),
                agg.rows_by_coarse.get(), A.rowptr.get(), nc, ecnt.get());
@@ -1521,10 +1496,8 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
     AGG_LAUNCH(k_gal_symbolic, static_cast<unsigned>((nc + kGalWarps - 1) / kGalWarps),
                kGalWarps * 32, 0, agg.agg_row_offsets.get(), agg.rows_by_coarse.get(),
                A.rowptr.get(), A.col.get(), agg.assignment.get(), nc, eoff.get(), g.entry.get(),
-               g.entry_row.get(), sorted_j.get(), cnnz.get(), big_list.get(), big_count.get(),
-               A.val.get(), pval, fused ? seg_val.get() : nullptr);
+               g.entry_row.get(), sorted_j.get(), cnnz.get(), big_list.get(), big_count.get());
   const int nbig = read_scalar(big_count.get());
-  const bool fused_vals = fused && nbig == 0;  // tier-2 rows: the numeric pass instead
   if (nbig > 0) {
     DevBuf<int> maxlen(1);
     maxlen.zero();
@@ -1564,18 +1537,10 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
   g.nnz_coarse = scan_to_offsets(cnnz.get(), g.coarse_rowptr.get(), nc);
   g.coarse_col.resize(g.nnz_coarse);
   g.segment_offsets.resize(g.nnz_coarse + 1);
-  DevCsrPtr Ac;
-  if (fused_vals) {
-    Ac = std::make_shared<DevCsr>();
-    Ac->n_rows = Ac->n_cols = nc;
-    Ac->nnz = g.nnz_coarse;
-    Ac->val.resize(g.nnz_coarse);
-  }
   if (nc > 0)
     AGG_LAUNCH(k_gal_fill, grid_for(nc * 32, 256), 256, 0, nc, eoff.get(), sorted_j.get(),
                g.entry.get(), g.coarse_rowptr.get(), g.coarse_col.get(), g.segment_offsets.get(),
-               g.slot_of_csr.get(), fused_vals ? seg_val.get() : nullptr,
-               fused_vals ? Ac->val.get() : nullptr);
+               g.slot_of_csr.get());
   const idx nnz32 = static_cast<idx>(total);  // == A.nnz unless partial
   AGG_CUDA(cudaMemcpyAsync(g.segment_offsets.get() + g.nnz_coarse, &nnz32, sizeof(idx),
                            cudaMemcpyHostToDevice, stream()));
@@ -1596,17 +1561,6 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
     g.max_coarse_row = read_scalar(mr.get());
   }
   if (!partial && fingerprint) g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
-  if (fused_vals) {
-    Ac->rowptr.resize(nc + 1);
-    Ac->col.resize(g.nnz_coarse);
-    AGG_CUDA(cudaMemcpyAsync(Ac->rowptr.get(), g.coarse_rowptr.get(), sizeof(idx) * (nc + 1),
-                             cudaMemcpyDeviceToDevice, stream()));
-    if (g.nnz_coarse > 0)
-      AGG_CUDA(cudaMemcpyAsync(Ac->col.get(), g.coarse_col.get(), sizeof(idx) * g.nnz_coarse,
-                               cudaMemcpyDeviceToDevice, stream()));
-    Ac->plan();
-    *Ac_out = Ac;
-  }
   return g;
 }
 

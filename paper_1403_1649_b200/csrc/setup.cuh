@@ -64,12 +64,8 @@ struct GalerkinDev {
 // skipped; the row-partitioned setup's extended row set) — no coverage check, no fingerprint.
 // fingerprint: the pattern hash apply_galerkin_cache checks for a caller-supplied A (galerkin.cpp:
 // 18-29, 101-103); a hierarchy applies its cache to its own stored operator and skips it.
-// With pval and Ac_out (a hierarchy's first setup): the coarse operator too, its values summed
-// by the symbolic kernel in the same order as apply_galerkin_cache (*Ac_out stays null when a
-// coarse row took the long-row path; the caller then applies the cache).
 GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial = false,
-                                 bool fingerprint = true, const double* pval = nullptr,
-                                 DevCsrPtr* Ac_out = nullptr);
+                                 bool fingerprint = true);
 // Ac values for the cached pattern.  pval: per fine row P weight.
 DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const double* pval);
 uint64_t pattern_fingerprint(const DevCsr& A, const idx* assignment);
