@@ -574,20 +574,34 @@ __global__ void __launch_bounds__(kGalWarps * 32)
     run += __shfl_sync(kFull, incl, 31);
   }
   __syncwarp();
-  for (idx p = lane; p < L; p += 32) {
-    idx lo = 0, hi = nm;  // the last member whose start is <= p
-    while (hi - lo > 1) {
-      const idx mid = (lo + hi) >> 1;
-      if (moff[mid] <= p)
-        lo = mid;
-      else
-        hi = mid;
+  // the loads of all (up to kGalCap / 32) rounds are issued together: every entry's column,
+  // then every column's aggregate (two dependent round trips for the row, not two per round)
+  constexpr int kRounds = kGalCap / 32;
+  idx kk[kRounds], cc[kRounds];
+#pragma unroll
+  for (int it = 0; it < kRounds; ++it) {
+    const idx p = lane + 32 * it;
+    kk[it] = 0;
+    if (p < L) {
+      idx lo = 0, hi = nm;  // the last member whose start is <= p
+      while (hi - lo > 1) {
+        const idx mid = (lo + hi) >> 1;
+        if (moff[mid] <= p)
+          lo = mid;
+        else
+          hi = mid;
+      }
+      kk[it] = mlo[lo] + (p - moff[lo]);
+      skk[p] = kk[it];
+      sri[p] = mrow[lo];
     }
-    const idx k = mlo[lo] + (p - moff[lo]);
-    sj[p] = assignment[acol[k]];
-    skk[p] = k;
-    sri[p] = mrow[lo];
   }
+#pragma unroll
+  for (int it = 0; it < kRounds; ++it)
+    if (lane + 32 * it < L) cc[it] = acol[kk[it]];
+#pragma unroll
+  for (int it = 0; it < kRounds; ++it)
+    if (lane + 32 * it < L) sj[lane + 32 * it] = assignment[cc[it]];
   __syncwarp();
   // ---- 2. distinct J, counts, starts ----
   bool over = false;
@@ -1182,36 +1196,58 @@ __global__ void __launch_bounds__(kWalkWarps * 32)
     }
     const idx excl = incl - len;
     const idx T = __shfl_sync(0xffffffffu, incl, 31);
-    for (idx pb = 0; pb < T; pb += 32) {
-      const idx p = pb + lane;
-      int a = 0, b = nm;  // last member with excl <= p
+    // batches of kWalkRounds 32-entry rounds: the loads of a whole batch issue together
+    // (aval, acol, then the column's P value: two dependent round trips per batch), then the
+    // rounds accumulate in entry order
+    constexpr int kWalkRounds = 4;
+    for (idx pb0 = 0; pb0 < T; pb0 += 32 * kWalkRounds) {
+      double c[kWalkRounds];
+      int sl[kWalkRounds];
+      idx kq[kWalkRounds], cq[kWalkRounds];
+      double mq[kWalkRounds], aq[kWalkRounds];
 #pragma unroll
-      for (int step = 0; step < 6; ++step) {
-        const int mid = (a + b) >> 1;
-        const idx em = __shfl_sync(0xffffffffu, excl, mid & 31);
-        if (b - a > 1) {
-          if (em <= p) a = mid;
-          else b = mid;
+      for (int q = 0; q < kWalkRounds; ++q) {
+        const idx p = pb0 + 32 * q + lane;
+        int a = 0, b = nm;  // last member with excl <= p
+#pragma unroll
+        for (int step = 0; step < 6; ++step) {
+          const int mid = (a + b) >> 1;
+          const idx em = __shfl_sync(0xffffffffu, excl, mid & 31);
+          if (b - a > 1) {
+            if (em <= p) a = mid;
+            else b = mid;
+          }
         }
+        const idx mlo = __shfl_sync(0xffffffffu, lo, a);
+        const idx mex = __shfl_sync(0xffffffffu, excl, a);
+        mq[q] = __shfl_sync(0xffffffffu, pvi, a);
+        kq[q] = mlo + (p - mex);
       }
-      const idx mlo = __shfl_sync(0xffffffffu, lo, a);
-      const idx mex = __shfl_sync(0xffffffffu, excl, a);
-      const double mpv = __shfl_sync(0xffffffffu, pvi, a);
-      int sl = -1 - lane;
-      double c = 0.0;
-      if (p < T) {
-        const idx k = mlo + (p - mex);
-        c = __dmul_rn(__dmul_rn(mpv, aval[k]), pv[acol[k]]);
-        sl = slot_of_csr[k] - s0;
-      }
-      const unsigned grp = __match_any_sync(0xffffffffu, sl);
-      const int rk = __popc(grp & ((1u << lane) - 1u));
-      int mx = rk;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      for (int step = 0; step <= mx; ++step) {
-        if (p < T && rk == step) acc[sl] = __dadd_rn(acc[sl], c);
-        __syncwarp();
+      for (int q = 0; q < kWalkRounds; ++q) {
+        const bool in = pb0 + 32 * q + lane < T;
+        aq[q] = in ? aval[kq[q]] : 0.0;
+        cq[q] = in ? acol[kq[q]] : 0;
+        sl[q] = in ? slot_of_csr[kq[q]] - s0 : -1 - lane;
+      }
+#pragma unroll
+      for (int q = 0; q < kWalkRounds; ++q) {
+        const bool in = pb0 + 32 * q + lane < T;
+        c[q] = in ? __dmul_rn(__dmul_rn(mq[q], aq[q]), pv[cq[q]]) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kWalkRounds; ++q) {
+        if (pb0 + 32 * q >= T) break;  // warp-uniform
+        const bool in = pb0 + 32 * q + lane < T;
+        const unsigned grp = __match_any_sync(0xffffffffu, sl[q]);
+        const int rk = __popc(grp & ((1u << lane) - 1u));
+        int mx = rk;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int step = 0; step <= mx; ++step) {
+          if (in && rk == step) acc[sl[q]] = __dadd_rn(acc[sl[q]], c[q]);
+          __syncwarp();
+        }
       }
     }
   }
