@@ -90,80 +90,6 @@ __global__ void __launch_bounds__(kGjThreads) k_gauss_jordan(double* aug, int n,
   }
 }
 
-// The same elimination for a coarsest level whose augmented matrix fits in shared memory
-// (2 n^2 doubles, n <= kGjSmemRows): one CTA, a __syncthreads per step instead of a grid
-// barrier (c2's 103-row level: 433 us -> tens of us).  Every element sees the same operations
-// in the same order as k_gauss_jordan, so the inverse is the same bit for bit.  The result is
-// written row-major, straight from shared memory.
-constexpr int kGjCtaThreads = 1024;
-constexpr int kGjSmemRows = 118;  // 2 * 118^2 * 8 B = 223 KB
-__global__ void __launch_bounds__(kGjCtaThreads) k_gauss_jordan_cta(const double* aug_in, int n,
-                                                                   double* inv, int* bad) {
-  extern __shared__ double aug[];
-  __shared__ double s_best[kGjCtaThreads / 32];
-  __shared__ int s_idx[kGjCtaThreads / 32];
-  __shared__ int s_piv;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  constexpr int kWarps = kGjCtaThreads / 32;
-  const int64_t nn = n;
-  for (int64_t t = threadIdx.x; t < 2 * nn * nn; t += kGjCtaThreads) aug[t] = aug_in[t];
-  __syncthreads();
-  for (int k = 0; k < n; ++k) {
-    const double* ck = aug + k * nn;
-    double best = -1.0;
-    int bi = n;
-    for (int i = k + threadIdx.x; i < n; i += kGjCtaThreads) {
-      const double v = fabs(ck[i]);
-      if (v > best) best = v, bi = i;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_down_sync(0xffffffffu, best, o);
-      const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) best = ob, bi = oi;
-    }
-    if (lane == 0) s_best[wid] = best, s_idx[wid] = bi;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = s_best[0];
-      int p = s_idx[0];
-      for (int w = 1; w < kWarps; ++w)
-        if (s_best[w] > b || (s_best[w] == b && s_idx[w] < p)) b = s_best[w], p = s_idx[w];
-      s_piv = b == 0.0 ? -1 : p;
-    }
-    __syncthreads();
-    const int p = s_piv;
-    if (p < 0) {
-      if (threadIdx.x == 0) *bad = k;
-      return;
-    }
-    const double inv_p = 1.0 / ck[p];
-    const double mk = ck[k];
-    // warp w updates columns j = k + 1 + w, + kWarps, ...; column k itself is read-only
-    for (int64_t j = k + 1 + wid; j < 2 * nn; j += kWarps) {
-      double* cj = aug + j * nn;
-      const double u = cj[p] * inv_p;
-      const double akj = cj[k];
-      __syncwarp();
-      for (int i = lane; i < n; i += 32) {
-        double v;
-        if (i == k)
-          v = u;
-        else if (i == p)
-          v = akj - mk * u;
-        else
-          v = cj[i] - ck[i] * u;
-        cj[i] = v;
-      }
-    }
-    __syncthreads();
-  }
-  for (int64_t t = threadIdx.x; t < nn * nn; t += kGjCtaThreads) {
-    const int64_t i = t / nn, j = t % nn;
-    inv[t] = aug[(nn + j) * nn + i];
-  }
-}
-
 // right half of the column-major augmented matrix -> row-major inverse
 __global__ void k_take_inverse(const double* aug, int64_t n, double* inv) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -185,20 +111,6 @@ void invert_coarsest(const DevCsr& A, DevBuf<double>& inv) {
              aug.get());
   DevBuf<int> bad(1);
   fill_int(bad.get(), 1, -1);
-  if (n <= kGjSmemRows) {  // one CTA, the augmented matrix in shared memory
-    const size_t smem = sizeof(double) * 2 * n * n;
-    static std::atomic<unsigned long long> raised{0};  // the attribute is per device
-    if (device_pending(raised)) {
-      AGG_CUDA(cudaFuncSetAttribute(k_gauss_jordan_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sizeof(double) * 2 * kGjSmemRows * kGjSmemRows)));
-      mark_device(raised);
-    }
-    AGG_LAUNCH(k_gauss_jordan_cta, 1, kGjCtaThreads, smem, aug.get(), static_cast<int>(n), inv.get(),
-               bad.get());
-    const int k = read_scalar(bad.get());
-    if (k >= 0) throw Error("lu_factor: zero pivot at index " + std::to_string(k));
-    return;
-  }
   int per_sm = 0, sms = 0, dev = current_device();
   AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gauss_jordan, kGjThreads, 0));
   AGG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

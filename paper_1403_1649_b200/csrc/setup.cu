@@ -1196,58 +1196,36 @@ __global__ void __launch_bounds__(kWalkWarps * 32)
     }
     const idx excl = incl - len;
     const idx T = __shfl_sync(0xffffffffu, incl, 31);
-    // batches of kWalkRounds 32-entry rounds: the loads of a whole batch issue together
-    // (aval, acol, then the column's P value: two dependent round trips per batch), then the
-    // rounds accumulate in entry order
-    constexpr int kWalkRounds = 4;
-    for (idx pb0 = 0; pb0 < T; pb0 += 32 * kWalkRounds) {
-      double c[kWalkRounds];
-      int sl[kWalkRounds];
-      idx kq[kWalkRounds], cq[kWalkRounds];
-      double mq[kWalkRounds], aq[kWalkRounds];
+    for (idx pb = 0; pb < T; pb += 32) {
+      const idx p = pb + lane;
+      int a = 0, b = nm;  // last member with excl <= p
 #pragma unroll
-      for (int q = 0; q < kWalkRounds; ++q) {
-        const idx p = pb0 + 32 * q + lane;
-        int a = 0, b = nm;  // last member with excl <= p
-#pragma unroll
-        for (int step = 0; step < 6; ++step) {
-          const int mid = (a + b) >> 1;
-          const idx em = __shfl_sync(0xffffffffu, excl, mid & 31);
-          if (b - a > 1) {
-            if (em <= p) a = mid;
-            else b = mid;
-          }
+      for (int step = 0; step < 6; ++step) {
+        const int mid = (a + b) >> 1;
+        const idx em = __shfl_sync(0xffffffffu, excl, mid & 31);
+        if (b - a > 1) {
+          if (em <= p) a = mid;
+          else b = mid;
         }
-        const idx mlo = __shfl_sync(0xffffffffu, lo, a);
-        const idx mex = __shfl_sync(0xffffffffu, excl, a);
-        mq[q] = __shfl_sync(0xffffffffu, pvi, a);
-        kq[q] = mlo + (p - mex);
       }
-#pragma unroll
-      for (int q = 0; q < kWalkRounds; ++q) {
-        const bool in = pb0 + 32 * q + lane < T;
-        aq[q] = in ? aval[kq[q]] : 0.0;
-        cq[q] = in ? acol[kq[q]] : 0;
-        sl[q] = in ? slot_of_csr[kq[q]] - s0 : -1 - lane;
+      const idx mlo = __shfl_sync(0xffffffffu, lo, a);
+      const idx mex = __shfl_sync(0xffffffffu, excl, a);
+      const double mpv = __shfl_sync(0xffffffffu, pvi, a);
+      int sl = -1 - lane;
+      double c = 0.0;
+      if (p < T) {
+        const idx k = mlo + (p - mex);
+        c = __dmul_rn(__dmul_rn(mpv, aval[k]), pv[acol[k]]);
+        sl = slot_of_csr[k] - s0;
       }
+      const unsigned grp = __match_any_sync(0xffffffffu, sl);
+      const int rk = __popc(grp & ((1u << lane) - 1u));
+      int mx = rk;
 #pragma unroll
-      for (int q = 0; q < kWalkRounds; ++q) {
-        const bool in = pb0 + 32 * q + lane < T;
-        c[q] = in ? __dmul_rn(__dmul_rn(mq[q], aq[q]), pv[cq[q]]) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < kWalkRounds; ++q) {
-        if (pb0 + 32 * q >= T) break;  // warp-uniform
-        const bool in = pb0 + 32 * q + lane < T;
-        const unsigned grp = __match_any_sync(0xffffffffu, sl[q]);
-        const int rk = __popc(grp & ((1u << lane) - 1u));
-        int mx = rk;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        for (int step = 0; step <= mx; ++step) {
-          if (in && rk == step) acc[sl[q]] = __dadd_rn(acc[sl[q]], c[q]);
-          __syncwarp();
-        }
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int step = 0; step <= mx; ++step) {
+        if (p < T && rk == step) acc[sl] = __dadd_rn(acc[sl], c);
+        __syncwarp();
       }
     }
   }
