@@ -99,26 +99,45 @@ __device__ __forceinline__ unsigned dict_hash(unsigned long long u) {
   return static_cast<unsigned>(u) & (kDictSlots - 1);
 }
 
-__global__ void k_dict_insert(const double* __restrict__ val, int64_t nnz,
-                              unsigned long long* slots, int* state /* [count, bad] */) {
+// Each CTA keeps the patterns it has seen in a shared-memory copy of the set: a value already
+// known to the CTA costs one shared probe; only patterns new to the CTA probe (and CAS into)
+// the global set.  A stencil operator's ~10^8 values thus cost ~one global probe per distinct
+// value per CTA.
+__global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ val, int64_t nnz,
+                                                     unsigned long long* slots,
+                                                     int* state /* [count, bad] */) {
+  __shared__ unsigned long long seen[kDictSlots];
+  for (int q = threadIdx.x; q < kDictSlots; q += blockDim.x) seen[q] = kDictEmpty;
+  __syncthreads();
   volatile int* bad = state + 1;
   auto give_up = [&] {
     if (!*bad) atomicExch(state + 1, 1);
   };
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t start = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  // warp-uniform trip count, so every lane reaches the flag check and __match_any_sync
+  int iter = 0;
+  // warp-uniform trip count, so every lane reaches the flag check
   for (int64_t base = start - (threadIdx.x & 31); base < nnz; base += stride) {
-    if (__shfl_sync(0xffffffffu, *bad, 0)) return;  // too many distinct values: stop reading
+    if ((++iter & 15) == 0 && __shfl_sync(0xffffffffu, *bad, 0)) return;  // > 256 patterns
     const int64_t i = base + (threadIdx.x & 31);
-    const unsigned long long u = i < nnz ? __double_as_longlong(val[i]) : kDictEmpty - 1;
-    const unsigned peers = __match_any_sync(0xffffffffu, u);
-    if (i >= nnz || (threadIdx.x & 31) != __ffs(peers) - 1) continue;  // one lane per pattern
+    if (i >= nnz) continue;
+    const unsigned long long u = __double_as_longlong(val[i]);
     if (u == kDictEmpty) {
       give_up();
       continue;
     }
     unsigned h = dict_hash(u);
+    bool known = false;
+    for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+      const unsigned long long cur = seen[h];
+      if (cur == u) {
+        known = true;
+        break;
+      }
+      if (cur == kDictEmpty) break;
+    }
+    if (known) continue;
+    h = dict_hash(u);  // new to this CTA: the global set, then the CTA's copy
     for (int probe = 0;; ++probe, h = (h + 1) & (kDictSlots - 1)) {
       if (probe == kDictSlots) {
         give_up();
@@ -134,23 +153,36 @@ __global__ void k_dict_insert(const double* __restrict__ val, int64_t nnz,
       }
       if (old == u) break;
     }
+    h = dict_hash(u);
+    for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+      const unsigned long long old = atomicCAS(seen + h, kDictEmpty, u);
+      if (old == kDictEmpty || old == u) break;
+    }
   }
 }
 
-__global__ void k_sell_codes(const idx* rowptr, const idx* col, const double* val, int64_t n,
-                             const idx* sptr, const unsigned long long* __restrict__ slots,
-                             const unsigned char* __restrict__ code_of_slot, unsigned char* scode,
-                             idx* pcol) {
+__global__ void __launch_bounds__(256) k_sell_codes(const idx* rowptr, const idx* col,
+                                                    const double* val, int64_t n, const idx* sptr,
+                                                    const unsigned long long* __restrict__ slots,
+                                                    const unsigned char* __restrict__ code_of_slot,
+                                                    unsigned char* scode, idx* pcol) {
+  __shared__ unsigned long long s_slots[kDictSlots];
+  __shared__ unsigned char s_code[kDictSlots];
+  for (int q = threadIdx.x; q < kDictSlots; q += blockDim.x) {
+    s_slots[q] = slots[q];
+    s_code[q] = code_of_slot[q];
+  }
+  __syncthreads();
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const idx k0 = rowptr[r], len = rowptr[r + 1] - k0;
   for (idx k = 0; k < len; ++k) {
     const unsigned long long u = __double_as_longlong(val[k0 + k]);
     unsigned h = dict_hash(u);
-    while (slots[h] != u) h = (h + 1) & (kDictSlots - 1);  // present by construction
+    while (s_slots[h] != u) h = (h + 1) & (kDictSlots - 1);  // present by construction
     // packed: the codes of slots 4g..4g+3 of a row are one 32-bit word (byte k & 3)
     const idx at = sptr[r >> 5] + 32 * (k & ~3) + 4 * (r & 31) + (k & 3);
-    scode[at] = code_of_slot[h];
+    scode[at] = s_code[h];
     pcol[at] = col[k0 + k];  // the same packing: 4 consecutive slots of a row are one int4
   }
 }
