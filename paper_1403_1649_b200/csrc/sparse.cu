@@ -116,73 +116,76 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t start = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int iter = 0;
-  // warp-uniform trip count, so every lane reaches the flag check
-  for (int64_t base = start - (threadIdx.x & 31); base < nnz; base += stride) {
-    if ((++iter & 15) == 0 && __shfl_sync(0xffffffffu, *bad, 0)) return;  // > 256 patterns
-    const int64_t i = base + (threadIdx.x & 31);
-    if (i >= nnz) continue;
-    const unsigned long long u = __double_as_longlong(val[i]);
-    if (u == kDictEmpty) {
-      give_up();
-      continue;
+  // warp-uniform trip count, so every lane reaches the flag check; four values in flight
+  constexpr int kU = 4;
+  for (int64_t base = start - (threadIdx.x & 31); base < nnz; base += kU * stride) {
+    if ((++iter & 3) == 0 && __shfl_sync(0xffffffffu, *bad, 0)) return;  // > 256 patterns
+    unsigned long long uu[kU];
+    unsigned in = 0;
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int64_t i = base + q * stride + (threadIdx.x & 31);
+      in |= (i < nnz ? 1u : 0u) << q;
+      uu[q] = i < nnz ? __double_as_longlong(val[i]) : 0ull;
     }
-    unsigned h = dict_hash(u);
-    bool known = false;
-    for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
-      const unsigned long long cur = seen[h];
-      if (cur == u) {
-        known = true;
-        break;
-      }
-      if (cur == kDictEmpty) break;
-    }
-    if (known) continue;
-    h = dict_hash(u);  // new to this CTA: the global set, then the CTA's copy
-    for (int probe = 0;; ++probe, h = (h + 1) & (kDictSlots - 1)) {
-      if (probe == kDictSlots) {
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const unsigned long long u = uu[q];
+      if (!((in >> q) & 1u)) continue;  // past the end
+      if (u == kDictEmpty) {
         give_up();
-        break;
+        continue;
       }
-      const unsigned long long cur = slots[h];
-      if (cur == u) break;
-      if (cur != kDictEmpty) continue;
-      const unsigned long long old = atomicCAS(slots + h, kDictEmpty, u);
-      if (old == kDictEmpty) {
-        if (atomicAdd(state, 1) >= kDictMax) give_up();
-        break;
+      unsigned h = dict_hash(u);
+      bool known = false;
+      for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+        const unsigned long long cur = seen[h];
+        if (cur == u) {
+          known = true;
+          break;
+        }
+        if (cur == kDictEmpty) break;
       }
-      if (old == u) break;
-    }
-    h = dict_hash(u);
-    for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
-      const unsigned long long old = atomicCAS(seen + h, kDictEmpty, u);
-      if (old == kDictEmpty || old == u) break;
+      if (known) continue;
+      h = dict_hash(u);  // new to this CTA: the global set, then the CTA's copy
+      for (int probe = 0;; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+        if (probe == kDictSlots) {
+          give_up();
+          break;
+        }
+        const unsigned long long cur = slots[h];
+        if (cur == u) break;
+        if (cur != kDictEmpty) continue;
+        const unsigned long long old = atomicCAS(slots + h, kDictEmpty, u);
+        if (old == kDictEmpty) {
+          if (atomicAdd(state, 1) >= kDictMax) give_up();
+          break;
+        }
+        if (old == u) break;
+      }
+      h = dict_hash(u);
+      for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+        const unsigned long long old = atomicCAS(seen + h, kDictEmpty, u);
+        if (old == kDictEmpty || old == u) break;
+      }
     }
   }
 }
 
-__global__ void __launch_bounds__(256) k_sell_codes(const idx* rowptr, const idx* col,
-                                                    const double* val, int64_t n, const idx* sptr,
-                                                    const unsigned long long* __restrict__ slots,
-                                                    const unsigned char* __restrict__ code_of_slot,
-                                                    unsigned char* scode, idx* pcol) {
-  __shared__ unsigned long long s_slots[kDictSlots];
-  __shared__ unsigned char s_code[kDictSlots];
-  for (int q = threadIdx.x; q < kDictSlots; q += blockDim.x) {
-    s_slots[q] = slots[q];
-    s_code[q] = code_of_slot[q];
-  }
-  __syncthreads();
+__global__ void k_sell_codes(const idx* rowptr, const idx* col, const double* val, int64_t n,
+                             const idx* sptr, const unsigned long long* __restrict__ slots,
+                             const unsigned char* __restrict__ code_of_slot, unsigned char* scode,
+                             idx* pcol) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const idx k0 = rowptr[r], len = rowptr[r + 1] - k0;
   for (idx k = 0; k < len; ++k) {
     const unsigned long long u = __double_as_longlong(val[k0 + k]);
     unsigned h = dict_hash(u);
-    while (s_slots[h] != u) h = (h + 1) & (kDictSlots - 1);  // present by construction
+    while (slots[h] != u) h = (h + 1) & (kDictSlots - 1);  // present by construction
     // packed: the codes of slots 4g..4g+3 of a row are one 32-bit word (byte k & 3)
     const idx at = sptr[r >> 5] + 32 * (k & ~3) + 4 * (r & 31) + (k & 3);
-    scode[at] = s_code[h];
+    scode[at] = code_of_slot[h];
     pcol[at] = col[k0 + k];  // the same packing: 4 consecutive slots of a row are one int4
   }
 }
