@@ -610,148 +610,6 @@ void host_to_device_values(double* dst, const double* src, size_t n) {
   }
 }
 
-// ---- int64 column indices over PCIe as one-byte codes -------------------------------------
-// A stencil operator's column index minus its row index takes a handful of values (7 for the
-// 7-point stencil).  Each 64 K-entry piece is coded on the host — a one-byte code per entry
-// into the piece's table of <= 256 distinct (col - row) offsets — and decoded on the device
-// (the entry's row from the already uploaded row offsets).  Range checks ride along; a piece
-// with more distinct offsets travels narrowed to int32 as before.
-namespace {
-constexpr size_t kColSlot = 256 * sizeof(int32_t) + kCodePiece;  // offset table + codes
-constexpr size_t kColRawBase = kCodeHdrBytes + kCodePieces * kColSlot;
-constexpr int kColPieces = kCodePieces;
-
-__global__ void k_decode_cols(const char* stage, const int32_t* rowptr, int64_t n_rows, int64_t k0,
-                              int64_t n, int32_t* dst) {
-  __shared__ int32_t tab[256];
-  const int p = blockIdx.x;
-  const CodeHeader h = reinterpret_cast<const CodeHeader*>(stage)[p];
-  const int64_t base = static_cast<int64_t>(p) * kCodePiece;
-  const int len = static_cast<int>(min(static_cast<int64_t>(kCodePiece), n - base));
-  if (h.coded) {
-    const int32_t* t = reinterpret_cast<const int32_t*>(stage + kCodeHdrBytes + p * kColSlot);
-    for (int i = threadIdx.x; i < h.ntab; i += blockDim.x) tab[i] = t[i];
-    __syncthreads();
-    const unsigned char* codes = reinterpret_cast<const unsigned char*>(t + 256);
-    for (int i = threadIdx.x; i < len; i += blockDim.x) {
-      const int64_t k = k0 + base + i;  // row = last r with rowptr[r] <= k
-      int64_t lo = 0, hi = n_rows;
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (__ldg(rowptr + mid) <= k) lo = mid;
-        else hi = mid;
-      }
-      dst[base + i] = static_cast<int32_t>(lo) + tab[codes[i]];
-    }
-  } else {
-    const int32_t* raw = reinterpret_cast<const int32_t*>(stage + h.raw_off);
-    for (int i = threadIdx.x; i < len; i += blockDim.x) dst[base + i] = raw[i];
-  }
-}
-
-// one piece [k0, k0 + len): offsets table + codes into slot; false when more than 256 distinct
-// offsets (or an index outside [0, hi): the caller then takes the checking path)
-bool code_cols_piece(const int64_t* col, const int64_t* rowptr, int64_t n_rows, int64_t k0, int len,
-                     int64_t hi, char* slot, int32_t* ntab_out) {
-  int32_t* tab = reinterpret_cast<int32_t*>(slot);
-  unsigned char* codes = reinterpret_cast<unsigned char*>(slot + 256 * sizeof(int32_t));
-  int64_t r = std::upper_bound(rowptr, rowptr + n_rows + 1, k0) - rowptr - 1;
-  if (r < 0 || r >= n_rows) return false;  // malformed offsets: the checking path reports them
-  int64_t rend = rowptr[r + 1];
-  int ntab = 0;
-  int64_t last = INT64_MIN;
-  unsigned char last_code = 0;
-  for (int i = 0; i < len; ++i) {
-    const int64_t k = k0 + i;
-    while (k >= rend) {
-      if (++r >= n_rows) return false;
-      rend = rowptr[r + 1];
-    }
-    const int64_t c = col[k];
-    if (c < 0 || c >= hi) return false;
-    const int64_t d = c - r;
-    if (d == last) {
-      codes[i] = last_code;
-      continue;
-    }
-    int q = 0;
-    while (q < ntab && tab[q] != d) ++q;  // few offsets: a linear scan beats hashing
-    if (q == ntab) {
-      if (ntab == 256) return false;
-      tab[ntab++] = static_cast<int32_t>(d);
-    }
-    codes[i] = static_cast<unsigned char>(q);
-    last = d;
-    last_code = static_cast<unsigned char>(q);
-  }
-  *ntab_out = ntab;
-  return true;
-}
-}  // namespace
-
-bool host_to_device_cols(int32_t* dst, const int64_t* col, const int64_t* rowptr, int64_t n_rows,
-                         size_t nnz, int64_t hi, const int32_t* rowptr_dev) {
-  ensure_init();
-  if (nnz * sizeof(int32_t) < kStagedMin || n_rows <= 0) return false;
-  Context& c = staged();
-  for (int b = 0; b < Context::kStages; ++b)
-    if (!c.dstage[b]) AGG_CUDA(cudaMalloc(&c.dstage[b], Context::kStageBytes));
-  // a first piece decides: general sparsity (many distinct offsets) takes the plain path
-  {
-    std::vector<char> probe(kColSlot);
-    int32_t nt = 0;
-    if (!code_cols_piece(col, rowptr, n_rows, 0, static_cast<int>(std::min<size_t>(kCodePiece, nnz)),
-                         hi, probe.data(), &nt))
-      return false;
-  }
-  const size_t per_chunk = static_cast<size_t>(kColPieces) * kCodePiece;
-  size_t off = 0;
-  for (int k = 0; off < nnz; ++k) {
-    const int b = k % Context::kStages;
-    const size_t len = std::min(per_chunk, nnz - off);
-    const int np = static_cast<int>((len + kCodePiece - 1) / kCodePiece);
-    AGG_CUDA(cudaEventSynchronize(c.stage_ev[b]));
-    char* st = c.stage[b];
-    CodeHeader* hdr = reinterpret_cast<CodeHeader*>(st);
-    std::atomic<int64_t> raw_used{0};
-    std::atomic<bool> out_of_range{false};
-    HostPool::get().run(np, [&](int p) {
-      const size_t p0 = static_cast<size_t>(p) * kCodePiece;
-      const int plen = static_cast<int>(std::min<size_t>(kCodePiece, len - p0));
-      int32_t ntab = 0;
-      if (code_cols_piece(col, rowptr, n_rows, static_cast<int64_t>(off + p0), plen, hi,
-                          st + kCodeHdrBytes + p * kColSlot, &ntab)) {
-        hdr[p] = CodeHeader{1, ntab, 0};
-        return;
-      }
-      const int64_t at = static_cast<int64_t>(kColRawBase) + raw_used.fetch_add(int64_t{4} * plen);
-      if (at + int64_t{4} * plen <= static_cast<int64_t>(Context::kStageBytes)) {
-        int32_t* out = reinterpret_cast<int32_t*>(st + at);
-        for (int i = 0; i < plen; ++i) {
-          const int64_t v = col[off + p0 + i];
-          if (v < 0 || v >= hi) out_of_range = true;
-          out[i] = static_cast<int32_t>(v);
-        }
-      }
-      hdr[p] = CodeHeader{0, 0, at};
-    });
-    const size_t used = kColRawBase + static_cast<size_t>(raw_used.load());
-    if (out_of_range.load() || used > Context::kStageBytes) {
-      sync();  // chunks already sent are overwritten by the caller's checking path
-      return false;
-    }
-    AGG_CUDA(cudaMemcpyAsync(c.dstage[b], st, used, cudaMemcpyHostToDevice, c.stream));
-    AGG_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));
-    k_decode_cols<<<np, 256, 0, c.stream>>>(c.dstage[b], rowptr_dev, n_rows,
-                                            static_cast<int64_t>(off), static_cast<int64_t>(len),
-                                            dst + off);
-    note_launch();
-    check_launch(__FILE__, __LINE__);
-    off += len;
-  }
-  return true;
-}
-
 void device_to_host(void* dst, const void* src, size_t bytes) {
   ensure_init();
   if (bytes < kStagedMin) {

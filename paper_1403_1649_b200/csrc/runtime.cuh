@@ -21,12 +21,6 @@ void host_to_device(void* dst, const void* src, size_t bytes);
 // fp64 arrays: large ones cross PCIe as one-byte codes per 64 K-value piece when the piece has
 // <= 256 distinct values (decoded on the device, bit-identical); other pieces travel raw
 void host_to_device_values(double* dst, const double* src, size_t n);
-// CSR column indices (int64 host, row offsets already on the device as rowptr_dev): coded as
-// one byte per entry into per-piece tables of (col - row) offsets when every piece has <= 256
-// of them and every index lies in [0, hi); false = not done (general sparsity, or an index
-// out of range: the caller takes host_to_device_narrow, which reports the first bad index)
-bool host_to_device_cols(int32_t* dst, const int64_t* col, const int64_t* rowptr, int64_t n_rows,
-                         size_t nnz, int64_t hi, const int32_t* rowptr_dev);
 void device_to_host(void* dst, const void* src, size_t bytes);
 // int64 host indices -> int32 device indices, narrowed on the host while staging (halves the
 // index bytes on the wire); *first_bad = first position whose value is outside [lo, hi), or -1.

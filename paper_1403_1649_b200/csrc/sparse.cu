@@ -375,10 +375,8 @@ DevCsrPtr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* rowptr, cons
   fill_int(bad.get(), 1, INT32_MAX);
   int64_t bad_rp = -1, bad_col = -1;
   host_to_device_narrow(A->rowptr.get(), rowptr, static_cast<size_t>(n_rows + 1), 0, nnz + 1, &bad_rp);
-  if (!host_to_device_cols(A->col.get(), col, rowptr, n_rows, static_cast<size_t>(nnz),
-                           validate ? n_cols : INT32_MAX, A->rowptr.get()))
-    host_to_device_narrow(A->col.get(), col, static_cast<size_t>(nnz), 0,
-                          validate ? n_cols : INT32_MAX, &bad_col);
+  host_to_device_narrow(A->col.get(), col, static_cast<size_t>(nnz), 0, validate ? n_cols : INT32_MAX,
+                        &bad_col);
   if (nnz > 0) host_to_device_values(A->val.get(), val, static_cast<size_t>(nnz));
   if (n_rows > 0)
     AGG_LAUNCH(k_check_rows, grid_for(n_rows, 256), 256, 0, A->rowptr.get(), A->col.get(), n_rows,
