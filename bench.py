@@ -506,7 +506,13 @@ def run_b200(args, world, rank, local):
     roof = None
     if jc > 0:
         achieved = (jb / jc) / ((jt / jc) / 1e3) / 1e9
-        if l0_vi:
+        if l0_vi and dims != 27:
+            # short rows (< 10 per row) on a dictionary copy: PCG's (r.z, r_old.z) ride on the sweep
+            tkey = "jacobidot2_sell_vi_l0_dram_bytes_per_launch"
+            kname = ("k_sell<Epi::kJacobiDot2, VI> on level 0: the damped-Jacobi post-smoothing "
+                     "sweep over the SELL-32 copy of the operator (values as one-byte dictionary "
+                     "codes) with PCG's two dot products (r.z, r_old.z) fused")
+        elif l0_vi:
             tkey = "jacobi_sell_vi_l0_dram_bytes_per_launch"
             kname = ("k_sell<Epi::kJacobi, VI> on level 0: the damped-Jacobi post-smoothing sweep "
                      "over the SELL-32 copy of the operator, values as one-byte dictionary codes")

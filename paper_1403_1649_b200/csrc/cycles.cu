@@ -316,7 +316,8 @@ void postsmooth(DevHierarchy& h, DevLevel& L, const double* b, double* x, const 
   // PCG's (r.z, r_old.z) ride on the last sweep — on CSR-stream operators.  With a SELL-32
   // copy the plain sweep (0.97 of peak) plus PCG's separate two-product dot measured faster
   // than the fused sweep (0.82-0.85): c2 solve -0.5 ms.
-  if (top && !pred && h.top_dot_out && !L.A->sell) {
+  if (top && !pred && h.top_dot_out &&
+      (!L.A->sell || (L.A->sell_vi && fuse_dots_on_dictionary()))) {
     SpmvArgs a;
     a.x = L.t.get();
     a.y = x;

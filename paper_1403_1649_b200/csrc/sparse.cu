@@ -664,7 +664,7 @@ void launch_stream(const DevCsr& A, const SpmvArgs& a) {
   if constexpr (E != Epi::kResidualZero) {
     // short rows (7-point level 0): the Jacobi + PCG-dots sweep measured faster as CSR-stream
     // (0.845 vs 0.824 of peak), every other epilogue faster as SELL (0.95-0.97 vs 0.86-0.89)
-    const bool skip = E == Epi::kJacobiDot2 && A.sell_short;
+    const bool skip = E == Epi::kJacobiDot2 && A.sell_short && !(A.sell_vi && fuse_dots_on_dictionary());
     if (A.sell && !skip) {
       launch_sell<E>(A, a);
       return;
@@ -696,11 +696,20 @@ void launch_stream(const DevCsr& A, const SpmvArgs& a) {
 
 }  // namespace
 
+// AGGMG_DICT_DOTS=0: PCG's (r.z, r_old.z) as a separate pass even on a dictionary operator
+bool fuse_dots_on_dictionary() {
+  static const bool on = [] {
+    const char* e = std::getenv("AGGMG_DICT_DOTS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 double spmv_bytes(const DevCsr& A, Epi epi) {
   const double n = static_cast<double>(A.n_rows), nnz = static_cast<double>(A.nnz);
   // the launch_stream dispatch: SELL with a value dictionary reads 4 + 1 bytes per entry
   const bool vi = A.sell && A.sell_vi && epi != Epi::kResidualZero &&
-                  !(epi == Epi::kJacobiDot2 && A.sell_short);
+                  !(epi == Epi::kJacobiDot2 && A.sell_short && !fuse_dots_on_dictionary());
   double b = (vi ? 5.0 : 12.0) * nnz + 4.0 * (n + 1) + 8.0 * static_cast<double>(A.n_cols) + 8.0 * n;
   switch (epi) {
     case Epi::kResidual: b += 8.0 * n; break;

@@ -109,6 +109,9 @@ DevCsrPtr generate_jump27_rows(int64_t nx, int64_t ny, int64_t nz, double jump, 
                                int64_t row0, int64_t nrows);
 
 double spmv_bytes(const DevCsr& A, Epi epi);
+// the fused damped-Jacobi + PCG dots sweep runs on a value-dictionary SELL copy (latency-bound:
+// the two extra streams ride along); false = the plain sweep and a separate dot pass
+bool fuse_dots_on_dictionary();
 
 // process-wide switch of the SELL value dictionary (default on; AGGMG_SELL_VI=0 starts it off);
 // takes effect for operators planned (or refreshed) afterwards
