@@ -498,7 +498,7 @@ __global__ void k_group_entry_counts(const idx* goff, const idx* rows, const idx
 }
 
 constexpr int kGalWarps = 8;
-constexpr int kGalCap = 256;     // tier 1: fine entries per coarse row, one warp, shared memory
+constexpr int kGalCap = 192;     // tier 1: fine entries per coarse row, one warp, shared memory (5 CTAs per SM)
 constexpr int kGalCapBig = 4096; // tier 2: one CTA per coarse row, shared memory (80 KB)
 constexpr int kGalCapSmem = 2048;  // tier 2 rows staged in shared memory per launch
 constexpr int kGalHash = 512;    // tier 2: distinct coarse columns per row (hash table slots)
