@@ -112,57 +112,6 @@ __global__ void __launch_bounds__(kStrThreads)
   }
 }
 
-// The same row rule over an operator's SELL-32 value-dictionary copy (sparse.cuh): a thread per
-// row, slot k of the 32 rows of a warp one coalesced request, the value a one-byte code into
-// the shared-memory table (the same double).  5 bytes per entry instead of 12: the level-0
-// strength passes of a stencil operator read 2.4x fewer bytes.
-__global__ void __launch_bounds__(256)
-    k_strength_vi(const idx* __restrict__ rowptr, const idx* __restrict__ sptr,
-                  const unsigned char* __restrict__ scode, const idx* __restrict__ pcol,
-                  const double* __restrict__ stab, int64_t n, double alpha, int fail_zero, int mode,
-                  const idx* out_rowptr, idx* out, int* bad_row) {
-  __shared__ double tab[256];
-  tab[threadIdx.x] = stab[threadIdx.x];  // blockDim.x == 256 == the table size
-  __syncthreads();
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const idx len = rowptr[i + 1] - rowptr[i];
-    const idx base = sptr[i >> 5] + 4 * static_cast<idx>(i & 31);
-    const idx ii = static_cast<idx>(i);
-    auto at = [&](idx k) { return base + 32 * (k & ~3) + (k & 3); };
-    double d = 0.0;
-    for (idx k = 0; k < len; ++k)
-      if (pcol[at(k)] == ii) d = tab[scode[at(k)]];
-    double sg;
-    if (d == 0.0) {  // strength.cpp:18-21
-      if (fail_zero) atomicMin(bad_row, static_cast<int>(i));
-      sg = 1.0;
-    } else {
-      sg = d > 0.0 ? 1.0 : -1.0;
-    }
-    const double ns = -sg;
-    double m = 0.0;
-    for (idx k = 0; k < len; ++k) {
-      if (pcol[at(k)] == ii) continue;
-      m = dmax_ref(m, __dmul_rn(ns, tab[scode[at(k)]]));
-    }
-    const double thr = __dmul_rn(alpha, m);
-    if (mode == 0) {
-      idx c = 0;
-      if (m > 0.0)
-        for (idx k = 0; k < len; ++k)
-          if (pcol[at(k)] != ii && __dmul_rn(ns, tab[scode[at(k)]]) > thr) ++c;
-      out[i] = c;
-    } else if (m > 0.0) {
-      idx p = out_rowptr[i];
-      for (idx k = 0; k < len; ++k) {
-        const idx c = pcol[at(k)];
-        if (c != ii && __dmul_rn(ns, tab[scode[at(k)]]) > thr) out[p++] = c;
-      }
-    }
-  }
-}
-
 // ---- a4/a5 influence + symmetrize -------------------------------------------------------
 __global__ void k_col_count(const idx* col, int64_t nnz, idx* cnt) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1320,22 +1269,6 @@ void strength_pass(const DevCsr& A, double alpha, int fail_zero, int mode, const
                    idx* out, int* bad) {
   const int64_t n = A.n_rows;
   if (n == 0) return;
-  if (A.sell && A.sell_vi && A.n_rows == A.n_cols) {  // the dictionary copy: 5 bytes per entry
-    static std::atomic<unsigned long long> seen{0};
-    static int per_sm[64] = {0};
-    const int dev = current_device() & 63;
-    if (device_pending(seen)) {
-      int p = 0;
-      AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, k_strength_vi, 256, 0));
-      per_sm[dev] = std::max(1, p);
-      mark_device(seen);
-    }
-    const int64_t grid = std::min<int64_t>(grid_for(n, 256), static_cast<int64_t>(per_sm[dev]) * sm_count());
-    AGG_LAUNCH(k_strength_vi, static_cast<unsigned>(grid), 256, 0, A.rowptr.get(), A.sell_ptr.get(),
-               A.sell_code.get(), A.sell_pcol.get(), A.sell_tab.get(), n, alpha, fail_zero, mode,
-               out_rowptr, out, bad);
-    return;
-  }
   const int stage = ((A.smem_entries + 3) / 2) * 2 + 2;
   const size_t smem = static_cast<size_t>(stage) * (sizeof(double) + sizeof(idx));
   // staging pays for long rows only (measured: 27-point 8.5 -> 4.3 ms; 7- and 14-entry rows
