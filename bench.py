@@ -289,14 +289,27 @@ def run_reference_arm(args, world, rank):
     for _ in range(args.warmup):
         cpu_reference_run(M, args.config, Aw, threads)
     del Aw
-    A = reference_matrix(args.config, grid)
+    # The full configuration every step, unless K steps of it cannot finish inside the arm's
+    # budget (the weak-scaling grids at 4 and 8 GPUs: 67 M / 134 M unknowns, minutes per step
+    # on 16 cores): then the largest grid of the same class that fits, halving the longest axis
+    # (the reference's DOF/s barely depends on the size; the line says which grid was timed).
+    budget = args.ref_budget_s
+    est_rate = 5.0e5 * threads / 16.0  # DOF/s of the reference on this class (c2, 16 cores: 5.9e5)
+    sgrid = list(grid)
+    while sgrid[0] * sgrid[1] * sgrid[2] * args.steps / est_rate > budget and max(sgrid) > 64:
+        sgrid[sgrid.index(max(sgrid))] //= 2
+    full = tuple(sgrid) == tuple(grid)
+    A = reference_matrix(args.config, tuple(sgrid))
     times = []
     for _ in range(args.steps):
         dt, res = cpu_reference_run(M, args.config, A, threads)
         times.append(dt)
     total = sum(times)
     value = A.n_rows * len(times) / total
-    sample = (f"the full configuration ({grid[0]}x{grid[1]}x{grid[2]}, {A.n_rows} unknowns) every timed step: "
+    what = (f"the full configuration ({grid[0]}x{grid[1]}x{grid[2]}, {A.n_rows} unknowns)" if full else
+            f"a {sgrid[0]}x{sgrid[1]}x{sgrid[2]} grid of the configuration's class ({A.n_rows} unknowns; the "
+            f"full {grid[0]}x{grid[1]}x{grid[2]} x {args.steps} steps exceeds the {budget:.0f} s arm budget)")
+    sample = (f"{what} every timed step: "
               f"setup_hierarchy + {'pcg' if CONFIGS[args.config][7] == 'pcg' else 'fgmres'} to 1e-8 "
               f"({res.report.iterations} iterations), the reference's default Galerkin path "
               f"(reuse_caches = false, its faster one); warm-up steps on a 64^{2 if dims == 2 else 3} grid")
@@ -310,7 +323,8 @@ def run_reference_arm(args, world, rank):
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "detail": {"step_seconds": times, "iterations": res.report.iterations,
+        "detail": {"timed_grid": sgrid, "full_configuration": full,
+                   "step_seconds": times, "iterations": res.report.iterations,
                    "setup_seconds": res.report.setup_seconds,
                    "solve_seconds": res.report.solve_seconds},
     }
@@ -789,7 +803,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-exact", action="store_true", help="skip the bit-identical-mode side number")
     ap.add_argument("--no-prof", action="store_true", help="skip per-launch CUDA-event timing")
-    ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--ref-budget-s", type=float, default=1400.0,
+                    help="--impl reference: seconds the timed steps may take; larger configurations "
+                         "time a same-class sample grid instead")
     ap.add_argument("--mode", default="auto", choices=["auto", "single", "dist", "replicas"],
                     help="auto: one GPU -> single, torchrun N>1 -> dist (row-partitioned)")
     ap.add_argument("--agglomerate", type=int, default=0,
