@@ -261,6 +261,60 @@ __global__ void __launch_bounds__(kLuThreads) k_lu_solve(int n, const double* __
   for (int i = t; i < n; i += kLuThreads) x[i] = xs[i];
 }
 
+// Small coarsest levels (n <= kLuWarpRows, the factors fit in shared memory): the CTA stages
+// the row-major factors into shared memory, then ONE warp runs the whole substitution with
+// warp barriers only.  Forward: lane l owns rows l, l + 32, ...; column j is applied once x_j
+// (row j's finished value) is published.  Backward: the lanes form row i's products
+// U_ij x_j (j > i) into a shared buffer, lane 0 subtracts them in ascending j and divides.
+// Exactly the reference's operation sequence per row (dense.cpp:63-79), so the same bits.
+constexpr int kLuWarpRows = 160;  // n^2 + 2n doubles <= 227 KB
+__global__ void __launch_bounds__(256) k_lu_solve_warp(int n, const double* __restrict__ lu,
+                                                     const int* __restrict__ perm,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ x, const int* pred) {
+  if (!on(pred)) return;
+  extern __shared__ double sh[];
+  double* f = sh;               // n * n: the factors, row-major
+  double* xs = sh + n * n;      // n: y, then x
+  double* pb = xs + n;          // n: row i's products
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  for (int64_t q = threadIdx.x; q < nn; q += blockDim.x) f[q] = lu[q];
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  // forward in place on xs (xs[i] = b[perm[i]], minus the finished columns); row j is final when
+  // column j is reached, and the lanes apply it to their rows i > j
+  for (int i = lane; i < n; i += 32) xs[i] = b[perm[i]];
+  __syncwarp();
+  for (int j = 0; j + 1 < n; ++j) {
+    const double xj = xs[j];
+    for (int i = j + 1 + lane; i < n; i += 32)
+      xs[i] = __dsub_rn(xs[i], __dmul_rn(f[static_cast<int64_t>(i) * n + j], xj));
+    __syncwarp();
+  }
+  __syncwarp();
+  for (int i = n - 1; i >= 0; --i) {
+    const double* ui = f + static_cast<int64_t>(i) * n;
+    for (int j = i + 1 + lane; j < n; j += 32) pb[j] = __dmul_rn(ui[j], xs[j]);
+    __syncwarp();
+    if (lane == 0) {
+      double acc = xs[i];
+      int j = i + 1;
+      for (; j + 4 <= n; j += 4) {
+        const double p0 = pb[j], p1 = pb[j + 1], p2 = pb[j + 2], p3 = pb[j + 3];
+        acc = __dsub_rn(acc, p0);
+        acc = __dsub_rn(acc, p1);
+        acc = __dsub_rn(acc, p2);
+        acc = __dsub_rn(acc, p3);
+      }
+      for (; j < n; ++j) acc = __dsub_rn(acc, pb[j]);
+      xs[i] = __ddiv_rn(acc, ui[i]);
+    }
+    __syncwarp();
+  }
+  for (int i = lane; i < n; i += 32) x[i] = xs[i];
+}
+
 __global__ void k_lu_serial(int64_t n, const double* __restrict__ lu, const int* __restrict__ perm,
                             const double* __restrict__ b, double* __restrict__ x, const int* pred) {
   if (!on(pred) || threadIdx.x != 0) return;
@@ -633,6 +687,19 @@ void coarse_solve(DevHierarchy& h, const double* b, double* x, const int* pred) 
   const int64_t n = h.levels.back().A->n_rows;
   if (n == 0) return;
   if (exact_reductions() && h.coarse_lu_ready) {  // bit-identical substitution (slow: n^2 chain)
+    if (n <= kLuWarpRows) {
+      const size_t wsmem = (static_cast<size_t>(n) * n + 2 * n) * sizeof(double);
+      static std::atomic<unsigned long long> wattr{0};  // the attribute is per device
+      if (device_pending(wattr)) {
+        AGG_CUDA(cudaFuncSetAttribute(k_lu_solve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>((kLuWarpRows * kLuWarpRows + 2 * kLuWarpRows) *
+                                                       sizeof(double))));
+        mark_device(wattr);
+      }
+      AGG_LAUNCH(k_lu_solve_warp, 1, 256, wsmem, static_cast<int>(n), h.coarse_lu.get(),
+                 h.coarse_perm.get(), b, x, pred);
+      return;
+    }
     const size_t smem = 3 * n * sizeof(double);
     if (n <= int64_t{kLuRows} * kLuThreads && smem <= 200 * 1024) {
       static std::atomic<unsigned long long> attr{0};  // the attribute is per device
