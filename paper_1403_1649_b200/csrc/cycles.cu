@@ -300,14 +300,22 @@ __global__ void __launch_bounds__(256) k_lu_solve_warp(int n, const double* __re
     if (lane == 0) {
       double acc = xs[i];
       int j = i + 1;
-      for (; j + 4 <= n; j += 4) {
-        const double p0 = pb[j], p1 = pb[j + 1], p2 = pb[j + 2], p3 = pb[j + 3];
-        acc = __dsub_rn(acc, p0);
-        acc = __dsub_rn(acc, p1);
-        acc = __dsub_rn(acc, p2);
-        acc = __dsub_rn(acc, p3);
+      // the next group's products load while this group's chain runs
+      double q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q[u] = j + u < n ? pb[j + u] : 0.0;
+      for (; j + 8 <= n; j += 8) {
+        double nq[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nq[u] = j + 8 + u < n ? pb[j + 8 + u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __dsub_rn(acc, q[u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) q[u] = nq[u];
       }
-      for (; j < n; ++j) acc = __dsub_rn(acc, pb[j]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j + u < n) acc = __dsub_rn(acc, q[u]);
       xs[i] = __ddiv_rn(acc, ui[i]);
     }
     __syncwarp();
