@@ -195,9 +195,10 @@ void dist_cycle(DistHierarchy& h, const CycleCfg& cfg, int64_t k, bool kc, const
   ja.b = b;
   ja.d = L.smoother.wdiag.get();
   ja.pred = pred;
-  // PCG's (r.z, r_old.z) ride on the last sweep on CSR-stream operators (SELL-32: plain sweep
-  // + PCG's separate dot, as on one GPU)
-  if (k == 0 && !pred && h.top_dot_out && !L.A->A.sell) {
+  // PCG's (r.z, r_old.z) ride on the last sweep on CSR-stream and value-dictionary operators
+  // (plain SELL-32: plain sweep + PCG's separate dot), as on one GPU
+  if (k == 0 && !pred && h.top_dot_out &&
+      (!L.A->A.sell || (L.A->A.sell_vi && fuse_dots_on_dictionary()))) {
     ja.c = h.top_dot_c;
     ja.dots_out = h.top_dot_out;
     dist_spmv(comm, *L.A, Epi::kJacobiDot2, ja, prof);
