@@ -405,6 +405,7 @@ DistCsrPtr make_dist(Comm& comm, const Partition& rows, const Partition& cols, D
   M->A.col.resize(gA.nnz);
   localize_cols(M->halo, gA.col.get(), gA.nnz, M->A.col.get(), err);
   gA.col.reset();
+  M->A.sell_sigma_ok = false;  // dist_spmv launches row sub-ranges
   M->A.plan();
   // overlap window: rows without halo columns around the middle of the slab
   const int64_t n = M->A.n_rows;

@@ -215,6 +215,8 @@ DevCsrPtr clone_csr(const DevCsr& A) {
   C->sell_ptr.copy_from(A.sell_ptr);
   C->sell_col.copy_from(A.sell_col);
   C->sell_val.copy_from(A.sell_val);
+  C->sell_perm.copy_from(A.sell_perm);
+  C->sell_sigma_ok = A.sell_sigma_ok;
   C->sell_vi = A.sell_vi;
   C->sell_pad4 = A.sell_pad4;
   C->sell_code.copy_from(A.sell_code);

@@ -63,20 +63,44 @@ __global__ void k_max_block_span(const idx* rowptr, int64_t n, int rpb, int* out
 }  // namespace
 
 // ---- SELL-32 copy -------------------------------------------------------------------------
-__global__ void k_slice_width(const idx* rowptr, int64_t n, int64_t nslices, int pad4, idx* w) {
+// SELL-C-sigma: inside every window of kSellSigma rows, rows ordered by descending length
+// (stable), so the 32 rows of a slice have similar lengths and a warp idles less on the short
+// ones (c2 level 1: 78% -> 95% of the slots are entries).  perm[q] = the row at position q.
+constexpr int kSellSigma = 256;
+__global__ void __launch_bounds__(kSellSigma) k_sell_sort_window(const idx* rowptr, int64_t n, idx* perm) {
+  __shared__ idx len[kSellSigma];
+  const int64_t w0 = static_cast<int64_t>(blockIdx.x) * kSellSigma;
+  const int t = threadIdx.x;
+  const int64_t r = w0 + t;
+  const int cnt = static_cast<int>(min(static_cast<int64_t>(kSellSigma), n - w0));
+  len[t] = r < n ? rowptr[r + 1] - rowptr[r] : -1;
+  __syncthreads();
+  if (t >= cnt) return;
+  const idx l = len[t];
+  int rank = 0;
+  for (int j = 0; j < cnt; ++j) rank += (len[j] > l || (len[j] == l && j < t)) ? 1 : 0;
+  perm[w0 + rank] = static_cast<idx>(r);
+}
+
+__global__ void k_slice_width(const idx* rowptr, int64_t n, int64_t nslices, int pad4, const idx* perm,
+                              idx* w) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= nslices) return;
   idx m = 0;
   const int64_t r1 = min(n, 32 * (s + 1));
-  for (int64_t r = 32 * s; r < r1; ++r) m = max(m, rowptr[r + 1] - rowptr[r]);
+  for (int64_t q = 32 * s; q < r1; ++q) {
+    const int64_t r = perm ? perm[q] : q;
+    m = max(m, rowptr[r + 1] - rowptr[r]);
+  }
   if (pad4) m = (m + 3) & ~3;  // packed dictionary codes: whole 4-slot groups per slice
   w[s] = 32 * m;
 }
 __global__ void k_sell_fill(const idx* rowptr, const idx* col, const double* val, int64_t n,
-                            const idx* sptr, idx* scol, double* sval, int with_cols) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const idx base = sptr[r >> 5] + static_cast<idx>(r & 31), k0 = rowptr[r], len = rowptr[r + 1] - k0;
+                            const idx* sptr, const idx* perm, idx* scol, double* sval, int with_cols) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // position
+  if (q >= n) return;
+  const int64_t r = perm ? perm[q] : q;
+  const idx base = sptr[q >> 5] + static_cast<idx>(q & 31), k0 = rowptr[r], len = rowptr[r + 1] - k0;
   for (idx k = 0; k < len; ++k) {
     if (with_cols) scol[base + 32 * k] = col[k0 + k];
     sval[base + 32 * k] = val[k0 + k];
@@ -256,8 +280,17 @@ void DevCsr::plan() {
     // slot budget (rows of 4-5 entries pad to 8), the plain unpadded layout is tried next
     const bool fits4 = ns * 32 * int64_t{max_row + 3} < INT32_MAX;
     for (const bool pad4 : {dict && fits4, false}) {
+      // the plain layout sorts rows by length inside windows (SELL-C-sigma) unless a row
+      // sub-range will be launched on it (sell_sigma_ok = false: partitioned operators)
+      if (!pad4 && sell_sigma_ok) {
+        sell_perm.resize(n_rows);
+        AGG_LAUNCH(k_sell_sort_window, static_cast<unsigned>((n_rows + kSellSigma - 1) / kSellSigma),
+                   kSellSigma, 0, rowptr.get(), n_rows, sell_perm.get());
+      } else {
+        sell_perm.reset();
+      }
       AGG_LAUNCH(k_slice_width, grid_for(ns, 256), 256, 0, rowptr.get(), n_rows, ns, pad4 ? 1 : 0,
-                 w.get());
+                 sell_perm.size() ? sell_perm.get() : nullptr, w.get());
       sell_ptr.resize(ns + 1);
       sell_slots = scan_to_offsets(w.get(), sell_ptr.get(), ns);
       if (sell_slots <= static_cast<int64_t>((pad4 ? 1.75 : 1.5) * static_cast<double>(nnz)) + 32 * 64) {
@@ -269,6 +302,7 @@ void DevCsr::plan() {
     }
     if (!sell) {
       sell_ptr.reset();
+      sell_perm.reset();
     } else if (sell_pad4) {
       build_codes(dslots);
     } else {
@@ -310,7 +344,8 @@ void DevCsr::fill_plain() {
   if (sell_col.size() != sell_slots) sell_col.resize(sell_slots);
   if (sell_val.size() != sell_slots) sell_val.resize(sell_slots);
   AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
-             sell_ptr.get(), sell_col.get(), sell_val.get(), 1);
+             sell_ptr.get(), sell_perm.size() ? sell_perm.get() : nullptr, sell_col.get(),
+             sell_val.get(), 1);
 }
 
 // the dictionary copy (packed columns + one-byte codes) from the slots of a successful
@@ -563,8 +598,8 @@ template <Epi E, bool VI>
 __global__ void __launch_bounds__(256)
     k_sell(const idx* __restrict__ rowptr, const idx* __restrict__ sptr, const idx* __restrict__ scol,
            const double* __restrict__ sval, const unsigned char* __restrict__ scode,
-           const idx* __restrict__ pcol, const double* __restrict__ stab, int64_t row0, int64_t n, SpmvArgs a, double* partials,
-           unsigned* ticket) {
+           const idx* __restrict__ pcol, const double* __restrict__ stab, const idx* __restrict__ perm,
+           int64_t row0, int64_t n, SpmvArgs a, double* partials, unsigned* ticket) {
   constexpr int NP = EpiTraits<E>::np;
   constexpr int NPX = NP > 0 ? NP : 1;
   __shared__ __align__(16) double red_smem[32 * 3 + 2];
@@ -579,18 +614,20 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int k = 0; k < NPX; ++k) v[k] = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  // rows [row0, row0 + n) (a sub-range for the partitioned path's interior / boundary split)
-  for (int64_t r = row0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < row0 + n;
-       r += stride) {
+  // positions [row0, row0 + n) (a sub-range of rows for the partitioned path's interior /
+  // boundary split; SELL-C-sigma copies are only built where no sub-range is launched)
+  for (int64_t q = row0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < row0 + n;
+       q += stride) {
+    const int64_t r = perm ? static_cast<int64_t>(__ldg(perm + q)) : q;
     const idx len = rowptr[r + 1] - rowptr[r];
-    const idx sbase = sptr[r >> 5];
-    const idx* c = scol + sbase + (r & 31);
+    const idx sbase = sptr[q >> 5];
+    const idx* c = scol + sbase + (q & 31);
     double sum = 0.0;
     if constexpr (VI) {
       // codes of slots k..k+3: one 32-bit word per row (the packed layout, sell_code)
-      const unsigned* cw = reinterpret_cast<const unsigned*>(scode + sbase) + (r & 31);
+      const unsigned* cw = reinterpret_cast<const unsigned*>(scode + sbase) + (q & 31);
       // columns in the same packing (sell_pcol): slots k..k+3 of a row are one int4
-      const int4* pc = reinterpret_cast<const int4*>(pcol + sbase) + (r & 31);
+      const int4* pc = reinterpret_cast<const int4*>(pcol + sbase) + (q & 31);
       for (idx k = 0; k < len; k += 4) {
         const unsigned w = __ldcs(cw + 8 * k);  // + 32 (k / 4) words
         const int4 q = __ldcs(pc + 8 * k);
@@ -608,7 +645,7 @@ __global__ void __launch_bounds__(256)
         }
       }
     } else {
-      const double* vv = sval + sbase + (r & 31);
+      const double* vv = sval + sbase + (q & 31);
       idx k = 0;
       for (; k + 4 <= len; k += 4) {
         const idx c0 = __ldcs(c + 32 * k), c1 = __ldcs(c + 32 * (k + 1)), c2 = __ldcs(c + 32 * (k + 2)),
@@ -645,8 +682,9 @@ void launch_sell_t(const DevCsr& A, const SpmvArgs& a) {
   const int64_t grid = std::min<int64_t>(grid_for(nrows, 256), static_cast<int64_t>(per_sm) * sm_count());
   const auto kern = k_sell<E, VI>;
   AGG_LAUNCH(kern, static_cast<unsigned>(grid), 256, 0, A.rowptr.get(), A.sell_ptr.get(),
-             A.sell_col.get(), A.sell_val.get(), A.sell_code.get(), A.sell_pcol.get(), A.sell_tab.get(), a.row_base,
-             nrows, a, reduce_partials(), reduce_ticket());
+             A.sell_col.get(), A.sell_val.get(), A.sell_code.get(), A.sell_pcol.get(), A.sell_tab.get(),
+             A.sell_perm.size() ? A.sell_perm.get() : nullptr, a.row_base, nrows, a, reduce_partials(),
+             reduce_ticket());
 }
 
 template <Epi E>

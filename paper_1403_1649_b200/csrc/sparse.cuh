@@ -31,6 +31,11 @@ struct DevCsr {
   bool sell_short = false;  // mean row length < 10
   DevBuf<idx> sell_ptr, sell_col;
   DevBuf<double> sell_val;
+  // SELL-C-sigma (plain layout only): position q of the copy holds row sell_perm[q], rows sorted
+  // by length inside windows of 256 (empty = identity).  Partitioned operators keep the identity
+  // (their interior / boundary launches address row sub-ranges): sell_sigma_ok = false.
+  DevBuf<idx> sell_perm;
+  bool sell_sigma_ok = true;
   // value dictionary (operators with <= 256 distinct values, e.g. stencil matrices): slot k's
   // value is sell_tab[sell_code[slot]] — the same double, one byte per entry instead of eight
   bool sell_vi = false;
