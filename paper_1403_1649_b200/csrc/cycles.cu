@@ -360,10 +360,14 @@ void presmooth(DevLevel& L, const double* b, const double* x_in, double* x_out, 
     smooth_sgs(L.smoother, *L.A, b, x_out, pred);
     return;
   }
-  if (x_in)
+  if (x_in) {
     smooth_sweep(L.smoother, *L.A, b, x_in, x_out, pred, top ? kProfSmoothL0 : 0);
-  else
+  } else if (L.zs_b == b && L.zs_x == x_out) {  // done by the restriction into this level
+    L.zs_b = nullptr;
+    L.zs_x = nullptr;
+  } else {
     AGG_LAUNCH(k_jacobi_zero, egrid(n), kB, 0, n, L.smoother.wdiag.get(), b, x_out, pred);
+  }
 }
 
 void postsmooth(DevHierarchy& h, DevLevel& L, const double* b, double* x, const int* pred, bool top) {
@@ -398,8 +402,11 @@ void postsmooth(DevHierarchy& h, DevLevel& L, const double* b, double* x, const 
 // zero guess the damped-Jacobi sweep and the residual fuse into one CSR-stream pass
 // (x1 = 0 + wd b is recomputed for the gathered neighbours, bit-identical to the
 // two-kernel sequence since A*0 sums to +0).
+// next_x: where the next level's cycle will put its iterate (the parent's coarse vector: xc
+// under a V-cycle, c under a K-cycle's first inner cycle) — the restriction then also writes
+// the next level's zero-guess sweep into it, one launch instead of two
 void descend(DevHierarchy& h, int64_t k, const double* b, const double* x_in, double* x_out,
-             const int* pred) {
+             const int* pred, double* next_x) {
   DevLevel& L = h.levels[k];
   SpmvArgs ra;
   ra.y = L.r.get();
@@ -422,6 +429,15 @@ void descend(DevHierarchy& h, int64_t k, const double* b, const double* x_in, do
   rr.x = L.r.get();
   rr.y = L.rc.get();
   rr.pred = pred;
+  DevLevel& N = h.levels[k + 1];
+  if (next_x && k + 1 < h.coarsest() && N.smoother.kind != 2) {
+    rr.x_out = next_x;
+    rr.d = N.smoother.wdiag.get();
+    spmv_run(*L.tr.R, Epi::kSpmvZero, rr);  // restriction + x_{k+1} = 0 + wd rc
+    N.zs_b = L.rc.get();
+    N.zs_x = next_x;
+    return;
+  }
   spmv_run(*L.tr.R, Epi::kSpmv, rr);  // restriction = spmv(R, r), cycles.cpp:56-57
 }
 
@@ -505,6 +521,8 @@ void subcycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b, 
     AGG_CUDA(cudaGraphDestroy(graph));
   }
   AGG_CUDA(cudaGraphLaunch(g->exec, stream()));
+  h.levels[k].zs_b = nullptr;  // the replayed capture consumed the fused sweep
+  h.levels[k].zs_x = nullptr;
   note_launches(g->kernels);
   ++h.graph_uses;
 }
@@ -563,7 +581,7 @@ void vcycle_dev(DevHierarchy& h, int64_t k, const double* b, const double* x_in,
     return;
   }
   DevLevel& L = h.levels[k];
-  descend(h, k, b, x_in, x_out, pred);
+  descend(h, k, b, x_in, x_out, pred, L.xc.get());
   coarse_correction(h, CycleCfg{}, false, k + 1, L.rc.get(), L.xc.get(), work_of(L), pred);
   postsmooth(h, L, b, x_out, pred, finest(h, k));
 }
@@ -576,7 +594,7 @@ void kcycle_dev(DevHierarchy& h, const CycleCfg& cfg, int64_t k, const double* b
     return;
   }
   DevLevel& L = h.levels[k];
-  descend(h, k, b, x_in, x_out, pred);
+  descend(h, k, b, x_in, x_out, pred, L.c.get());
   coarse_correction(h, cfg, true, k + 1, L.rc.get(), L.xc.get(), work_of(L), pred);
   postsmooth(h, L, b, x_out, pred, finest(h, k));
 }

@@ -49,6 +49,10 @@ struct DevLevel {
   // coarse-side vectors owned by this level's cycle (size n_{k+1})
   DevBuf<double> rc, xc, c, v, rt, d, w;
   DevBuf<KScalars> ks;
+  // set while capturing / issuing a cycle: the restriction into this level already wrote the
+  // zero-guess damped-Jacobi sweep of right-hand side zs_b into zs_x (Epi::kSpmvZero)
+  const double* zs_b = nullptr;
+  double* zs_x = nullptr;
 };
 
 // Captured CUDA graph of one coarse sub-cycle launch (levels >= 1 are launch-latency

@@ -484,6 +484,9 @@ __device__ __forceinline__ void row_epilogue(const SpmvArgs& a, const double* __
     a.x_out[rg] = __dadd_rn(0.0, __dmul_rn(a.d[rg], br));         // x1 = 0 + wd b
   } else if constexpr (E == Epi::kJacobi) {
     a.y[rg] = __dadd_rn(x[rg], __dmul_rn(a.d[rg], __dsub_rn(a.b[rg], sum)));
+  } else if constexpr (E == Epi::kSpmvZero) {
+    a.y[rg] = sum;
+    a.x_out[rg] = __dadd_rn(0.0, __dmul_rn(a.d[rg], sum));  // k_jacobi_zero's operation
   } else if constexpr (E == Epi::kScaleDiag) {
     a.y[rg] = __dmul_rn(sum, a.d[rg]);
   }
@@ -754,6 +757,7 @@ double spmv_bytes(const DevCsr& A, Epi epi) {
     case Epi::kResidualZero: b += 8.0 * n + 16.0 * n; break;  // wd gathered, x1 written
     case Epi::kJacobi: b += 16.0 * n; break;
     case Epi::kScaleDiag: b += 8.0 * n; break;
+    case Epi::kSpmvZero: b += 16.0 * n; break;
     case Epi::kSpmvDot1: b += 8.0 * n; break;
     case Epi::kSpmvDot2: b += 8.0 * n; break;
     case Epi::kSpmvDot3: b += 16.0 * n; break;
@@ -772,6 +776,7 @@ void spmv_run(const DevCsr& A, Epi epi, const SpmvArgs& a, int prof_family) {
     case Epi::kResidualZero: launch_stream<Epi::kResidualZero>(A, a); break;
     case Epi::kJacobi: launch_stream<Epi::kJacobi>(A, a); break;
     case Epi::kScaleDiag: launch_stream<Epi::kScaleDiag>(A, a); break;
+    case Epi::kSpmvZero: launch_stream<Epi::kSpmvZero>(A, a); break;
     case Epi::kSpmvDot1: launch_stream<Epi::kSpmvDot1>(A, a); break;
     case Epi::kSpmvDot2: launch_stream<Epi::kSpmvDot2>(A, a); break;
     case Epi::kSpmvDot3: launch_stream<Epi::kSpmvDot3>(A, a); break;

@@ -71,6 +71,7 @@ enum class Epi {
   kSpmvDot3,   // y = A x ; dots (y.u, y.y, y.c) [gmres] or (x.u, x.y, x.c) [cg]
   kSpmvDot1,   // y = A x ; dot (u . y)
   kJacobiDot2, // y = x + wd .* (b - A x) ; dots (b . y, c . y)  (PCG's r.z, r_old.z fused)
+  kSpmvZero,   // y = A x ; x_out = 0 + d .* y  (restriction + the next level's zero-guess sweep)
 };
 
 struct SpmvArgs {
