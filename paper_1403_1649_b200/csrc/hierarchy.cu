@@ -222,6 +222,7 @@ DevCsrPtr clone_csr(const DevCsr& A) {
   C->sell_code.copy_from(A.sell_code);
   C->sell_tab.copy_from(A.sell_tab);
   C->sell_pcol.copy_from(A.sell_pcol);
+  C->sell_len.copy_from(A.sell_len);
   C->sell_slots = A.sell_slots;
   return C;
 }

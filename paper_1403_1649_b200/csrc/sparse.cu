@@ -96,11 +96,13 @@ __global__ void k_slice_width(const idx* rowptr, int64_t n, int64_t nslices, int
   w[s] = 32 * m;
 }
 __global__ void k_sell_fill(const idx* rowptr, const idx* col, const double* val, int64_t n,
-                            const idx* sptr, const idx* perm, idx* scol, double* sval, int with_cols) {
+                            const idx* sptr, const idx* perm, idx* scol, double* sval, int with_cols,
+                            unsigned char* slen) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // position
   if (q >= n) return;
   const int64_t r = perm ? perm[q] : q;
   const idx base = sptr[q >> 5] + static_cast<idx>(q & 31), k0 = rowptr[r], len = rowptr[r + 1] - k0;
+  slen[q] = static_cast<unsigned char>(len);
   for (idx k = 0; k < len; ++k) {
     if (with_cols) scol[base + 32 * k] = col[k0 + k];
     sval[base + 32 * k] = val[k0 + k];
@@ -199,10 +201,11 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
 __global__ void k_sell_codes(const idx* rowptr, const idx* col, const double* val, int64_t n,
                              const idx* sptr, const unsigned long long* __restrict__ slots,
                              const unsigned char* __restrict__ code_of_slot, unsigned char* scode,
-                             idx* pcol) {
+                             idx* pcol, unsigned char* slen) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const idx k0 = rowptr[r], len = rowptr[r + 1] - k0;
+  slen[r] = static_cast<unsigned char>(len);
   for (idx k = 0; k < len; ++k) {
     const unsigned long long u = __double_as_longlong(val[k0 + k]);
     unsigned h = dict_hash(u);
@@ -303,6 +306,7 @@ void DevCsr::plan() {
     if (!sell) {
       sell_ptr.reset();
       sell_perm.reset();
+      sell_len.reset();
     } else if (sell_pad4) {
       build_codes(dslots);
     } else {
@@ -343,9 +347,10 @@ void DevCsr::fill_plain() {
   // (padding slots are never read: every row stops at its own length)
   if (sell_col.size() != sell_slots) sell_col.resize(sell_slots);
   if (sell_val.size() != sell_slots) sell_val.resize(sell_slots);
+  sell_len.resize(n_rows);
   AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
              sell_ptr.get(), sell_perm.size() ? sell_perm.get() : nullptr, sell_col.get(),
-             sell_val.get(), 1);
+             sell_val.get(), 1, sell_len.get());
 }
 
 // the dictionary copy (packed columns + one-byte codes) from the slots of a successful
@@ -370,8 +375,9 @@ void DevCsr::build_codes(const DevBuf<unsigned long long>& slots) {
     sell_code.resize(sell_slots);
     sell_pcol.resize(sell_slots);
   }
+  sell_len.resize(n_rows);
   AGG_LAUNCH(k_sell_codes, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
-             sell_ptr.get(), slots.get(), cos.get(), sell_code.get(), sell_pcol.get());
+             sell_ptr.get(), slots.get(), cos.get(), sell_code.get(), sell_pcol.get(), sell_len.get());
   sync();  // the temporaries above are freed on return
   sell_vi = true;
   sell_col.reset();
@@ -466,46 +472,82 @@ struct EpiTraits {
 // across row blocks and are reduced once per CTA (fixed grid => deterministic).
 // Per-row epilogue of the SpMV family: y / residual / Jacobi / scaled output and the fused
 // dot contributions, from the row's sequential sum.
+// The row's epilogue operands (x_r, d_r, b_r, c_r, u_r as the epilogue needs them), loaded
+// apart from the sum so the SELL kernels can issue them before the row's gathers.
+struct EpiIn {
+  double xr, d, b, c, u;
+};
 template <Epi E>
-__device__ __forceinline__ void row_epilogue(const SpmvArgs& a, const double* __restrict__ x,
-                                             int64_t rg, double sum, double* v) {
+__device__ __forceinline__ EpiIn epi_load(const SpmvArgs& a, const double* __restrict__ x, int64_t rg) {
+  constexpr int NP = EpiTraits<E>::np;
+  EpiIn e{0.0, 0.0, 0.0, 0.0, 0.0};
+  if constexpr (E == Epi::kJacobiDot2 || E == Epi::kJacobi) {
+    e.xr = x[rg];
+    e.d = a.d[rg];
+    e.b = a.b[rg];
+    if constexpr (E == Epi::kJacobiDot2) e.c = a.c[rg];
+  } else if constexpr (E == Epi::kResidual) {
+    e.b = a.b[rg];
+  } else if constexpr (E == Epi::kResidualZero) {
+    e.b = a.b[rg];
+    e.d = a.d[rg];
+  } else if constexpr (E == Epi::kSpmvZero || E == Epi::kScaleDiag) {
+    e.d = a.d[rg];
+  } else if constexpr (NP == 1) {
+    e.u = a.u[rg];
+  } else if constexpr (NP > 1) {
+    if (a.dot_with_x) e.xr = x[rg];
+    e.c = a.c[rg];
+    if constexpr (NP == 3) e.u = a.u[rg];
+  }
+  return e;
+}
+
+template <Epi E>
+__device__ __forceinline__ void row_epilogue_in(const SpmvArgs& a, const EpiIn& e, int64_t rg,
+                                                double sum, double* v) {
   constexpr int NP = EpiTraits<E>::np;
   double yv = sum;
   if constexpr (E == Epi::kJacobiDot2) {
-    yv = __dadd_rn(x[rg], __dmul_rn(a.d[rg], __dsub_rn(a.b[rg], sum)));
+    yv = __dadd_rn(e.xr, __dmul_rn(e.d, __dsub_rn(e.b, sum)));
     a.y[rg] = yv;
   } else if constexpr (E == Epi::kSpmv || NP > 0) {
     a.y[rg] = sum;
   } else if constexpr (E == Epi::kResidual) {
-    a.y[rg] = __dsub_rn(a.b[rg], sum);
+    a.y[rg] = __dsub_rn(e.b, sum);
   } else if constexpr (E == Epi::kResidualZero) {
-    const double br = a.b[rg];
-    a.y[rg] = __dsub_rn(br, sum);                                // r = b - A x1
-    a.x_out[rg] = __dadd_rn(0.0, __dmul_rn(a.d[rg], br));         // x1 = 0 + wd b
+    a.y[rg] = __dsub_rn(e.b, sum);                          // r = b - A x1
+    a.x_out[rg] = __dadd_rn(0.0, __dmul_rn(e.d, e.b));      // x1 = 0 + wd b
   } else if constexpr (E == Epi::kJacobi) {
-    a.y[rg] = __dadd_rn(x[rg], __dmul_rn(a.d[rg], __dsub_rn(a.b[rg], sum)));
+    a.y[rg] = __dadd_rn(e.xr, __dmul_rn(e.d, __dsub_rn(e.b, sum)));
   } else if constexpr (E == Epi::kSpmvZero) {
     a.y[rg] = sum;
-    a.x_out[rg] = __dadd_rn(0.0, __dmul_rn(a.d[rg], sum));  // k_jacobi_zero's operation
+    a.x_out[rg] = __dadd_rn(0.0, __dmul_rn(e.d, sum));  // k_jacobi_zero's operation
   } else if constexpr (E == Epi::kScaleDiag) {
-    a.y[rg] = __dmul_rn(sum, a.d[rg]);
+    a.y[rg] = __dmul_rn(sum, e.d);
   }
   if constexpr (E == Epi::kJacobiDot2) {
-    v[0] = __dadd_rn(v[0], __dmul_rn(a.b[rg], yv));  // r . z
-    v[1] = __dadd_rn(v[1], __dmul_rn(a.c[rg], yv));  // r_old . z
+    v[0] = __dadd_rn(v[0], __dmul_rn(e.b, yv));  // r . z
+    v[1] = __dadd_rn(v[1], __dmul_rn(e.c, yv));  // r_old . z
   } else if constexpr (NP > 0) {
-    const double lhs = a.dot_with_x ? x[rg] : sum;
+    const double lhs = a.dot_with_x ? e.xr : sum;
     if constexpr (NP == 1) {
-      v[0] = __dadd_rn(v[0], __dmul_rn(a.u[rg], sum));
+      v[0] = __dadd_rn(v[0], __dmul_rn(e.u, sum));
     } else if constexpr (NP == 2) {
-      v[0] = __dadd_rn(v[0], __dmul_rn(lhs, sum));     // rho  = v.v (gmres) | c.v (cg)
-      v[1] = __dadd_rn(v[1], __dmul_rn(lhs, a.c[rg]));  // alpha = v.rc       | c.rc
+      v[0] = __dadd_rn(v[0], __dmul_rn(lhs, sum));  // rho  = v.v (gmres) | c.v (cg)
+      v[1] = __dadd_rn(v[1], __dmul_rn(lhs, e.c));  // alpha = v.rc       | c.rc
     } else {
-      v[0] = __dadd_rn(v[0], __dmul_rn(lhs, a.u[rg]));  // gamma = w.v | d.v
-      v[1] = __dadd_rn(v[1], __dmul_rn(lhs, sum));     // beta  = w.w | d.w
-      v[2] = __dadd_rn(v[2], __dmul_rn(lhs, a.c[rg]));  // alpha2 = w.rt | d.rt
+      v[0] = __dadd_rn(v[0], __dmul_rn(lhs, e.u));  // gamma = w.v | d.v
+      v[1] = __dadd_rn(v[1], __dmul_rn(lhs, sum));  // beta  = w.w | d.w
+      v[2] = __dadd_rn(v[2], __dmul_rn(lhs, e.c));  // alpha2 = w.rt | d.rt
     }
   }
+}
+
+template <Epi E>
+__device__ __forceinline__ void row_epilogue(const SpmvArgs& a, const double* __restrict__ x,
+                                             int64_t rg, double sum, double* v) {
+  row_epilogue_in<E>(a, epi_load<E>(a, x, rg), rg, sum, v);
 }
 
 template <Epi E>
@@ -597,12 +639,39 @@ __global__ void __launch_bounds__(kStreamThreads)
 // epilogues apply: bit-identical to k_csr_stream.
 // With the value dictionary (VI) a slot's value is one byte, its code into the operator's
 // table of distinct values (shared memory); the value, and so every sum, is the same double.
-template <Epi E, bool VI>
-__global__ void __launch_bounds__(256)
+// Tuning variants of the SELL kernels: g = 4-slot groups per step (VI layout), pf = the next
+// step's columns / codes load under this step's gathers, pre = the row's epilogue operands
+// load before its gathers, minb = __launch_bounds__ min blocks (caps registers for occupancy).
+// Each (epilogue, layout) pair uses the variant sell_tune() picks (tools/kernel_bench.py over
+// a sweep build: tools/build_variant.sh NAME -DAGGMG_SELL_SWEEP, AGGMG_SELL_TUNE=<variant>).
+struct SellTune {
+  int g, pf, pre, minb, legacy = 0;  // legacy: 4 slots per step, loads then gathers, no predication
+};
+constexpr SellTune kSellTunes[] = {
+    {1, 0, 0, 1}, {1, 0, 0, 8}, {1, 1, 0, 8}, {1, 1, 1, 6}, {2, 1, 0, 1}, {1, 1, 1, 1},
+    {2, 1, 1, 1}, {1, 1, 0, 6}, {2, 1, 0, 6}, {1, 0, 1, 8}, {1, 1, 0, 1}, {2, 1, 0, 4},
+    {1, 0, 0, 1, 1}, {1, 0, 0, 8, 1}, {1, 0, 1, 1, 1}, {1, 0, 0, 6, 1},
+};
+constexpr int kSellTuneCount = sizeof(kSellTunes) / sizeof(kSellTunes[0]);
+// measured on B200 (profiles/r02_sell_tune_sweep.txt, tools/kernel_bench.py at c2 and c4):
+// the plain layout wants prefetch at full occupancy; the dictionary layout with short rows
+// (7-point) wants 32 registers (8 CTAs per SM); with long rows (27-point) the plain-loop
+// variants win, at 32 registers for the fused-dot epilogues and 2-group prefetch otherwise
+constexpr int sell_tune(Epi e, bool vi, bool short_rows) {
+  if (!vi) return 10;
+  const bool dots = e == Epi::kSpmvDot1 || e == Epi::kSpmvDot2 || e == Epi::kSpmvDot3 ||
+                    e == Epi::kJacobiDot2;
+  if (short_rows) return e == Epi::kSpmvDot1 ? 2 : 1;
+  return dots ? 13 : 4;
+}
+
+template <Epi E, bool VI, int T>
+__global__ void __launch_bounds__(256, kSellTunes[T].minb)
     k_sell(const idx* __restrict__ rowptr, const idx* __restrict__ sptr, const idx* __restrict__ scol,
            const double* __restrict__ sval, const unsigned char* __restrict__ scode,
            const idx* __restrict__ pcol, const double* __restrict__ stab, const idx* __restrict__ perm,
-           int64_t row0, int64_t n, SpmvArgs a, double* partials, unsigned* ticket) {
+           const unsigned char* __restrict__ slen, int64_t row0, int64_t n, SpmvArgs a,
+           double* partials, unsigned* ticket) {
   constexpr int NP = EpiTraits<E>::np;
   constexpr int NPX = NP > 0 ? NP : 1;
   __shared__ __align__(16) double red_smem[32 * 3 + 2];
@@ -621,35 +690,39 @@ __global__ void __launch_bounds__(256)
   // boundary split; SELL-C-sigma copies are only built where no sub-range is launched)
   for (int64_t q = row0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < row0 + n;
        q += stride) {
+    // the position's length and slice base and the row's epilogue operands are independent
+    // loads: they all issue before the first column load (no rowptr round trip)
     const int64_t r = perm ? static_cast<int64_t>(__ldg(perm + q)) : q;
-    const idx len = rowptr[r + 1] - rowptr[r];
+    const int len = slen[q];
     const idx sbase = sptr[q >> 5];
-    const idx* c = scol + sbase + (q & 31);
+    constexpr SellTune tune = kSellTunes[T];
+    EpiIn ein;
+    if constexpr (tune.pre) ein = epi_load<E>(a, x, r);
     double sum = 0.0;
-    if constexpr (VI) {
-      // codes of slots k..k+3: one 32-bit word per row (the packed layout, sell_code)
+    if constexpr (VI && tune.legacy) {
       const unsigned* cw = reinterpret_cast<const unsigned*>(scode + sbase) + (q & 31);
-      // columns in the same packing (sell_pcol): slots k..k+3 of a row are one int4
       const int4* pc = reinterpret_cast<const int4*>(pcol + sbase) + (q & 31);
-      for (idx k = 0; k < len; k += 4) {
+      for (int k = 0; k < len; k += 4) {
         const unsigned w = __ldcs(cw + 8 * k);  // + 32 (k / 4) words
-        const int4 q = __ldcs(pc + 8 * k);
+        const int4 cq4 = __ldcs(pc + 8 * k);
         if (k + 4 <= len) {
-          const double x0 = __ldg(x + q.x), x1 = __ldg(x + q.y), x2 = __ldg(x + q.z), x3 = __ldg(x + q.w);
+          const double x0 = __ldg(x + cq4.x), x1 = __ldg(x + cq4.y), x2 = __ldg(x + cq4.z),
+                       x3 = __ldg(x + cq4.w);
           sum = __dadd_rn(sum, __dmul_rn(s_tab[w & 255u], x0));
           sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> 8) & 255u], x1));
           sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> 16) & 255u], x2));
           sum = __dadd_rn(sum, __dmul_rn(s_tab[w >> 24], x3));
         } else {
-          const idx cq[4] = {q.x, q.y, q.z, q.w};
+          const idx cq[4] = {cq4.x, cq4.y, cq4.z, cq4.w};
 #pragma unroll
           for (int j = 0; j < 3; ++j)
             if (j < len - k) sum = __dadd_rn(sum, __dmul_rn(s_tab[(w >> (8 * j)) & 255u], __ldg(x + cq[j])));
         }
       }
-    } else {
+    } else if constexpr (!VI && tune.legacy) {
+      const idx* c = scol + sbase + (q & 31);
       const double* vv = sval + sbase + (q & 31);
-      idx k = 0;
+      int k = 0;
       for (; k + 4 <= len; k += 4) {
         const idx c0 = __ldcs(c + 32 * k), c1 = __ldcs(c + 32 * (k + 1)), c2 = __ldcs(c + 32 * (k + 2)),
                   c3 = __ldcs(c + 32 * (k + 3));
@@ -662,8 +735,91 @@ __global__ void __launch_bounds__(256)
         sum = __dadd_rn(sum, __dmul_rn(v3, x3));
       }
       for (; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldcs(vv + 32 * k), __ldg(x + __ldcs(c + 32 * k))));
+    } else if constexpr (VI) {
+      // codes of slots k..k+3: one 32-bit word per row (the packed layout, sell_code)
+      const unsigned* cw = reinterpret_cast<const unsigned*>(scode + sbase) + (q & 31);
+      // columns in the same packing (sell_pcol): slots k..k+3 of a row are one int4
+      const int4* pc = reinterpret_cast<const int4*>(pcol + sbase) + (q & 31);
+      // G 4-slot groups per step; with pf the next step's codes and columns load under this
+      // step's gathers
+      constexpr int G = tune.g;
+      unsigned w[G];
+      int4 c[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        w[g] = 4 * g < len ? __ldcs(cw + 32 * g) : 0u;
+        c[g] = 4 * g < len ? __ldcs(pc + 32 * g) : make_int4(0, 0, 0, 0);
+      }
+      for (int k = 0; k < len; k += 4 * G) {
+        const int m = len - k;  // slots left in this row
+        if (!tune.pf && k > 0) {
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+            if (4 * g < m) {
+              w[g] = __ldcs(cw + 8 * (k + 4 * g));
+              c[g] = __ldcs(pc + 8 * (k + 4 * g));
+            }
+        }
+        double xs[4 * G];
+        unsigned u[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          u[g] = w[g];
+          xs[4 * g] = 4 * g < m ? __ldg(x + c[g].x) : 0.0;
+          xs[4 * g + 1] = 4 * g + 1 < m ? __ldg(x + c[g].y) : 0.0;
+          xs[4 * g + 2] = 4 * g + 2 < m ? __ldg(x + c[g].z) : 0.0;
+          xs[4 * g + 3] = 4 * g + 3 < m ? __ldg(x + c[g].w) : 0.0;
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if (tune.pf && 4 * (G + g) < m) {
+            w[g] = __ldcs(cw + 8 * (k + 4 * (G + g)));
+            c[g] = __ldcs(pc + 8 * (k + 4 * (G + g)));
+          }
+#pragma unroll
+        for (int j = 0; j < 4 * G; ++j)
+          if (j < m) sum = __dadd_rn(sum, __dmul_rn(s_tab[(u[j >> 2] >> (8 * (j & 3))) & 255u], xs[j]));
+      }
+    } else {
+      const idx* c = scol + sbase + (q & 31);
+      const double* vv = sval + sbase + (q & 31);
+      // 4 slots per step; the next step's columns and values load under this step's gathers
+      idx cc[4];
+      double vq[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        cc[j] = j < len ? __ldcs(c + 32 * j) : 0;
+        vq[j] = j < len ? __ldcs(vv + 32 * j) : 0.0;
+      }
+      for (int k = 0; k < len; k += 4) {
+        const int m = len - k;
+        if (!tune.pf && k > 0) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            cc[j] = j < m ? __ldcs(c + 32 * (k + j)) : 0;
+            vq[j] = j < m ? __ldcs(vv + 32 * (k + j)) : 0.0;
+          }
+        }
+        double xs[4], vs[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          xs[j] = j < m ? __ldg(x + cc[j]) : 0.0;
+          vs[j] = vq[j];
+        }
+        if (tune.pf) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            cc[j] = j + 4 < m ? __ldcs(c + 32 * (k + 4 + j)) : 0;
+            vq[j] = j + 4 < m ? __ldcs(vv + 32 * (k + 4 + j)) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < m) sum = __dadd_rn(sum, __dmul_rn(vs[j], xs[j]));
+      }
     }
-    row_epilogue<E>(a, x, r, sum, v);
+    if constexpr (!tune.pre) ein = epi_load<E>(a, x, r);
+    row_epilogue_in<E>(a, ein, r, sum, v);
   }
   if constexpr (NP > 0) {
     block_reduce<NPX>(v, red_smem);
@@ -674,28 +830,64 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <Epi E, bool VI>
+template <Epi E, bool VI, int T>
 void launch_sell_t(const DevCsr& A, const SpmvArgs& a) {
-  static thread_local int per_sm = 0;
+  static std::atomic<int> per_sm_cache{0};
+  int per_sm = per_sm_cache.load();
   if (!per_sm) {
-    AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sell<E, VI>, 256, 0));
+    AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sell<E, VI, T>, 256, 0));
     per_sm = std::max(1, per_sm);
+    per_sm_cache.store(per_sm);
   }
   const int64_t nrows = a.row_count >= 0 ? a.row_count : A.n_rows - a.row_base;
   const int64_t grid = std::min<int64_t>(grid_for(nrows, 256), static_cast<int64_t>(per_sm) * sm_count());
-  const auto kern = k_sell<E, VI>;
+  const auto kern = k_sell<E, VI, T>;
   AGG_LAUNCH(kern, static_cast<unsigned>(grid), 256, 0, A.rowptr.get(), A.sell_ptr.get(),
              A.sell_col.get(), A.sell_val.get(), A.sell_code.get(), A.sell_pcol.get(), A.sell_tab.get(),
-             A.sell_perm.size() ? A.sell_perm.get() : nullptr, a.row_base, nrows, a, reduce_partials(),
-             reduce_ticket());
+             A.sell_perm.size() ? A.sell_perm.get() : nullptr, A.sell_len.get(), a.row_base, nrows, a,
+             reduce_partials(), reduce_ticket());
+}
+
+#ifdef AGGMG_SELL_SWEEP
+// tuning build: AGGMG_SELL_TUNE=<variant> runs every SELL launch with that variant
+template <Epi E, bool VI, int T = 0>
+void launch_sell_sweep(const DevCsr& A, const SpmvArgs& a, int t) {
+  if constexpr (T < kSellTuneCount) {
+    if (t == T)
+      launch_sell_t<E, VI, T>(A, a);
+    else
+      launch_sell_sweep<E, VI, T + 1>(A, a, t);
+  }
+}
+int sell_sweep_variant() {
+  static const int t = [] {
+    const char* e = std::getenv("AGGMG_SELL_TUNE");
+    return e ? std::atoi(e) : -1;
+  }();
+  return t;
+}
+#endif
+
+template <Epi E, bool VI>
+void launch_sell_v(const DevCsr& A, const SpmvArgs& a) {
+#ifdef AGGMG_SELL_SWEEP
+  if (sell_sweep_variant() >= 0) {
+    launch_sell_sweep<E, VI>(A, a, sell_sweep_variant());
+    return;
+  }
+#endif
+  if (A.sell_short)
+    launch_sell_t<E, VI, sell_tune(E, VI, true)>(A, a);
+  else
+    launch_sell_t<E, VI, sell_tune(E, VI, false)>(A, a);
 }
 
 template <Epi E>
 void launch_sell(const DevCsr& A, const SpmvArgs& a) {
   if (A.sell_vi)
-    launch_sell_t<E, true>(A, a);
+    launch_sell_v<E, true>(A, a);
   else
-    launch_sell_t<E, false>(A, a);
+    launch_sell_v<E, false>(A, a);
 }
 
 template <Epi E>

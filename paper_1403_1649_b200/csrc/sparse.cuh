@@ -43,6 +43,9 @@ struct DevCsr {
   DevBuf<unsigned char> sell_code;  // byte of slot k of row r: slice base + 32(k & ~3) + 4(r & 31) + (k & 3)
   DevBuf<double> sell_tab;
   DevBuf<idx> sell_pcol;  // the columns in sell_code's packing (int4 per 4 slots of a row)
+  // length of the row at position q (<= 64): the SELL kernels read it beside the slice base,
+  // so a row's column loads wait on no rowptr / perm round trip
+  DevBuf<unsigned char> sell_len;
 
   void plan();          // computes max_row / rows_per_block, builds the SELL copy (synchronises)
   int64_t sell_slots = 0;  // padded slot count of the SELL layout
