@@ -680,6 +680,189 @@ __global__ void __launch_bounds__(kGalWarps * 32)
   if (lane == 0) cnnz[I] = nd;
 }
 
+// Tier 1 without a length cap — warp per coarse row I, nothing per entry kept in shared
+// memory: pass A gathers J = assignment[acol[k]] for the row's entries (4 x 32 in flight per
+// lane group) and counts the distinct J in a per-warp hash table; the distinct J are ranked
+// into start offsets; pass B re-gathers the same entries (L1 / L2 hits) in gather order and
+// scatters them stably (match_any rank + the J's cursor).  The same output as k_gal_symbolic
+// for any L; rows with more than kGalMembersW members or kGalHashW / 2 distinct J go to tier 2.
+constexpr int kGalMembersW = 128;
+constexpr int kGalHashW = 256;
+constexpr int kGalU = 4;  // 32-entry groups whose loads are issued together
+__device__ __forceinline__ idx gal_member_of(const idx* moff, idx nm, idx p) {
+  idx lo = 0, hi = nm;  // the last member whose start is <= p
+  while (hi - lo > 1) {
+    const idx mid = (lo + hi) >> 1;
+    if (moff[mid] <= p)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+__global__ void __launch_bounds__(kGalWarps * 32)
+    k_gal_symbolic_w(const idx* goff, const idx* rows, const idx* arp, const idx* acol,
+                     const idx* assignment, int64_t nc, const idx* eoff, idx* entry, idx* entry_row,
+                     idx* sorted_j, idx* cnnz, idx* big_list, int* big_count) {
+  __shared__ idx s_moff[kGalWarps][kGalMembersW + 1], s_mlo[kGalWarps][kGalMembersW],
+      s_mrow[kGalWarps][kGalMembersW];
+  __shared__ idx s_hj[kGalWarps][kGalHashW], s_hc[kGalWarps][kGalHashW];
+  __shared__ idx s_ds[kGalWarps][kGalHashW / 2];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned kFull = 0xffffffffu;
+  const int64_t I = static_cast<int64_t>(blockIdx.x) * kGalWarps + w;
+  if (I >= nc) return;
+  const idx base_e = eoff[I];
+  const idx L = eoff[I + 1] - base_e;
+  const idx m0 = goff[I], nm = goff[I + 1] - m0;
+  if (nm > kGalMembersW) {
+    if (lane == 0) big_list[atomicAdd(big_count, 1)] = static_cast<idx>(I);
+    return;
+  }
+  idx* moff = s_moff[w];
+  idx* mlo = s_mlo[w];
+  idx* mrow = s_mrow[w];
+  idx* hj = s_hj[w];
+  idx* hc = s_hc[w];
+  for (int q = lane; q < kGalHashW; q += 32) {
+    hj[q] = -1;
+    hc[q] = 0;
+  }
+  idx run = 0;
+  for (idx mb = 0; mb < nm; mb += 32) {
+    const idx m = mb + lane;
+    idx len = 0;
+    if (m < nm) {
+      const idx i = rows[m0 + m];
+      const idx lo = arp[i];
+      len = arp[i + 1] - lo;
+      mlo[m] = lo;
+      mrow[m] = i;
+    }
+    idx incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const idx t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (m < nm) moff[m] = run + incl - len;
+    run += __shfl_sync(kFull, incl, 31);
+  }
+  __syncwarp();
+  // ---- A. distinct J and their counts ----
+  bool over = false;
+  for (idx pb = 0; pb < L; pb += 32 * kGalU) {
+    idx J[kGalU];
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) {
+      const idx p = pb + 32 * u + lane;
+      J[u] = -1;
+      if (p < L) {
+        const idx m = gal_member_of(moff, nm, p);
+        J[u] = acol[mlo[m] + (p - moff[m])];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u)
+      if (J[u] >= 0) J[u] = assignment[J[u]];
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) {
+      const idx Jv = pb + 32 * u + lane < L ? J[u] : -2 - lane;  // inactive lanes: unique keys
+      const unsigned peers = __match_any_sync(kFull, Jv);
+      if (Jv >= 0 && lane == __ffs(peers) - 1) {
+        unsigned h = (static_cast<unsigned>(Jv) * 2654435761u) & (kGalHashW - 1);
+        int probes = 0;
+        while (true) {
+          const idx old = atomicCAS(&hj[h], -1, Jv);
+          if (old == -1 || old == Jv) break;
+          h = (h + 1) & (kGalHashW - 1);
+          if (++probes == kGalHashW) break;
+        }
+        if (probes == kGalHashW)
+          over = true;
+        else
+          atomicAdd(&hc[h], static_cast<idx>(__popc(peers)));
+      }
+    }
+  }
+  __syncwarp();
+  // the occupied slots, compacted (at most kGalHashW / 2 distinct J: the load factor)
+  idx nd = 0;
+  idx* ds = s_ds[w];
+  for (int q0 = 0; q0 < kGalHashW; q0 += 32) {
+    const bool occ = hj[q0 + lane] != -1;
+    const unsigned bal = __ballot_sync(kFull, occ);
+    const idx at = nd + __popc(bal & ((1u << lane) - 1));
+    if (occ && at < kGalHashW / 2) ds[at] = q0 + lane;
+    nd += __popc(bal);
+  }
+  if (__any_sync(kFull, over) || nd > kGalHashW / 2) {
+    if (lane == 0) big_list[atomicAdd(big_count, 1)] = static_cast<idx>(I);
+    return;
+  }
+  __syncwarp();
+  // start of each distinct J = sum of the counts of the smaller J
+  idx start[kGalHashW / 64];
+#pragma unroll
+  for (int r = 0; r < kGalHashW / 64; ++r) {
+    const idx d = lane + 32 * r;
+    start[r] = 0;
+    if (d < nd) {
+      const idx J = hj[ds[d]];
+      for (idx e = 0; e < nd; ++e) {
+        const idx se = ds[e];
+        start[r] += hj[se] < J ? hc[se] : 0;
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < kGalHashW / 64; ++r)  // counts -> cursors
+    if (lane + 32 * r < nd) hc[ds[lane + 32 * r]] = start[r];
+  __syncwarp();
+  // ---- B. stable scatter in gather order ----
+  for (idx pb = 0; pb < L; pb += 32 * kGalU) {
+    idx K[kGalU], R[kGalU], J[kGalU];
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) {
+      const idx p = pb + 32 * u + lane;
+      K[u] = -1;
+      R[u] = 0;
+      if (p < L) {
+        const idx m = gal_member_of(moff, nm, p);
+        K[u] = mlo[m] + (p - moff[m]);
+        R[u] = mrow[m];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) J[u] = K[u] >= 0 ? acol[K[u]] : -1;
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u)
+      if (K[u] >= 0) J[u] = assignment[J[u]];
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) {
+      if (pb + 32 * u >= L) break;  // warp-uniform
+      const bool act = K[u] >= 0;
+      const idx Jv = act ? J[u] : -2 - lane;
+      unsigned h = (static_cast<unsigned>(Jv) * 2654435761u) & (kGalHashW - 1);
+      if (act)
+        while (hj[h] != Jv) h = (h + 1) & (kGalHashW - 1);
+      const unsigned peers = __match_any_sync(kFull, Jv);
+      const idx cur = act ? hc[h] : 0;
+      const idx slot = cur + __popc(peers & ((1u << lane) - 1));
+      if (act) {
+        entry[base_e + slot] = K[u];
+        entry_row[base_e + slot] = R[u];
+        sorted_j[base_e + slot] = Jv;
+      }
+      __syncwarp();
+      if (act && lane == __ffs(peers) - 1) hc[h] = cur + __popc(peers);
+      __syncwarp();
+    }
+  }
+  if (lane == 0) cnnz[I] = nd;
+}
+
 // Tier 2 — one CTA (256 threads) per long coarse row (L > kGalCap gathered entries).
 // Per-entry slots (J, k, row, hash slot, scratch) live in shared memory when L <= cap (the
 // launch's largest L, at most kGalCapBig), else in global scratch at [base_e, base_e + L).
@@ -1506,11 +1689,18 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
                agg.rows_by_coarse.get(), A.rowptr.get(), nc, ecnt.get());
   const int64_t total = scan_to_offsets(ecnt.get(), eoff.get(), nc);
   require(partial || total == A.nnz, "galerkin: aggregation does not cover the matrix rows");
+  // AGGMG_GAL_TIER1=1: the length-capped tier 1 (comparison runs)
+  static const bool capped_tier1 = [] {
+    const char* e = std::getenv("AGGMG_GAL_TIER1");
+    return e && e[0] == '1';
+  }();
+  const auto tier1 = capped_tier1 ? k_gal_symbolic : k_gal_symbolic_w;
   if (nc > 0)
-    AGG_LAUNCH(k_gal_symbolic, static_cast<unsigned>((nc + kGalWarps - 1) / kGalWarps),
-               kGalWarps * 32, 0, agg.agg_row_offsets.get(), agg.rows_by_coarse.get(),
-               A.rowptr.get(), A.col.get(), agg.assignment.get(), nc, eoff.get(), g.entry.get(),
-               g.entry_row.get(), sorted_j.get(), cnnz.get(), big_list.get(), big_count.get());
+    AGG_LAUNCH(tier1,
+               static_cast<unsigned>((nc + kGalWarps - 1) / kGalWarps), kGalWarps * 32, 0,
+               agg.agg_row_offsets.get(), agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(),
+               agg.assignment.get(), nc, eoff.get(), g.entry.get(), g.entry_row.get(),
+               sorted_j.get(), cnnz.get(), big_list.get(), big_count.get());
   const int nbig = read_scalar(big_count.get());
   if (nbig > 0) {
     DevBuf<int> maxlen(1);

@@ -273,8 +273,17 @@ void DevCsr::plan() {
   // halo); not the restriction (n_c x n)
   // (slot offsets are int32: every slice padded to the longest row must stay below 2^31)
   const bool fits = ((n_rows + 31) / 32) * 32 * static_cast<int64_t>(max_row) < INT32_MAX;
-  if (sell_on && fits && n_cols >= n_rows && n_cols <= n_rows + n_rows / 2 &&
-      mean >= sell_min_mean && n_rows >= (int64_t{1} << 19) && max_row <= 64) {
+  // AGGMG_SELL_MIN_ROWS / AGGMG_SELL_RECT=1 (restrictions too): tuning experiments
+  static const int64_t sell_min_rows = [] {
+    const char* e = std::getenv("AGGMG_SELL_MIN_ROWS");
+    return e ? std::atoll(e) : (int64_t{1} << 19);
+  }();
+  static const bool sell_rect = [] {
+    const char* e = std::getenv("AGGMG_SELL_RECT");
+    return e && e[0] == '1';
+  }();
+  const bool shape_ok = sell_rect || (n_cols >= n_rows && n_cols <= n_rows + n_rows / 2);
+  if (sell_on && fits && shape_ok && mean >= sell_min_mean && n_rows >= sell_min_rows && max_row <= 64) {
     const int64_t ns = (n_rows + 31) / 32;
     DevBuf<idx> w(ns);
     DevBuf<unsigned long long> dslots;

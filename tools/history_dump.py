@@ -31,7 +31,11 @@ hist = np.zeros(600)
 x = np.zeros(n ** 3)
 for step in range(3):
     h = C.c_void_p()
+    lib.fn("synchronize")()
+    ts = time.perf_counter()
     assert lib.fn("setup_hierarchy_device")(dm, C.byref(s), C.byref(h)) == 0
+    lib.fn("synchronize")()
+    setup_ms = 1e3 * (time.perf_counter() - ts)
     rep = _abi.SolveReportC()
     rep.history = hist.ctypes.data_as(_abi.f64p)
     rep.history_capacity = 600
@@ -43,5 +47,5 @@ for step in range(3):
     dt = time.perf_counter() - t0
     lib.fn("hierarchy_free")(h)
 hh = hist[: rep.history_length]
-print(f"its={rep.iterations} solve_ms={1e3 * dt:.2f} history_sha={hashlib.sha256(hh.tobytes()).hexdigest()[:16]} "
+print(f"its={rep.iterations} setup_ms={setup_ms:.2f} solve_ms={1e3 * dt:.2f} history_sha={hashlib.sha256(hh.tobytes()).hexdigest()[:16]} "
       f"x_sha={hashlib.sha256(x.tobytes()).hexdigest()[:16]}")
