@@ -15,21 +15,31 @@ namespace aggmg_b200 {
 constexpr int64_t kDenseSolveCap = 5000;  // hierarchy.cpp:23
 
 namespace {
-// AGGMG_SETUP_TIMING=1: per-phase GPU-synchronised wall time of setup_hierarchy (stderr)
+// AGGMG_SETUP_TIMING=1: per-phase GPU-synchronised wall time of setup_hierarchy (stderr);
+// =2: no synchronisation — an event per phase boundary on the stream (the overlapped run's
+// own critical path) beside the host's issue time of the boundary
 struct SetupTimer {
-  bool on = false;
-  std::chrono::steady_clock::time_point t;
+  int mode = 0;
+  std::chrono::steady_clock::time_point t, t0;
   std::vector<std::pair<std::string, double>> acc;
+  std::vector<std::tuple<std::string, cudaEvent_t, double>> ev;
   SetupTimer() {
     const char* e = std::getenv("AGGMG_SETUP_TIMING");
-    on = e && e[0] == '1';
-    if (on) {
-      sync();
-      t = std::chrono::steady_clock::now();
-    }
+    mode = e ? std::atoi(e) : 0;
+    if (mode == 1) sync();
+    t = t0 = std::chrono::steady_clock::now();
+    if (mode == 2) push("start");
+  }
+  void push(const std::string& name) {
+    cudaEvent_t x;
+    AGG_CUDA(cudaEventCreate(&x));
+    AGG_CUDA(cudaEventRecord(x, stream()));
+    ev.emplace_back(name, x,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
   void mark(const std::string& name) {
-    if (!on) return;
+    if (mode == 2) push(name);
+    if (mode != 1) return;
     sync();
     const auto now = std::chrono::steady_clock::now();
     const double ms = std::chrono::duration<double, std::milli>(now - t).count();
@@ -42,8 +52,17 @@ struct SetupTimer {
     acc.emplace_back(name, ms);
   }
   ~SetupTimer() {
-    if (!on) return;
     for (auto& a : acc) std::fprintf(stderr, "[setup] %-14s %8.3f ms\n", a.first.c_str(), a.second);
+    if (mode != 2 || ev.empty()) return;
+    sync();
+    for (size_t k = 1; k < ev.size(); ++k) {
+      float ms = 0.f, at = 0.f;
+      cudaEventElapsedTime(&ms, std::get<1>(ev[k - 1]), std::get<1>(ev[k]));
+      cudaEventElapsedTime(&at, std::get<1>(ev[0]), std::get<1>(ev[k]));
+      std::fprintf(stderr, "[setup-ev] %-14s gpu %8.3f ms (ends at %8.3f)  host issued at %8.3f\n",
+                   std::get<0>(ev[k]).c_str(), ms, at, std::get<2>(ev[k]));
+    }
+    for (auto& e : ev) cudaEventDestroy(std::get<1>(e));
   }
 };
 }  // namespace
@@ -140,7 +159,7 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     st.mark(lv + "transfer");
     DevCsrPtr Ac;
     if (cfg.reuse_caches) {  // hierarchy.cpp:69-71: cached sort / segmented reduce
-      fine.gal = build_galerkin_cache(A, agg, false, false);
+      fine.gal = build_galerkin_cache(A, agg, false, false, true);
       Ac = apply_galerkin_cache(fine.gal, A, fine.tr.pval.get());
     } else {  // hierarchy.cpp:73: galerkin_direct, the reference default
       Ac = galerkin_direct(A, agg, fine.tr.pval.get());
@@ -298,6 +317,7 @@ std::unique_ptr<DevHierarchy> clone_hierarchy(const DevHierarchy& h) {
     d.gal.group_rows.copy_from(s.gal.group_rows);
     d.gal.max_coarse_row = s.gal.max_coarse_row;
     d.gal.pattern_hash = s.gal.pattern_hash;
+    d.gal.lean = s.gal.lean;
   }
   sync();
   return c;

@@ -22,6 +22,8 @@ struct Context {
   int sms = 148;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // halo exchanges that overlap interior rows (dist path)
+  cudaStream_t background = nullptr;  // lowest priority: setup's Arnoldi chains under the coarsening
+  int prio_main = 0, prio_side = 0;
   double* pinned = nullptr;
   int pinned_n = 0;
   // pinned staging ring for large host <-> device copies
@@ -34,6 +36,7 @@ struct Context {
     if (!ready) return;
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
+    if (background) cudaStreamDestroy(background);
     if (pinned) cudaFreeHost(pinned);
     for (int b = 0; b < kStages; ++b) {
       if (stage[b]) cudaFreeHost(stage[b]);
@@ -116,7 +119,18 @@ void init_device(int device) {
     throw CudaError(std::string("aggmg_b200 is built for sm_100a; found ") + prop.name);
   c.device = device;
   c.sms = prop.multiProcessorCount;
-  AGG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  // the main stream at the highest priority, the side stream (setup's Arnoldi chains) at the
+  // lowest: the block scheduler then hands freed SMs to the coarsening first
+  // (AGGMG_STREAM_PRIO=0: both at the default priority)
+  static const bool prio = [] {
+    const char* e = std::getenv("AGGMG_STREAM_PRIO");
+    return !(e && e[0] == '0');
+  }();
+  int least = 0, greatest = 0;
+  AGG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  c.prio_main = prio ? greatest : 0;
+  c.prio_side = prio ? least : 0;
+  AGG_CUDA(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, c.prio_main));
   cudaMemPool_t pool;
   AGG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t threshold = UINT64_MAX;  // keep freed blocks cached: setup reallocates per level
@@ -159,6 +173,13 @@ cudaStream_t side_stream() {
   Context& c = ctx();
   if (!c.side) AGG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
   return c.side;
+}
+cudaStream_t background_stream() {
+  ensure_init();
+  Context& c = ctx();
+  if (!c.background)
+    AGG_CUDA(cudaStreamCreateWithPriority(&c.background, cudaStreamNonBlocking, c.prio_side));
+  return c.background;
 }
 int current_device() {
   ensure_init();

@@ -37,6 +37,7 @@ inline void mark_device(std::atomic<unsigned long long>& seen) {
   seen.fetch_or(1ull << (current_device() & 63));
 }
 cudaStream_t side_stream();  // a second stream of the calling thread (overlapped exchanges)
+cudaStream_t background_stream();  // a low-priority stream of the calling thread (setup overlap)
 // While alive, the calling thread's kernels and stream-ordered allocations go to `s` instead
 // of its main stream (work that overlaps the main stream, e.g. the smoother's Arnoldi chains
 // during setup).  Allocations made inside bypass the per-thread block cache, whose reuse rule

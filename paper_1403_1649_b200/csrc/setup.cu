@@ -863,6 +863,174 @@ __global__ void __launch_bounds__(kGalWarps * 32)
   if (lane == 0) cnnz[I] = nd;
 }
 
+// Lean cache (a hierarchy's own setup): only what the numeric reduce and refresh_values read —
+// coarse pattern and slot_of_csr — without the per-entry sorted arrays (entry, entry_row,
+// segment_offsets: the standalone cache API builds those).  Two warp-per-coarse-row passes:
+//  count: the distinct J of the row, sorted (rank = number of smaller J), into the row's
+//         scratch range and its length into cnnz;
+//  fill:  after the scan, the coarse columns and every fine entry's slot (crp[I] + rank of J).
+// A row with more than kGalMembersW members or kLeanSlots distinct J sets *bad (the full path
+// then runs instead).
+constexpr int kLeanSlots = 64;   // = the row-walk numeric reduce's slots
+constexpr int kLeanHash = 128;
+__device__ __forceinline__ void gal_members(const idx* goff, const idx* rows, const idx* arp, int64_t I,
+                                            int lane, idx* moff, idx* mlo, idx& nm_out) {
+  const idx m0 = goff[I], nm = goff[I + 1] - m0;
+  idx run = 0;
+  for (idx mb = 0; mb < nm; mb += 32) {
+    const idx m = mb + lane;
+    idx len = 0;
+    if (m < nm) {
+      const idx i = rows[m0 + m];
+      const idx lo = arp[i];
+      len = arp[i + 1] - lo;
+      mlo[m] = lo;
+    }
+    idx incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const idx t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (m < nm) moff[m] = run + incl - len;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  nm_out = nm;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kGalWarps * 32)
+    k_gal_lean_count(const idx* goff, const idx* rows, const idx* arp, const idx* acol,
+                     const idx* assignment, int64_t nc, const idx* eoff, idx* tmpj, idx* cnnz, int* bad) {
+  __shared__ idx s_moff[kGalWarps][kGalMembersW], s_mlo[kGalWarps][kGalMembersW];
+  __shared__ idx s_hj[kGalWarps][kLeanHash], s_dj[kGalWarps][kLeanSlots];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned kFull = 0xffffffffu;
+  const int64_t I = static_cast<int64_t>(blockIdx.x) * kGalWarps + w;
+  if (I >= nc) return;
+  if (goff[I + 1] - goff[I] > kGalMembersW) {
+    if (lane == 0) *bad = 1;
+    return;
+  }
+  const idx base_e = eoff[I], L = eoff[I + 1] - base_e;
+  idx* moff = s_moff[w];
+  idx* mlo = s_mlo[w];
+  idx* hj = s_hj[w];
+  for (int q = lane; q < kLeanHash; q += 32) hj[q] = -1;
+  idx nm;
+  gal_members(goff, rows, arp, I, lane, moff, mlo, nm);
+  bool over = false;
+  for (idx pb = 0; pb < L; pb += 32 * kGalU) {
+    idx J[kGalU];
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) {
+      const idx p = pb + 32 * u + lane;
+      J[u] = -1;
+      if (p < L) {
+        const idx m = gal_member_of(moff, nm, p);
+        J[u] = acol[mlo[m] + (p - moff[m])];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u)
+      if (J[u] >= 0) J[u] = assignment[J[u]];
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) {
+      const idx Jv = pb + 32 * u + lane < L ? J[u] : -2 - lane;
+      const unsigned peers = __match_any_sync(kFull, Jv);
+      if (Jv >= 0 && lane == __ffs(peers) - 1) {
+        unsigned h = (static_cast<unsigned>(Jv) * 2654435761u) & (kLeanHash - 1);
+        int probes = 0;
+        while (true) {
+          const idx old = atomicCAS(&hj[h], -1, Jv);
+          if (old == -1 || old == Jv) break;
+          h = (h + 1) & (kLeanHash - 1);
+          if (++probes == kLeanHash) {
+            over = true;
+            break;
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // the distinct J compacted; rank = number of smaller distinct J
+  idx* dj = s_dj[w];
+  idx nd = 0;
+#pragma unroll
+  for (int r = 0; r < kLeanHash / 32; ++r) {
+    const idx J = hj[lane + 32 * r];
+    const unsigned bal = __ballot_sync(kFull, J != -1);
+    const idx at = nd + __popc(bal & ((1u << lane) - 1));
+    if (J != -1 && at < kLeanSlots) dj[at] = J;
+    nd += __popc(bal);
+  }
+  if (__any_sync(kFull, over) || nd > kLeanSlots) {
+    if (lane == 0) *bad = 1;
+    return;
+  }
+  __syncwarp();
+  for (idx d = lane; d < nd; d += 32) {
+    const idx J = dj[d];
+    idx rank = 0;
+    for (idx e = 0; e < nd; ++e) rank += dj[e] < J ? 1 : 0;
+    tmpj[base_e + rank] = J;
+  }
+  if (lane == 0) cnnz[I] = nd;
+}
+
+__global__ void __launch_bounds__(kGalWarps * 32)
+    k_gal_lean_fill(const idx* goff, const idx* rows, const idx* arp, const idx* acol,
+                    const idx* assignment, int64_t nc, const idx* eoff, const idx* tmpj, const idx* crp,
+                    idx* ccol, idx* slot_of_csr) {
+  __shared__ idx s_moff[kGalWarps][kGalMembersW], s_mlo[kGalWarps][kGalMembersW];
+  __shared__ idx s_hj[kGalWarps][kLeanHash], s_hr[kGalWarps][kLeanHash];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t I = static_cast<int64_t>(blockIdx.x) * kGalWarps + w;
+  if (I >= nc) return;
+  const idx base_e = eoff[I], L = eoff[I + 1] - base_e;
+  const idx c0 = crp[I], nd = crp[I + 1] - c0;
+  idx* moff = s_moff[w];
+  idx* mlo = s_mlo[w];
+  idx* hj = s_hj[w];
+  idx* hr = s_hr[w];
+  for (int q = lane; q < kLeanHash; q += 32) hj[q] = -1;
+  __syncwarp();
+  for (idx r = lane; r < nd; r += 32) {  // J -> rank (distinct J: plain inserts)
+    const idx J = tmpj[base_e + r];
+    ccol[c0 + r] = J;
+    unsigned h = (static_cast<unsigned>(J) * 2654435761u) & (kLeanHash - 1);
+    while (atomicCAS(&hj[h], -1, J) != -1) h = (h + 1) & (kLeanHash - 1);
+    hr[h] = r;
+  }
+  idx nm;
+  gal_members(goff, rows, arp, I, lane, moff, mlo, nm);
+  for (idx pb = 0; pb < L; pb += 32 * kGalU) {
+    idx K[kGalU], J[kGalU];
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) {
+      const idx p = pb + 32 * u + lane;
+      K[u] = -1;
+      if (p < L) {
+        const idx m = gal_member_of(moff, nm, p);
+        K[u] = mlo[m] + (p - moff[m]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) J[u] = K[u] >= 0 ? acol[K[u]] : 0;
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u)
+      if (K[u] >= 0) J[u] = assignment[J[u]];
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) {
+      if (K[u] < 0) continue;
+      unsigned h = (static_cast<unsigned>(J[u]) * 2654435761u) & (kLeanHash - 1);
+      while (hj[h] != J[u]) h = (h + 1) & (kLeanHash - 1);
+      slot_of_csr[K[u]] = c0 + hr[h];
+    }
+  }
+}
+
 // Tier 2 — one CTA (256 threads) per long coarse row (L > kGalCap gathered entries).
 // Per-entry slots (J, k, row, hash slot, scratch) live in shared memory when L <= cap (the
 // launch's largest L, at most kGalCapBig), else in global scratch at [base_e, base_e + L).
@@ -1670,7 +1838,28 @@ TransferDev build_transfer(const AggDev& agg, const double* fine_b) {
   return t;
 }
 
-GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial, bool fingerprint) {
+namespace {
+// the coarse-row walk's inputs shared by both cache builds: grouping copies and the longest row
+void finish_cache(GalerkinDev& g, const DevCsr& A, const AggDev& agg) {
+  const int64_t nc = g.n_coarse;
+  g.group_offsets.resize(nc + 1);
+  AGG_CUDA(cudaMemcpyAsync(g.group_offsets.get(), agg.agg_row_offsets.get(), sizeof(idx) * (nc + 1),
+                           cudaMemcpyDeviceToDevice, stream()));
+  g.group_rows.resize(A.n_rows);
+  if (A.n_rows > 0)
+    AGG_CUDA(cudaMemcpyAsync(g.group_rows.get(), agg.rows_by_coarse.get(), sizeof(idx) * A.n_rows,
+                             cudaMemcpyDeviceToDevice, stream()));
+  DevBuf<int> mr(1);
+  mr.zero();
+  if (nc > 0)
+    AGG_LAUNCH(k_max_rowlen, grid_for(nc, 256, 4 * sm_count()), 256, 0, g.coarse_rowptr.get(), nc,
+               mr.get());
+  g.max_coarse_row = read_scalar(mr.get());
+}
+}  // namespace
+
+GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial, bool fingerprint,
+                                 bool lean) {
   require(partial || A.n_rows == A.n_cols, "galerkin: matrix must be square");
   require(agg.n_fine == A.n_rows, "galerkin: aggregation size mismatch");
   const int64_t nc = agg.n_agg;
@@ -1678,10 +1867,8 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
   g.n_fine = A.n_rows;
   g.n_coarse = nc;
   g.nnz_fine = A.nnz;
-  g.entry.resize(A.nnz);
-  g.entry_row.resize(A.nnz);
   g.slot_of_csr.resize(A.nnz);
-  DevBuf<idx> ecnt(nc), eoff(nc + 1), sorted_j(A.nnz), cnnz(nc), big_list(nc > 0 ? nc : 1);
+  DevBuf<idx> ecnt(nc), eoff(nc + 1), cnnz(nc);
   DevBuf<int> big_count(1);
   big_count.zero();
   if (nc > 0)
@@ -1689,6 +1876,36 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
                agg.rows_by_coarse.get(), A.rowptr.get(), nc, ecnt.get());
   const int64_t total = scan_to_offsets(ecnt.get(), eoff.get(), nc);
   require(partial || total == A.nnz, "galerkin: aggregation does not cover the matrix rows");
+  // AGGMG_GAL_LEAN=0: the full cache in a hierarchy too (comparison runs)
+  static const bool lean_on = [] {
+    const char* e = std::getenv("AGGMG_GAL_LEAN");
+    return !(e && e[0] == '0');
+  }();
+  if (lean && lean_on && !partial && nc > 0) {
+    DevBuf<idx> tmpj(A.nnz);
+    DevBuf<int> bad(1);
+    bad.zero();
+    const unsigned grid = static_cast<unsigned>((nc + kGalWarps - 1) / kGalWarps);
+    AGG_LAUNCH(k_gal_lean_count, grid, kGalWarps * 32, 0, agg.agg_row_offsets.get(),
+               agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(), agg.assignment.get(), nc,
+               eoff.get(), tmpj.get(), cnnz.get(), bad.get());
+    if (read_scalar(bad.get()) == 0) {
+      g.lean = true;
+      g.coarse_rowptr.resize(nc + 1);
+      g.nnz_coarse = scan_to_offsets(cnnz.get(), g.coarse_rowptr.get(), nc);
+      g.coarse_col.resize(g.nnz_coarse);
+      AGG_LAUNCH(k_gal_lean_fill, grid, kGalWarps * 32, 0, agg.agg_row_offsets.get(),
+                 agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(), agg.assignment.get(), nc,
+                 eoff.get(), tmpj.get(), g.coarse_rowptr.get(), g.coarse_col.get(), g.slot_of_csr.get());
+      finish_cache(g, A, agg);
+      if (fingerprint) g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
+      sync();  // tmpj dies here
+      return g;
+    }
+  }
+  g.entry.resize(A.nnz);
+  g.entry_row.resize(A.nnz);
+  DevBuf<idx> sorted_j(A.nnz), big_list(nc > 0 ? nc : 1);
   // AGGMG_GAL_TIER1=1: the length-capped tier 1 (comparison runs)
   static const bool capped_tier1 = [] {
     const char* e = std::getenv("AGGMG_GAL_TIER1");
@@ -1749,21 +1966,7 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
   AGG_CUDA(cudaMemcpyAsync(g.segment_offsets.get() + g.nnz_coarse, &nnz32, sizeof(idx),
                            cudaMemcpyHostToDevice, stream()));
   sync();  // nnz32 lives on the host stack
-  if (!partial) {
-    g.group_offsets.resize(nc + 1);
-    AGG_CUDA(cudaMemcpyAsync(g.group_offsets.get(), agg.agg_row_offsets.get(), sizeof(idx) * (nc + 1),
-                             cudaMemcpyDeviceToDevice, stream()));
-    g.group_rows.resize(A.n_rows);
-    if (A.n_rows > 0)
-      AGG_CUDA(cudaMemcpyAsync(g.group_rows.get(), agg.rows_by_coarse.get(), sizeof(idx) * A.n_rows,
-                               cudaMemcpyDeviceToDevice, stream()));
-    DevBuf<int> mr(1);
-    mr.zero();
-    if (nc > 0)
-      AGG_LAUNCH(k_max_rowlen, grid_for(nc, 256, 4 * sm_count()), 256, 0, g.coarse_rowptr.get(), nc,
-                 mr.get());
-    g.max_coarse_row = read_scalar(mr.get());
-  }
+  if (!partial) finish_cache(g, A, agg);
   if (!partial && fingerprint) g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
   return g;
 }
@@ -1780,6 +1983,7 @@ DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const doub
   if (g.nnz_coarse > 0) {
     AGG_CUDA(cudaMemcpyAsync(Ac->col.get(), g.coarse_col.get(), sizeof(idx) * g.nnz_coarse,
                              cudaMemcpyDeviceToDevice, stream()));
+    require(!g.lean || g.max_coarse_row <= kWalkSlots, "galerkin: lean cache beyond the row walk");
     if (g.group_offsets.size() == g.n_coarse + 1 && g.max_coarse_row <= kWalkSlots)
       AGG_LAUNCH(k_gal_numeric_walk, static_cast<unsigned>((g.n_coarse + kWalkWarps - 1) / kWalkWarps),
                  kWalkWarps * 32, 0, g.n_coarse, g.group_offsets.get(), g.group_rows.get(),

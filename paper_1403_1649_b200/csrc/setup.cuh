@@ -59,13 +59,16 @@ struct GalerkinDev {
                                           // caches): the row-walk numeric reduce
   int max_coarse_row = 0;
   uint64_t pattern_hash = 0;
+  bool lean = false;  // entry / entry_row / segment_offsets not built (max_coarse_row <= 64)
 };
 // partial: the groups cover only some rows of A (rows of other groups, and halo rows, are
 // skipped; the row-partitioned setup's extended row set) — no coverage check, no fingerprint.
 // fingerprint: the pattern hash apply_galerkin_cache checks for a caller-supplied A (galerkin.cpp:
 // 18-29, 101-103); a hierarchy applies its cache to its own stored operator and skips it.
+// lean: a hierarchy's own cache — only the coarse pattern and slot_of_csr when every coarse row
+// fits the row-walk reduce (the per-entry sorted arrays are for the standalone cache API)
 GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial = false,
-                                 bool fingerprint = true);
+                                 bool fingerprint = true, bool lean = false);
 // Ac values for the cached pattern.  pval: per fine row P weight.
 DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const double* pval);
 uint64_t pattern_fingerprint(const DevCsr& A, const idx* assignment);

@@ -243,7 +243,7 @@ struct SmootherBatch::Job {
 SmootherBatch::SmootherBatch() = default;
 
 SmootherBatch::~SmootherBatch() {
-  if (!jobs_.empty()) cudaStreamSynchronize(side_stream());  // buffers die after the chains
+  if (!jobs_.empty()) cudaStreamSynchronize(background_stream());  // buffers die after the chains
 }
 
 void SmootherBatch::add(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed, SmootherDev& s,
@@ -284,7 +284,7 @@ void SmootherBatch::add(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed,
   cudaEvent_t ready;
   AGG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   AGG_CUDA(cudaEventRecord(ready, stream()));  // A, inv_diag and the buffers are ready
-  cudaStream_t side = side_stream();
+  cudaStream_t side = background_stream();
   AGG_CUDA(cudaStreamWaitEvent(side, ready, 0));
   cudaEventDestroy(ready);
   {
@@ -332,7 +332,7 @@ void SmootherBatch::add(const DevCsr& A, int kind, int arnoldi_m, uint64_t seed,
 
 void SmootherBatch::finish(const std::function<SmootherDev&(int)>& level) {
   if (jobs_.empty()) return;
-  AGG_CUDA(cudaStreamSynchronize(side_stream()));
+  AGG_CUDA(cudaStreamSynchronize(background_stream()));
   auto jobs = std::move(jobs_);
   for (auto& j : jobs) {
     const int m = j->m;

@@ -141,11 +141,10 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
   };
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t start = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  int iter = 0;
   // warp-uniform trip count, so every lane reaches the flag check; four values in flight
   constexpr int kU = 4;
   for (int64_t base = start - (threadIdx.x & 31); base < nnz; base += kU * stride) {
-    if ((++iter & 3) == 0 && __shfl_sync(0xffffffffu, *bad, 0)) return;  // > 256 patterns
+    if (__shfl_sync(0xffffffffu, *bad, 0)) return;  // > 256 patterns
     unsigned long long uu[kU];
     unsigned in = 0;
 #pragma unroll
@@ -162,9 +161,12 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
         give_up();
         continue;
       }
+      // the CTA's copy is only a cache: short probe runs (a non-dictionary operator fills it
+      // before the give-up is seen, and full-table probes would then cost O(slots) per value)
+      constexpr int kLocalProbes = 8;
       unsigned h = dict_hash(u);
       bool known = false;
-      for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+      for (int probe = 0; probe < kLocalProbes; ++probe, h = (h + 1) & (kDictSlots - 1)) {
         const unsigned long long cur = seen[h];
         if (cur == u) {
           known = true;
@@ -187,10 +189,11 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
           if (atomicAdd(state, 1) >= kDictMax) give_up();
           break;
         }
+        if (*bad) break;  // already lost: stop probing
         if (old == u) break;
       }
       h = dict_hash(u);
-      for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+      for (int probe = 0; probe < kLocalProbes; ++probe, h = (h + 1) & (kDictSlots - 1)) {
         const unsigned long long old = atomicCAS(seen + h, kDictEmpty, u);
         if (old == kDictEmpty || old == u) break;
       }
