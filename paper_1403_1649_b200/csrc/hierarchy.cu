@@ -159,8 +159,10 @@ std::unique_ptr<DevHierarchy> setup_hierarchy(DevCsrPtr A0, const double* B0_dev
     st.mark(lv + "transfer");
     DevCsrPtr Ac;
     if (cfg.reuse_caches) {  // hierarchy.cpp:69-71: cached sort / segmented reduce
-      fine.gal = build_galerkin_cache(A, agg, false, false, true);
-      Ac = apply_galerkin_cache(fine.gal, A, fine.tr.pval.get());
+      DevBuf<double> vals;
+      fine.gal = build_galerkin_cache(A, agg, false, false, true, fine.tr.pval.get(), &vals);
+      Ac = fine.gal.lean ? coarse_from_cache(fine.gal, std::move(vals))
+                         : apply_galerkin_cache(fine.gal, A, fine.tr.pval.get());
     } else {  // hierarchy.cpp:73: galerkin_direct, the reference default
       Ac = galerkin_direct(A, agg, fine.tr.pval.get());
     }

@@ -874,7 +874,8 @@ __global__ void __launch_bounds__(kGalWarps * 32)
 constexpr int kLeanSlots = 64;   // = the row-walk numeric reduce's slots
 constexpr int kLeanHash = 128;
 __device__ __forceinline__ void gal_members(const idx* goff, const idx* rows, const idx* arp, int64_t I,
-                                            int lane, idx* moff, idx* mlo, idx& nm_out) {
+                                            int lane, idx* moff, idx* mlo, idx& nm_out,
+                                            const double* pv = nullptr, double* mpv = nullptr) {
   const idx m0 = goff[I], nm = goff[I + 1] - m0;
   idx run = 0;
   for (idx mb = 0; mb < nm; mb += 32) {
@@ -885,6 +886,7 @@ __device__ __forceinline__ void gal_members(const idx* goff, const idx* rows, co
       const idx lo = arp[i];
       len = arp[i + 1] - lo;
       mlo[m] = lo;
+      if (mpv) mpv[m] = pv[i];
     }
     idx incl = len;
 #pragma unroll
@@ -982,9 +984,12 @@ __global__ void __launch_bounds__(kGalWarps * 32)
 __global__ void __launch_bounds__(kGalWarps * 32)
     k_gal_lean_fill(const idx* goff, const idx* rows, const idx* arp, const idx* acol,
                     const idx* assignment, int64_t nc, const idx* eoff, const idx* tmpj, const idx* crp,
-                    idx* ccol, idx* slot_of_csr) {
+                    idx* ccol, idx* slot_of_csr, const double* aval, const double* pv, double* out) {
+  // with pv / out: also Ac = the row-walk numeric reduce (k_gal_numeric_walk's sums: products
+  // added into their slot in gather order, equal-slot lanes of a round lowest lane first)
   __shared__ idx s_moff[kGalWarps][kGalMembersW], s_mlo[kGalWarps][kGalMembersW];
   __shared__ idx s_hj[kGalWarps][kLeanHash], s_hr[kGalWarps][kLeanHash];
+  __shared__ double s_mpv[kGalWarps][kGalMembersW], s_acc[kGalWarps][kLeanSlots];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t I = static_cast<int64_t>(blockIdx.x) * kGalWarps + w;
   if (I >= nc) return;
@@ -1003,31 +1008,61 @@ __global__ void __launch_bounds__(kGalWarps * 32)
     while (atomicCAS(&hj[h], -1, J) != -1) h = (h + 1) & (kLeanHash - 1);
     hr[h] = r;
   }
+  const bool num = out != nullptr;
+  double* mpv = s_mpv[w];
+  double* acc = s_acc[w];
+  if (num)
+    for (int q = lane; q < kLeanSlots; q += 32) acc[q] = 0.0;
   idx nm;
-  gal_members(goff, rows, arp, I, lane, moff, mlo, nm);
+  gal_members(goff, rows, arp, I, lane, moff, mlo, nm, pv, num ? mpv : nullptr);
   for (idx pb = 0; pb < L; pb += 32 * kGalU) {
-    idx K[kGalU], J[kGalU];
+    idx K[kGalU], J[kGalU], C[kGalU];
+    double pm[kGalU];
 #pragma unroll
     for (int u = 0; u < kGalU; ++u) {
       const idx p = pb + 32 * u + lane;
       K[u] = -1;
+      pm[u] = 0.0;
       if (p < L) {
         const idx m = gal_member_of(moff, nm, p);
         K[u] = mlo[m] + (p - moff[m]);
+        if (num) pm[u] = mpv[m];
       }
     }
 #pragma unroll
-    for (int u = 0; u < kGalU; ++u) J[u] = K[u] >= 0 ? acol[K[u]] : 0;
-#pragma unroll
-    for (int u = 0; u < kGalU; ++u)
-      if (K[u] >= 0) J[u] = assignment[J[u]];
+    for (int u = 0; u < kGalU; ++u) C[u] = K[u] >= 0 ? acol[K[u]] : 0;
+    double c[kGalU];
 #pragma unroll
     for (int u = 0; u < kGalU; ++u) {
-      if (K[u] < 0) continue;
-      unsigned h = (static_cast<unsigned>(J[u]) * 2654435761u) & (kLeanHash - 1);
-      while (hj[h] != J[u]) h = (h + 1) & (kLeanHash - 1);
-      slot_of_csr[K[u]] = c0 + hr[h];
+      J[u] = K[u] >= 0 ? assignment[C[u]] : 0;
+      c[u] = (num && K[u] >= 0) ? __dmul_rn(__dmul_rn(pm[u], aval[K[u]]), pv[C[u]]) : 0.0;
     }
+#pragma unroll
+    for (int u = 0; u < kGalU; ++u) {
+      if (pb + 32 * u >= L) break;  // warp-uniform
+      int r = -1 - lane;
+      if (K[u] >= 0) {
+        unsigned h = (static_cast<unsigned>(J[u]) * 2654435761u) & (kLeanHash - 1);
+        while (hj[h] != J[u]) h = (h + 1) & (kLeanHash - 1);
+        r = hr[h];
+        slot_of_csr[K[u]] = c0 + r;
+      }
+      if (num) {
+        const unsigned grp = __match_any_sync(0xffffffffu, r);
+        const int rk = __popc(grp & ((1u << lane) - 1u));
+        int mx = rk;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int step = 0; step <= mx; ++step) {
+          if (K[u] >= 0 && rk == step) acc[r] = __dadd_rn(acc[r], c[u]);
+          __syncwarp();
+        }
+      }
+    }
+  }
+  if (num) {
+    __syncwarp();
+    for (idx t = lane; t < nd; t += 32) out[c0 + t] = acc[t];
   }
 }
 
@@ -1859,7 +1894,7 @@ void finish_cache(GalerkinDev& g, const DevCsr& A, const AggDev& agg) {
 }  // namespace
 
 GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial, bool fingerprint,
-                                 bool lean) {
+                                 bool lean, const double* pval, DevBuf<double>* values) {
   require(partial || A.n_rows == A.n_cols, "galerkin: matrix must be square");
   require(agg.n_fine == A.n_rows, "galerkin: aggregation size mismatch");
   const int64_t nc = agg.n_agg;
@@ -1894,9 +1929,11 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
       g.coarse_rowptr.resize(nc + 1);
       g.nnz_coarse = scan_to_offsets(cnnz.get(), g.coarse_rowptr.get(), nc);
       g.coarse_col.resize(g.nnz_coarse);
+      if (values) values->resize(g.nnz_coarse);
       AGG_LAUNCH(k_gal_lean_fill, grid, kGalWarps * 32, 0, agg.agg_row_offsets.get(),
                  agg.rows_by_coarse.get(), A.rowptr.get(), A.col.get(), agg.assignment.get(), nc,
-                 eoff.get(), tmpj.get(), g.coarse_rowptr.get(), g.coarse_col.get(), g.slot_of_csr.get());
+                 eoff.get(), tmpj.get(), g.coarse_rowptr.get(), g.coarse_col.get(), g.slot_of_csr.get(),
+                 A.val.get(), pval, values ? values->get() : nullptr);
       finish_cache(g, A, agg);
       if (fingerprint) g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
       sync();  // tmpj dies here
@@ -1969,6 +2006,22 @@ GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partia
   if (!partial) finish_cache(g, A, agg);
   if (!partial && fingerprint) g.pattern_hash = pattern_fingerprint(A, agg.assignment.get());
   return g;
+}
+
+DevCsrPtr coarse_from_cache(const GalerkinDev& g, DevBuf<double>&& values) {
+  auto Ac = std::make_shared<DevCsr>();
+  Ac->n_rows = Ac->n_cols = g.n_coarse;
+  Ac->nnz = g.nnz_coarse;
+  Ac->rowptr.resize(g.n_coarse + 1);
+  Ac->col.resize(g.nnz_coarse);
+  AGG_CUDA(cudaMemcpyAsync(Ac->rowptr.get(), g.coarse_rowptr.get(), sizeof(idx) * (g.n_coarse + 1),
+                           cudaMemcpyDeviceToDevice, stream()));
+  if (g.nnz_coarse > 0)
+    AGG_CUDA(cudaMemcpyAsync(Ac->col.get(), g.coarse_col.get(), sizeof(idx) * g.nnz_coarse,
+                             cudaMemcpyDeviceToDevice, stream()));
+  Ac->val = std::move(values);
+  Ac->plan();
+  return Ac;
 }
 
 DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const double* pval) {

@@ -67,8 +67,13 @@ struct GalerkinDev {
 // 18-29, 101-103); a hierarchy applies its cache to its own stored operator and skips it.
 // lean: a hierarchy's own cache — only the coarse pattern and slot_of_csr when every coarse row
 // fits the row-walk reduce (the per-entry sorted arrays are for the standalone cache API)
+// values (lean path only): also the coarse values for P weights pval (the numeric reduce fused
+// into the fill pass); left empty when the full path ran
 GalerkinDev build_galerkin_cache(const DevCsr& A, const AggDev& agg, bool partial = false,
-                                 bool fingerprint = true, bool lean = false);
+                                 bool fingerprint = true, bool lean = false,
+                                 const double* pval = nullptr, DevBuf<double>* values = nullptr);
+// the coarse operator of a cache and its values
+DevCsrPtr coarse_from_cache(const GalerkinDev& g, DevBuf<double>&& values);
 // Ac values for the cached pattern.  pval: per fine row P weight.
 DevCsrPtr apply_galerkin_cache(const GalerkinDev& g, const DevCsr& A, const double* pval);
 uint64_t pattern_fingerprint(const DevCsr& A, const idx* assignment);
