@@ -361,6 +361,7 @@ def run_b200(args, world, rank, local):
     check(lib.fn("dmatrix_format")(dm, C.byref(sell_)))
     l0_sell = bool(sell_.value)
     l0_vi = sell_.value == 2  # SELL-32 with the one-byte value dictionary
+    l0_pat = sell_.value == 3  # the row-pattern dictionary (two bytes per row)
     n, nnz = n_.value, nnz_.value
     hist = np.zeros(solver.max_iters + 2)
 
@@ -520,7 +521,13 @@ def run_b200(args, world, rank, local):
     roof = None
     if jc > 0:
         achieved = (jb / jc) / ((jt / jc) / 1e3) / 1e9
-        if l0_vi and dims != 27:
+        if l0_pat:
+            tkey = "jacobidot2_pat_l0_dram_bytes_per_launch"
+            kname = ("k_pat<Epi::kJacobiDot2> on level 0: the damped-Jacobi post-smoothing sweep "
+                     "over the row-pattern copy of the operator (a two-byte pattern id per row; "
+                     "offsets and values from the pattern tables) with PCG's two dot products "
+                     "(r.z, r_old.z) fused")
+        elif l0_vi and dims != 27:
             # short rows (< 10 per row) on a dictionary copy: PCG's (r.z, r_old.z) ride on the sweep
             tkey = "jacobidot2_sell_vi_l0_dram_bytes_per_launch"
             kname = ("k_sell<Epi::kJacobiDot2, VI> on level 0: the damped-Jacobi post-smoothing "
@@ -662,7 +669,8 @@ def rank_bench(comm, rank, local, args, sync_max, sync_sum):
     jt, jc, jb = fam.get("jacobi_l0", (0, 0, 0))
     if jc > 0:
         achieved = (jb / jc) / ((jt / jc) / 1e3) / 1e9
-        kname = {2: "k_sell<Epi::kJacobi, VI> (SELL-32, one-byte value codes)",
+        kname = {3: "k_pat<Epi::kJacobi> (row-pattern ids)",
+                 2: "k_sell<Epi::kJacobi, VI> (SELL-32, one-byte value codes)",
                  1: "k_sell<Epi::kJacobi> (SELL-32)",
                  0: "k_csr_stream<Epi::kJacobi>"}[fmt.value]
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -122,6 +122,11 @@ int aggmg_exact_reductions(void);
  * results).  on = 0 keeps plain fp64 values: operators planned or refreshed afterwards use the
  * 12-byte-per-entry layout (the variable-coefficient case; bench.py's no-dictionary line). */
 void aggmg_set_value_dictionary(int on);
+/* A large operator with a value dictionary and rows of <= 16 entries whose rows repeat a few
+ * patterns (offsets from the diagonal position and values: stencil matrices) is stored as a
+ * two-byte pattern id per row plus the pattern tables (same doubles, same order, same
+ * results).  on = 0: operators planned or refreshed afterwards keep the SELL-32 copy. */
+void aggmg_set_row_patterns(int on);
 void aggmg_setup_config_default(aggmg_setup_config* c);
 void aggmg_cycle_config_default(aggmg_cycle_config* c);
 void aggmg_solver_config_default(aggmg_solver_config* c);

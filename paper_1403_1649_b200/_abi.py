@@ -167,6 +167,7 @@ SIGNATURES = {
     "set_exact_reductions": (None, [I]),
     "exact_reductions": (I, []),
     "set_value_dictionary": (None, [I]),
+    "set_row_patterns": (None, [I]),
     "timer_start": (I, []),
     "timer_stop": (I, [f64p]),
     "setup_config_default": (None, [C.POINTER(SetupConfigC)]),

@@ -281,6 +281,7 @@ void aggmg_set_num_threads(int) {}
 void aggmg_set_exact_reductions(int on) { set_exact_reductions(on != 0); }
 int aggmg_exact_reductions(void) { return exact_reductions() ? 1 : 0; }
 void aggmg_set_value_dictionary(int on) { value_dictionary_switch().store(on ? 1 : 0); }
+void aggmg_set_row_patterns(int on) { row_pattern_switch().store(on ? 1 : 0); }
 int aggmg_num_threads(void) {
   int n = 0;
   guarded([&] { n = sm_count(); });
@@ -971,7 +972,7 @@ int aggmg_dmatrix_jump27(int64_t nx, int64_t ny, int64_t nz, double jump, int64_
   });
 }
 int aggmg_dmatrix_format(const aggmg_dmatrix* A, int* sell) {
-  return guarded([&] { *sell = A->A->sell ? (A->A->sell_vi ? 2 : 1) : 0; });
+  return guarded([&] { *sell = A->A->pat ? 3 : A->A->sell ? (A->A->sell_vi ? 2 : 1) : 0; });
 }
 
 int aggmg_dmatrix_size(const aggmg_dmatrix* A, int64_t* n, int64_t* nnz) {
@@ -1240,7 +1241,7 @@ int aggmg_dist_matrix_format(const aggmg_dist_matrix* A, int* sell) {
   return guarded([&] {
     require(A && A->A, "null dist matrix");
     const DevCsr& M = A->A->A;
-    *sell = M.sell ? (M.sell_vi ? 2 : 1) : 0;
+    *sell = M.pat ? 3 : M.sell ? (M.sell_vi ? 2 : 1) : 0;
   });
 }
 

@@ -245,6 +245,12 @@ DevCsrPtr clone_csr(const DevCsr& A) {
   C->sell_pcol.copy_from(A.sell_pcol);
   C->sell_len.copy_from(A.sell_len);
   C->sell_slots = A.sell_slots;
+  C->pat = A.pat;
+  C->pat_w = A.pat_w;
+  C->pat_id.copy_from(A.pat_id);
+  C->pat_len.copy_from(A.pat_len);
+  C->pat_delta.copy_from(A.pat_delta);
+  C->pat_val.copy_from(A.pat_val);
   return C;
 }
 

@@ -47,6 +47,17 @@ struct DevCsr {
   // so a row's column loads wait on no rowptr / perm round trip
   DevBuf<unsigned char> sell_len;
 
+  // Row-pattern dictionary (stencil-like operators: at most kPatMax distinct rows up to the
+  // diagonal shift): row r's entries are (r + pat_delta[p][j], pat_val[p][j]), j < pat_len[p],
+  // p = pat_id[r] — two bytes per row instead of a column and a value code per entry.  Same
+  // values in the same order: every sum bit-identical to CSR / SELL.
+  bool pat = false;
+  int pat_w = 0;  // table row width (the longest pattern)
+  DevBuf<unsigned short> pat_id;
+  DevBuf<unsigned char> pat_len;
+  DevBuf<int> pat_delta;
+  DevBuf<double> pat_val;
+  bool build_patterns();  // false (and no pattern format) beyond kPatMax patterns
   void plan();          // computes max_row / rows_per_block, builds the SELL copy (synchronises)
   int64_t sell_slots = 0;  // padded slot count of the SELL layout
   void refresh_sell();  // after val changed in place: rebuild the SELL copy (dictionary or plain)
@@ -125,5 +136,6 @@ bool fuse_dots_on_dictionary();
 // process-wide switch of the SELL value dictionary (default on; AGGMG_SELL_VI=0 starts it off);
 // takes effect for operators planned (or refreshed) afterwards
 std::atomic<int>& value_dictionary_switch();
+std::atomic<int>& row_pattern_switch();
 
 }  // namespace aggmg_b200

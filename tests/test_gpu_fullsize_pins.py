@@ -88,7 +88,8 @@ def test_fullsize_bit_identical_to_reference(gpu, name):
         h = _setup(gpu, dm, name)
         assert h.n_levels() == len(pin["levels"])
         if pin["n"] >= (1 << 19):
-            # the headline kernels: SELL-32 at level 0, with the value dictionary on stencils
+            # the headline kernels at level 0: row patterns (7-point) or SELL-32 with the value
+            # dictionary (27-point)
             assert _level_format(gpu, h, 0) >= 1
         for k, want in enumerate(pin["levels"]):
             got = level_digest(h, k)

@@ -52,18 +52,20 @@ def _cases():
     from oracle.checkers import oracle, ref
 
     return {
-        # level 0 SELL-32 + value dictionary (7-point stencil, 2.1 M rows)
-        "poisson3d-128": (lambda: ref().generate_poisson(3, 128, 128, 128), 0.5, M.PCG, 2),
+        # level 0 as row patterns (7-point stencil, 2.1 M rows)
+        "poisson3d-128": (lambda: ref().generate_poisson(3, 128, 128, 128), 0.5, M.PCG, 3),
+        # the same with the pattern format off: SELL-32 + value dictionary
+        "poisson3d-128-sell": (lambda: ref().generate_poisson(3, 128, 128, 128), 0.5, M.PCG, 2),
         # 27-point jumping coefficients (config c4's class, 885 k rows): SELL + dictionary
         "jump27-96": (lambda: oracle().generate_jump27(96, 96, 96, 1e6, 32), 0.5, M.PCG, 2),
-        # anisotropic (config c3's class, 4.1 M rows): FGMRES(30), SELL + dictionary
-        "aniso3d-160": (lambda: ref().generate_poisson(3, 160, 160, 160, 1e-3), 0.5, M.FGMRES, 2),
+        # anisotropic (config c3's class, 4.1 M rows): FGMRES(30), row patterns
+        "aniso3d-160": (lambda: ref().generate_poisson(3, 160, 160, 160, 1e-3), 0.5, M.FGMRES, 3),
         # variable coefficients (884 k rows, values all distinct): plain SELL-32
         "variable3d-96": (lambda: variable_poisson3d(96, 11), 0.5, M.PCG, 1),
     }
 
 
-CASES = ["poisson3d-128", "jump27-96", "aniso3d-160", "variable3d-96"]
+CASES = ["poisson3d-128", "poisson3d-128-sell", "jump27-96", "aniso3d-160", "variable3d-96"]
 
 
 def _solve(backend, A, h, method):
@@ -109,17 +111,21 @@ def test_sell_hierarchy_and_solve_match_reference(gpu, ref, case):
     cfg = M.SetupConfig(alpha=alpha, reuse_caches=True)
     hr = ref.setup_hierarchy(A, None, cfg)
     rr = _solve(ref, A, hr, method)
-    hg = gpu.setup_hierarchy(A, None, cfg)
-    assert _level_format(gpu, hg, 0) == fmt  # the kernel family under test actually runs
-    _assert_levels(hg, hr)
-    _assert_solve_close(_solve(gpu, A, hg, method), rr)
-    del hg
-    gpu.lib.fn("set_exact_reductions")(1)
+    gpu.lib.fn("set_row_patterns")(0 if case.endswith("-sell") else 1)
     try:
         hg = gpu.setup_hierarchy(A, None, cfg)
-        re = _solve(gpu, A, hg, method)
+        assert _level_format(gpu, hg, 0) == fmt  # the kernel family under test actually runs
+        _assert_levels(hg, hr)
+        _assert_solve_close(_solve(gpu, A, hg, method), rr)
+        del hg
+        gpu.lib.fn("set_exact_reductions")(1)
+        try:
+            hg = gpu.setup_hierarchy(A, None, cfg)
+            re = _solve(gpu, A, hg, method)
+        finally:
+            gpu.lib.fn("set_exact_reductions")(0)
     finally:
-        gpu.lib.fn("set_exact_reductions")(0)
+        gpu.lib.fn("set_row_patterns")(1)
     _assert_solve_bits(re, rr)
 
 
