@@ -549,7 +549,7 @@ bool DevCsr::build_patterns() {
       rep_rows.push_back(hr[q]);
     }
   const int npat = static_cast<int>(rep_rows.size());
-  const int w = max_row;
+  const int w = (max_row + 7) & ~7;  // whole 8-entry groups: the kernel loads them as vectors
   DevBuf<int> drep(npat);
   drep.upload(rep_rows.data(), npat);
   DevBuf<unsigned short> dsid(kPatSlots);
@@ -1082,8 +1082,11 @@ void launch_sell(const DevCsr& A, const SpmvArgs& a) {
 // Row-pattern SpMV family: a thread per row reads its two-byte pattern id; the pattern's
 // offsets and values come from the (L1-resident) tables, the x gathers and the epilogue as
 // in k_sell.  Same products, same order: bit-identical to k_csr_stream / k_sell.
+#ifndef AGGMG_PAT_MINB
+#define AGGMG_PAT_MINB 1
+#endif
 template <Epi E>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, AGGMG_PAT_MINB)
     k_pat(const unsigned short* __restrict__ pid, const unsigned char* __restrict__ plen,
           const int* __restrict__ pdelta, const double* __restrict__ pval, int w, int64_t row0,
           int64_t n, SpmvArgs a, double* partials, unsigned* ticket) {
@@ -1096,30 +1099,35 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int k = 0; k < NPX; ++k) v[k] = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t r = row0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < row0 + n;
-       r += stride) {
-    const int p = pid[r];
+  int64_t r = row0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int p = r < row0 + n ? pid[r] : 0;
+  for (; r < row0 + n; r += stride) {
+    const int pn = r + stride < row0 + n ? pid[r + stride] : 0;  // the next row's id in flight
     const EpiIn ein = epi_load<E>(a, x, r);
     const int len = __ldg(plen + p);
-    const int* dl = pdelta + p * w;
-    const double* vl = pval + p * w;
+    // the pattern's offsets and values: 8-entry groups as 16-byte loads (w is a multiple of 8)
+    const int4* dl = reinterpret_cast<const int4*>(pdelta + p * w);
+    const double2* vl = reinterpret_cast<const double2*>(pval + p * w);
     double sum = 0.0;
     for (int k = 0; k < len; k += 8) {
-      double xs[8], vs[8];
+      const int4 d0 = __ldg(dl + k / 4), d1 = __ldg(dl + k / 4 + 1);
+      const int dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+      double xs[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        vs[j] = 0.0;
-        xs[j] = 0.0;
-        if (k + j < len) {
-          vs[j] = __ldg(vl + k + j);
-          xs[j] = __ldg(x + r + __ldg(dl + k + j));
-        }
+      for (int j = 0; j < 8; ++j) xs[j] = k + j < len ? __ldg(x + r + dd[j]) : 0.0;
+      double vs[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double2 t = __ldg(vl + k / 2 + j);
+        vs[2 * j] = t.x;
+        vs[2 * j + 1] = t.y;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (k + j < len) sum = __dadd_rn(sum, __dmul_rn(vs[j], xs[j]));
     }
     row_epilogue_in<E>(a, ein, r, sum, v);
+    p = pn;
   }
   if constexpr (NP > 0) {
     block_reduce<NPX>(v, red_smem);
