@@ -756,6 +756,18 @@ void cycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, bool accelerated_top
 void apply_preconditioner(DevHierarchy& h, const CycleCfg& cfg, const double* r, double* z) {
   h.ensure_workspace();
   inner_cycle(h, cfg, 0, r, z, nullptr);
+  h.levels[0].zs_b = nullptr;  // a mark the cycle did not consume never outlives it
+  h.levels[0].zs_x = nullptr;
+}
+
+const double* top_zero_sweep_diag(const DevHierarchy& h) {
+  if (h.levels.empty() || h.coarsest() == 0 || h.levels[0].smoother.kind == 2) return nullptr;
+  return h.levels[0].smoother.wdiag.get();
+}
+
+void mark_top_zero_sweep(DevHierarchy& h, const double* r, double* z) {
+  h.levels[0].zs_b = r;
+  h.levels[0].zs_x = z;
 }
 
 void flush_cycle_warnings() {

@@ -24,6 +24,11 @@ void cycle(DevHierarchy& h, const CycleCfg& cfg, int64_t k, bool accelerated_top
 
 // z = M r (apply_preconditioner, cycles.cpp:140-146)
 void apply_preconditioner(DevHierarchy& h, const CycleCfg& cfg, const double* r, double* z);
+// The level-0 damped-Jacobi zero-guess sweep z = 0 + wd .* r every cycle of h starts with
+// (nullptr when it does not: one level, or SGS).  A caller that produces r elementwise can
+// write that z alongside and mark it done for the next apply_preconditioner(h, cfg, r, z).
+const double* top_zero_sweep_diag(const DevHierarchy& h);
+void mark_top_zero_sweep(DevHierarchy& h, const double* r, double* z);
 
 // Host-visible warnings raised by device-side branch fallbacks (cycles.cpp:97,124).
 void flush_cycle_warnings();

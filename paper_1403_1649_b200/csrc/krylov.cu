@@ -24,12 +24,15 @@ struct PcgSlots {
 };
 
 // alpha = rz/pAp; x += alpha p; rn = r + (-alpha) Ap; res2 = ||rn||^2  (krylov.cpp:181-186)
+// wd: also the preconditioner's first operation, z = 0 + wd .* rn (the level-0 zero-guess
+// damped-Jacobi sweep, k_jacobi_zero's arithmetic), while rn is in registers
 __global__ void __launch_bounds__(kB) k_pcg_update(int64_t n, PcgSlots* s, int par,
                                                    const double* __restrict__ p,
                                                    const double* __restrict__ Ap,
                                                    const double* __restrict__ r, double* __restrict__ x,
                                                    double* __restrict__ rn, double* partials,
-                                                   unsigned* ticket) {
+                                                   unsigned* ticket, const double* __restrict__ wd,
+                                                   double* __restrict__ z) {
   __shared__ double smem[32];
   const double alpha = __ddiv_rn(s->q[par][0], s->pAp);
   const double malpha = -alpha;
@@ -48,6 +51,11 @@ __global__ void __launch_bounds__(kB) k_pcg_update(int64_t n, PcgSlots* s, int p
     const double v0 = __dadd_rn(rq.x, __dmul_rn(malpha, aq.x));
     const double v1 = __dadd_rn(rq.y, __dmul_rn(malpha, aq.y));
     reinterpret_cast<double2*>(rn)[q] = make_double2(v0, v1);
+    if (wd) {
+      const double2 w = reinterpret_cast<const double2*>(wd)[q];
+      reinterpret_cast<double2*>(z)[q] =
+          make_double2(__dadd_rn(0.0, __dmul_rn(w.x, v0)), __dadd_rn(0.0, __dmul_rn(w.y, v1)));
+    }
     acc[0] = __dadd_rn(acc[0], __dmul_rn(v0, v0));
     acc[0] = __dadd_rn(acc[0], __dmul_rn(v1, v1));
   }
@@ -56,6 +64,7 @@ __global__ void __launch_bounds__(kB) k_pcg_update(int64_t n, PcgSlots* s, int p
     x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
     const double v = __dadd_rn(r[i], __dmul_rn(malpha, Ap[i]));
     rn[i] = v;
+    if (wd) z[i] = __dadd_rn(0.0, __dmul_rn(wd[i], v));
     acc[0] = __dadd_rn(acc[0], __dmul_rn(v, v));
   }
   block_reduce<1>(acc, smem);
@@ -284,6 +293,8 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
   };
   precond_dots(r, r, &slots.get()->q[0][0], 1);
   copy_double(p.get(), z.get(), n);
+  // the update pass also writes the preconditioner's level-0 zero-guess sweep into z
+  const double* wd0 = (fuse && !dist && M.h && !M.host_fn) ? top_zero_sweep_diag(*M.h) : nullptr;
   double* pinned = pinned_scratch(8);
   int par = 0;  // q[par][0] holds the current r.z
   while (res > target && out.iterations < cfg.max_iters) {
@@ -315,7 +326,7 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
         spmv_run(A, Epi::kSpmvDot1, a, kProfSpmvL0);
       reduce(dist, &slots.get()->pAp, 1);
       AGG_LAUNCH(k_pcg_update, reduce_grid(n), kB, 0, n, slots.get(), par, p.get(), Ap.get(), r, x,
-                 rn, reduce_partials(), reduce_ticket());
+                 rn, reduce_partials(), reduce_ticket(), wd0, z.get());
       reduce(dist, &slots.get()->res2, 1);
     }
     AGG_CUDA(cudaMemcpyAsync(pinned, slots.get(), 2 * sizeof(double), cudaMemcpyDeviceToHost,
@@ -329,6 +340,7 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     std::swap(r, rn);  // r = new residual, rn = r_old
     if (res <= target) break;
     const int cur = par ^ 1;
+    if (wd0) mark_top_zero_sweep(*M.h, r, z.get());  // z = 0 + wd .* r is in place already
     precond_dots(r, rn, &slots.get()->q[cur][0], 2);  // {r.z, r_old.z}
     AGG_LAUNCH(k_pcg_p, egrid(n), kB, 0, n, slots.get(), cur, z.get(), p.get());
     par = cur;

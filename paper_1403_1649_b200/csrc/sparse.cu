@@ -1082,11 +1082,16 @@ void launch_sell(const DevCsr& A, const SpmvArgs& a) {
 // Row-pattern SpMV family: a thread per row reads its two-byte pattern id; the pattern's
 // offsets and values come from the (L1-resident) tables, the x gathers and the epilogue as
 // in k_sell.  Same products, same order: bit-identical to k_csr_stream / k_sell.
-#ifndef AGGMG_PAT_MINB
-#define AGGMG_PAT_MINB 1
-#endif
+// __launch_bounds__ min blocks per epilogue (register caps; measured on the c2 level 0 with
+// tools/kernel_bench.py: spmv / residual / Arnoldi 93-98 us at 5 CTAs per SM, the fused dots
+// of the Jacobi sweep 125 us at 4, the plain Jacobi and PCG's SpMV + dot uncapped)
+constexpr int pat_min_blocks(Epi e) {
+  return (e == Epi::kSpmv || e == Epi::kResidual || e == Epi::kScaleDiag) ? 5
+         : (e == Epi::kJacobiDot2 || e == Epi::kSpmvDot2 || e == Epi::kSpmvDot3) ? 4
+                                                                                  : 1;
+}
 template <Epi E>
-__global__ void __launch_bounds__(256, AGGMG_PAT_MINB)
+__global__ void __launch_bounds__(256, pat_min_blocks(E))
     k_pat(const unsigned short* __restrict__ pid, const unsigned char* __restrict__ plen,
           const int* __restrict__ pdelta, const double* __restrict__ pval, int w, int64_t row0,
           int64_t n, SpmvArgs a, double* partials, unsigned* ticket) {
@@ -1108,13 +1113,15 @@ __global__ void __launch_bounds__(256, AGGMG_PAT_MINB)
     // the pattern's offsets and values: 8-entry groups as 16-byte loads (w is a multiple of 8)
     const int4* dl = reinterpret_cast<const int4*>(pdelta + p * w);
     const double2* vl = reinterpret_cast<const double2*>(pval + p * w);
+    const int ri = static_cast<int>(r);  // operators are < 2^31 rows
     double sum = 0.0;
+#pragma unroll 1
     for (int k = 0; k < len; k += 8) {
       const int4 d0 = __ldg(dl + k / 4), d1 = __ldg(dl + k / 4 + 1);
       const int dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
       double xs[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) xs[j] = k + j < len ? __ldg(x + r + dd[j]) : 0.0;
+      for (int j = 0; j < 8; ++j) xs[j] = k + j < len ? __ldg(x + (ri + dd[j])) : 0.0;
       double vs[8];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -1122,9 +1129,11 @@ __global__ void __launch_bounds__(256, AGGMG_PAT_MINB)
         vs[2 * j] = t.x;
         vs[2 * j + 1] = t.y;
       }
+      // a group's slots past the row's length hold the value +0 and the x operand is +0, so
+      // they add +0: the running sum, which starts at +0 and so is never -0 (round to
+      // nearest), is unchanged bit for bit — no per-slot predicate on the chain
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (k + j < len) sum = __dadd_rn(sum, __dmul_rn(vs[j], xs[j]));
+      for (int j = 0; j < 8; ++j) sum = __dadd_rn(sum, __dmul_rn(vs[j], xs[j]));
     }
     row_epilogue_in<E>(a, ein, r, sum, v);
     p = pn;
