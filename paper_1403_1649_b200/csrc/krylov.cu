@@ -23,7 +23,8 @@ struct PcgSlots {
   double pad[2];
 };
 
-// alpha = rz/pAp; x += alpha p; rn = r + (-alpha) Ap; res2 = ||rn||^2  (krylov.cpp:181-186)
+// alpha = rz/pAp; rn = r + (-alpha) Ap; res2 = ||rn||^2  (krylov.cpp:181-186).  x += alpha p
+// is deferred to k_pcg_p (which reads p anyway) or, after the last iteration, to k_pcg_x.
 // wd: also the preconditioner's first operation, z = 0 + wd .* rn (the level-0 zero-guess
 // damped-Jacobi sweep, k_jacobi_zero's arithmetic), while rn is in registers
 __global__ void __launch_bounds__(kB) k_pcg_update(int64_t n, PcgSlots* s, int par,
@@ -41,13 +42,8 @@ __global__ void __launch_bounds__(kB) k_pcg_update(int64_t n, PcgSlots* s, int p
   const int64_t npair = n >> 1;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < npair; q += stride) {
-    const double2 pq = reinterpret_cast<const double2*>(p)[q];
     const double2 aq = reinterpret_cast<const double2*>(Ap)[q];
     const double2 rq = reinterpret_cast<const double2*>(r)[q];
-    double2 xq = reinterpret_cast<double2*>(x)[q];
-    xq.x = __dadd_rn(xq.x, __dmul_rn(alpha, pq.x));
-    xq.y = __dadd_rn(xq.y, __dmul_rn(alpha, pq.y));
-    reinterpret_cast<double2*>(x)[q] = xq;
     const double v0 = __dadd_rn(rq.x, __dmul_rn(malpha, aq.x));
     const double v1 = __dadd_rn(rq.y, __dmul_rn(malpha, aq.y));
     reinterpret_cast<double2*>(rn)[q] = make_double2(v0, v1);
@@ -61,7 +57,6 @@ __global__ void __launch_bounds__(kB) k_pcg_update(int64_t n, PcgSlots* s, int p
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t i = n - 1;
-    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
     const double v = __dadd_rn(r[i], __dmul_rn(malpha, Ap[i]));
     rn[i] = v;
     if (wd) z[i] = __dadd_rn(0.0, __dmul_rn(wd[i], v));
@@ -72,13 +67,39 @@ __global__ void __launch_bounds__(kB) k_pcg_update(int64_t n, PcgSlots* s, int p
   finish_reduction<1>(partials, ticket, &s->res2, smem);
 }
 
+// x += alpha p (this iteration's alpha = rz / pAp, krylov.cpp:182), then
 // beta = (rz_new - r_old.z) / rz ; p = z + beta p  (krylov.cpp:191-195)
 __global__ void k_pcg_p(int64_t n, const PcgSlots* s, int cur, const double* __restrict__ z,
-                        double* __restrict__ p) {
+                        double* __restrict__ p, double* __restrict__ x) {
+  const double alpha = __ddiv_rn(s->q[cur ^ 1][0], s->pAp);
   const double beta = __ddiv_rn(__dsub_rn(s->q[cur][0], s->q[cur][1]), s->q[cur ^ 1][0]);
+  const int64_t np = n >> 1, stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < np; q += stride) {
+    const double2 pq = reinterpret_cast<const double2*>(p)[q];
+    const double2 zq = reinterpret_cast<const double2*>(z)[q];
+    if (x) {
+      double2 xq = reinterpret_cast<double2*>(x)[q];
+      xq.x = __dadd_rn(xq.x, __dmul_rn(alpha, pq.x));
+      xq.y = __dadd_rn(xq.y, __dmul_rn(alpha, pq.y));
+      reinterpret_cast<double2*>(x)[q] = xq;
+    }
+    reinterpret_cast<double2*>(p)[q] =
+        make_double2(__dadd_rn(zq.x, __dmul_rn(beta, pq.x)), __dadd_rn(zq.y, __dmul_rn(beta, pq.y)));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t i = n - 1;
+    const double pi = p[i];
+    if (x) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, pi));
+  }
+}
+// the last iteration's x += alpha p (no p update follows)
+__global__ void k_pcg_x(int64_t n, const PcgSlots* s, int par, const double* __restrict__ p,
+                        double* __restrict__ x) {
+  const double alpha = __ddiv_rn(s->q[par][0], s->pAp);
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
 }
 
 // MGS step i of column j (krylov.cpp:85-89): w = w + (-h_i) V_i, then the next
@@ -338,11 +359,18 @@ SolveOut pcg(const DevCsr& A, const double* b, double* x, const Precond& M, cons
     res = std::sqrt(pinned[1]);
     out.history.push_back(res);
     std::swap(r, rn);  // r = new residual, rn = r_old
-    if (res <= target) break;
+    if (res <= target) {
+      if (!exact) AGG_LAUNCH(k_pcg_x, egrid(n), kB, 0, n, slots.get(), par, p.get(), x);
+      break;
+    }
     const int cur = par ^ 1;
     if (wd0) mark_top_zero_sweep(*M.h, r, z.get());  // z = 0 + wd .* r is in place already
     precond_dots(r, rn, &slots.get()->q[cur][0], 2);  // {r.z, r_old.z}
-    AGG_LAUNCH(k_pcg_p, egrid(n), kB, 0, n, slots.get(), cur, z.get(), p.get());
+    if (exact) {
+      AGG_LAUNCH(k_pcg_p, reduce_grid(n), kB, 0, n, slots.get(), cur, z.get(), p.get(), nullptr);
+    } else {
+      AGG_LAUNCH(k_pcg_p, reduce_grid(n), kB, 0, n, slots.get(), cur, z.get(), p.get(), x);
+    }
     par = cur;
   }
   if (dist && dist->flush_warnings)
