@@ -452,17 +452,18 @@ def run_b200(args, world, rank, local):
                        "calls": "aggmg_setup_hierarchy + aggmg_pcg/aggmg_fgmres (C-ABI, host arrays)"}
         del Ah
 
-    # ---- side number: the step with plain fp64 SELL values (no value dictionary): the cost
-    # on operators with more than 256 distinct values (variable coefficients)
-    no_dict = None
-    if not args.no_exact and world == 1 and l0_vi:
-        lib.fn("set_value_dictionary")(0)
+    # ---- side numbers: the step with the level-0 operator in the other formats — plain fp64
+    # SELL values (no value dictionary: operators with more than 256 distinct values, variable
+    # coefficients) and, for a row-pattern operator, the dictionary SELL-32 copy
+    def side_step(switch, note):
+        nonlocal dm
+        lib.fn(switch)(0)
         dm2 = C.c_void_p()
         if dims == 27:
             check(lib.fn("dmatrix_jump27")(nx, ny, nz, eps, JUMP_BLOCK, C.byref(dm2)))
         else:
             check(lib.fn("dmatrix_poisson")(dims, nx, ny, nz, eps, -1, C.byref(dm2)))
-        dm_saved, dm = dm, dm2
+        saved, dm = dm, dm2
         step(None)
         nrec = []
         check(lib.fn("synchronize")())
@@ -470,13 +471,22 @@ def run_b200(args, world, rank, local):
         for _ in range(2):
             step(nrec)
         check(lib.fn("timer_stop")(C.byref(ms)))
-        lib.fn("set_value_dictionary")(1)
-        dm = dm_saved
+        lib.fn(switch)(1)
+        dm = saved
         lib.fn("dmatrix_free")(dm2)
-        no_dict = {"ms_per_step": ms.value / 2, "setup_ms": nrec[0]["setup_ms"],
-                   "solve_ms": 1e3 * nrec[0]["solve_s"], "iterations": nrec[0]["iterations"],
-                   "note": "aggmg_set_value_dictionary(0): SELL-32 with 8-byte values, as on a "
-                           "variable-coefficient operator; not the headline"}
+        return {"ms_per_step": ms.value / 2, "setup_ms": nrec[0]["setup_ms"],
+                "solve_ms": 1e3 * nrec[0]["solve_s"], "iterations": nrec[0]["iterations"],
+                "note": note}
+
+    no_dict = sell_dict = None
+    if not args.no_exact and world == 1 and (l0_vi or l0_pat):
+        no_dict = side_step("set_value_dictionary",
+                            "aggmg_set_value_dictionary(0): SELL-32 with 8-byte values, as on a "
+                            "variable-coefficient operator; not the headline")
+    if not args.no_exact and world == 1 and l0_pat:
+        sell_dict = side_step("set_row_patterns",
+                              "aggmg_set_row_patterns(0): level 0 as the SELL-32 copy with one-byte "
+                              "value codes instead of row patterns; not the headline")
 
     # ---- side number: the same step in bit-identical mode (aggmg_set_exact_reductions) ----
     exact = None
@@ -571,6 +581,7 @@ def run_b200(args, world, rank, local):
                    "l2": f"inputs larger than L2 (A alone is {(12 * nnz + 4 * n) / 1e9:.2f} GB)",
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                    "exact_mode": exact, "no_value_dictionary": no_dict,
+                   "sell_dictionary_level0": sell_dict,
                    "e2e_reference_call_sequence": e2e_ref_api},
         "roofline": roof,
         "cpu_baseline": cpu,
