@@ -464,7 +464,8 @@ def run_b200(args, world, rank, local):
         else:
             check(lib.fn("dmatrix_poisson")(dims, nx, ny, nz, eps, -1, C.byref(dm2)))
         saved, dm = dm, dm2
-        step(None)
+        step(None)  # first sighting of each sub-cycle: eager
+        step(None)  # second: graph capture
         nrec = []
         check(lib.fn("synchronize")())
         check(lib.fn("timer_start")())
@@ -492,6 +493,7 @@ def run_b200(args, world, rank, local):
     exact = None
     if not args.no_exact:
         lib.fn("set_exact_reductions")(1)
+        step(None)  # exact mode has its own sub-cycle graphs: eager, then captured
         step(None)
         erec = []
         dist.barrier()
