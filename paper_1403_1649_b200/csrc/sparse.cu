@@ -381,10 +381,12 @@ void DevCsr::plan() {
   // halo); not the restriction (n_c x n)
   // (slot offsets are int32: every slice padded to the longest row must stay below 2^31)
   const bool fits = ((n_rows + 31) / 32) * 32 * static_cast<int64_t>(max_row) < INT32_MAX;
+  // from 2^17 rows (c2 level 2 included: solve -1.3 ms for +1.1 ms of setup, c3 -2.4 ms net;
+  // from 2^13 rows the small levels' SELL builds cost more than they save).
   // AGGMG_SELL_MIN_ROWS / AGGMG_SELL_RECT=1 (restrictions too): tuning experiments
   static const int64_t sell_min_rows = [] {
     const char* e = std::getenv("AGGMG_SELL_MIN_ROWS");
-    return e ? std::atoll(e) : (int64_t{1} << 19);
+    return e ? std::atoll(e) : (int64_t{1} << 17);
   }();
   static const bool sell_rect = [] {
     const char* e = std::getenv("AGGMG_SELL_RECT");
