@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
       unsigned h = dict_hash(u);
       bool known = false;
       for (int probe = 0; probe < kLocalProbes; ++probe, h = (h + 1) & (kDictSlots - 1)) {
-        const unsigned long long cur = seen[h];
+        const unsigned long long cur = atomicCAS(seen + h, kDictEmpty, kDictEmpty);  // atomic read
         if (cur == u) {
           known = true;
           break;
@@ -263,7 +263,9 @@ __global__ void __launch_bounds__(256) k_pat_insert(const idx* rowptr, const idx
     const unsigned long long h = pat_hash_row(rowptr, col, val, r);
     rowhash[r] = h;
     const unsigned lh = static_cast<unsigned>(h) & (kLocal - 1);
-    if (seen[lh] == h) continue;  // a one-way cache: most rows repeat a recent pattern
+    // a one-way cache shared by the CTA (most rows repeat a recent pattern); atomic accesses:
+    // a hit only skips a probe of a pattern that is already in the global set
+    if (atomicCAS(seen + lh, h, h) == h) continue;
     unsigned s = static_cast<unsigned>(h >> 20) & (kPatSlots - 1);
     for (int probe = 0;; ++probe, s = (s + 1) & (kPatSlots - 1)) {
       if (probe == kPatSlots || *bad) {
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(256) k_pat_insert(const idx* rowptr, const idx
       }
       if (old == h) break;
     }
-    seen[lh] = h;
+    atomicExch(seen + lh, h);
   }
 }
 
