@@ -7,7 +7,7 @@ import re
 import sys
 
 
-def main(path, out=None):
+def main(path, out=None, setup_launches=None, align="k_max_row"):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
@@ -19,8 +19,15 @@ def main(path, out=None):
             continue
         name = re.sub(r"\(.*", "", r[ki]).replace("void unnamed>::", "").replace("unnamed>::", "")
         launches.append((name, r[gi], float(r[vi].replace(",", ""))))
-    first_solve = next((i for i, l in enumerate(launches) if "pcg" in l[0] or "k_kstep1" in l[0]),
-                       len(launches))
+    # the window may start a few launches early (launches ncu counts and the library's counter
+    # does not): align it on the setup's first kernel, then split at the library's setup count
+    start = next((i for i, l in enumerate(launches) if l[0].startswith(align)), 0)
+    launches = launches[start:]
+    if setup_launches is not None:
+        first_solve = min(int(setup_launches), len(launches))
+    else:
+        first_solve = next((i for i, l in enumerate(launches) if "pcg" in l[0] or "k_kstep1" in l[0]),
+                           len(launches))
     lines = []
     for label, part in (("setup", launches[:first_solve]), ("solve", launches[first_solve:])):
         tot = collections.defaultdict(float)
@@ -40,4 +47,5 @@ def main(path, out=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None,
+         sys.argv[3] if len(sys.argv) > 3 else None)
