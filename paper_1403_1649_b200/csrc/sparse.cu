@@ -201,22 +201,44 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
   }
 }
 
-__global__ void k_sell_codes(const idx* rowptr, const idx* col, const double* val, int64_t n,
-                             const idx* sptr, const unsigned long long* __restrict__ slots,
-                             const unsigned char* __restrict__ code_of_slot, unsigned char* scode,
-                             idx* pcol, unsigned char* slen) {
+// A thread per row writes its 4-slot groups whole: one int4 of columns and one 32-bit code
+// word per group, so a warp's stores of a group are 512 and 128 contiguous bytes.  The
+// dictionary's hash set is looked up from shared memory.
+__global__ void __launch_bounds__(256)
+    k_sell_codes(const idx* rowptr, const idx* col, const double* val, int64_t n, const idx* sptr,
+                 const unsigned long long* __restrict__ slots,
+                 const unsigned char* __restrict__ code_of_slot, unsigned char* scode, idx* pcol,
+                 unsigned char* slen) {
+  __shared__ unsigned long long s_slots[kDictSlots];
+  __shared__ unsigned char s_code[kDictSlots];
+  for (int q = threadIdx.x; q < kDictSlots; q += blockDim.x) {
+    s_slots[q] = slots[q];
+    s_code[q] = code_of_slot[q];
+  }
+  __syncthreads();
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const idx k0 = rowptr[r], len = rowptr[r + 1] - k0;
   slen[r] = static_cast<unsigned char>(len);
-  for (idx k = 0; k < len; ++k) {
-    const unsigned long long u = __double_as_longlong(val[k0 + k]);
-    unsigned h = dict_hash(u);
-    while (slots[h] != u) h = (h + 1) & (kDictSlots - 1);  // present by construction
-    // packed: the codes of slots 4g..4g+3 of a row are one 32-bit word (byte k & 3)
-    const idx at = sptr[r >> 5] + 32 * (k & ~3) + 4 * (r & 31) + (k & 3);
-    scode[at] = code_of_slot[h];
-    pcol[at] = col[k0 + k];  // the same packing: 4 consecutive slots of a row are one int4
+  // slots 4g..4g+3 of the row: int4 number sbase / 4 + 32 g + (r & 31) of the packed layout
+  int4* pc4 = reinterpret_cast<int4*>(pcol + sptr[r >> 5]) + (r & 31);
+  unsigned* cw = reinterpret_cast<unsigned*>(scode + sptr[r >> 5]) + (r & 31);
+  for (idx g = 0; 4 * g < len; ++g) {
+    int c[4] = {0, 0, 0, 0};
+    unsigned w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const idx k = 4 * g + j;
+      if (k < len) {
+        const unsigned long long u = __double_as_longlong(val[k0 + k]);
+        unsigned h = dict_hash(u);
+        while (s_slots[h] != u) h = (h + 1) & (kDictSlots - 1);  // present by construction
+        w |= static_cast<unsigned>(s_code[h]) << (8 * j);
+        c[j] = col[k0 + k];
+      }
+    }
+    pc4[32 * g] = make_int4(c[0], c[1], c[2], c[3]);
+    cw[32 * g] = w;
   }
 }
 
