@@ -155,8 +155,12 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const unsigned long long u = uu[q];
-      if (!((in >> q) & 1u)) continue;  // past the end
+      // warp-uniform: every lane takes part in the match; lanes past the end hold a key no
+      // value has (the empty marker) and do nothing else
+      const bool act = (in >> q) & 1u;
+      const unsigned long long u = act ? uu[q] : kDictEmpty;
+      const unsigned peers = __match_any_sync(0xffffffffu, u);
+      if (!act || (threadIdx.x & 31) != __ffs(peers) - 1) continue;  // one lane per pattern
       if (u == kDictEmpty) {
         give_up();
         continue;
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
       if (known) continue;
       h = dict_hash(u);  // new to this CTA: the global set, then the CTA's copy
       for (int probe = 0;; ++probe, h = (h + 1) & (kDictSlots - 1)) {
-        if (probe == kDictSlots) {
+        if (probe == kDictSlots || *bad) {  // full, or already lost: stop probing
           give_up();
           break;
         }
@@ -189,7 +193,6 @@ __global__ void __launch_bounds__(256) k_dict_insert(const double* __restrict__ 
           if (atomicAdd(state, 1) >= kDictMax) give_up();
           break;
         }
-        if (*bad) break;  // already lost: stop probing
         if (old == u) break;
       }
       h = dict_hash(u);
