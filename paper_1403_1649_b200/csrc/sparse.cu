@@ -410,14 +410,16 @@ void DevCsr::plan() {
   const bool fits = ((n_rows + 31) / 32) * 32 * static_cast<int64_t>(max_row) < INT32_MAX;
   // from 2^17 rows (c2 level 2 included: solve -1.3 ms for +1.1 ms of setup, c3 -2.4 ms net;
   // from 2^13 rows the small levels' SELL builds cost more than they save).
-  // AGGMG_SELL_MIN_ROWS / AGGMG_SELL_RECT=1 (restrictions too): tuning experiments
+  // AGGMG_SELL_MIN_ROWS: tuning experiments
   static const int64_t sell_min_rows = [] {
     const char* e = std::getenv("AGGMG_SELL_MIN_ROWS");
     return e ? std::atoll(e) : (int64_t{1} << 17);
   }();
+  // rectangular operators too (the restrictions R: c2 level-0 R 84 -> 59 us with the value
+  // dictionary, solve -1.1 ms); AGGMG_SELL_RECT=0: square operators only
   static const bool sell_rect = [] {
     const char* e = std::getenv("AGGMG_SELL_RECT");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   const bool shape_ok = sell_rect || (n_cols >= n_rows && n_cols <= n_rows + n_rows / 2);
   pat = false;
@@ -430,7 +432,8 @@ void DevCsr::plan() {
     // stencil-like operators (a value dictionary and short rows) try the row patterns first
     // (measured: the 7-point level 0 sweeps 1.3-1.4x faster than the dictionary SELL copy;
     // the 27-point rows are slower through the pattern tables and keep SELL)
-    if (dict && max_row <= kPatShortRow && build_patterns()) {
+    const bool square = n_cols >= n_rows && n_cols <= n_rows + n_rows / 2;  // not a restriction
+    if (dict && square && max_row <= kPatShortRow && build_patterns()) {
       sell_ptr.reset();
       sell_perm.reset();
       sell_len.reset();
