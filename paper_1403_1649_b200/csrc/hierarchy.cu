@@ -244,6 +244,8 @@ DevCsrPtr clone_csr(const DevCsr& A) {
   C->sell_tab.copy_from(A.sell_tab);
   C->sell_pcol.copy_from(A.sell_pcol);
   C->sell_len.copy_from(A.sell_len);
+  C->sell_d16 = A.sell_d16;
+  C->sell_col16.copy_from(A.sell_col16);
   C->sell_slots = A.sell_slots;
   C->pat = A.pat;
   C->pat_w = A.pat_w;

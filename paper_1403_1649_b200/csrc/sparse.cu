@@ -47,6 +47,16 @@ __global__ void k_max_row(const idx* rowptr, int64_t n, int* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
+// largest |col - row| over the entries (whether the columns fit 16-bit offsets)
+__global__ void k_max_offset(const idx* rowptr, const idx* col, int64_t n, int* out) {
+  int m = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    for (idx k = rowptr[i]; k < rowptr[i + 1]; ++k) m = max(m, abs(col[k] - static_cast<idx>(i)));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 // largest staged span (e1 - (e0 & ~1)) over the row blocks of rpb rows
 __global__ void k_max_block_span(const idx* rowptr, int64_t n, int rpb, int* out) {
   int m = 0;
@@ -97,14 +107,19 @@ __global__ void k_slice_width(const idx* rowptr, int64_t n, int64_t nslices, int
 }
 __global__ void k_sell_fill(const idx* rowptr, const idx* col, const double* val, int64_t n,
                             const idx* sptr, const idx* perm, idx* scol, double* sval, int with_cols,
-                            unsigned char* slen) {
+                            unsigned char* slen, short* scol16) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // position
   if (q >= n) return;
   const int64_t r = perm ? perm[q] : q;
   const idx base = sptr[q >> 5] + static_cast<idx>(q & 31), k0 = rowptr[r], len = rowptr[r + 1] - k0;
   slen[q] = static_cast<unsigned char>(len);
   for (idx k = 0; k < len; ++k) {
-    if (with_cols) scol[base + 32 * k] = col[k0 + k];
+    if (with_cols) {
+      if (scol16)
+        scol16[base + 32 * k] = static_cast<short>(col[k0 + k] - static_cast<idx>(r));
+      else
+        scol[base + 32 * k] = col[k0 + k];
+    }
     sval[base + 32 * k] = val[k0 + k];
   }
 }
@@ -510,12 +525,32 @@ void DevCsr::fill_plain() {
   sell_tab.reset();
   sell_pcol.reset();
   // (padding slots are never read: every row stops at its own length)
-  if (sell_col.size() != sell_slots) sell_col.resize(sell_slots);
+  // columns as 16-bit offsets from the row when every entry is within 32767 of its row (the
+  // coarse operators of the structured problems: c2 / c3 level 1; AGGMG_SELL_D16=0: never)
+  static const bool d16_on = [] {
+    const char* e = std::getenv("AGGMG_SELL_D16");
+    return !(e && e[0] == '0');
+  }();
+  sell_d16 = false;
+  if (d16_on) {
+    DevBuf<int> m(1);
+    m.zero();
+    AGG_LAUNCH(k_max_offset, grid_for(n_rows, 256, 8 * sm_count()), 256, 0, rowptr.get(), col.get(), n_rows,
+               m.get());
+    sell_d16 = read_scalar(m.get()) <= 32767;
+  }
+  if (sell_d16) {
+    sell_col.reset();
+    if (sell_col16.size() != sell_slots) sell_col16.resize(sell_slots);
+  } else {
+    sell_col16.reset();
+    if (sell_col.size() != sell_slots) sell_col.resize(sell_slots);
+  }
   if (sell_val.size() != sell_slots) sell_val.resize(sell_slots);
   sell_len.resize(n_rows);
   AGG_LAUNCH(k_sell_fill, grid_for(n_rows, 256), 256, 0, rowptr.get(), col.get(), val.get(), n_rows,
              sell_ptr.get(), sell_perm.size() ? sell_perm.get() : nullptr, sell_col.get(),
-             sell_val.get(), 1, sell_len.get());
+             sell_val.get(), 1, sell_len.get(), sell_d16 ? sell_col16.get() : nullptr);
 }
 
 // the dictionary copy (packed columns + one-byte codes) from the slots of a successful
@@ -547,6 +582,8 @@ void DevCsr::build_codes(const DevBuf<unsigned long long>& slots) {
   sell_vi = true;
   sell_col.reset();
   sell_val.reset();
+  sell_col16.reset();
+  sell_d16 = false;
 }
 
 // AGGMG_PAT=0 / aggmg_set_row_patterns(0): no row-pattern format
@@ -886,13 +923,15 @@ constexpr int sell_tune(Epi e, bool vi, bool short_rows) {
   return dots ? 13 : 4;
 }
 
-template <Epi E, bool VI, int T>
+// D16 (plain layout only): columns stored as 16-bit offsets from the row
+template <Epi E, bool VI, int T, bool D16 = false>
 __global__ void __launch_bounds__(256, kSellTunes[T].minb)
     k_sell(const idx* __restrict__ rowptr, const idx* __restrict__ sptr, const idx* __restrict__ scol,
            const double* __restrict__ sval, const unsigned char* __restrict__ scode,
            const idx* __restrict__ pcol, const double* __restrict__ stab, const idx* __restrict__ perm,
            const unsigned char* __restrict__ slen, int64_t row0, int64_t n, SpmvArgs a,
-           double* partials, unsigned* ticket) {
+           double* partials, unsigned* ticket, const short* __restrict__ scol16) {
+  static_assert(!(VI && D16), "16-bit offsets only in the plain layout");
   constexpr int NP = EpiTraits<E>::np;
   constexpr int NPX = NP > 0 ? NP : 1;
   __shared__ __align__(16) double red_smem[32 * 3 + 2];
@@ -1002,14 +1041,23 @@ __global__ void __launch_bounds__(256, kSellTunes[T].minb)
           if (j < m) sum = __dadd_rn(sum, __dmul_rn(s_tab[(u[j >> 2] >> (8 * (j & 3))) & 255u], xs[j]));
       }
     } else {
+      static_assert(!(D16 && tune.legacy), "16-bit offsets in the prefetching loop only");
       const idx* c = scol + sbase + (q & 31);
+      const short* c16 = scol16 + sbase + (q & 31);
       const double* vv = sval + sbase + (q & 31);
+      const idx ri = static_cast<idx>(r);
+      auto ldc = [&](int off) -> idx {
+        if constexpr (D16)
+          return ri + static_cast<idx>(__ldcs(c16 + off));
+        else
+          return __ldcs(c + off);
+      };
       // 4 slots per step; the next step's columns and values load under this step's gathers
       idx cc[4];
       double vq[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        cc[j] = j < len ? __ldcs(c + 32 * j) : 0;
+        cc[j] = j < len ? ldc(32 * j) : 0;
         vq[j] = j < len ? __ldcs(vv + 32 * j) : 0.0;
       }
       for (int k = 0; k < len; k += 4) {
@@ -1017,7 +1065,7 @@ __global__ void __launch_bounds__(256, kSellTunes[T].minb)
         if (!tune.pf && k > 0) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            cc[j] = j < m ? __ldcs(c + 32 * (k + j)) : 0;
+            cc[j] = j < m ? ldc(32 * (k + j)) : 0;
             vq[j] = j < m ? __ldcs(vv + 32 * (k + j)) : 0.0;
           }
         }
@@ -1030,7 +1078,7 @@ __global__ void __launch_bounds__(256, kSellTunes[T].minb)
         if (tune.pf) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            cc[j] = j + 4 < m ? __ldcs(c + 32 * (k + 4 + j)) : 0;
+            cc[j] = j + 4 < m ? ldc(32 * (k + 4 + j)) : 0;
             vq[j] = j + 4 < m ? __ldcs(vv + 32 * (k + 4 + j)) : 0.0;
           }
         }
@@ -1051,22 +1099,22 @@ __global__ void __launch_bounds__(256, kSellTunes[T].minb)
   }
 }
 
-template <Epi E, bool VI, int T>
+template <Epi E, bool VI, int T, bool D16 = false>
 void launch_sell_t(const DevCsr& A, const SpmvArgs& a) {
   static std::atomic<int> per_sm_cache{0};
   int per_sm = per_sm_cache.load();
   if (!per_sm) {
-    AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sell<E, VI, T>, 256, 0));
+    AGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sell<E, VI, T, D16>, 256, 0));
     per_sm = std::max(1, per_sm);
     per_sm_cache.store(per_sm);
   }
   const int64_t nrows = a.row_count >= 0 ? a.row_count : A.n_rows - a.row_base;
   const int64_t grid = std::min<int64_t>(grid_for(nrows, 256), static_cast<int64_t>(per_sm) * sm_count());
-  const auto kern = k_sell<E, VI, T>;
+  const auto kern = k_sell<E, VI, T, D16>;
   AGG_LAUNCH(kern, static_cast<unsigned>(grid), 256, 0, A.rowptr.get(), A.sell_ptr.get(),
              A.sell_col.get(), A.sell_val.get(), A.sell_code.get(), A.sell_pcol.get(), A.sell_tab.get(),
              A.sell_perm.size() ? A.sell_perm.get() : nullptr, A.sell_len.get(), a.row_base, nrows, a,
-             reduce_partials(), reduce_ticket());
+             reduce_partials(), reduce_ticket(), A.sell_col16.get());
 }
 
 #ifdef AGGMG_SELL_SWEEP
@@ -1092,11 +1140,20 @@ int sell_sweep_variant() {
 template <Epi E, bool VI>
 void launch_sell_v(const DevCsr& A, const SpmvArgs& a) {
 #ifdef AGGMG_SELL_SWEEP
-  if (sell_sweep_variant() >= 0) {
+  if (sell_sweep_variant() >= 0 && !A.sell_d16) {
     launch_sell_sweep<E, VI>(A, a, sell_sweep_variant());
     return;
   }
 #endif
+  if constexpr (!VI) {
+    if (A.sell_d16) {
+      if (A.sell_short)
+        launch_sell_t<E, false, sell_tune(E, false, true), true>(A, a);
+      else
+        launch_sell_t<E, false, sell_tune(E, false, false), true>(A, a);
+      return;
+    }
+  }
   if (A.sell_short)
     launch_sell_t<E, VI, sell_tune(E, VI, true)>(A, a);
   else
@@ -1252,7 +1309,10 @@ double spmv_bytes(const DevCsr& A, Epi epi) {
   // the launch_stream dispatch: SELL with a value dictionary reads 4 + 1 bytes per entry
   const bool vi = A.sell && A.sell_vi && epi != Epi::kResidualZero &&
                   !(epi == Epi::kJacobiDot2 && A.sell_short && !fuse_dots_on_dictionary());
-  double b = (vi ? 5.0 : 12.0) * nnz + 4.0 * (n + 1) + 8.0 * static_cast<double>(A.n_cols) + 8.0 * n;
+  const bool d16 = A.sell && A.sell_d16 && epi != Epi::kResidualZero &&
+                   !(epi == Epi::kJacobiDot2 && A.sell_short);
+  double b = (vi ? 5.0 : d16 ? 10.0 : 12.0) * nnz + 4.0 * (n + 1) + 8.0 * static_cast<double>(A.n_cols) +
+             8.0 * n;
   // the row-pattern format: a two-byte pattern id per row (the tables are L1-resident)
   if (A.pat && epi != Epi::kResidualZero) b = 2.0 * n + 8.0 * static_cast<double>(A.n_cols) + 8.0 * n;
   switch (epi) {

@@ -46,6 +46,9 @@ struct DevCsr {
   // length of the row at position q (<= 64): the SELL kernels read it beside the slice base,
   // so a row's column loads wait on no rowptr / perm round trip
   DevBuf<unsigned char> sell_len;
+  // plain layout with every column within 32767 of its row: 16-bit offsets instead of columns
+  bool sell_d16 = false;
+  DevBuf<short> sell_col16;
 
   // Row-pattern dictionary (stencil-like operators: at most kPatMax distinct rows up to the
   // diagonal shift): row r's entries are (r + pat_delta[p][j], pat_val[p][j]), j < pat_len[p],
