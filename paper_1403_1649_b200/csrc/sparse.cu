@@ -1052,38 +1052,39 @@ __global__ void __launch_bounds__(256, kSellTunes[T].minb)
         else
           return __ldcs(c + off);
       };
-      // 4 slots per step; the next step's columns and values load under this step's gathers
-      idx cc[4];
-      double vq[4];
+      // W = 4 g slots per step; the next step's columns and values load under this step's gathers
+      constexpr int W = 4 * tune.g;
+      idx cc[W];
+      double vq[W];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < W; ++j) {
         cc[j] = j < len ? ldc(32 * j) : 0;
         vq[j] = j < len ? __ldcs(vv + 32 * j) : 0.0;
       }
-      for (int k = 0; k < len; k += 4) {
+      for (int k = 0; k < len; k += W) {
         const int m = len - k;
         if (!tune.pf && k > 0) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < W; ++j) {
             cc[j] = j < m ? ldc(32 * (k + j)) : 0;
             vq[j] = j < m ? __ldcs(vv + 32 * (k + j)) : 0.0;
           }
         }
-        double xs[4], vs[4];
+        double xs[W], vs[W];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < W; ++j) {
           xs[j] = j < m ? __ldg(x + cc[j]) : 0.0;
           vs[j] = vq[j];
         }
         if (tune.pf) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            cc[j] = j + 4 < m ? ldc(32 * (k + 4 + j)) : 0;
-            vq[j] = j + 4 < m ? __ldcs(vv + 32 * (k + 4 + j)) : 0.0;
+          for (int j = 0; j < W; ++j) {
+            cc[j] = j + W < m ? ldc(32 * (k + W + j)) : 0;
+            vq[j] = j + W < m ? __ldcs(vv + 32 * (k + W + j)) : 0.0;
           }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < W; ++j)
           if (j < m) sum = __dadd_rn(sum, __dmul_rn(vs[j], xs[j]));
       }
     }
