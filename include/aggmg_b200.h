@@ -283,7 +283,9 @@ int aggmg_dmatrix_jump27(int64_t nx, int64_t ny, int64_t nz, double jump, int64_
 int aggmg_dmatrix_size(const aggmg_dmatrix* A, int64_t* n_rows, int64_t* nnz);
 /* 1 in *sell when the operator carries a SELL-32 copy (large operators, 4-64 entries per row:
  * its SpMV-family kernels run sliced-ELL), 2 when that copy also stores its values as one-byte
- * codes into a table of the <= 256 distinct values (stencil operators), else 0 (CSR-stream) */
+ * codes into a table of the <= 256 distinct values (stencil operators), 3 when the operator is
+ * stored as row-pattern ids (stencil operators with <= 16 entries per row and <= 4096
+ * distinct rows up to the diagonal shift: aggmg_set_row_patterns), else 0 (CSR-stream) */
 int aggmg_dmatrix_format(const aggmg_dmatrix* A, int* sell);
 int aggmg_dmatrix_to_host(const aggmg_dmatrix* A, aggmg_csr* out);
 void aggmg_dmatrix_free(aggmg_dmatrix* A);
@@ -351,7 +353,8 @@ int aggmg_dist_matrix_jump27(aggmg_comm* c, int64_t nx, int64_t ny, int64_t nz, 
                              int64_t block, aggmg_dist_matrix** out);
 int aggmg_dist_matrix_info(const aggmg_dist_matrix* A, int64_t* n_global, int64_t* row0,
                            int64_t* n_local, int64_t* nnz_local);
-/* this rank's rows: 1 = SELL-32 copy, 2 = SELL-32 with the value dictionary, 0 = CSR-stream */
+/* this rank's rows: 1 = SELL-32 copy, 2 = SELL-32 with the value dictionary, 3 = row-pattern
+ * ids, 0 = CSR-stream */
 int aggmg_dist_matrix_format(const aggmg_dist_matrix* A, int* sell);
 void aggmg_dist_matrix_free(aggmg_dist_matrix* A);
 
